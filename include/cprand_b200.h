@@ -1,0 +1,218 @@
+/* cprand_b200.h — C ABI of the B200 (sm_100a) CPRAND / CPRAND-MIX hot path.
+ *
+ * Drop-in boundary for the reference's C++ entry points (paths relative to
+ * /root/reference/proj/include/cprand/):
+ *   cprand()          sampling.hpp:257      -> cprand_solve(CPRAND_METHOD_RAND, ...)
+ *   cprand_mix()      mixing.hpp:326, :340  -> cprand_solve(CPRAND_METHOD_MIX, ...)
+ *   cprand_premix()   mixing.hpp:351, :372  -> cprand_solve(CPRAND_METHOD_PREMIX, ...)
+ *   SolveOptions      solver.hpp:40-64      -> cprand_options_t
+ *   SolveResult       solver.hpp:83-90      -> cprand_result_t + out buffers
+ *   TraceRecord       solver.hpp:75-81      -> cprand_trace_record_t
+ *   StopReason        solver.hpp:66-73      -> CPRAND_STOP_*
+ * Operator-level entry points mirror the reference's free functions:
+ *   gather_fibers     tensor.hpp:188        -> cprand_gather_fibers
+ *   skr               sampling.hpp:75       -> cprand_skr
+ *   sampled_update +  sampling.hpp:96,      -> cprand_mode_update (one fused
+ *   normalize_columns kruskal.hpp:51           mode step, teacher-forced)
+ *   make_fit_estimator sampling.hpp:155     -> cprand_fit_values
+ *   estimate_fit      sampling.hpp:191      -> cprand_estimate_fit
+ *   mix_tensor        mixing.hpp:131        -> cprand_mix_tensor
+ *   mix_factor        mixing.hpp:160        -> cprand_mix_factor
+ *   unmix_sampled_rhs mixing.hpp:219        -> cprand_unmix_rows
+ *   unmix_factor      mixing.hpp:191        -> cprand_unmix_factor
+ *   default_sample_count sampling.hpp:18    -> cprand_default_sample_count
+ *
+ * Conventions: plain pointers and sizes, no C++ or CUDA types. Matrices are
+ * column-major (Eigen's default, so an Eigen::Map over the caller's storage
+ * is zero-copy); tensors are generalized column-major, mode-1 fastest
+ * (tensor.hpp:11-33). Index tables are int64 S x (N-1) column-major
+ * (IndexTable, types.hpp:33). Every call blocks the calling thread until its
+ * result is on the host, like the reference.
+ *
+ * Errors (the reference throws; the ABI returns a status, message in
+ * cprand_last_error(), thread-local):
+ *   0 ok
+ *   2 std::invalid_argument / std::out_of_range   (CLI exit 2)
+ *   3 numerical_consistency_error                 (CLI exit 3)
+ *   4 CUDA / NCCL runtime failure
+ *   5 valid for the reference but outside this path (e.g. R > 64, FFT mixing)
+ *   1 anything else
+ */
+#ifndef CPRAND_B200_H
+#define CPRAND_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  CPRAND_OK = 0,
+  CPRAND_ERR_INTERNAL = 1,
+  CPRAND_ERR_INVALID = 2,
+  CPRAND_ERR_NUMERICAL = 3,
+  CPRAND_ERR_CUDA = 4,
+  CPRAND_ERR_UNSUPPORTED = 5
+};
+
+enum { CPRAND_METHOD_ALS = 0, CPRAND_METHOD_RAND = 1, CPRAND_METHOD_MIX = 2, CPRAND_METHOD_PREMIX = 3 };
+enum {
+  CPRAND_TRANSFORM_UNSET = -1,
+  CPRAND_TRANSFORM_FFT = 0,
+  CPRAND_TRANSFORM_DCT = 1,
+  CPRAND_TRANSFORM_WHT = 2,
+  CPRAND_TRANSFORM_IDENTITY = 3
+};
+enum { CPRAND_INIT_RANDOM = 0, CPRAND_INIT_HOSVD = 1, CPRAND_INIT_GIVEN = 2 };
+enum {
+  CPRAND_STOP_MAX_ITERATIONS = 0,
+  CPRAND_STOP_FIT_STAGNATION = 1,
+  CPRAND_STOP_FIT_THRESHOLD = 2,
+  CPRAND_STOP_BEST_FIT_STALL = 3,
+  CPRAND_STOP_ZERO_TENSOR = 4,
+  CPRAND_STOP_BENCH_COMPLETE = 5
+};
+
+/* SolveOptions (solver.hpp:40-64); first 12 fields mirror it one to one. */
+typedef struct cprand_options {
+  int32_t max_iters;          /* 200 */
+  double fit_tolerance;       /* 1e-4 (ALS only; validated) */
+  int32_t has_fit_threshold;  /* std::optional<double> fit_threshold */
+  double fit_threshold;
+  uint64_t rng_seed;          /* 0 */
+  int32_t init;               /* CPRAND_INIT_*; given -> init_lambda/init_factors */
+  int64_t fit_sample_count;   /* 1 << 14 */
+  int32_t stall_limit;        /* 10 */
+  int32_t transform;          /* CPRAND_TRANSFORM_*; -1 = method default */
+  int32_t bench_mode;
+  int32_t exhaustive_samples; /* test hook */
+  int32_t exact_fit_trace;    /* test hook */
+  /* B200 extensions */
+  int32_t device;             /* CUDA ordinal, -1 = current */
+  int32_t x_is_device;        /* cprand_solve: x is a device pointer */
+  int32_t x_mutable;          /* device x may be mixed in place (MIX/PREMIX) */
+  void* comm;                 /* cprand_comm_t for slab-sharded runs, NULL = 1 GPU */
+} cprand_options_t;
+
+typedef struct cprand_trace_record {
+  int32_t iteration;
+  double elapsed_seconds;
+  double fit;
+  int32_t fit_is_estimate;
+  double best_fit_so_far;
+} cprand_trace_record_t;
+
+typedef struct cprand_result {
+  int32_t iterations;
+  int32_t reason;             /* CPRAND_STOP_* */
+  double setup_seconds;
+  double total_seconds;
+  int32_t trace_len;          /* records produced (may exceed trace_cap) */
+  double loop_seconds_device; /* CUDA-event time of the outer loop */
+} cprand_result_t;
+
+void cprand_options_init(cprand_options_t* opts);
+const char* cprand_last_error(void);
+int cprand_device_count(void);
+int64_t cprand_default_sample_count(int64_t r); /* -1 on invalid r */
+const char* cprand_build_info(void);
+
+/* One-shot drop-in solve. x: host (or device with x_is_device) tensor in
+ * storage order; dims[order]. Outputs: out_lambda[r], out_factors[n] ->
+ * dims[n] x r column-major (caller-allocated). trace may be NULL. */
+int cprand_solve(int32_t method, const double* x, const int64_t* dims, int32_t order, int64_t r,
+                 int64_t s, const cprand_options_t* opts, const double* init_lambda,
+                 const double* const* init_factors, double* out_lambda, double* const* out_factors,
+                 cprand_trace_record_t* trace, int32_t trace_cap, cprand_result_t* res);
+
+/* ---- device-resident tensors and solver sessions (bench / serving) ---- */
+typedef struct cprand_tensor_s* cprand_tensor_t;
+typedef struct cprand_session_s* cprand_session_t;
+
+int cprand_tensor_create(const int64_t* dims, int32_t order, int32_t device, cprand_tensor_t* out);
+int cprand_tensor_upload(cprand_tensor_t t, const double* host);
+int cprand_tensor_download(cprand_tensor_t t, double* host);
+/* BASELINE.json generator in HBM: factors G_n L^T (host RNG, seeded_engine
+ * (seed, 5)), lambda = 1, eta-scaled Philox Gaussian noise. out_factors
+ * (nullable) receives the truth, column-major. */
+int cprand_tensor_synth(cprand_tensor_t t, int64_t r, double collinearity, double eta,
+                        uint64_t seed, double* const* out_factors);
+double* cprand_tensor_device_ptr(cprand_tensor_t t);
+void cprand_tensor_destroy(cprand_tensor_t t);
+
+/* Setup (init, sample tables, fit estimator, mixing pass). The session keeps
+ * a reference to t; MIX/PREMIX mix t in place when opts->x_mutable, else
+ * into a private copy. */
+int cprand_session_create(int32_t method, cprand_tensor_t t, int64_t r, int64_t s,
+                          const cprand_options_t* opts, const double* init_lambda,
+                          const double* const* init_factors, cprand_session_t* out);
+/* Runs up to n more outer iterations (fewer if the stop rule fires or
+ * max_iters is reached) and waits for them. *ran = iterations executed. */
+int cprand_session_run(cprand_session_t s, int32_t n, int32_t* ran);
+/* Bench mode only: enqueues n iterations on the session stream, no wait. */
+int cprand_session_enqueue(cprand_session_t s, int32_t n);
+int cprand_session_sync(cprand_session_t s);
+/* Bench mode: waits for queued work, then enqueues n iterations between two
+ * CUDA events on the session stream and waits; *ms = event time. */
+int cprand_session_timed_enqueue(cprand_session_t s, int32_t n, double* ms);
+void* cprand_session_stream(cprand_session_t s); /* cudaStream_t */
+/* Per-launch CUDA-event timing of the fused gather/SKR/RHS kernel
+ * (on the session stream). Enable before enqueueing. */
+int cprand_session_set_kernel_timing(cprand_session_t s, int32_t on);
+/* Totals per mode over the timed launches since enabling: count, ms, and
+ * the algorithmic bytes those launches moved (B_min accounting). */
+int cprand_session_kernel_stats(cprand_session_t s, int32_t mode, int64_t* launches,
+                                double* total_ms, double* bytes);
+int cprand_session_result(cprand_session_t s, double* out_lambda, double* const* out_factors,
+                          cprand_trace_record_t* trace, int32_t trace_cap, cprand_result_t* res);
+void cprand_session_destroy(cprand_session_t s);
+
+/* Page-locked host buffers (cudaHostAlloc) for fast H2D of large tensors. */
+void* cprand_host_alloc_pinned(uint64_t bytes);
+void cprand_host_free_pinned(void* p);
+
+/* ---- operator-level entry points (host buffers in/out) ---- */
+int cprand_gather_fibers(const double* x, const int64_t* dims, int32_t order, int32_t mode,
+                         const int64_t* idxs, int64_t s, double* out /* I_n x S */);
+int cprand_skr(const int64_t* idxs, int64_t s, const int64_t* dims, int32_t order, int32_t mode,
+               int64_t r, const double* const* factors, double* out /* S x R */);
+/* One fused mode update (gather + SKR + Gram + RHS + solve + normalize)
+ * from the given factors: writes the new factor (dims[mode] x r) and lambda
+ * (in/out). mixing_transform >= 0 runs the MIX step (x already mixed,
+ * factors unmixed; signs from seed). */
+int cprand_mode_update(const double* x, const int64_t* dims, int32_t order, int32_t mode,
+                       const int64_t* idxs, int64_t s, int64_t r, const double* const* factors,
+                       double* lambda, int32_t first_of_pass, int32_t mixing_transform,
+                       uint64_t mixing_seed, double* out_factor, int32_t* rank);
+int cprand_fit_values(const double* x, const int64_t* dims, int32_t order, const int64_t* offsets,
+                      int64_t n, double* out_values, double* out_norm);
+int cprand_estimate_fit(const double* lambda, const double* const* factors, const int64_t* dims,
+                        int32_t order, int64_t r, const int64_t* idxs /* P_hat x N */,
+                        const double* values, int64_t phat, double x_norm, int64_t total,
+                        double* out_fit);
+int cprand_mix_tensor(const double* x, const int64_t* dims, int32_t order, int32_t transform,
+                      uint64_t seed, double* out);
+int cprand_mix_factor(const double* a, int64_t rows, int64_t r, const int64_t* dims, int32_t order,
+                      int32_t transform, uint64_t seed, int32_t mode, double* out);
+int cprand_unmix_factor(const double* a, int64_t rows, int64_t r, const int64_t* dims,
+                        int32_t order, int32_t transform, uint64_t seed, int32_t mode, double* out);
+/* unmix_sampled_rhs on G (S x I_n column-major) */
+int cprand_unmix_rows(const double* g, int64_t s, int64_t in, const int64_t* dims, int32_t order,
+                      int32_t transform, uint64_t seed, int32_t mode, double* out);
+/* Device normalize-RNG self check: n normals from seeded_engine(seed, 8)
+ * drawn by the device mt19937_64 + polar method. */
+int cprand_debug_normal_stream(uint64_t seed, int32_t n, double* out);
+
+/* ---- slab sharding over NCCL (one process per GPU) ---- */
+typedef struct cprand_comm_s* cprand_comm_t;
+int cprand_comm_unique_id(uint8_t out[128]);
+int cprand_comm_create(const uint8_t id[128], int32_t rank, int32_t nranks, int32_t device,
+                       cprand_comm_t* out);
+void cprand_comm_destroy(cprand_comm_t c);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CPRAND_B200_H */

@@ -1,0 +1,124 @@
+// Launch wrappers for the sm_100a kernels (kernels.cu, mix.cu, synth.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace cpb {
+
+// ---- plain operators (parity / operator-level C ABI) -----------------------
+// X_S (I_n x S, column-major) = fibers named by base offsets (tensor.hpp:188).
+void launch_gather_fibers(const double* x, i64 in, i64 stride, const i64* base, int s,
+                          double* out, cudaStream_t st);
+// Z_S (S x R, column-major), ascending-mode Hadamard fold (sampling.hpp:74-92).
+void launch_skr(const ModeView& v, double* out, cudaStream_t st);
+// base[s] = sum_c rows[c][s] * kstride[c]  (int32 rows -> int64 offsets)
+void launch_base_offsets(const int* rows, int kept, int s, const i64* kstride_host, i64* base,
+                         cudaStream_t st);
+
+// ---- fused per-mode update --------------------------------------------------
+struct ModeWork {
+  double* part_rhs;    // [ks][I_n][R]
+  double* part_gram;   // [ks][R][R]
+  double* ginv;        // [R][R]   (pinv of the Gram, written by the last m-tile-0 CTA)
+  int* info;           // [0] = numerical rank of the Gram
+  unsigned* ticket;    // [0] gram ticket, [1] norm ticket (self-resetting)
+  double* ssq;         // [grid][R] column sum-of-squares partials
+  double* norms;       // [R]
+  double* lambda;      // [R]
+  double* a;           // I_n x R row-major factor (output, normalized by launch_normalize)
+  const int* stop;     // device stop flag (kernels return early when set), may be null
+  int ks;              // sample splits
+  int ks_len;          // samples per split (multiple of the K tile)
+  double tol;          // Gram pivot threshold (relative to the largest pivot)
+};
+
+int rank_bucket(int r);  // 16 / 32 / 64
+// grid sizing used by the solver to allocate partials
+void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms);
+
+void launch_mode_rhs(const ModeView& v, const ModeWork& w, cudaStream_t st);
+// rhs_override != null: use it (I_n x R row-major, already reduced) instead of
+// summing part_rhs (the MIX path unmixes the RHS first).
+void launch_mode_apply(const ModeView& v, const ModeWork& w, const double* rhs_override,
+                       int first_of_pass, cudaStream_t st);
+// A /= norms (column-wise), zero columns refilled from the device normalize RNG.
+void launch_normalize(const ModeWork& w, i64 in, int r, unsigned long long* norm_rng_state,
+                      cudaStream_t st);
+
+// ---- fit estimator ----------------------------------------------------------
+void launch_gather_values(const double* x, const i64* offsets, i64 n, double* out,
+                          cudaStream_t st);
+// sum of squares, deterministic two-level reduction into *out
+void launch_sumsq(const double* x, i64 n, double* partials, int nparts, double* out,
+                  cudaStream_t st);
+struct FitState {
+  double best_fit;
+  int stall_count;
+  int stopped;
+  int reason;
+  int iterations;
+  long long t_start_ns;
+};
+struct TraceRec {
+  int iteration;
+  int pad;
+  long long t_ns;
+  double fit;
+  double best_fit;
+};
+struct FitArgs {
+  int order;
+  int r;
+  i64 phat;
+  const int* idx[kMaxOrder];     // per mode: P_hat row indices
+  const double* fac[kMaxOrder];  // row-major factors (normalized)
+  const double* lambda;
+  const double* values;          // x at the sampled entries
+  double x_norm;
+  double total;                  // P as double
+  double* partials;              // [blocks]
+  unsigned* ticket;
+  FitState* state;
+  TraceRec* trace;
+  int* stop_host_mapped;         // zero-copy mirror of state->stopped (may be null)
+  int iteration;
+  int max_iters;
+  int has_threshold;
+  double threshold;
+  int stall_limit;
+  int exact;                     // 1 when values cover every entry (fit_is_estimate = 0 not implied)
+};
+void launch_estimate_fit(const FitArgs& a, cudaStream_t st);
+void launch_stamp_start(FitState* s, cudaStream_t st);
+
+// ---- normalize RNG (device mt19937_64 + libstdc++ polar normal) ----------
+void launch_rng_seed(unsigned long long* state, unsigned long long seed_value, cudaStream_t st);
+// test hook: n normals from a fresh distribution object
+void launch_rng_normals(unsigned long long* state, int n, double* out, cudaStream_t st);
+
+// ---- mixing (mix.cu) ----------------------------------------------------
+struct DctPlan {
+  int n = 0;
+  int nrad = 0;
+  int radix[24];
+  double2* tw = nullptr;     // n-th roots exp(-2 pi i t / n), t < n
+  double2* phase = nullptr;  // exp(-i pi k / (2n)), k < n
+  double s0 = 0, sk = 0;     // orthonormal scales sqrt(1/n), sqrt(2/n)
+};
+DctPlan make_dct_plan(int n);  // allocates device tables
+void free_dct_plan(DctPlan& p);
+// Applies sign-then-DCT-II (forward) or DCT-III-then-sign (adjoint) along a
+// mode: fiber f = (hi, lo) with element i at hi*st*n + lo + i*st, f < nfib.
+// in and out may alias (in place).
+void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 st, i64 nfib,
+                           const double* sign, int forward, const double* col_scale,
+                           cudaStream_t st_);
+// MIX path: RHS (I_n x R row-major) = D_n C^T (sum_ks part_rhs) per column
+void launch_reduce_rhs(const double* part_rhs, int ks, i64 in, int r, double* out,
+                       cudaStream_t st);
+
+// ---- synthetic generator (synth.cu) ------------------------------------
+void launch_synth(double* x, int order, const i64* dims, int r, const double* const* fac_dev,
+                  double eta, unsigned long long seed, double* scratch, cudaStream_t st);
+
+}  // namespace cpb

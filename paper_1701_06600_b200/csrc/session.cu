@@ -1,0 +1,824 @@
+// Host orchestration of the B200 CPRAND / CPRAND-MIX outer loop.
+//
+// Mirrors cprand() (sampling.hpp:257-310), cprand_mix_impl()
+// (mixing.hpp:258-318) and cprand_premix() (mixing.hpp:351-370):
+//  * every RNG draw happens on the host with the reference's libstdc++
+//    engines and distributions, so sample tables, fit offsets, init values
+//    and mixing signs are identical to the reference by construction;
+//    sampling is data-independent, so all tables are drawn and uploaded once
+//    during setup;
+//  * the per-mode chain (gather/SKR/Gram/RHS -> pinv -> solve+norms ->
+//    normalize [-> mix_factor]) and the fit + stop rule run on the device,
+//    with no host round trip per iteration: the fit kernel evaluates
+//    should_stop and raises a device flag that later kernels honour; the
+//    host keeps a bounded number of iterations in flight.
+#include "session.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <unordered_set>
+
+namespace cpb {
+
+namespace {
+using Clock = std::chrono::steady_clock;
+double seconds_since(Clock::time_point t) {
+  return std::chrono::duration<double>(Clock::now() - t).count();
+}
+constexpr int kInFlight = 4;  // outer iterations enqueued ahead of the stop check
+
+std::uint64_t splitmix_step(std::uint64_t& s) {
+  std::uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+double host_stable_norm(const double* v, i64 n) {
+  double scale = 0.0, ssq = 1.0;
+  for (i64 i = 0; i < n; ++i) {
+    if (v[i] != 0.0) {
+      const double a = std::abs(v[i]);
+      if (scale < a) {
+        ssq = 1.0 + ssq * (scale / a) * (scale / a);
+        scale = a;
+      } else {
+        ssq += (a / scale) * (a / scale);
+      }
+    }
+  }
+  return scale * std::sqrt(ssq);
+}
+
+template <class T>
+T* dalloc(size_t n) {
+  T* p = nullptr;
+  if (n == 0) n = 1;
+  CPB_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return p;
+}
+
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+// column-major (rows x r) <-> row-major
+std::vector<double> to_row_major(const double* cm, i64 rows, int r) {
+  std::vector<double> out(static_cast<size_t>(rows * r));
+  for (int c = 0; c < r; ++c)
+    for (i64 i = 0; i < rows; ++i) out[static_cast<size_t>(i * r + c)] = cm[i + c * rows];
+  return out;
+}
+void from_row_major(const std::vector<double>& rm, i64 rows, int r, double* cm) {
+  for (int c = 0; c < r; ++c)
+    for (i64 i = 0; i < rows; ++i) cm[i + c * rows] = rm[static_cast<size_t>(i * r + c)];
+}
+
+int current_device() {
+  int d = 0;
+  CPB_CUDA(cudaGetDevice(&d));
+  return d;
+}
+
+}  // namespace
+
+std::mt19937_64 seeded_engine(std::uint64_t seed, std::uint64_t stream) {
+  return std::mt19937_64(seeded_engine_seed_value(seed, stream));
+}
+
+std::uint64_t seeded_engine_seed_value(std::uint64_t seed, std::uint64_t stream) {
+  std::uint64_t st = seed ^ (0xA0761D6478BD642Full * (stream + 1));  // rng.hpp:30
+  splitmix_step(st);
+  return splitmix_step(st);
+}
+
+void Options::validate() const {  // solver.hpp:54-63
+  if (max_iters < 1) throw InvalidArgument("max_iters must be >= 1");
+  if (!(fit_tolerance > 0.0)) throw InvalidArgument("fit_tolerance must be > 0");
+  if (fit_sample_count < 1) throw InvalidArgument("fit_sample_count must be >= 1");
+  if (stall_limit < 1) throw InvalidArgument("stall_limit must be >= 1");
+}
+
+Tensor::Tensor(const std::vector<i64>& d, int dev) : dims(d), device(dev) {
+  if (dims.empty()) throw InvalidArgument("tensor order must be >= 1");
+  p = 1;
+  for (i64 v : dims) {
+    if (v < 1) throw InvalidArgument("tensor dims must be >= 1");
+    strides.push_back(p);
+    p *= v;
+  }
+  CPB_CUDA(cudaSetDevice(device));
+  CPB_CUDA(cudaMalloc(&this->d, static_cast<size_t>(p) * sizeof(double)));
+}
+
+Tensor::~Tensor() {
+  if (owned && d) cudaFree(d);
+}
+
+HostModel init_random(const std::vector<i64>& dims, int r, std::uint64_t seed) {
+  HostModel m;
+  m.lambda.assign(static_cast<size_t>(r), 1.0);
+  auto rng = seeded_engine(seed, kInitStream);
+  std::uniform_real_distribution<double> unif(0.0, 1.0);
+  for (size_t n = 0; n < dims.size(); ++n) {
+    std::vector<double> a(static_cast<size_t>(dims[n] * r), 0.0);
+    if (n != 0)
+      for (int j = 0; j < r; ++j)
+        for (i64 i = 0; i < dims[n]; ++i) a[static_cast<size_t>(i + j * dims[n])] = unif(rng);
+    m.factors.push_back(std::move(a));
+  }
+  return m;
+}
+
+void normalize_columns_host(HostModel& m, const std::vector<i64>& dims, int mode, bool first,
+                            std::mt19937_64& rng) {
+  std::vector<double>& a = m.factors[static_cast<size_t>(mode)];
+  const i64 rows = dims[static_cast<size_t>(mode)];
+  const int r = static_cast<int>(m.lambda.size());
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  for (int c = 0; c < r; ++c) {
+    double* col = a.data() + static_cast<i64>(c) * rows;
+    const double nrm = host_stable_norm(col, rows);
+    if (nrm == 0.0) {
+      for (i64 i = 0; i < rows; ++i) col[i] = gauss(rng);
+      const double fn = host_stable_norm(col, rows);
+      for (i64 i = 0; i < rows; ++i) col[i] = col[i] / fn;
+      m.lambda[static_cast<size_t>(c)] = 0.0;
+      continue;
+    }
+    for (i64 i = 0; i < rows; ++i) col[i] = col[i] / nrm;
+    m.lambda[static_cast<size_t>(c)] = first ? m.lambda[static_cast<size_t>(c)] * nrm : nrm;
+  }
+}
+
+// sampling.hpp:121-149
+std::vector<i64> sample_offsets_without_replacement(i64 total, i64 want, std::mt19937_64& rng) {
+  std::vector<i64> out;
+  if (want >= total) {
+    out.resize(static_cast<size_t>(total));
+    std::iota(out.begin(), out.end(), i64{0});
+    return out;
+  }
+  if (total <= 4 * want) {
+    std::vector<i64> pool(static_cast<size_t>(total));
+    std::iota(pool.begin(), pool.end(), i64{0});
+    for (i64 i = 0; i < want; ++i) {
+      std::uniform_int_distribution<long> pick(i, total - 1);
+      std::swap(pool[static_cast<size_t>(i)], pool[static_cast<size_t>(pick(rng))]);
+    }
+    out.assign(pool.begin(), pool.begin() + want);
+  } else {
+    std::unordered_set<i64> seen;
+    seen.reserve(static_cast<size_t>(want) * 2);
+    std::uniform_int_distribution<long> pick(0, total - 1);
+    out.reserve(static_cast<size_t>(want));
+    while (static_cast<i64>(out.size()) < want) {
+      const i64 cand = pick(rng);
+      if (seen.insert(cand).second) out.push_back(cand);
+    }
+  }
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+std::vector<std::vector<double>> mixing_signs(const std::vector<i64>& dims, int kind,
+                                              std::uint64_t seed) {
+  std::vector<std::vector<double>> out;
+  auto rng = seeded_engine(seed, kMixingStream);
+  std::bernoulli_distribution coin(0.5);
+  for (i64 d : dims) {
+    std::vector<double> s(static_cast<size_t>(d), 1.0);
+    if (kind != 3)
+      for (auto& v : s) v = coin(rng) ? 1.0 : -1.0;
+    out.push_back(std::move(s));
+  }
+  return out;
+}
+
+void baseline_factors_host(const std::vector<i64>& dims, int r, double c, std::uint64_t seed,
+                           std::vector<std::vector<double>>& out) {
+  if (!(c >= 0.0 && c < 1.0)) throw InvalidArgument("collinearity must be in [0, 1)");
+  std::vector<double> l(static_cast<size_t>(r * r), 0.0);  // row-major lower
+  for (int j = 0; j < r; ++j) {
+    double d = 1.0;
+    for (int k = 0; k < j; ++k) d -= l[j * r + k] * l[j * r + k];
+    l[j * r + j] = std::sqrt(d);
+    for (int i = j + 1; i < r; ++i) {
+      double s = c;
+      for (int k = 0; k < j; ++k) s -= l[i * r + k] * l[j * r + k];
+      l[i * r + j] = s / l[j * r + j];
+    }
+  }
+  auto rng = seeded_engine(seed, kSynthStream);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  out.clear();
+  for (i64 d : dims) {
+    std::vector<double> g(static_cast<size_t>(d * r));
+    for (int j = 0; j < r; ++j)
+      for (i64 i = 0; i < d; ++i) g[static_cast<size_t>(i + j * d)] = gauss(rng);
+    std::vector<double> a(static_cast<size_t>(d * r));
+    for (int j = 0; j < r; ++j)
+      for (i64 i = 0; i < d; ++i) {
+        double s = 0.0;
+        for (int k = 0; k <= j; ++k) s += g[static_cast<size_t>(i + k * d)] * l[j * r + k];
+        a[static_cast<size_t>(i + j * d)] = s;
+      }
+    out.push_back(std::move(a));
+  }
+}
+
+// ============================================================== Session
+Session::Session(int method, Tensor* x, int r, int s, const Options& o, const double* init_lambda,
+                 const double* const* init_factors)
+    : method_(method), x_(x), order_(static_cast<int>(x->dims.size())), r_(r), s_(s), o_(o) {
+  o_.validate();
+  if (method == 0) throw Unsupported("cp_als is outside the randomized B200 path");
+  if (method < 1 || method > 3) throw InvalidArgument("unknown method");
+  if (o_.init == 2 && init_factors == nullptr)
+    throw InvalidArgument("init=given requires an init model");
+  if (r < 1) throw InvalidArgument("rank must be >= 1");
+  if (method != 3 || true) {
+    if (s < r) throw InvalidArgument("sample count must be at least the rank");
+  }
+  if (method == 2) transform_ = o_.transform >= 0 ? o_.transform : 0;
+  if (method == 3) transform_ = o_.transform >= 0 ? o_.transform : 1;
+  if (method >= 2) {
+    if (transform_ == 2)
+      for (i64 d : x->dims)
+        if ((d & (d - 1)) != 0) throw InvalidArgument("wht requires power-of-two mode lengths");
+    if (method == 3 && transform_ == 0)
+      throw InvalidArgument("premix requires a real orthogonal transform");
+    if (transform_ == 0) throw Unsupported("FFT (complex) mixing is not on the B200 path yet; use dct");
+    if (transform_ == 2) throw Unsupported("WHT mixing is not on the B200 path yet; use dct");
+  }
+  if (order_ > kMaxOrder) throw Unsupported("tensor order > 8");
+  if (r > kMaxRank) throw Unsupported("rank > 64 is not supported by the fused sm_100a kernels");
+  if (o_.init == 1) throw Unsupported("hosvd init is outside the randomized B200 path");
+  mix_ = (method == 2 && transform_ == 1);
+  premix_ = (method == 3 && transform_ == 1);
+  dims_ = x->dims;
+  strides_ = x->strides;
+  p_ = x->p;
+  CPB_CUDA(cudaSetDevice(x->device));
+  CPB_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, x->device));
+  CPB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  CPB_CUDA(cudaEventCreate(&ev_loop0_));
+  CPB_CUDA(cudaEventCreate(&ev_loop1_));
+  k_launches_.assign(static_cast<size_t>(order_), 0);
+  k_ms_.assign(static_cast<size_t>(order_), 0.0);
+  k_bytes_.assign(static_cast<size_t>(order_), 0.0);
+  setup(init_lambda, init_factors);
+}
+
+Session::~Session() {
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& f : fac_) dfree(f);
+  for (auto& f : mixed_) dfree(f);
+  for (auto& f : fit_idx_) dfree(f);
+  for (auto& s : signs_) dfree(s);
+  for (auto& p : plans_) free_dct_plan(p);
+  dfree(lambda_);
+  dfree(norms_);
+  dfree(rows_);
+  dfree(base_);
+  dfree(part_rhs_);
+  dfree(part_gram_);
+  dfree(ginv_);
+  dfree(info_);
+  dfree(tickets_);
+  dfree(ssq_);
+  dfree(rhs_full_);
+  dfree(rng_state_);
+  dfree(fit_vals_);
+  dfree(fit_part_);
+  dfree(state_);
+  dfree(trace_dev_);
+  dfree(xcopy_);
+  if (stop_host_) cudaFreeHost(stop_host_);
+  for (auto& e : it_events_) cudaEventDestroy(e);
+  for (auto& e : ev_pool_) cudaEventDestroy(e);
+  for (auto& p : pending_) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  if (ev_loop0_) cudaEventDestroy(ev_loop0_);
+  if (ev_loop1_) cudaEventDestroy(ev_loop1_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Session::setup(const double* init_lambda, const double* const* init_factors) {
+  const int nparts = 1024;
+  fit_part_ = dalloc<double>(std::max<i64>(nparts + 1, 8192));
+  // ---- zero tensor short-circuit (sampling.hpp:263-264, solver.hpp:204-216)
+  if (!o_.bench_mode) {
+    launch_sumsq(x_->d, p_, fit_part_, nparts, fit_part_ + nparts, stream_);
+    double ss = 0.0;
+    CPB_CUDA(cudaMemcpyAsync(&ss, fit_part_ + nparts, sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+    x_norm_ = std::sqrt(ss);
+    if (x_norm_ == 0.0) {
+      finish_zero_tensor();
+      return;
+    }
+  }
+  t0_ = Clock::now();
+  // ---- init (solver.hpp:185-201)
+  HostModel m;
+  if (o_.init == 2) {
+    m.lambda.assign(init_lambda, init_lambda + r_);
+    for (int n = 0; n < order_; ++n)
+      m.factors.emplace_back(init_factors[n], init_factors[n] + dims_[static_cast<size_t>(n)] * r_);
+  } else {
+    m = init_random(dims_, r_, o_.rng_seed);
+  }
+  for (int n = 0; n < order_; ++n) {
+    const i64 rows = dims_[static_cast<size_t>(n)];
+    fac_.push_back(dalloc<double>(static_cast<size_t>(rows * r_)));
+    const auto rm = to_row_major(m.factors[static_cast<size_t>(n)].data(), rows, r_);
+    CPB_CUDA(cudaMemcpyAsync(fac_.back(), rm.data(), rm.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, stream_));
+  }
+  lambda_ = dalloc<double>(static_cast<size_t>(r_));
+  CPB_CUDA(cudaMemcpyAsync(lambda_, m.lambda.data(), sizeof(double) * r_, cudaMemcpyHostToDevice, stream_));
+  norms_ = dalloc<double>(static_cast<size_t>(order_ * r_));
+  rng_state_ = dalloc<unsigned long long>(313);
+  launch_rng_seed(rng_state_, seeded_engine_seed_value(o_.rng_seed, kInitStream + 7), stream_);
+
+  // ---- sample tables (data independent: all drawn up front)
+  build_tables();
+
+  // ---- estimator on the ORIGINAL tensor for rand / mix (mixing.hpp:268-273)
+  xsolve_ = x_->d;
+  if (!o_.bench_mode && !premix_) build_fit_estimator(x_->d);
+  if (mix_ || premix_) mix_setup();
+  if (!o_.bench_mode && premix_) {
+    // cprand(x_hat) builds its estimator and norm on the mixed tensor
+    launch_sumsq(xsolve_, p_, fit_part_, nparts, fit_part_ + nparts, stream_);
+    double ss = 0.0;
+    CPB_CUDA(cudaMemcpyAsync(&ss, fit_part_ + nparts, sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+    x_norm_ = std::sqrt(ss);
+    build_fit_estimator(xsolve_);
+  }
+
+  // ---- per-mode work buffers
+  i64 max_part = 1, max_in = 1, max_apply = 1;
+  int max_ks = 1;
+  for (int n = 0; n < order_; ++n) {
+    int ks, len;
+    mode_splits(dims_[static_cast<size_t>(n)], s_mode_[static_cast<size_t>(n)], rank_bucket(r_), &ks, &len, sms_);
+    ks_.push_back(ks);
+    ks_len_.push_back(len);
+    max_part = std::max(max_part, static_cast<i64>(ks) * dims_[static_cast<size_t>(n)] * r_);
+    max_ks = std::max(max_ks, ks);
+    max_in = std::max(max_in, dims_[static_cast<size_t>(n)]);
+    max_apply = std::max<i64>(max_apply, ceil_div(dims_[static_cast<size_t>(n)], 16));
+  }
+  part_rhs_ = dalloc<double>(static_cast<size_t>(max_part));
+  part_gram_ = dalloc<double>(static_cast<size_t>(max_ks * r_ * r_));
+  ginv_ = dalloc<double>(static_cast<size_t>(r_ * r_));
+  info_ = dalloc<int>(4);
+  tickets_ = dalloc<unsigned>(8);
+  CPB_CUDA(cudaMemsetAsync(tickets_, 0, 8 * sizeof(unsigned), stream_));
+  ssq_ = dalloc<double>(static_cast<size_t>(max_apply * r_));
+  if (mix_) rhs_full_ = dalloc<double>(static_cast<size_t>(max_in * r_));
+
+  // ---- fit / stop state
+  state_ = dalloc<FitState>(1);
+  FitState fs{};
+  fs.best_fit = -INFINITY;
+  CPB_CUDA(cudaMemcpyAsync(state_, &fs, sizeof(fs), cudaMemcpyHostToDevice, stream_));
+  trace_dev_ = dalloc<TraceRec>(static_cast<size_t>(o_.max_iters));
+  CPB_CUDA(cudaHostAlloc(&stop_host_, sizeof(int), cudaHostAllocMapped));
+  *stop_host_ = 0;
+  CPB_CUDA(cudaHostGetDevicePointer(&stop_dev_, stop_host_, 0));
+  CPB_CUDA(cudaStreamSynchronize(stream_));
+  setup_seconds_ = seconds_since(t0_);
+}
+
+void Session::finish_zero_tensor() {
+  zero_tensor_ = true;
+  finished_ = true;
+  final_reason_ = 4;
+  zero_model_ = init_random(dims_, r_, o_.rng_seed);
+  auto rng = seeded_engine(o_.rng_seed, kInitStream);
+  for (int n = 0; n < order_; ++n) normalize_columns_host(zero_model_, dims_, n, false, rng);
+  std::fill(zero_model_.lambda.begin(), zero_model_.lambda.end(), 0.0);
+}
+
+void Session::build_tables() {
+  const int N = order_;
+  s_mode_.resize(static_cast<size_t>(N));
+  for (int n = 0; n < N; ++n)
+    s_mode_[static_cast<size_t>(n)] = o_.exhaustive_samples
+                                          ? static_cast<int>(p_ / dims_[static_cast<size_t>(n)])
+                                          : s_;
+  if (o_.exhaustive_samples) {
+    for (int n = 0; n < N; ++n)
+      if (s_mode_[static_cast<size_t>(n)] < r_)
+        throw InvalidArgument("sampled_update: need at least R samples");
+  }
+  table_iters_ = o_.exhaustive_samples ? 1 : o_.max_iters;
+  i64 rows_total = 0, base_total = 0;
+  for (int it = 0; it < table_iters_; ++it)
+    for (int n = 0; n < N; ++n) {
+      row_off_.push_back(rows_total);
+      base_off_.push_back(base_total);
+      rows_total += static_cast<i64>(N - 1) * s_mode_[static_cast<size_t>(n)];
+      base_total += s_mode_[static_cast<size_t>(n)];
+    }
+  std::vector<int> rows(static_cast<size_t>(std::max<i64>(rows_total, 1)));
+  std::vector<i64> base(static_cast<size_t>(std::max<i64>(base_total, 1)), 0);
+  auto rng = seeded_engine(o_.rng_seed, kSamplingStream);
+  for (int it = 0; it < table_iters_; ++it)
+    for (int n = 0; n < N; ++n) {
+      const int sn = s_mode_[static_cast<size_t>(n)];
+      int* rb = rows.data() + row_off_[static_cast<size_t>(it * N + n)];
+      i64* bb = base.data() + base_off_[static_cast<size_t>(it * N + n)];
+      std::vector<int> km;
+      for (int k = 0; k < N; ++k)
+        if (k != n) km.push_back(k);
+      if (o_.exhaustive_samples) {
+        // sampling.hpp:54-69: unfolding column order
+        for (int j = 0; j < sn; ++j) {
+          i64 rem = j, b = 0;
+          for (int c = 0; c < N - 1; ++c) {
+            const i64 d = dims_[static_cast<size_t>(km[static_cast<size_t>(c)])];
+            const i64 idx = rem % d;
+            rem /= d;
+            rb[static_cast<i64>(c) * sn + j] = static_cast<int>(idx);
+            b += idx * strides_[static_cast<size_t>(km[static_cast<size_t>(c)])];
+          }
+          bb[j] = b;
+        }
+      } else {
+        // sampling.hpp:35-51: one uniform_int per kept mode, row by row
+        std::vector<std::uniform_int_distribution<long>> dist;
+        for (int k : km) dist.emplace_back(0L, static_cast<long>(dims_[static_cast<size_t>(k)] - 1));
+        for (int j = 0; j < sn; ++j) {
+          i64 b = 0;
+          for (int c = 0; c < N - 1; ++c) {
+            const long idx = dist[static_cast<size_t>(c)](rng);
+            rb[static_cast<i64>(c) * sn + j] = static_cast<int>(idx);
+            b += static_cast<i64>(idx) * strides_[static_cast<size_t>(km[static_cast<size_t>(c)])];
+          }
+          bb[j] = b;
+        }
+      }
+    }
+  rows_ = dalloc<int>(rows.size());
+  base_ = dalloc<i64>(base.size());
+  CPB_CUDA(cudaMemcpyAsync(rows_, rows.data(), rows.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
+  CPB_CUDA(cudaMemcpyAsync(base_, base.data(), base.size() * sizeof(i64), cudaMemcpyHostToDevice, stream_));
+  CPB_CUDA(cudaStreamSynchronize(stream_));  // host vectors die here
+}
+
+void Session::build_fit_estimator(const double* xsrc) {
+  // sampling.hpp:155-179 (exhaustive: sampling.hpp:182-186)
+  if (o_.exact_fit_trace && p_ > (i64{1} << 26))
+    throw Unsupported("exact_fit_trace on a tensor this large");
+  std::vector<i64> offs;
+  if (o_.exhaustive_samples || o_.exact_fit_trace) {
+    offs.resize(static_cast<size_t>(p_));
+    std::iota(offs.begin(), offs.end(), i64{0});
+  } else {
+    auto rng = seeded_engine(o_.rng_seed, kFitStream);
+    offs = sample_offsets_without_replacement(p_, o_.fit_sample_count, rng);
+  }
+  phat_ = static_cast<i64>(offs.size());
+  i64* d_off = dalloc<i64>(offs.size());
+  CPB_CUDA(cudaMemcpyAsync(d_off, offs.data(), offs.size() * sizeof(i64), cudaMemcpyHostToDevice, stream_));
+  fit_vals_ = dalloc<double>(offs.size());
+  launch_gather_values(xsrc, d_off, phat_, fit_vals_, stream_);
+  std::vector<int> idx(offs.size());
+  for (int n = 0; n < order_; ++n) {
+    const i64 d = dims_[static_cast<size_t>(n)], st = strides_[static_cast<size_t>(n)];
+    for (size_t j = 0; j < offs.size(); ++j) idx[j] = static_cast<int>((offs[j] / st) % d);
+    fit_idx_.push_back(dalloc<int>(idx.size()));
+    CPB_CUDA(cudaMemcpyAsync(fit_idx_.back(), idx.data(), idx.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+  }
+  CPB_CUDA(cudaStreamSynchronize(stream_));
+  cudaFree(d_off);
+  has_fit_ = true;
+}
+
+void Session::mix_setup() {
+  const auto tm = Clock::now();
+  signs_host_ = mixing_signs(dims_, transform_, o_.rng_seed);
+  for (int n = 0; n < order_; ++n) {
+    signs_.push_back(dalloc<double>(static_cast<size_t>(dims_[static_cast<size_t>(n)])));
+    CPB_CUDA(cudaMemcpyAsync(signs_.back(), signs_host_[static_cast<size_t>(n)].data(),
+                             sizeof(double) * dims_[static_cast<size_t>(n)], cudaMemcpyHostToDevice, stream_));
+    plans_.push_back(make_dct_plan(static_cast<int>(dims_[static_cast<size_t>(n)])));
+  }
+  if (o_.x_mutable) {
+    xsolve_ = x_->d;
+  } else {
+    xcopy_ = dalloc<double>(static_cast<size_t>(p_));
+    CPB_CUDA(cudaMemcpyAsync(xcopy_, x_->d, sizeof(double) * p_, cudaMemcpyDeviceToDevice, stream_));
+    xsolve_ = xcopy_;
+  }
+  // mix_tensor (mixing.hpp:130-156): per mode, sign then DCT-II, in place
+  for (int n = 0; n < order_; ++n)
+    launch_mode_transform(plans_[static_cast<size_t>(n)], xsolve_, xsolve_, strides_[static_cast<size_t>(n)],
+                          p_ / dims_[static_cast<size_t>(n)], signs_[static_cast<size_t>(n)], 1, nullptr, stream_);
+  if (mix_) {
+    for (int n = 0; n < order_; ++n) {
+      const i64 rows = dims_[static_cast<size_t>(n)];
+      mixed_.push_back(dalloc<double>(static_cast<size_t>(rows * r_)));
+      launch_mode_transform(plans_[static_cast<size_t>(n)], fac_[static_cast<size_t>(n)], mixed_.back(), r_, r_,
+                            signs_[static_cast<size_t>(n)], 1, nullptr, stream_);
+    }
+  }
+  CPB_CUDA(cudaStreamSynchronize(stream_));
+  mix_seconds_ = seconds_since(tm);
+}
+
+ModeView Session::view(int it, int n) const {
+  const int N = order_;
+  const int ti = o_.exhaustive_samples ? 0 : it - 1;
+  const int sn = s_mode_[static_cast<size_t>(n)];
+  ModeView v{};
+  v.x = xsolve_;
+  v.in = dims_[static_cast<size_t>(n)];
+  v.stride = strides_[static_cast<size_t>(n)];
+  v.s = sn;
+  v.r = r_;
+  v.kept = N - 1;
+  const int* rb = rows_ + row_off_[static_cast<size_t>(ti * N + n)];
+  int c = 0;
+  for (int m = 0; m < N; ++m) {
+    if (m == n) continue;
+    v.rows[c] = rb + static_cast<i64>(c) * sn;
+    v.fac[c] = mix_ ? mixed_[static_cast<size_t>(m)] : fac_[static_cast<size_t>(m)];
+    ++c;
+  }
+  v.base = base_ + base_off_[static_cast<size_t>(ti * N + n)];
+  return v;
+}
+
+ModeWork Session::work(int n) const {
+  ModeWork w{};
+  w.part_rhs = part_rhs_;
+  w.part_gram = part_gram_;
+  w.ginv = ginv_;
+  w.info = info_;
+  w.ticket = tickets_;
+  w.ssq = ssq_;
+  w.norms = norms_ + static_cast<i64>(n) * r_;
+  w.lambda = lambda_;
+  w.a = fac_[static_cast<size_t>(n)];
+  w.stop = has_fit_ ? &state_->stopped : nullptr;
+  w.ks = ks_[static_cast<size_t>(n)];
+  w.ks_len = ks_len_[static_cast<size_t>(n)];
+  // Gram-domain image of the reference's rank threshold max(S,R)*eps on
+  // |R_kk|/|R_11| (kr_linalg.hpp:88-92): pivots are squared singular values.
+  w.tol = static_cast<double>(std::max(s_mode_[static_cast<size_t>(n)], r_)) * 2.220446049250313e-16;
+  return w;
+}
+
+void Session::enqueue_iteration() {
+  const int it = it_ + 1;
+  if (!loop_started_) {
+    CPB_CUDA(cudaEventRecord(ev_loop0_, stream_));
+    launch_stamp_start(state_, stream_);
+    loop_started_ = true;
+  }
+  for (int n = 0; n < order_; ++n) {
+    const ModeView v = view(it, n);
+    const ModeWork w = work(n);
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (timing_) {
+      if (ev_pool_.size() < 2) {
+        cudaEvent_t e1, e2;
+        CPB_CUDA(cudaEventCreate(&e1));
+        CPB_CUDA(cudaEventCreate(&e2));
+        ev_pool_.push_back(e1);
+        ev_pool_.push_back(e2);
+      }
+      ea = ev_pool_.back();
+      ev_pool_.pop_back();
+      eb = ev_pool_.back();
+      ev_pool_.pop_back();
+      CPB_CUDA(cudaEventRecord(ea, stream_));
+    }
+    launch_mode_rhs(v, w, stream_);
+    if (timing_) {
+      CPB_CUDA(cudaEventRecord(eb, stream_));
+      pending_.push_back({n, ea, eb});
+    }
+    if (mix_) {
+      launch_reduce_rhs(part_rhs_, w.ks, v.in, r_, rhs_full_, stream_);
+      launch_mode_transform(plans_[static_cast<size_t>(n)], rhs_full_, rhs_full_, r_, r_,
+                            signs_[static_cast<size_t>(n)], 0, nullptr, stream_);
+      launch_mode_apply(v, w, rhs_full_, n == 0, stream_);
+    } else {
+      launch_mode_apply(v, w, nullptr, n == 0, stream_);
+    }
+    launch_normalize(w, v.in, r_, rng_state_, stream_);
+    if (mix_)
+      launch_mode_transform(plans_[static_cast<size_t>(n)], fac_[static_cast<size_t>(n)], mixed_[static_cast<size_t>(n)], r_,
+                            r_, signs_[static_cast<size_t>(n)], 1, nullptr, stream_);
+  }
+  if (has_fit_) {
+    FitArgs a{};
+    a.order = order_;
+    a.r = r_;
+    a.phat = phat_;
+    for (int n = 0; n < order_; ++n) {
+      a.idx[n] = fit_idx_[static_cast<size_t>(n)];
+      a.fac[n] = fac_[static_cast<size_t>(n)];
+    }
+    a.lambda = lambda_;
+    a.values = fit_vals_;
+    a.x_norm = x_norm_;
+    a.total = static_cast<double>(p_);
+    a.partials = fit_part_;
+    a.ticket = tickets_ + 4;
+    a.state = state_;
+    a.trace = trace_dev_;
+    a.stop_host_mapped = stop_dev_;
+    a.iteration = it;
+    a.max_iters = o_.max_iters;
+    a.has_threshold = o_.fit_threshold.has_value();
+    a.threshold = o_.fit_threshold.value_or(0.0);
+    a.stall_limit = o_.stall_limit;
+    launch_estimate_fit(a, stream_);
+  }
+  CPB_CUDA(cudaEventRecord(ev_loop1_, stream_));
+  it_ = it;
+}
+
+int Session::run(int n) {
+  if (finished_) return 0;
+  const int start = it_;
+  int todo = std::min(n, o_.max_iters - it_);
+  if (todo <= 0) return 0;
+  if (it_events_.empty()) {
+    it_events_.resize(kInFlight);
+    for (auto& e : it_events_) CPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  for (int k = 0; k < todo; ++k) {
+    if (has_fit_ && k >= kInFlight) {
+      // keep kInFlight iterations queued; stop enqueueing once the device
+      // stop rule has fired
+      CPB_CUDA(cudaEventSynchronize(it_events_[static_cast<size_t>(k % kInFlight)]));
+      if (*reinterpret_cast<volatile int*>(stop_host_)) break;
+    }
+    enqueue_iteration();
+    CPB_CUDA(cudaEventRecord(it_events_[static_cast<size_t>(k % kInFlight)], stream_));
+  }
+  sync();
+  int ran = it_ - start;
+  if (has_fit_) {
+    FitState fs;
+    CPB_CUDA(cudaMemcpy(&fs, state_, sizeof(fs), cudaMemcpyDeviceToHost));
+    ran = fs.iterations - start;
+    it_ = fs.iterations;
+    if (fs.stopped) {
+      finished_ = true;
+      final_reason_ = fs.reason;
+    }
+  }
+  if (it_ >= o_.max_iters) {
+    finished_ = true;
+    if (o_.bench_mode) final_reason_ = 5;
+  }
+  return ran;
+}
+
+void Session::enqueue(int n) {
+  if (has_fit_) throw InvalidArgument("enqueue is for bench-mode sessions");
+  const int todo = std::min(n, o_.max_iters - it_);
+  for (int k = 0; k < todo; ++k) enqueue_iteration();
+  if (it_ >= o_.max_iters) {
+    finished_ = true;
+    final_reason_ = 5;
+  }
+}
+
+double Session::timed_enqueue(int n) {
+  sync();
+  cudaEvent_t a, b;
+  CPB_CUDA(cudaEventCreate(&a));
+  CPB_CUDA(cudaEventCreate(&b));
+  CPB_CUDA(cudaEventRecord(a, stream_));
+  enqueue(n);
+  CPB_CUDA(cudaEventRecord(b, stream_));
+  CPB_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  CPB_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  sync();
+  return ms;
+}
+
+void Session::sync() {
+  CPB_CUDA(cudaStreamSynchronize(stream_));
+  collect_kernel_times();
+}
+
+void Session::collect_kernel_times() {
+  for (auto& p : pending_) {
+    float ms = 0.f;
+    CPB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    const size_t m = static_cast<size_t>(p.mode);
+    k_launches_[m] += 1;
+    k_ms_[m] += ms;
+    // B_min accounting: 8 B per element for mode 1's
+    // contiguous fibers, one 32 B sector per element for strided modes.
+    k_bytes_[m] += static_cast<double>(s_mode_[m]) * static_cast<double>(dims_[m]) * (m == 0 ? 8.0 : 32.0);
+    ev_pool_.push_back(p.a);
+    ev_pool_.push_back(p.b);
+  }
+  pending_.clear();
+}
+
+void Session::kernel_stats(int mode, i64* launches, double* ms, double* bytes) {
+  if (mode < 0 || mode >= order_) throw InvalidArgument("mode out of range");
+  sync();
+  *launches = k_launches_[static_cast<size_t>(mode)];
+  *ms = k_ms_[static_cast<size_t>(mode)];
+  *bytes = k_bytes_[static_cast<size_t>(mode)];
+}
+
+void Session::download_model(HostModel& m) {
+  m.lambda.resize(static_cast<size_t>(r_));
+  CPB_CUDA(cudaMemcpy(m.lambda.data(), lambda_, sizeof(double) * r_, cudaMemcpyDeviceToHost));
+  m.factors.clear();
+  for (int n = 0; n < order_; ++n) {
+    const i64 rows = dims_[static_cast<size_t>(n)];
+    std::vector<double> rm(static_cast<size_t>(rows * r_));
+    CPB_CUDA(cudaMemcpy(rm.data(), fac_[static_cast<size_t>(n)], rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<double> cm(rm.size());
+    from_row_major(rm, rows, r_, cm.data());
+    m.factors.push_back(std::move(cm));
+  }
+}
+
+void Session::result(double* out_lambda, double* const* out_factors, std::vector<Trace>& trace,
+                     int* iterations, int* reason, double* setup_s, double* total_s,
+                     double* loop_dev_s) {
+  trace.clear();
+  if (zero_tensor_) {
+    std::memcpy(out_lambda, zero_model_.lambda.data(), sizeof(double) * r_);
+    for (int n = 0; n < order_; ++n)
+      std::memcpy(out_factors[n], zero_model_.factors[static_cast<size_t>(n)].data(),
+                  sizeof(double) * zero_model_.factors[static_cast<size_t>(n)].size());
+    trace.push_back({0, 0.0, 1.0, false, 1.0});
+    *iterations = 0;
+    *reason = 4;
+    *setup_s = *total_s = *loop_dev_s = 0.0;
+    return;
+  }
+  sync();
+  const double total = seconds_since(t0_);
+  HostModel m;
+  download_model(m);
+  if (premix_) {
+    // unmix_factor (mixing.hpp:190-212): DCT-III then sign, column-wise
+    for (int n = 0; n < order_; ++n) {
+      const i64 rows = dims_[static_cast<size_t>(n)];
+      double* d = dalloc<double>(static_cast<size_t>(rows * r_));
+      CPB_CUDA(cudaMemcpy(d, m.factors[static_cast<size_t>(n)].data(), sizeof(double) * rows * r_, cudaMemcpyHostToDevice));
+      launch_mode_transform(plans_[static_cast<size_t>(n)], d, d, 1, r_, signs_[static_cast<size_t>(n)], 0, nullptr, stream_);
+      CPB_CUDA(cudaMemcpyAsync(m.factors[static_cast<size_t>(n)].data(), d, sizeof(double) * rows * r_,
+                               cudaMemcpyDeviceToHost, stream_));
+      CPB_CUDA(cudaStreamSynchronize(stream_));
+      cudaFree(d);
+    }
+  }
+  std::memcpy(out_lambda, m.lambda.data(), sizeof(double) * r_);
+  for (int n = 0; n < order_; ++n)
+    std::memcpy(out_factors[n], m.factors[static_cast<size_t>(n)].data(),
+                sizeof(double) * m.factors[static_cast<size_t>(n)].size());
+  int iters = it_;
+  if (has_fit_) {
+    FitState fs;
+    CPB_CUDA(cudaMemcpy(&fs, state_, sizeof(fs), cudaMemcpyDeviceToHost));
+    iters = fs.iterations;
+    std::vector<TraceRec> tr(static_cast<size_t>(iters));
+    if (iters > 0)
+      CPB_CUDA(cudaMemcpy(tr.data(), trace_dev_, sizeof(TraceRec) * iters, cudaMemcpyDeviceToHost));
+    for (const auto& t : tr)
+      trace.push_back({t.iteration, setup_seconds_ + 1e-9 * static_cast<double>(t.t_ns), t.fit,
+                       !o_.exact_fit_trace, t.best_fit});
+    *reason = fs.stopped ? fs.reason : 0;
+  } else {
+    *reason = 5;
+  }
+  *iterations = iters;
+  *setup_s = setup_seconds_;
+  *total_s = total;
+  float ms = 0.f;
+  if (loop_started_) CPB_CUDA(cudaEventElapsedTime(&ms, ev_loop0_, ev_loop1_));
+  *loop_dev_s = 1e-3 * ms;
+}
+
+}  // namespace cpb

@@ -1,0 +1,189 @@
+// Host runtime of the B200 CPRAND path: device tensors, solver sessions.
+#pragma once
+
+#include <chrono>
+#include <cstdint>
+#include <optional>
+#include <random>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace cpb {
+
+// rng.hpp:11-34 stream ids and seeding (identical libstdc++ engine).
+constexpr std::uint64_t kInitStream = 1, kSamplingStream = 2, kFitStream = 3, kMixingStream = 4,
+                        kSynthStream = 5;
+std::mt19937_64 seeded_engine(std::uint64_t seed, std::uint64_t stream);
+std::uint64_t seeded_engine_seed_value(std::uint64_t seed, std::uint64_t stream);
+
+struct Options {  // SolveOptions (solver.hpp:40-64) + device extensions
+  int max_iters = 200;
+  double fit_tolerance = 1e-4;
+  std::optional<double> fit_threshold;
+  std::uint64_t rng_seed = 0;
+  int init = 0;  // 0 random, 1 hosvd, 2 given
+  i64 fit_sample_count = i64{1} << 14;
+  int stall_limit = 10;
+  int transform = -1;
+  bool bench_mode = false;
+  bool exhaustive_samples = false;
+  bool exact_fit_trace = false;
+  int device = -1;
+  bool x_mutable = false;
+  void validate() const;
+};
+
+struct Trace {
+  int iteration;
+  double elapsed;
+  double fit;
+  bool is_estimate;
+  double best;
+};
+
+struct Tensor {
+  std::vector<i64> dims, strides;
+  i64 p = 0;
+  int device = 0;
+  double* d = nullptr;
+  bool owned = true;
+  explicit Tensor(const std::vector<i64>& dims, int device);
+  ~Tensor();
+};
+
+// Host-side model in the reference layout (column-major factors).
+struct HostModel {
+  std::vector<double> lambda;
+  std::vector<std::vector<double>> factors;  // dims[n] x R column-major
+};
+
+HostModel init_random(const std::vector<i64>& dims, int r, std::uint64_t seed);  // solver.hpp:104-123
+void normalize_columns_host(HostModel& m, const std::vector<i64>& dims, int mode, bool first,
+                            std::mt19937_64& rng);                                 // kruskal.hpp:51-67
+std::vector<i64> sample_offsets_without_replacement(i64 total, i64 want, std::mt19937_64& rng);
+std::vector<std::vector<double>> mixing_signs(const std::vector<i64>& dims, int kind,
+                                              std::uint64_t seed);                // mixing.hpp:25-49
+void baseline_factors_host(const std::vector<i64>& dims, int r, double c, std::uint64_t seed,
+                           std::vector<std::vector<double>>& out);
+
+class Session {
+ public:
+  Session(int method, Tensor* x, int r, int s, const Options& o, const double* init_lambda,
+          const double* const* init_factors);
+  ~Session();
+  int run(int n);  // returns iterations executed
+  void enqueue(int n);
+  double timed_enqueue(int n);  // ms between events around n enqueued iterations
+  void sync();
+  cudaStream_t stream() const { return stream_; }
+  void set_timing(bool on) { timing_ = on; }
+  void kernel_stats(int mode, i64* launches, double* ms, double* bytes);
+  void result(double* out_lambda, double* const* out_factors, std::vector<Trace>& trace,
+              int* iterations, int* reason, double* setup_s, double* total_s, double* loop_dev_s);
+
+ private:
+  void setup(const double* init_lambda, const double* const* init_factors);
+  void build_tables();
+  void build_fit_estimator(const double* xsrc);
+  void mix_setup();
+  void enqueue_iteration();
+  void finish_zero_tensor();
+  ModeView view(int it, int n) const;
+  ModeWork work(int n) const;
+  void download_model(HostModel& m);
+  void collect_kernel_times();
+
+  int method_;
+  Tensor* x_;
+  int order_, r_, s_;
+  Options o_;
+  int transform_ = -1;
+  bool mix_ = false, premix_ = false;
+  std::vector<i64> dims_, strides_;
+  i64 p_ = 0;
+  int sms_ = 148;
+  cudaStream_t stream_ = nullptr;
+  double* xsolve_ = nullptr;  // tensor the iterations gather from (mixed for MIX/PREMIX)
+  double* xcopy_ = nullptr;   // private mixed copy when x is not mutable
+  // model
+  std::vector<double*> fac_, mixed_;
+  double* lambda_ = nullptr;
+  double* norms_ = nullptr;  // [N][R]
+  // tables
+  std::vector<int> s_mode_;         // samples per mode (S, or P/I_n when exhaustive)
+  int table_iters_ = 0;
+  int* rows_ = nullptr;             // [iter][mode] blocks of (N-1) x S_n
+  i64* base_ = nullptr;             // [iter][mode] blocks of S_n
+  std::vector<i64> row_off_, base_off_;  // block offsets per (iter, mode)
+  // work
+  std::vector<int> ks_, ks_len_;
+  double* part_rhs_ = nullptr;
+  double* part_gram_ = nullptr;
+  double* ginv_ = nullptr;
+  int* info_ = nullptr;
+  unsigned* tickets_ = nullptr;
+  double* ssq_ = nullptr;
+  double* rhs_full_ = nullptr;
+  unsigned long long* rng_state_ = nullptr;
+  // fit
+  bool has_fit_ = false;
+  i64 phat_ = 0;
+  std::vector<int*> fit_idx_;
+  double* fit_vals_ = nullptr;
+  double* fit_part_ = nullptr;
+  FitState* state_ = nullptr;
+  TraceRec* trace_dev_ = nullptr;
+  int* stop_host_ = nullptr;  // pinned mapped
+  int* stop_dev_ = nullptr;
+  double x_norm_ = 0.0;
+  // mixing
+  std::vector<DctPlan> plans_;
+  std::vector<double*> signs_;
+  std::vector<std::vector<double>> signs_host_;
+  // progress
+  int it_ = 0;  // iterations enqueued
+  bool finished_ = false;
+  int final_reason_ = 0;
+  bool zero_tensor_ = false;
+  HostModel zero_model_;
+  double setup_seconds_ = 0.0, mix_seconds_ = 0.0;
+  std::chrono::steady_clock::time_point t0_;
+  cudaEvent_t ev_loop0_ = nullptr, ev_loop1_ = nullptr;
+  bool loop_started_ = false;
+  std::vector<cudaEvent_t> it_events_;
+  // kernel timing
+  bool timing_ = false;
+  struct Pending {
+    int mode;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending_;
+  std::vector<cudaEvent_t> ev_pool_;
+  std::vector<i64> k_launches_;
+  std::vector<double> k_ms_, k_bytes_;
+};
+
+// operator-level helpers (capi.cu)
+void op_gather(const double* x, const std::vector<i64>& dims, int mode, const i64* idxs, i64 s,
+               double* out);
+void op_skr(const i64* idxs, i64 s, const std::vector<i64>& dims, int mode, int r,
+            const double* const* factors, double* out);
+int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, const i64* idxs, i64 s,
+                   int r, const double* const* factors, double* lambda, int first, int transform,
+                   std::uint64_t mix_seed, double* out_factor);
+void op_fit_values(const double* x, i64 p, const i64* offsets, i64 n, double* out, double* norm);
+double op_estimate_fit(const double* lambda, const double* const* factors,
+                       const std::vector<i64>& dims, int r, const i64* idxs, const double* values,
+                       i64 phat, double x_norm, i64 total);
+void op_transform_tensor(const double* x, const std::vector<i64>& dims, int transform,
+                         std::uint64_t seed, double* out);
+void op_transform_factor(const double* a, i64 rows, int r, const std::vector<i64>& dims,
+                         int transform, std::uint64_t seed, int mode, int forward, double* out);
+void op_unmix_rows(const double* g, i64 s, i64 in, const std::vector<i64>& dims, int transform,
+                   std::uint64_t seed, int mode, double* out);
+void op_debug_normals(std::uint64_t seed, int n, double* out);
+void op_synth(Tensor* t, int r, double c, double eta, std::uint64_t seed,
+              double* const* out_factors);
+
+}  // namespace cpb

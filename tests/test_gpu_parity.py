@@ -1,0 +1,347 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): gathered fibers, Z_S and sampled entries
+bit-exact given identical sample tables; solved factors 1e-10 relative
+(fp64); end-to-end final fit within 1e-3 of the oracle over seeded runs.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import paper_1701_06600_b200 as pb
+    assert pb.device_count() > 0, "GPU tests need a visible CUDA device"
+    return pb
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+SHAPES = [(3, 4, 5), (17, 9, 13), (64, 33, 20), (9, 7, 6, 5), (100, 100, 100)]
+
+
+@pytest.mark.parametrize("dims", SHAPES)
+def test_gather_bit_exact(pb, orc, dims):
+    x = orc.random_tensor(dims, 37)
+    g = orc.Engine(38, raw=True)
+    for mode in range(len(dims)):
+        idxs = orc.draw_samples(g, dims, mode, 257)
+        assert np.array_equal(pb.gather_fibers(x, mode, idxs), orc.gather_fibers(x, mode, idxs))
+
+
+@pytest.mark.parametrize("dims,r", [((4, 5, 3, 2), 3), ((30, 20, 10), 10), ((50, 40, 30), 50),
+                                    ((8, 9, 10), 17)])
+def test_skr_bit_exact(pb, orc, dims, r):
+    g = orc.Engine(807, raw=True)
+    fs = [g.matrix(d, r) for d in dims]
+    for mode in range(len(dims)):
+        idxs = orc.draw_samples(g, dims, mode, 301)
+        assert np.array_equal(pb.skr(idxs, fs, mode), orc.skr(idxs, fs, mode))
+        if np.prod(dims) // dims[mode] <= 4000:
+            ex = orc.exhaustive_samples(dims, mode)
+            assert np.array_equal(pb.skr(ex, fs, mode), orc.skr(ex, fs, mode))
+
+
+def oracle_mode_update(orc, x, mode, idxs, fs, lam, first, seed=0):
+    zs = orc.skr(idxs, fs, mode)
+    xs = orc.gather_fibers(x, mode, idxs)
+    a = orc.sampled_update(zs, xs)
+    f2 = list(fs)
+    f2[mode] = a
+    return orc.normalize_columns(f2, lam, mode, first, orc.Engine(seed, 8))
+
+
+@pytest.mark.parametrize("dims,r,s", [((30, 25, 20), 5, 80), ((64, 50, 40), 10, 300),
+                                      ((40, 30, 20, 10), 20, 200), ((120, 90, 70), 50, 700),
+                                      ((300, 300, 30), 10, 300)])
+def test_mode_update_teacher_forced(pb, orc, dims, r, s):
+    """One GPU mode step from the oracle's factors vs oracle skr+gather+
+    sampled_update+normalize (sampling.hpp:283-290): 1e-10 relative."""
+    x = orc.random_tensor(dims, 901)
+    g = orc.Engine(902, raw=True)
+    fs = [g.matrix(d, r) for d in dims]
+    lam = g.uniform_real(0.5, 2.0, r)
+    for mode in range(len(dims)):
+        idxs = orc.draw_samples(g, dims, mode, s)
+        for first in (True, False):
+            got, glam, rank = pb.mode_update(x, mode, idxs, fs, lam, first)
+            want_fs, wlam = oracle_mode_update(orc, x, mode, idxs, fs, lam, first)
+            assert rank == r
+            assert rel(got, want_fs[mode]) < 1e-10
+            assert rel(glam, wlam) < 1e-10
+
+
+def test_mode_update_exhaustive_is_dense_solve(pb, orc):
+    """test_sampling.cpp:97-115 on the GPU: all rows -> the dense normal solve."""
+    dims = (4, 5, 3)
+    x = orc.random_tensor(dims, 811)
+    g = orc.Engine(813, raw=True)
+    fs = [g.matrix(d, 2) for d in dims]
+    for mode in range(3):
+        ex = orc.exhaustive_samples(dims, mode)
+        got, _, _ = pb.mode_update(x, mode, ex, fs, np.ones(2), True)
+        want, _ = oracle_mode_update(orc, x, mode, ex, fs, np.ones(2), True)
+        assert rel(got, want[mode]) < 1e-10
+
+
+def test_mode_update_rank_deficient_min_norm(pb, orc):
+    """A duplicated factor column makes Z_S rank deficient: min-norm path
+    (kr_linalg.hpp:113-117) -> same minimum-norm update as the oracle."""
+    dims = (12, 10, 8)
+    x = orc.random_tensor(dims, 5)
+    g = orc.Engine(6, raw=True)
+    fs = [g.matrix(d, 3) for d in dims]
+    for f in fs:
+        f[:, 2] = f[:, 1]
+    idxs = orc.draw_samples(g, dims, 0, 60)
+    got, glam, rank = pb.mode_update(x, 0, idxs, fs, np.ones(3), False)
+    assert rank == 2
+    zs = orc.skr(idxs, fs, 0)
+    xs = orc.gather_fibers(x, 0, idxs)
+    want = orc.sampled_update(zs, xs)
+    # compare before normalization: unnormalize with lambda
+    assert rel(got * glam[None, :], want) < 1e-8
+
+
+def test_fit_values_and_estimate(pb, orc):
+    dims = (20, 15, 12)
+    x = orc.random_tensor(dims, 823)
+    est = orc.make_fit_estimator(x, 500, orc.Engine(824, raw=True))
+    offs = [int(np.ravel_multi_index(tuple(i), dims, order="F")) for i in est.idxs]
+    vals, nrm = pb.fit_values(x, offs)
+    assert np.array_equal(vals, est.x_values)
+    assert nrm == pytest.approx(est.x_norm, rel=1e-13)
+    g = orc.Engine(828, raw=True)
+    lam = g.uniform_real(0.2, 1.0, 3)
+    fs = [g.matrix(d, 3) for d in dims]
+    got = pb.estimate_fit(lam, fs, est.idxs, est.x_values, est.x_norm, est.total_count)
+    assert got == pytest.approx(orc.estimate_fit(lam, fs, est), rel=1e-12, abs=1e-13)
+
+
+def test_device_normalize_rng_matches_libstdcxx(pb, orc):
+    """Zero-column refill draws (kruskal.hpp:53-63) come from a device
+    mt19937_64 + polar normal that must replay seeded_engine(seed, 8)."""
+    for seed in (0, 3, 17):
+        want = orc.Engine(seed, 8).normal(501)
+        got = pb.debug_normal_stream(seed, 501)
+        assert np.max(np.abs(got - want)) <= 4e-16 * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("dims", [(4, 3, 5), (80, 16, 12), (20, 7, 9, 11), (320, 6, 5), (1, 5, 3)])
+def test_mix_tensor_matches_oracle(pb, orc, dims):
+    x = orc.random_tensor(dims, 901)
+    got = pb.mix_tensor(x, "dct", 9)
+    want = orc.mix_tensor(x, "dct", 9)
+    assert rel(got, want) < 1e-12
+    assert np.array_equal(pb.mix_tensor(x, "identity", 9), x)
+
+
+def test_mix_unmix_factor_and_rows(pb, orc):
+    dims = (7, 80, 320)
+    g = orc.Engine(911, raw=True)
+    for mode in range(3):
+        a = g.matrix(dims[mode], 5)
+        m = pb.mix_factor(a, dims, "dct", 13, mode)
+        assert rel(m, orc.mix_factor(a, dims, "dct", 13, mode)) < 1e-12
+        assert rel(pb.unmix_factor(m, dims, "dct", 13, mode), a) < 1e-12
+        gg = np.asfortranarray(m.T)
+        assert rel(pb.unmix_sampled_rhs(gg, dims, "dct", 13, mode),
+                   orc.unmix_sampled_rhs(gg, dims, "dct", 13, mode)) < 1e-12
+
+
+def test_mode_update_mix_teacher_forced(pb, orc):
+    """The MIX mode step (mixing.hpp:286-296) on an oracle-mixed tensor."""
+    dims = (16, 12, 10, 8)
+    x = orc.random_tensor(dims, 3)
+    xh = orc.mix_tensor(x, "dct", 21)
+    g = orc.Engine(4, raw=True)
+    fs = [g.matrix(d, 4) for d in dims]
+    lam = np.ones(4)
+    for mode in range(4):
+        idxs = orc.draw_samples(g, dims, mode, 90)
+        got, glam, _ = pb.mode_update(xh, mode, idxs, fs, lam, mode == 0, "dct", 21)
+        mixed = [orc.mix_factor(f, dims, "dct", 21, m) for m, f in enumerate(fs)]
+        zs = orc.skr(idxs, mixed, mode)
+        gathered = orc.gather_fibers(xh, mode, idxs)
+        rhs = orc.unmix_sampled_rhs(np.asfortranarray(gathered.T), dims, "dct", 21, mode)
+        a, _ = orc.least_squares(zs, rhs)
+        f2 = list(fs)
+        f2[mode] = np.asfortranarray(a.T)
+        want, wlam = orc.normalize_columns(f2, lam, mode, mode == 0, orc.Engine(0, 8))
+        assert rel(got, want[mode]) < 1e-10
+        assert rel(glam, wlam) < 1e-10
+
+
+# ---------------------------------------------------------------- end to end
+def c1_problem(orc, seed=1):
+    """configs[0]: 100^3, rank-5 N(0,1) factors, 1% noise, seeded N(0,1) init."""
+    x, _ = orc.gen_baseline((100, 100, 100), 5, 0.0, 0.01, seed)
+    init = orc.Engine(seed, 1)
+    fs0 = [init.normal(100 * 5).reshape(100, 5, order="F") for _ in range(3)]
+    return x, (np.ones(5), fs0)
+
+
+def test_config1_end_to_end_matches_oracle(pb, orc):
+    x, init = c1_problem(orc)
+    opts = dict(rng_seed=1, max_iters=20, fit_sample_count=4096, init="given", init_model=init,
+                stall_limit=1000)
+    ref = orc.cprand(x, 5, 100, orc.SolveOptions(**opts))
+    got = pb.cprand(x, 5, 100, pb.SolveOptions(**opts))
+    assert got.iterations == ref.iterations == 20
+    assert got.reason == ref.reason
+    fits_g = np.array([t[2] for t in got.trace])
+    fits_r = np.array([t[2] for t in ref.trace])
+    assert np.max(np.abs(fits_g - fits_r)) < 1e-8
+    assert abs(fits_g[-1] - fits_r[-1]) < 1e-3
+    for a, b in zip(got.factors, ref.factors):
+        assert rel(a, b) < 1e-6
+    assert rel(got.lam, ref.lam) < 1e-6
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_free_running_stop_rule_matches_oracle(pb, orc, seed):
+    """Default stopping (best-fit stall, sampling.hpp:237-251) on a 40^3
+    collinear problem: same stop iteration and reason, fit within 1e-3."""
+    x, _ = orc.gen_baseline((40, 40, 40), 4, 0.5, 0.01, seed)
+    opts = dict(rng_seed=seed, max_iters=200)
+    ref = orc.cprand(x, 4, 60, orc.SolveOptions(**opts))
+    got = pb.cprand(x, 4, 60, pb.SolveOptions(**opts))
+    assert abs(got.trace[-1][2] - ref.trace[-1][2]) < 1e-3
+    assert got.iterations == ref.iterations
+    assert got.reason == ref.reason
+    assert abs(orc.exact_fit(x, got.lam, got.factors) - orc.exact_fit(x, ref.lam, ref.factors)) < 1e-3
+
+
+def test_readme_run_on_gpu(pb, orc):
+    """proj/README.md:58-65 through the B200 path."""
+    x, lam, fs = orc.gen_problem([50, 50, 50], 5, 0.5, 0.01, 3)
+    res = pb.cprand(x, 5, 80, pb.SolveOptions(rng_seed=3))
+    assert res.iterations == 53 and res.reason == "best_fit_stall"
+    assert f"{res.trace[-1][2]:.5f}" == "0.98870"
+    assert orc.score(res.factors, fs) > 0.9999
+
+
+def test_exhaustive_gpu_reproduces_cp_als(pb, orc):
+    """acceptance.cpp:175-203 on the GPU: exhaustive CPRAND == CP-ALS iterates."""
+    x, _, _ = orc.gen_problem([6, 7, 8], 3, 0.3, 0.1, 4)
+    opts = dict(rng_seed=4, fit_tolerance=1e-300, stall_limit=1 << 20, max_iters=20,
+                exhaustive_samples=True, exact_fit_trace=True)
+    als = orc.cp_als(x, 3, orc.SolveOptions(**opts))
+    rnd = pb.cprand(x, 3, 3, pb.SolveOptions(**opts))
+    for fa, fb in zip(als.factors, rnd.factors):
+        assert rel(fb, fa) <= 1e-8
+    assert abs(als.trace[-1][2] - rnd.trace[-1][2]) <= 1e-8
+    assert not rnd.trace[-1][3]  # exact fit in the trace
+
+
+def test_identity_mix_is_bit_identical_on_gpu(pb, orc):
+    """test_mixing.cpp:254-277: identity mixing == plain cprand, bitwise."""
+    x = orc.random_tensor((6, 5, 4), 929)
+    base = dict(rng_seed=31, max_iters=12, stall_limit=6)
+    plain = pb.cprand(x, 2, 20, pb.SolveOptions(**base))
+    mixed = pb.cprand_mix(x, 2, 20, pb.SolveOptions(transform="identity", **base))
+    pre = pb.cprand_premix(x, 2, 20, pb.SolveOptions(transform="identity", **base))
+    assert [t[2] for t in plain.trace] == [t[2] for t in mixed.trace] == [t[2] for t in pre.trace]
+    for a, b, c in zip(plain.factors, mixed.factors, pre.factors):
+        assert np.array_equal(a, b) and np.array_equal(a, c)
+    ref = orc.cprand(x, 2, 20, orc.SolveOptions(**base))
+    assert abs(plain.trace[-1][2] - ref.trace[-1][2]) < 1e-8
+
+
+@pytest.mark.parametrize("method", ["mix", "premix"])
+def test_dct_mix_end_to_end_matches_oracle(pb, orc, method):
+    x, _ = orc.gen_baseline((16, 12, 10, 8), 3, 0.9, 0.01, 5)
+    opts = dict(rng_seed=5, max_iters=15, transform="dct", stall_limit=1000)
+    ref = orc.solve(method, x, 3, 60, orc.SolveOptions(**opts))
+    got = pb.solve(method, x, 3, 60, pb.SolveOptions(**opts))
+    assert got.iterations == ref.iterations
+    fg = np.array([t[2] for t in got.trace])
+    fr = np.array([t[2] for t in ref.trace])
+    assert np.max(np.abs(fg - fr)) < 1e-7
+    for a, b in zip(got.factors, ref.factors):
+        assert rel(a, b) < 1e-6
+
+
+def test_mixed_solver_recovers(pb, orc):
+    g = orc.Engine(931, raw=True)
+    fs = [g.matrix(d, 2, 0.1, 1.0) for d in (10, 9, 8)]
+    x = np.einsum("ir,jr,kr->ijk", *fs)
+    res = pb.cprand_mix(x, 2, 60, pb.SolveOptions(rng_seed=37, max_iters=100, stall_limit=30,
+                                                  transform="dct"))
+    assert orc.exact_fit(x, res.lam, res.factors) >= 0.99
+
+
+def test_zero_tensor_and_validation(pb, orc):
+    res = pb.cprand(np.zeros((4, 4, 4)), 2, 14)
+    ref = orc.cprand(np.zeros((4, 4, 4)), 2, 14)
+    assert res.reason == "zero_tensor" and np.linalg.norm(res.lam) == 0.0
+    for a, b in zip(res.factors, ref.factors):
+        assert np.array_equal(a, b)
+    x = orc.random_tensor((6, 5, 4), 833)
+    with pytest.raises(pb.InvalidArgument):
+        pb.cprand(x, 3, 2)
+    with pytest.raises(pb.InvalidArgument):
+        pb.cprand(x, 2, 4, pb.SolveOptions(max_iters=0))
+    with pytest.raises(pb.InvalidArgument):
+        pb.cprand_premix(x, 1, 4, pb.SolveOptions(transform="fft"))
+    with pytest.raises(pb.InvalidArgument):
+        pb.gather_fibers(x, 0, np.zeros((2, 5), dtype=np.int64))
+    with pytest.raises(pb.UnsupportedOnDevice):
+        pb.cprand(x, 65, 100)
+
+
+def test_deterministic_bitwise(pb, orc):
+    x, _ = orc.gen_baseline((30, 30, 30), 4, 0.5, 0.01, 9)
+    a = pb.cprand(x, 4, 50, pb.SolveOptions(rng_seed=23, max_iters=10))
+    b = pb.cprand(x, 4, 50, pb.SolveOptions(rng_seed=23, max_iters=10))
+    assert np.array_equal(a.lam, b.lam)
+    for fa, fb in zip(a.factors, b.factors):
+        assert np.array_equal(fa, fb)
+    assert [t[2] for t in a.trace] == [t[2] for t in b.trace]
+
+
+def test_device_synth_matches_oracle_generator(pb, orc):
+    dims = (30, 20, 10)
+    t = pb.DeviceTensor(dims)
+    fs = t.synth(4, 0.5, 0.01, 7, want_factors=True)
+    x = t.download()
+    xo, fo = orc.gen_baseline(dims, 4, 0.5, 0.01, 7)
+    for a, b in zip(fs, fo):
+        assert np.array_equal(a, b)
+    assert rel(x, xo) < 1e-13
+
+
+def test_session_bench_mode_and_kernel_stats(pb, orc):
+    dims = (60, 50, 40)
+    t = pb.DeviceTensor(dims)
+    t.synth(5, 0.5, 0.01, 11)
+    x = t.download()
+    s = pb.Session("rand", t, 5, 80, pb.SolveOptions(rng_seed=11, max_iters=30, bench_mode=True))
+    s.set_kernel_timing(True)
+    s.enqueue(10)
+    s.sync()
+    assert s.run(20) == 20
+    for m in range(3):
+        n, ms, b = s.kernel_stats(m)
+        assert n == 30 and ms > 0 and b > 0
+    res = s.result()
+    assert res.iterations == 30 and res.reason == "bench_complete" and res.trace == []
+    ref = orc.cprand(x, 5, 80, orc.SolveOptions(rng_seed=11, max_iters=30, bench_mode=True))
+    for a, b_ in zip(res.factors, ref.factors):
+        assert rel(a, b_) < 1e-6
+
+
+def test_cpp_dropin_program(pb):
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "build", "dropin_smoke")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", root, "dropin"], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout
+    kv = dict(p.split("=") for p in out.strip().split(","))
+    assert float(kv["fit"]) > 0.999 - 1e-3 and kv["invalid_caught"] == "1" and kv["dsc5"] == "80"
