@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""CPRAND iters/sec on B200 (BASELINE.json metric), one JSON line.
+
+Workload (default `c4` = configs[3]): 1000^3 fp64 tensor (8 GB) from rank-50
+factors with congruence 0.9 and 1% noise, generated in HBM; CPRAND R=50,
+S=2000; bench mode = exactly K outer iterations with no fit checks
+(`cprand bench-iter`, tools/cprand_main.cpp:179-206). A step = one outer
+iteration (3 mode updates). The tensor (8 GB) is ~64x the 126 MB L2 and each
+iteration gathers fresh uniform samples, so no L2 flush is needed between
+steps ("inputs larger than L2").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
+  python bench.py --impl reference ...   # the reference's CPU path (oracle port)
+
+Multi-GPU (N > 1, torchrun): one process per GPU; the slab-sharded NCCL
+path is not enabled yet, so each rank runs an independent replica and the
+line says scaling "weak" / parallelism "replicas".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: dims, R, S, P_hat, congruence, eta, method, transform
+    "c1": dict(dims=(100, 100, 100), r=5, s=100, phat=4096, c=0.0, eta=0.01, method="rand", transform=None),
+    "c2": dict(dims=(300, 300, 300), r=10, s=300, phat=1 << 14, c=0.5, eta=0.01, method="rand", transform=None),
+    "c3": dict(dims=(80, 80, 80, 80), r=10, s=300, phat=1 << 14, c=0.9, eta=0.01, method="mix", transform="dct"),
+    "c4": dict(dims=(1000, 1000, 1000), r=50, s=2000, phat=1 << 16, c=0.9, eta=0.01, method="rand", transform=None),
+    "c5": dict(dims=(320, 320, 320, 320), r=20, s=1200, phat=1 << 18, c=0.5, eta=0.001, method="mix", transform="dct"),
+}
+METRIC = "CPRAND iters/sec"
+SEED = 1
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append((time.perf_counter(), parts))
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter() + 0.05
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", float("inf"))
+        during = [r for (ts, r) in self.rows if t0 <= ts <= t1]
+        window = "timed region"
+        if not during:  # region shorter than the sampling period: nearest samples
+            during = [r for (ts, r) in sorted(self.rows, key=lambda q: abs(q[0] - t0))[:3]]
+            window = "nearest samples to a timed region shorter than the 20 ms sampling period"
+        if not during:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        rows = during
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows),
+                "window": window}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def dist_init(ws):
+    if ws <= 1:
+        return None
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo")
+    return dist
+
+
+def allreduce_max(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def launches_per_iter(cfg) -> int:
+    n = len(cfg["dims"])
+    # gather, skr_gram, gram_inverse, rhs_gemm, mode_apply, normalize
+    per_mode = 6 + (3 if cfg["method"] == "mix" and cfg["transform"] == "dct" else 0)
+    return n * per_mode
+
+
+def cpu_oracle_rate(x_host: np.ndarray, cfg, budget_s: float = 15.0, max_iters: int = 40):
+    """Reference CPU path (oracle port) in bench mode on the same tensor:
+    (total - setup) / iters, as bench-iter reports. Bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+    os.environ.setdefault("CPRAND_THREADS", str(os.cpu_count() or 1))
+    kw = dict(rng_seed=SEED, bench_mode=True, transform=cfg["transform"])
+    probe = orc.solve(cfg["method"], x_host, cfg["r"], cfg["s"], orc.SolveOptions(max_iters=1, **kw))
+    per = max(probe.total_seconds - probe.setup_seconds, 1e-6)
+    n = int(max(1, min(max_iters, budget_s / per)))
+    res = orc.solve(cfg["method"], x_host, cfg["r"], cfg["s"], orc.SolveOptions(max_iters=n, **kw))
+    t = max(res.total_seconds - res.setup_seconds, 1e-9)
+    return n / t, n, t
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("CPRAND_THREADS", str(cores))
+    x, _ = orc.gen_baseline(cfg["dims"], cfg["r"], cfg["c"], cfg["eta"], SEED)
+    kw = dict(rng_seed=SEED, bench_mode=True, transform=cfg["transform"])
+    # warm-up steps (one outer iteration each), then K timed steps; the
+    # reference's own bench-iter timing excludes its setup
+    if args.warmup > 0:
+        orc.solve(cfg["method"], x, cfg["r"], cfg["s"], orc.SolveOptions(max_iters=args.warmup, **kw))
+    res = orc.solve(cfg["method"], x, cfg["r"], cfg["s"], orc.SolveOptions(max_iters=args.steps, **kw))
+    t = max(res.total_seconds - res.setup_seconds, 1e-9)
+    value = args.steps / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE.json generator, seed 1)",
+        "config": {"workload": args.config, "dims": list(cfg["dims"]), "R": cfg["r"], "S": cfg["s"],
+                   "method": cfg["method"], "transform": cfg["transform"], "bench_mode": True,
+                   "l2": "tensor >> L2 (host run)"},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} bench-mode outer iterations of {args.config} "
+                                   f"(oracle restatement of the C++ reference; gather on "
+                                   f"{cores} threads, LS single-threaded as the reference)"},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-iters", type=int, default=100, help="iterations per e2e solve call")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import paper_1701_06600_b200 as pb
+    ws, rank, local = dist_env()
+    dist = dist_init(ws)
+    dev = local
+    hbm_peak, peak_src = peaks()
+
+    # ---- inputs resident in HBM
+    t = pb.DeviceTensor(cfg["dims"], device=dev)
+    t.synth(cfg["r"], cfg["c"], cfg["eta"], SEED)
+    timing_iters = max(args.steps, 10)
+    total_iters = args.warmup + args.steps + timing_iters + 2
+    opts = pb.SolveOptions(rng_seed=SEED, max_iters=total_iters, bench_mode=True,
+                           transform=cfg["transform"], x_mutable=False, device=dev)
+    s = pb.Session(cfg["method"], t, cfg["r"], cfg["s"], opts)
+    clk = ClockSampler(dev).__enter__()
+    s.run(args.warmup)
+    time.sleep(0.3)  # sampler live before the timed region
+
+    # ---- timed region: K steps between CUDA events on the solver stream
+    barrier(dist)
+    s.sync()
+    clk.mark_start()
+    ms = s.timed_enqueue(args.steps)
+    clk.mark_end()
+    clk.__exit__(None, None, None)
+    ms = allreduce_max(dist, ms)
+    barrier(dist)
+    value = ws * args.steps / (ms * 1e-3)
+
+    # ---- roofline: the fused gather/SKR/Gram/RHS kernel, per-launch CUDA events
+    s.set_kernel_timing(True)
+    s.enqueue(timing_iters)
+    s.sync()
+    n_modes = len(cfg["dims"])
+    per_mode = [s.kernel_stats(m, 0) for m in range(n_modes)]
+    gemm = [s.kernel_stats(m, 1) for m in range(n_modes)]
+    launches = sum(p[0] for p in per_mode)
+    kms = sum(p[1] for p in per_mode)
+    kbytes = sum(p[2] for p in per_mode)
+    achieved = (kbytes / launches) / (kms / launches * 1e-3) / 1e9
+    share = (kms / timing_iters) / (ms / args.steps)
+    gemm_tflops = sum(g[2] for g in gemm) / (sum(g[1] for g in gemm) * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("traffic_bytes_per_launch")
+    s.close()
+
+    # ---- e2e through the public one-shot call with host buffers
+    e2e, cpu = None, None
+    if rank == 0 and (args.e2e_steps > 0 or not args.no_cpu):
+        p = int(np.prod(cfg["dims"]))
+        buf = pb.PinnedBuffer(p)
+        flat = t.download().reshape(-1, order="F")
+        buf.array[:] = flat
+        del flat
+        xh = buf.array.reshape(cfg["dims"], order="F")
+        eo = pb.SolveOptions(rng_seed=SEED, max_iters=args.e2e_iters, bench_mode=True,
+                             transform=cfg["transform"], device=dev)
+        if args.e2e_steps > 0:
+            pb.solve(cfg["method"], xh, cfg["r"], cfg["s"], eo)  # warm
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                res = pb.solve(cfg["method"], xh, cfg["r"], cfg["s"], eo)
+                _ = float(res.lam[0])  # result on the host
+            dt = (time.perf_counter() - t0) / args.e2e_steps
+            table_bytes = args.e2e_iters * n_modes * cfg["s"] * ((n_modes - 1) * 4 + 8)
+            e2e = {"value": args.e2e_iters / dt, "unit": "iters/s",
+                   "h2d_bytes_per_step": p * 8 + table_bytes,
+                   "d2h_bytes_per_step": 8 * cfg["r"] * (sum(cfg["dims"]) + 1),
+                   "iters_per_step": args.e2e_iters, "seconds_per_step": dt,
+                   "note": "cprand_solve(host pinned tensor): H2D + setup + bench-mode loop + D2H"}
+        if not args.no_cpu and ws == 1:
+            rate, n_it, secs = cpu_oracle_rate(xh, cfg)
+            cpu = {"value": rate, "unit": "iters/s", "cores": os.cpu_count() or 1, "kind": "port",
+                   "sample": f"{n_it} bench-mode outer iterations of {args.config} on the same "
+                             f"tensor ({secs:.1f} s); gather on all host threads, LS single-threaded"}
+        buf.close()
+    t.close()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE.json generator in HBM, seed 1)",
+            "config": {"workload": args.config, "dims": list(cfg["dims"]), "R": cfg["r"],
+                       "S": cfg["s"], "P_hat": cfg["phat"], "method": cfg["method"],
+                       "transform": cfg["transform"], "bench_mode": True,
+                       "parallelism": "replicas" if ws > 1 else "single",
+                       "l2": "inputs larger than L2 (8 GB tensor, fresh random samples per step)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "kernel": "gather_rows_kernel (sampled-fiber gather, all modes)",
+                         "bytes_model": "B_min: 8 B/elem mode 1, 32 B/elem strided modes",
+                         "per_mode_gbs": [p[2] / (p[1] * 1e-3) / 1e9 for p in per_mode],
+                         "share_of_step": share, "peak_source": peak_src,
+                         "rhs_gemm_fp64_tflops": gemm_tflops,
+                         "rhs_gemm_per_mode_us": [g[1] / g[0] * 1e3 for g in gemm]},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "gpu_launches": launches_per_iter(cfg) * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -157,13 +157,13 @@ int cprand_session_sync(cprand_session_t s);
  * CUDA events on the session stream and waits; *ms = event time. */
 int cprand_session_timed_enqueue(cprand_session_t s, int32_t n, double* ms);
 void* cprand_session_stream(cprand_session_t s); /* cudaStream_t */
-/* Per-launch CUDA-event timing of the fused gather/SKR/RHS kernel
- * (on the session stream). Enable before enqueueing. */
+/* Per-launch CUDA-event timing (on the launching stream) of the sampled-
+ * fiber gather (kind 0) and the RHS GEMM (kind 1). Enable before enqueueing. */
 int cprand_session_set_kernel_timing(cprand_session_t s, int32_t on);
-/* Totals per mode over the timed launches since enabling: count, ms, and
- * the algorithmic bytes those launches moved (B_min accounting). */
-int cprand_session_kernel_stats(cprand_session_t s, int32_t mode, int64_t* launches,
-                                double* total_ms, double* bytes);
+/* Totals per mode over the timed launches since enabling: count, ms, and the
+ * algorithmic work: bytes under B_min accounting (kind 0) or flops (kind 1). */
+int cprand_session_kernel_stats(cprand_session_t s, int32_t mode, int32_t kind, int64_t* launches,
+                                double* total_ms, double* work);
 int cprand_session_result(cprand_session_t s, double* out_lambda, double* const* out_factors,
                           cprand_trace_record_t* trace, int32_t trace_cap, cprand_result_t* res);
 void cprand_session_destroy(cprand_session_t s);

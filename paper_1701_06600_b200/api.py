@@ -238,9 +238,12 @@ class Session:
     def set_kernel_timing(self, on: bool) -> None:
         check(lib().cprand_session_set_kernel_timing(self.h, int(on)))
 
-    def kernel_stats(self, mode: int):
+    def kernel_stats(self, mode: int, kind: int = 0):
+        """(launches, total ms, work) of the gather (kind 0, B_min bytes) or
+        the RHS GEMM (kind 1, flops) over timed launches."""
         n, ms, b = C.c_int64(), C.c_double(), C.c_double()
-        check(lib().cprand_session_kernel_stats(self.h, mode, C.byref(n), C.byref(ms), C.byref(b)))
+        check(lib().cprand_session_kernel_stats(self.h, mode, kind, C.byref(n), C.byref(ms),
+                                                C.byref(b)))
         return n.value, ms.value, b.value
 
     def result(self) -> SolveResult:

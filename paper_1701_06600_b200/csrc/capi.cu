@@ -260,11 +260,11 @@ int cprand_session_set_kernel_timing(cprand_session_t s, int32_t on) {
   return guarded([&] { s->s->set_timing(on != 0); });
 }
 
-int cprand_session_kernel_stats(cprand_session_t s, int32_t mode, int64_t* launches,
-                                double* total_ms, double* bytes) {
+int cprand_session_kernel_stats(cprand_session_t s, int32_t mode, int32_t kind, int64_t* launches,
+                                double* total_ms, double* work) {
   return guarded([&] {
     i64 l = 0;
-    s->s->kernel_stats(mode, &l, total_ms, bytes);
+    s->s->kernel_stats(mode, kind, &l, total_ms, work);
     *launches = l;
   });
 }

@@ -61,23 +61,7 @@ __global__ void skr_kernel(ModeView v, double* __restrict__ out) {
   out[e] = skr_entry(v, s, r);  // column-major S x R
 }
 
-// ---------------------------------------------- fused SKR + Gram + RHS
-// CTA tile: BM rows of I_n x all R (padded to RT) x a K-range of samples.
-// Per K tile: X tile (BK samples x BM rows) gathered straight from the
-// tensor (coalesced along i for mode 0, one sector per element otherwise),
-// Z tile (BK x RT) formed from factor rows; register-tiled DFMA
-// accumulation. m-tile 0 CTAs also accumulate Z^T Z. The last of them
-// reduces the Gram partials and writes its pivoted pseudo-inverse.
-constexpr int BM = 64;
-constexpr int BK = 32;
 constexpr int kThreads = 256;
-
-template <int RT>
-struct RhsTile {
-  static constexpr int TN = RT / 16;     // cols per thread
-  static constexpr int TM = BM / 16;     // rows per thread (4)
-  static constexpr int GPER = RT * RT / kThreads > 0 ? RT * RT / kThreads : 1;
-};
 
 // Pivoted Cholesky of the R x R Gram in shared memory (warp 0), then its
 // (pseudo-)inverse. g: [RT][RT+1]; w: [RT][RT+1] scratch. On exit ginv
@@ -242,129 +226,269 @@ __device__ void gram_pinv(double* g, double* w, int* perm, int r, double tol, do
   if (tid == 0) info[0] = rank;
 }
 
-template <int RT>
-__global__ void __launch_bounds__(kThreads, 2) mode_rhs_kernel(ModeView v, ModeWork w) {
-  using T = RhsTile<RT>;
-  constexpr int TN = T::TN, TM = T::TM;
-  if (w.stop && *w.stop) return;
-  extern __shared__ __align__(16) double smem[];
-  double* xs = smem;                 // [BK][BM]
-  double* zs = smem + BK * BM;       // [BK][RT]
-  __shared__ bool s_last;
+// ---------------------------------------------- Z_S + Gram partials
+// One CTA per SB samples: Z rows (ones, then *= factor rows in ascending
+// mode, sampling.hpp:82-90) written to a dense [S][RT] buffer (zero padded
+// for r >= R) and Z_tile^T Z_tile accumulated into a per-CTA Gram partial.
+// Loads are issued mode by mode for all of a thread's entries at once so the
+// index -> factor-row dependency costs two load latencies per mode, not two
+// per entry.
+constexpr int SB = 64;
 
+template <int RT>
+__global__ void __launch_bounds__(kThreads) skr_gram_kernel(ModeView v, double* __restrict__ z,
+                                                            double* __restrict__ part_gram,
+                                                            const int* stop) {
+  if (stop && *stop) return;
+  constexpr int Q = SB * RT / kThreads;  // entries per thread
+  constexpr int GP = RT * RT / kThreads;
+  __shared__ double zt[SB][RT];
+  const int tid = threadIdx.x;
+  const int s0 = blockIdx.x * SB;
+  double zv[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) zv[q] = 1.0;
+  for (int c = 0; c < v.kept; ++c) {
+    int row[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int e = tid + q * kThreads, s = s0 + e / RT;
+      row[q] = (s < v.s) ? __ldg(v.rows[c] + s) : 0;
+    }
+    double f[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int e = tid + q * kThreads, rr = e % RT;
+      f[q] = (rr < v.r) ? __ldg(v.fac[c] + static_cast<i64>(row[q]) * v.r + rr) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) zv[q] = __dmul_rn(zv[q], f[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int e = tid + q * kThreads, sl = e / RT, rr = e % RT, s = s0 + sl;
+    const double val = (s < v.s && rr < v.r) ? zv[q] : 0.0;
+    zt[sl][rr] = val;
+    if (s < v.s) z[static_cast<i64>(s) * RT + rr] = val;
+  }
+  __syncthreads();
+  double g[GP];
+#pragma unroll
+  for (int q = 0; q < GP; ++q) g[q] = 0.0;
+  for (int sl = 0; sl < SB; ++sl) {
+#pragma unroll
+    for (int q = 0; q < GP; ++q) {
+      const int e = tid + q * kThreads;
+      g[q] = fma(zt[sl][e / RT], zt[sl][e % RT], g[q]);
+    }
+  }
+  double* pg = part_gram + static_cast<i64>(blockIdx.x) * RT * RT;
+#pragma unroll
+  for (int q = 0; q < GP; ++q) pg[tid + q * kThreads] = g[q];
+}
+
+// ---------------------------------------------- Gram pseudo-inverse
+// One CTA: G = sum of the Gram partials (fixed order); in-place
+// Gauss-Jordan inversion (SPD, no pivoting) with every pivot checked against
+// tol * max diag; a failed check (numerical rank < R) falls back to the
+// pivoted Cholesky pseudo-inverse (gram_pinv).
+template <int RT>
+__global__ void __launch_bounds__(kThreads) gram_inverse_kernel(const double* __restrict__ part_gram,
+                                                                int nparts, int r, double tol,
+                                                                double* __restrict__ ginv, int* info,
+                                                                const int* stop) {
+  if (stop && *stop) return;
+  constexpr int LD = RT + 1;
+  extern __shared__ __align__(16) double sm[];
+  double* a = sm;             // working copy [RT][LD]
+  double* g0 = sm + RT * LD;  // original G (for the fallback)
+  double* wk = g0 + RT * LD;  // fallback scratch [RT][LD] + 2 RT
+  __shared__ double col[RT], rowk[RT];
+  __shared__ int perm[RT];
+  __shared__ int s_fail;
+  __shared__ double s_dmax;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < r * r; e += blockDim.x) {
+    const int i = e / r, j = e % r;
+    double s = 0.0;
+    for (int k = 0; k < nparts; ++k) s += part_gram[static_cast<i64>(k) * RT * RT + i * RT + j];
+    a[i * LD + j] = s;
+    g0[i * LD + j] = s;
+  }
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  if (tid == 0) {
+    double d = 0.0;
+    for (int i = 0; i < r; ++i) d = fmax(d, a[i * LD + i]);
+    s_dmax = d;
+  }
+  __syncthreads();
+  const double thr = tol * s_dmax;
+  for (int k = 0; k < r; ++k) {
+    const double piv = a[k * LD + k];
+    if (!(piv > thr) || !(piv > 0.0)) {
+      if (tid == 0) s_fail = 1;
+      break;  // uniform: every thread reads the same pivot
+    }
+    const double p = 1.0 / piv;
+    for (int i = tid; i < r; i += blockDim.x) {
+      col[i] = a[i * LD + k];
+      rowk[i] = (i == k) ? p : a[k * LD + i] * p;
+    }
+    __syncthreads();
+    for (int e = tid; e < r * r; e += blockDim.x) {
+      const int i = e / r, j = e % r;
+      double v;
+      if (i == k) v = rowk[j];
+      else if (j == k) v = -col[i] * p;
+      else v = a[i * LD + j] - col[i] * rowk[j];
+      a[i * LD + j] = v;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (!s_fail) {
+    for (int e = tid; e < r * r; e += blockDim.x) ginv[e] = a[(e / r) * LD + (e % r)];
+    if (tid == 0) info[0] = r;
+    return;
+  }
+  // rank-deficient (or numerically so): pivoted Cholesky pseudo-inverse
+  for (int e = tid; e < RT * LD; e += blockDim.x) a[e] = (e % LD < r && e / LD < r) ? g0[e] : 0.0;
+  __syncthreads();
+  gram_pinv<RT>(a, wk, perm, r, tol, ginv, info);
+}
+
+// ---------------------------------------------- sampled-fiber gather
+// X_S rows (one per sample, the fiber contiguous, ld >= I_n) straight from
+// the tensor: coalesced along i for mode 1, one 32 B sector per element for
+// strided modes. Streaming loads (evict-first) keep the random tensor
+// traffic from displacing the X_S ring in L2. Pure copies: bit-exact.
+constexpr int kGatherThreads = 256;
+constexpr int kGatherUnroll = 4;
+
+__global__ void __launch_bounds__(kGatherThreads) gather_rows_kernel(
+    const double* __restrict__ x, i64 in, i64 stride, const i64* __restrict__ base, int s,
+    double* __restrict__ xs, i64 ld) {
+  const int row = blockIdx.y;
+  const i64 b = base[row];
+  const double* src = x + b;
+  double* dst = xs + static_cast<i64>(row) * ld;
+  for (i64 i0 = static_cast<i64>(blockIdx.x) * kGatherThreads * kGatherUnroll + threadIdx.x; i0 < in;
+       i0 += static_cast<i64>(gridDim.x) * kGatherThreads * kGatherUnroll) {
+    double v[kGatherUnroll];
+#pragma unroll
+    for (int u = 0; u < kGatherUnroll; ++u) {
+      const i64 i = i0 + u * kGatherThreads;
+      v[u] = (i < in) ? __ldcs(src + i * stride) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kGatherUnroll; ++u) {
+      const i64 i = i0 + u * kGatherThreads;
+      if (i < in) dst[i] = v[u];
+    }
+  }
+}
+
+// ---------------------------------------------- RHS GEMM (split-K)
+// part[kb](i, r) = sum_{s in split kb} X_S(s, i) Z(s, r): M = I_n, N = R
+// (padded RT), K = S. CTA tile 64 x RT x 16, two-stage cp.async pipeline,
+// 4 x RT/16 register tile per thread, FP64 FMA. Deterministic: fixed
+// per-thread accumulation order, splits reduced in order by mode_apply.
+constexpr int GBM = 64;
+constexpr int GBK = 16;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int src_bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int RT>
+__global__ void __launch_bounds__(kThreads) rhs_gemm_kernel(const double* __restrict__ xs, i64 ld,
+                                                            const double* __restrict__ z, i64 in,
+                                                            int s_total, int r, int ks_len,
+                                                            double* __restrict__ part,
+                                                            const int* stop) {
+  if (stop && *stop) return;
+  constexpr int TN = RT / 16, TM = GBM / 16;
+  __shared__ __align__(16) double as[2][GBK][GBM];
+  __shared__ __align__(16) double bs[2][GBK][RT];
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-  const int mt = blockIdx.x, kb = blockIdx.y;
-  const i64 i0 = static_cast<i64>(mt) * BM;
-  const int s_begin = kb * w.ks_len;
-  const int s_end = min(v.s, s_begin + w.ks_len);
-  const bool do_gram = (mt == 0);
-  const int r = v.r;
+  const i64 i0 = static_cast<i64>(blockIdx.x) * GBM;
+  const int kb = blockIdx.y;
+  const int s_begin = kb * ks_len;
+  const int s_end = min(s_total, s_begin + ks_len);
+  const int ntiles = (s_end - s_begin + GBK - 1) / GBK;
+
+  auto load_tile = [&](int t, int buf) {
+    const int sbase = s_begin + t * GBK;
+    // A: GBK rows x 64 doubles = 512 chunks of 16 B (2 per thread)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = tid + q * kThreads;
+      const int sl = c / 32, ic = (c % 32) * 2;
+      const int s = sbase + sl;
+      const i64 i = i0 + ic;
+      const bool ok = (s < s_end) && (i < ld);
+      const double* src = ok ? xs + static_cast<i64>(s) * ld + i : xs;
+      cp_async16(&as[buf][sl][ic], src, ok ? 16 : 0);
+    }
+    // B: GBK rows x RT doubles = GBK*RT/2 chunks
+    for (int c = tid; c < GBK * RT / 2; c += kThreads) {
+      const int sl = c / (RT / 2), rc = (c % (RT / 2)) * 2;
+      const int s = sbase + sl;
+      const bool ok = s < s_end;
+      const double* src = ok ? z + static_cast<i64>(s) * RT + rc : z;
+      cp_async16(&bs[buf][sl][rc], src, ok ? 16 : 0);
+    }
+    cp_async_commit();
+  };
 
   double acc[TM][TN];
 #pragma unroll
   for (int a = 0; a < TM; ++a)
 #pragma unroll
     for (int b = 0; b < TN; ++b) acc[a][b] = 0.0;
-  double gacc[T::GPER];
-#pragma unroll
-  for (int q = 0; q < T::GPER; ++q) gacc[q] = 0.0;
 
-  constexpr int XPER = BK * BM / kThreads;  // 8 elements per thread
-  double xr[XPER];
-  auto load_x = [&](int tile) {
-#pragma unroll
-    for (int q = 0; q < XPER; ++q) {
-      const int e = tid + q * kThreads;
-      const int sl = e / BM, il = e % BM;
-      const int s = tile + sl;
-      const i64 i = i0 + il;
-      xr[q] = (s < s_end && i < v.in) ? __ldg(v.x + v.base[s] + i * v.stride) : 0.0;
-    }
-  };
-
-  if (s_begin < s_end) load_x(s_begin);
-  for (int tile = s_begin; tile < s_end; tile += BK) {
-#pragma unroll
-    for (int q = 0; q < XPER; ++q) xs[tid + q * kThreads] = xr[q];
-    for (int e = tid; e < BK * RT; e += kThreads) {
-      const int sl = e / RT, rr = e % RT;
-      const int s = tile + sl;
-      zs[e] = (s < s_end && rr < r) ? skr_entry(v, s, rr) : 0.0;
+  if (ntiles > 0) load_tile(0, 0);
+  for (int t = 0; t < ntiles; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < ntiles) {
+      load_tile(t + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    if (tile + BK < s_end) load_x(tile + BK);  // prefetch next tile during the FMAs
-#pragma unroll 4
-    for (int kk = 0; kk < BK; ++kk) {
+#pragma unroll
+    for (int kk = 0; kk < GBK; ++kk) {
       double af[TM], bf[TN];
 #pragma unroll
-      for (int a = 0; a < TM; ++a) af[a] = xs[kk * BM + ty * TM + a];
+      for (int a = 0; a < TM; ++a) af[a] = as[buf][kk][ty * TM + a];
 #pragma unroll
-      for (int b = 0; b < TN; ++b) bf[b] = zs[kk * RT + tx * TN + b];
+      for (int b = 0; b < TN; ++b) bf[b] = bs[buf][kk][tx * TN + b];
 #pragma unroll
       for (int a = 0; a < TM; ++a)
 #pragma unroll
         for (int b = 0; b < TN; ++b) acc[a][b] = fma(af[a], bf[b], acc[a][b]);
     }
-    if (do_gram) {
-#pragma unroll 2
-      for (int kk = 0; kk < BK; ++kk) {
-#pragma unroll
-        for (int q = 0; q < T::GPER; ++q) {
-          const int e = tid + q * kThreads;
-          if (e < RT * RT) gacc[q] = fma(zs[kk * RT + e / RT], zs[kk * RT + e % RT], gacc[q]);
-        }
-      }
-    }
     __syncthreads();
   }
-
-  // partial RHS: [kb][i][r]
-  double* pr = w.part_rhs + static_cast<i64>(kb) * v.in * r;
+  double* pr = part + static_cast<i64>(kb) * in * r;
 #pragma unroll
   for (int a = 0; a < TM; ++a) {
     const i64 i = i0 + ty * TM + a;
-    if (i >= v.in) continue;
+    if (i >= in) continue;
 #pragma unroll
     for (int b = 0; b < TN; ++b) {
       const int rr = tx * TN + b;
       if (rr < r) pr[i * r + rr] = acc[a][b];
     }
   }
-  if (!do_gram) return;
-
-  double* pg = w.part_gram + static_cast<i64>(kb) * r * r;
-#pragma unroll
-  for (int q = 0; q < T::GPER; ++q) {
-    const int e = tid + q * kThreads;
-    if (e < RT * RT) {
-      const int a = e / RT, b = e % RT;
-      if (a < r && b < r) pg[a * r + b] = gacc[q];
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const unsigned t = atomicAdd(&w.ticket[0], 1u);
-    s_last = (t == static_cast<unsigned>(gridDim.y) - 1u);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  // Last m-tile-0 CTA: G = sum of partials in split order, then pinv(G).
-  constexpr int LD = RT + 1;
-  double* g = smem;             // [RT][LD]
-  double* wk = smem + RT * LD;  // [RT][LD]
-  __shared__ int perm[RT];
-  for (int e = tid; e < RT * LD; e += kThreads) g[e] = 0.0;
-  __syncthreads();
-  for (int e = tid; e < r * r; e += kThreads) {
-    double sacc = 0.0;
-    for (int k = 0; k < gridDim.y; ++k) sacc += w.part_gram[static_cast<i64>(k) * r * r + e];
-    g[(e / r) * LD + (e % r)] = sacc;
-  }
-  __syncthreads();
-  gram_pinv<RT>(g, wk, perm, r, w.tol, w.ginv, w.info);
-  if (tid == 0) w.ticket[0] = 0u;
 }
 
 // A_un(i, :) = (sum_ks part_rhs(ks, i, :)) * Ginv; column sum-of-squares
@@ -711,47 +835,84 @@ int rank_bucket(int r) {
 }
 
 void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms) {
-  const int mtiles = ceil_div(in, BM);
-  const int want = 3 * sms;  // ~3 CTAs per SM
+  (void)rt;
+  const int mtiles = ceil_div(in, GBM);
+  const int want = 2 * sms;  // ~2 CTAs per SM
   int k = ceil_div(want, mtiles);
-  const int tiles = ceil_div(s, BK);
+  const int tiles = ceil_div(s, GBK);
   if (k > tiles) k = tiles;
   if (k > 64) k = 64;
   if (k < 1) k = 1;
-  int len = ceil_div(ceil_div(s, k), BK) * BK;
-  k = ceil_div(s, len);
-  (void)rt;
-  *ks = k;
+  const int len = ceil_div(ceil_div(s, k), GBK) * GBK;
+  *ks = ceil_div(s, len);
   *ks_len = len;
 }
 
-template <int RT>
-static size_t rhs_smem() {
-  const size_t tile = static_cast<size_t>(BK * BM + BK * RT) * sizeof(double);
-  const size_t inv = static_cast<size_t>(2 * RT * (RT + 1) + 2 * RT) * sizeof(double);
-  return tile > inv ? tile : inv;
-}
+int skr_gram_parts(int s) { return ceil_div(s, SB); }
 
 template <int RT>
-static void launch_rhs_t(const ModeView& v, const ModeWork& w, cudaStream_t st) {
-  const size_t sm = rhs_smem<RT>();
-  static bool configured = false;
-  if (!configured) {
-    CPB_CUDA(cudaFuncSetAttribute(mode_rhs_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sm)));
-    configured = true;
-  }
-  dim3 grid(ceil_div(v.in, BM), w.ks);
-  mode_rhs_kernel<RT><<<grid, kThreads, sm, st>>>(v, w);
+static void skr_gram_t(const ModeView& v, double* z, double* pg, const int* stop, cudaStream_t st) {
+  skr_gram_kernel<RT><<<ceil_div(v.s, SB), kThreads, 0, st>>>(v, z, pg, stop);
   CPB_LAUNCH_CHECK();
 }
 
-void launch_mode_rhs(const ModeView& v, const ModeWork& w, cudaStream_t st) {
+void launch_skr_gram(const ModeView& v, double* z, double* part_gram, const int* stop,
+                     cudaStream_t st) {
   switch (rank_bucket(v.r)) {
-    case 16: launch_rhs_t<16>(v, w, st); break;
-    case 32: launch_rhs_t<32>(v, w, st); break;
-    default: launch_rhs_t<64>(v, w, st); break;
+    case 16: skr_gram_t<16>(v, z, part_gram, stop, st); break;
+    case 32: skr_gram_t<32>(v, z, part_gram, stop, st); break;
+    default: skr_gram_t<64>(v, z, part_gram, stop, st); break;
   }
+}
+
+template <int RT>
+static void gram_inverse_t(const double* pg, int nparts, int r, double tol, double* ginv, int* info,
+                           const int* stop, cudaStream_t st) {
+  const size_t sm = static_cast<size_t>(3 * RT * (RT + 1) + 2 * RT) * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    CPB_CUDA(cudaFuncSetAttribute(gram_inverse_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sm)));
+    configured = true;
+  }
+  gram_inverse_kernel<RT><<<1, kThreads, sm, st>>>(pg, nparts, r, tol, ginv, info, stop);
+  CPB_LAUNCH_CHECK();
+}
+
+void launch_gram_inverse(const double* part_gram, int nparts, int r, double tol, double* ginv,
+                         int* info, const int* stop, cudaStream_t st) {
+  switch (rank_bucket(r)) {
+    case 16: gram_inverse_t<16>(part_gram, nparts, r, tol, ginv, info, stop, st); break;
+    case 32: gram_inverse_t<32>(part_gram, nparts, r, tol, ginv, info, stop, st); break;
+    default: gram_inverse_t<64>(part_gram, nparts, r, tol, ginv, info, stop, st); break;
+  }
+}
+
+void launch_gather_rows(const double* x, i64 in, i64 stride, const i64* base, int s, double* xs,
+                        i64 ld, cudaStream_t st) {
+  if (s <= 0) return;
+  const int per = kGatherThreads * kGatherUnroll;
+  int gx = ceil_div(in, per);
+  if (gx > 64) gx = 64;
+  int rows = s;
+  for (int r0 = 0; r0 < s; r0 += 65535) {
+    const int ny = (s - r0) < 65535 ? (s - r0) : 65535;
+    gather_rows_kernel<<<dim3(gx, ny), kGatherThreads, 0, st>>>(x, in, stride, base + r0, ny,
+                                                                xs + static_cast<i64>(r0) * ld, ld);
+    CPB_LAUNCH_CHECK();
+  }
+  (void)rows;
+}
+
+void launch_rhs_gemm(const double* xs, i64 ld, const double* z, i64 in, int s, int r, int ks,
+                     int ks_len, double* part, const int* stop, cudaStream_t st) {
+  const dim3 grid(ceil_div(in, GBM), ks);
+  switch (rank_bucket(r)) {
+    case 16: rhs_gemm_kernel<16><<<grid, kThreads, 0, st>>>(xs, ld, z, in, s, r, ks_len, part, stop); break;
+    case 32: rhs_gemm_kernel<32><<<grid, kThreads, 0, st>>>(xs, ld, z, in, s, r, ks_len, part, stop); break;
+    default: rhs_gemm_kernel<64><<<grid, kThreads, 0, st>>>(xs, ld, z, in, s, r, ks_len, part, stop); break;
+  }
+  CPB_LAUNCH_CHECK();
 }
 
 void launch_mode_apply(const ModeView& v, const ModeWork& w, const double* rhs_override,

@@ -15,28 +15,44 @@ void launch_skr(const ModeView& v, double* out, cudaStream_t st);
 void launch_base_offsets(const int* rows, int kept, int s, const i64* kstride_host, i64* base,
                          cudaStream_t st);
 
-// ---- fused per-mode update --------------------------------------------------
+// ---- per-mode update --------------------------------------------------------
+// Chain per mode (stream s1 unless noted):
+//   gather_rows (side stream, ahead)  X_S rows from the tensor       tensor.hpp:188
+//   skr_gram                          Z_S [S][RT] + Gram partials    sampling.hpp:74
+//   gram_inverse (stream s2)          pinv(Z_S^T Z_S)                kr_linalg.hpp:105
+//   rhs_gemm                          split-K Z_S^T X_S^T partials
+//   mode_apply                        A = RHS * Ginv, column norms, lambda
+//   normalize                         A /= norms                     kruskal.hpp:51
 struct ModeWork {
+  double* z;           // [S][RT] sampled Khatri-Rao rows (zero padded)
+  double* part_gram;   // [gram_parts][RT][RT]
+  int gram_parts;
   double* part_rhs;    // [ks][I_n][R]
-  double* part_gram;   // [ks][R][R]
-  double* ginv;        // [R][R]   (pinv of the Gram, written by the last m-tile-0 CTA)
+  double* ginv;        // [R][R]
   int* info;           // [0] = numerical rank of the Gram
-  unsigned* ticket;    // [0] gram ticket, [1] norm ticket (self-resetting)
+  unsigned* ticket;    // [1] norm ticket (self-resetting)
   double* ssq;         // [grid][R] column sum-of-squares partials
   double* norms;       // [R]
   double* lambda;      // [R]
-  double* a;           // I_n x R row-major factor (output, normalized by launch_normalize)
+  double* a;           // I_n x R row-major factor (output)
   const int* stop;     // device stop flag (kernels return early when set), may be null
-  int ks;              // sample splits
+  int ks;              // sample splits of the RHS GEMM
   int ks_len;          // samples per split (multiple of the K tile)
-  double tol;          // Gram pivot threshold (relative to the largest pivot)
+  double tol;          // Gram pivot threshold (relative to the largest diagonal)
 };
 
 int rank_bucket(int r);  // 16 / 32 / 64
-// grid sizing used by the solver to allocate partials
 void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms);
+int skr_gram_parts(int s);
 
-void launch_mode_rhs(const ModeView& v, const ModeWork& w, cudaStream_t st);
+void launch_gather_rows(const double* x, i64 in, i64 stride, const i64* base, int s, double* xs,
+                        i64 ld, cudaStream_t st);
+void launch_skr_gram(const ModeView& v, double* z, double* part_gram, const int* stop,
+                     cudaStream_t st);
+void launch_gram_inverse(const double* part_gram, int nparts, int r, double tol, double* ginv,
+                         int* info, const int* stop, cudaStream_t st);
+void launch_rhs_gemm(const double* xs, i64 ld, const double* z, i64 in, int s, int r, int ks,
+                     int ks_len, double* part, const int* stop, cudaStream_t st);
 // rhs_override != null: use it (I_n x R row-major, already reduced) instead of
 // summing part_rhs (the MIX path unmixes the RHS first).
 void launch_mode_apply(const ModeView& v, const ModeWork& w, const double* rhs_override,

@@ -193,18 +193,24 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
     ++c;
   }
   int ks, len;
-  mode_splits(in, static_cast<int>(s), rank_bucket(r), &ks, &len, sms);
-  DBuf prhs(static_cast<size_t>(ks) * in * r * sizeof(double)), pgram(static_cast<size_t>(ks) * r * r * sizeof(double));
+  const int rt = rank_bucket(r);
+  mode_splits(in, static_cast<int>(s), rt, &ks, &len, sms);
+  const int gp = skr_gram_parts(static_cast<int>(s));
+  const i64 ld = (in + 1) & ~i64{1};
+  DBuf prhs(static_cast<size_t>(ks) * in * r * sizeof(double)), pgram(static_cast<size_t>(gp) * rt * rt * sizeof(double));
   DBuf ginv(static_cast<size_t>(r * r) * sizeof(double)), info(4 * sizeof(int)), tickets(8 * sizeof(unsigned));
   DBuf ssq(static_cast<size_t>(ceil_div(in, 16)) * r * sizeof(double)), norms(r * sizeof(double));
   DBuf dlam(r * sizeof(double)), da(static_cast<size_t>(in * r) * sizeof(double)), rng(313 * sizeof(unsigned long long));
-  DBuf rhs(static_cast<size_t>(in * r) * sizeof(double));
+  DBuf rhs(static_cast<size_t>(in * r) * sizeof(double)), dz(static_cast<size_t>(s * rt) * sizeof(double));
+  DBuf xs(static_cast<size_t>(s * ld + 2) * sizeof(double));
   CPB_CUDA(cudaMemset(tickets.p, 0, 8 * sizeof(unsigned)));
   h2d(dlam.p, lambda, static_cast<size_t>(r));
   launch_rng_seed(rng.as<unsigned long long>(), 0ULL, stream);
   ModeWork w{};
-  w.part_rhs = prhs.as<double>();
+  w.z = dz.as<double>();
   w.part_gram = pgram.as<double>();
+  w.gram_parts = gp;
+  w.part_rhs = prhs.as<double>();
   w.ginv = ginv.as<double>();
   w.info = info.as<int>();
   w.ticket = tickets.as<unsigned>();
@@ -216,7 +222,10 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
   w.ks = ks;
   w.ks_len = len;
   w.tol = static_cast<double>(std::max<i64>(s, r)) * 2.220446049250313e-16;
-  launch_mode_rhs(v, w, stream);
+  launch_gather_rows(v.x, in, v.stride, v.base, static_cast<int>(s), xs.as<double>(), ld, stream);
+  launch_skr_gram(v, w.z, w.part_gram, nullptr, stream);
+  launch_gram_inverse(w.part_gram, gp, r, w.tol, w.ginv, w.info, nullptr, stream);
+  launch_rhs_gemm(xs.as<double>(), ld, w.z, in, static_cast<int>(s), r, ks, len, w.part_rhs, nullptr, stream);
   if (mix) {
     launch_reduce_rhs(prhs.as<double>(), ks, in, r, rhs.as<double>(), stream);
     launch_mode_transform(plans[static_cast<size_t>(mode)], rhs.as<double>(), rhs.as<double>(), r, r,

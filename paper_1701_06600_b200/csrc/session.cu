@@ -241,9 +241,7 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
   if (o_.init == 2 && init_factors == nullptr)
     throw InvalidArgument("init=given requires an init model");
   if (r < 1) throw InvalidArgument("rank must be >= 1");
-  if (method != 3 || true) {
-    if (s < r) throw InvalidArgument("sample count must be at least the rank");
-  }
+  if (s < r) throw InvalidArgument("sample count must be at least the rank");
   if (method == 2) transform_ = o_.transform >= 0 ? o_.transform : 0;
   if (method == 3) transform_ = o_.transform >= 0 ? o_.transform : 1;
   if (method >= 2) {
@@ -265,17 +263,36 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
   p_ = x->p;
   CPB_CUDA(cudaSetDevice(x->device));
   CPB_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, x->device));
+  rt_ = rank_bucket(r);
   CPB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  CPB_CUDA(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
+  CPB_CUDA(cudaStreamCreateWithFlags(&gstream_, cudaStreamNonBlocking));
   CPB_CUDA(cudaEventCreate(&ev_loop0_));
   CPB_CUDA(cudaEventCreate(&ev_loop1_));
-  k_launches_.assign(static_cast<size_t>(order_), 0);
-  k_ms_.assign(static_cast<size_t>(order_), 0.0);
-  k_bytes_.assign(static_cast<size_t>(order_), 0.0);
+  CPB_CUDA(cudaEventCreateWithFlags(&ev_z_, cudaEventDisableTiming));
+  CPB_CUDA(cudaEventCreateWithFlags(&ev_inv_, cudaEventDisableTiming));
+  // Strided-mode gathers touch one 32 B sector per useful 8 B element with no
+  // reuse: cap the L2 fetch granularity so DRAM moves only that sector.
+  cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
+  cudaGetLastError();
+  for (int k = 0; k < 2; ++k) {
+    k_launches_[k].assign(static_cast<size_t>(order_), 0);
+    k_ms_[k].assign(static_cast<size_t>(order_), 0.0);
+    k_work_[k].assign(static_cast<size_t>(order_), 0.0);
+  }
   setup(init_lambda, init_factors);
 }
 
 Session::~Session() {
   if (stream_) cudaStreamSynchronize(stream_);
+  if (stream2_) cudaStreamSynchronize(stream2_);
+  if (gstream_) cudaStreamSynchronize(gstream_);
+  for (auto& b : ring_) dfree(b);
+  for (auto& e : ev_gathered_) cudaEventDestroy(e);
+  for (auto& e : ev_consumed_) cudaEventDestroy(e);
+  if (ev_z_) cudaEventDestroy(ev_z_);
+  if (ev_inv_) cudaEventDestroy(ev_inv_);
+  dfree(z_);
   for (auto& f : fac_) dfree(f);
   for (auto& f : mixed_) dfree(f);
   for (auto& f : fit_idx_) dfree(f);
@@ -308,6 +325,8 @@ Session::~Session() {
   if (ev_loop0_) cudaEventDestroy(ev_loop0_);
   if (ev_loop1_) cudaEventDestroy(ev_loop1_);
   if (stream_) cudaStreamDestroy(stream_);
+  if (stream2_) cudaStreamDestroy(stream2_);
+  if (gstream_) cudaStreamDestroy(gstream_);
 }
 
 void Session::setup(const double* init_lambda, const double* const* init_factors) {
@@ -366,20 +385,24 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   }
 
   // ---- per-mode work buffers
-  i64 max_part = 1, max_in = 1, max_apply = 1;
-  int max_ks = 1;
+  i64 max_part = 1, max_in = 1, max_apply = 1, max_s = 1;
+  int max_gp = 1;
   for (int n = 0; n < order_; ++n) {
     int ks, len;
-    mode_splits(dims_[static_cast<size_t>(n)], s_mode_[static_cast<size_t>(n)], rank_bucket(r_), &ks, &len, sms_);
+    const int sn = s_mode_[static_cast<size_t>(n)];
+    mode_splits(dims_[static_cast<size_t>(n)], sn, rt_, &ks, &len, sms_);
     ks_.push_back(ks);
     ks_len_.push_back(len);
     max_part = std::max(max_part, static_cast<i64>(ks) * dims_[static_cast<size_t>(n)] * r_);
-    max_ks = std::max(max_ks, ks);
     max_in = std::max(max_in, dims_[static_cast<size_t>(n)]);
     max_apply = std::max<i64>(max_apply, ceil_div(dims_[static_cast<size_t>(n)], 16));
+    max_s = std::max<i64>(max_s, sn);
+    max_gp = std::max(max_gp, skr_gram_parts(sn));
   }
+  z_ = dalloc<double>(static_cast<size_t>(max_s * rt_));
   part_rhs_ = dalloc<double>(static_cast<size_t>(max_part));
-  part_gram_ = dalloc<double>(static_cast<size_t>(max_ks * r_ * r_));
+  part_gram_ = dalloc<double>(static_cast<size_t>(max_gp) * rt_ * rt_);
+  alloc_ring();
   ginv_ = dalloc<double>(static_cast<size_t>(r_ * r_));
   info_ = dalloc<int>(4);
   tickets_ = dalloc<unsigned>(8);
@@ -539,6 +562,11 @@ void Session::mix_setup() {
   mix_seconds_ = seconds_since(tm);
 }
 
+const i64* Session::base_ptr(int it, int n) const {
+  const int ti = o_.exhaustive_samples ? 0 : it - 1;
+  return base_ + base_off_[static_cast<size_t>(ti * order_ + n)];
+}
+
 ModeView Session::view(int it, int n) const {
   const int N = order_;
   const int ti = o_.exhaustive_samples ? 0 : it - 1;
@@ -558,14 +586,16 @@ ModeView Session::view(int it, int n) const {
     v.fac[c] = mix_ ? mixed_[static_cast<size_t>(m)] : fac_[static_cast<size_t>(m)];
     ++c;
   }
-  v.base = base_ + base_off_[static_cast<size_t>(ti * N + n)];
+  v.base = base_ptr(it, n);
   return v;
 }
 
 ModeWork Session::work(int n) const {
   ModeWork w{};
-  w.part_rhs = part_rhs_;
+  w.z = z_;
   w.part_gram = part_gram_;
+  w.gram_parts = skr_gram_parts(s_mode_[static_cast<size_t>(n)]);
+  w.part_rhs = part_rhs_;
   w.ginv = ginv_;
   w.info = info_;
   w.ticket = tickets_;
@@ -577,9 +607,66 @@ ModeWork Session::work(int n) const {
   w.ks = ks_[static_cast<size_t>(n)];
   w.ks_len = ks_len_[static_cast<size_t>(n)];
   // Gram-domain image of the reference's rank threshold max(S,R)*eps on
-  // |R_kk|/|R_11| (kr_linalg.hpp:88-92): pivots are squared singular values.
+  // |R_kk|/|R_11| (kr_linalg.hpp:88-92): Gram pivots are squared singular
+  // values, so the pivot test is d_k <= max(S,R)*eps * max_j G_jj.
   w.tol = static_cast<double>(std::max(s_mode_[static_cast<size_t>(n)], r_)) * 2.220446049250313e-16;
   return w;
+}
+
+void Session::alloc_ring() {
+  // X_S rows of each (iteration, mode), gathered ahead of the solve chain.
+  i64 per_iter = 0;
+  for (int n = 0; n < order_; ++n) {
+    const i64 ld = (dims_[static_cast<size_t>(n)] + 1) & ~i64{1};  // 16 B rows for cp.async
+    ld_.push_back(ld);
+    per_iter += static_cast<i64>(s_mode_[static_cast<size_t>(n)]) * ld;
+  }
+  const i64 budget = i64{3} << 30;  // bytes
+  depth_ = (2 * per_iter * 8 <= budget) ? 2 : 1;
+  for (int d = 0; d < depth_; ++d)
+    for (int n = 0; n < order_; ++n) {
+      // +2 doubles of slack: the GEMM's 16 B chunks may read one element past I_n
+      ring_.push_back(dalloc<double>(static_cast<size_t>(s_mode_[static_cast<size_t>(n)] * ld_[static_cast<size_t>(n)] + 2)));
+      cudaEvent_t e1, e2;
+      CPB_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+      CPB_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      ev_gathered_.push_back(e1);
+      ev_consumed_.push_back(e2);
+      slot_used_.push_back(0);
+    }
+}
+
+cudaEvent_t Session::timing_event() {
+  if (ev_pool_.empty()) {
+    cudaEvent_t e;
+    CPB_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = ev_pool_.back();
+  ev_pool_.pop_back();
+  return e;
+}
+
+void Session::enqueue_gather(int git) {
+  for (int n = 0; n < order_; ++n) {
+    const size_t slot = static_cast<size_t>(((git - 1) % depth_) * order_ + n);
+    if (slot_used_[slot]) CPB_CUDA(cudaStreamWaitEvent(gstream_, ev_consumed_[slot], 0));
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (timing_) {
+      ea = timing_event();
+      eb = timing_event();
+      CPB_CUDA(cudaEventRecord(ea, gstream_));
+    }
+    launch_gather_rows(xsolve_, dims_[static_cast<size_t>(n)], strides_[static_cast<size_t>(n)], base_ptr(git, n),
+                       s_mode_[static_cast<size_t>(n)], ring_[slot], ld_[static_cast<size_t>(n)], gstream_);
+    if (timing_) {
+      CPB_CUDA(cudaEventRecord(eb, gstream_));
+      pending_.push_back({n, 0, ea, eb});
+    }
+    CPB_CUDA(cudaEventRecord(ev_gathered_[slot], gstream_));
+    slot_used_[slot] = 1;
+  }
+  gathered_ = git;
 }
 
 void Session::enqueue_iteration() {
@@ -589,29 +676,36 @@ void Session::enqueue_iteration() {
     launch_stamp_start(state_, stream_);
     loop_started_ = true;
   }
+  // producer: gathers for this iteration and up to depth_-1 ahead (within the horizon)
+  const int want = std::min(it + depth_ - 1, std::max(horizon_, it));
+  while (gathered_ < want) enqueue_gather(gathered_ + 1);
+  const int* stop = has_fit_ ? &state_->stopped : nullptr;
   for (int n = 0; n < order_; ++n) {
     const ModeView v = view(it, n);
     const ModeWork w = work(n);
+    const size_t slot = static_cast<size_t>(((it - 1) % depth_) * order_ + n);
+    // Z_S + Gram partials; the pseudo-inverse runs on s2 beside the GEMM
+    launch_skr_gram(v, w.z, w.part_gram, stop, stream_);
+    CPB_CUDA(cudaEventRecord(ev_z_, stream_));
+    CPB_CUDA(cudaStreamWaitEvent(stream2_, ev_z_, 0));
+    launch_gram_inverse(w.part_gram, w.gram_parts, r_, w.tol, w.ginv, w.info, stop, stream2_);
+    CPB_CUDA(cudaEventRecord(ev_inv_, stream2_));
+    // RHS GEMM on the gathered X_S rows
+    CPB_CUDA(cudaStreamWaitEvent(stream_, ev_gathered_[slot], 0));
     cudaEvent_t ea = nullptr, eb = nullptr;
     if (timing_) {
-      if (ev_pool_.size() < 2) {
-        cudaEvent_t e1, e2;
-        CPB_CUDA(cudaEventCreate(&e1));
-        CPB_CUDA(cudaEventCreate(&e2));
-        ev_pool_.push_back(e1);
-        ev_pool_.push_back(e2);
-      }
-      ea = ev_pool_.back();
-      ev_pool_.pop_back();
-      eb = ev_pool_.back();
-      ev_pool_.pop_back();
+      ea = timing_event();
+      eb = timing_event();
       CPB_CUDA(cudaEventRecord(ea, stream_));
     }
-    launch_mode_rhs(v, w, stream_);
+    launch_rhs_gemm(ring_[slot], ld_[static_cast<size_t>(n)], w.z, v.in, v.s, r_, w.ks, w.ks_len, w.part_rhs, stop,
+                    stream_);
     if (timing_) {
       CPB_CUDA(cudaEventRecord(eb, stream_));
-      pending_.push_back({n, ea, eb});
+      pending_.push_back({n, 1, ea, eb});
     }
+    CPB_CUDA(cudaEventRecord(ev_consumed_[slot], stream_));
+    CPB_CUDA(cudaStreamWaitEvent(stream_, ev_inv_, 0));
     if (mix_) {
       launch_reduce_rhs(part_rhs_, w.ks, v.in, r_, rhs_full_, stream_);
       launch_mode_transform(plans_[static_cast<size_t>(n)], rhs_full_, rhs_full_, r_, r_,
@@ -657,8 +751,9 @@ void Session::enqueue_iteration() {
 int Session::run(int n) {
   if (finished_) return 0;
   const int start = it_;
-  int todo = std::min(n, o_.max_iters - it_);
+  const int todo = std::min(n, o_.max_iters - it_);
   if (todo <= 0) return 0;
+  horizon_ = it_ + todo;
   if (it_events_.empty()) {
     it_events_.resize(kInFlight);
     for (auto& e : it_events_) CPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -695,6 +790,7 @@ int Session::run(int n) {
 void Session::enqueue(int n) {
   if (has_fit_) throw InvalidArgument("enqueue is for bench-mode sessions");
   const int todo = std::min(n, o_.max_iters - it_);
+  horizon_ = it_ + todo;  // no gathers for iterations outside this call
   for (int k = 0; k < todo; ++k) enqueue_iteration();
   if (it_ >= o_.max_iters) {
     finished_ = true;
@@ -703,13 +799,15 @@ void Session::enqueue(int n) {
 }
 
 double Session::timed_enqueue(int n) {
-  sync();
+  sync();  // every stream idle: nothing of the timed iterations runs early
   cudaEvent_t a, b;
   CPB_CUDA(cudaEventCreate(&a));
   CPB_CUDA(cudaEventCreate(&b));
   CPB_CUDA(cudaEventRecord(a, stream_));
+  CPB_CUDA(cudaStreamWaitEvent(gstream_, a, 0));  // gathers start inside the region
+  CPB_CUDA(cudaStreamWaitEvent(stream2_, a, 0));
   enqueue(n);
-  CPB_CUDA(cudaEventRecord(b, stream_));
+  CPB_CUDA(cudaEventRecord(b, stream_));  // joins s2 and the gathers through the chain
   CPB_CUDA(cudaEventSynchronize(b));
   float ms = 0.f;
   CPB_CUDA(cudaEventElapsedTime(&ms, a, b));
@@ -720,6 +818,8 @@ double Session::timed_enqueue(int n) {
 }
 
 void Session::sync() {
+  CPB_CUDA(cudaStreamSynchronize(gstream_));
+  CPB_CUDA(cudaStreamSynchronize(stream2_));
   CPB_CUDA(cudaStreamSynchronize(stream_));
   collect_kernel_times();
 }
@@ -729,23 +829,30 @@ void Session::collect_kernel_times() {
     float ms = 0.f;
     CPB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
     const size_t m = static_cast<size_t>(p.mode);
-    k_launches_[m] += 1;
-    k_ms_[m] += ms;
-    // B_min accounting: 8 B per element for mode 1's
-    // contiguous fibers, one 32 B sector per element for strided modes.
-    k_bytes_[m] += static_cast<double>(s_mode_[m]) * static_cast<double>(dims_[m]) * (m == 0 ? 8.0 : 32.0);
+    const int k = p.kind;
+    k_launches_[k][m] += 1;
+    k_ms_[k][m] += ms;
+    const double elems = static_cast<double>(s_mode_[m]) * static_cast<double>(dims_[m]);
+    if (k == 0) {
+      // B_min accounting: 8 B per element for mode 1's
+      // contiguous fibers, one 32 B sector per element for strided modes.
+      k_work_[k][m] += elems * (m == 0 ? 8.0 : 32.0);
+    } else {
+      k_work_[k][m] += 2.0 * elems * static_cast<double>(r_);  // RHS flops
+    }
     ev_pool_.push_back(p.a);
     ev_pool_.push_back(p.b);
   }
   pending_.clear();
 }
 
-void Session::kernel_stats(int mode, i64* launches, double* ms, double* bytes) {
+void Session::kernel_stats(int mode, int kind, i64* launches, double* ms, double* work) {
   if (mode < 0 || mode >= order_) throw InvalidArgument("mode out of range");
+  if (kind < 0 || kind > 1) throw InvalidArgument("kernel kind must be 0 (gather) or 1 (gemm)");
   sync();
-  *launches = k_launches_[static_cast<size_t>(mode)];
-  *ms = k_ms_[static_cast<size_t>(mode)];
-  *bytes = k_bytes_[static_cast<size_t>(mode)];
+  *launches = k_launches_[kind][static_cast<size_t>(mode)];
+  *ms = k_ms_[kind][static_cast<size_t>(mode)];
+  *work = k_work_[kind][static_cast<size_t>(mode)];
 }
 
 void Session::download_model(HostModel& m) {

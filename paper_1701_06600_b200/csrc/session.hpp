@@ -78,7 +78,8 @@ class Session {
   void sync();
   cudaStream_t stream() const { return stream_; }
   void set_timing(bool on) { timing_ = on; }
-  void kernel_stats(int mode, i64* launches, double* ms, double* bytes);
+  // kind 0: sampled-fiber gather (bytes = B_min); kind 1: RHS GEMM (flops)
+  void kernel_stats(int mode, int kind, i64* launches, double* ms, double* work);
   void result(double* out_lambda, double* const* out_factors, std::vector<Trace>& trace,
               int* iterations, int* reason, double* setup_s, double* total_s, double* loop_dev_s);
 
@@ -87,23 +88,30 @@ class Session {
   void build_tables();
   void build_fit_estimator(const double* xsrc);
   void mix_setup();
+  void alloc_ring();
+  void enqueue_gather(int git);
   void enqueue_iteration();
   void finish_zero_tensor();
   ModeView view(int it, int n) const;
   ModeWork work(int n) const;
+  const i64* base_ptr(int it, int n) const;
   void download_model(HostModel& m);
   void collect_kernel_times();
+  cudaEvent_t timing_event();
 
   int method_;
   Tensor* x_;
   int order_, r_, s_;
+  int rt_ = 16;
   Options o_;
   int transform_ = -1;
   bool mix_ = false, premix_ = false;
   std::vector<i64> dims_, strides_;
   i64 p_ = 0;
   int sms_ = 148;
-  cudaStream_t stream_ = nullptr;
+  cudaStream_t stream_ = nullptr;   // s1: solve chain
+  cudaStream_t stream2_ = nullptr;  // s2: Gram pseudo-inverse
+  cudaStream_t gstream_ = nullptr;  // gather ring producer
   double* xsolve_ = nullptr;  // tensor the iterations gather from (mixed for MIX/PREMIX)
   double* xcopy_ = nullptr;   // private mixed copy when x is not mutable
   // model
@@ -116,8 +124,18 @@ class Session {
   int* rows_ = nullptr;             // [iter][mode] blocks of (N-1) x S_n
   i64* base_ = nullptr;             // [iter][mode] blocks of S_n
   std::vector<i64> row_off_, base_off_;  // block offsets per (iter, mode)
+  // gather ring: depth_ iterations x N modes of X_S rows
+  int depth_ = 2;
+  std::vector<i64> ld_;             // X_S row stride per mode
+  std::vector<double*> ring_;       // [slot] = [S_n][ld_n]
+  std::vector<cudaEvent_t> ev_gathered_, ev_consumed_;
+  std::vector<char> slot_used_;
+  int gathered_ = 0;                // last iteration whose gathers are enqueued
+  int horizon_ = 0;                 // do not gather beyond this iteration
+  cudaEvent_t ev_z_ = nullptr, ev_inv_ = nullptr;
   // work
   std::vector<int> ks_, ks_len_;
+  double* z_ = nullptr;
   double* part_rhs_ = nullptr;
   double* part_gram_ = nullptr;
   double* ginv_ = nullptr;
@@ -155,13 +173,13 @@ class Session {
   // kernel timing
   bool timing_ = false;
   struct Pending {
-    int mode;
+    int mode, kind;
     cudaEvent_t a, b;
   };
   std::vector<Pending> pending_;
   std::vector<cudaEvent_t> ev_pool_;
-  std::vector<i64> k_launches_;
-  std::vector<double> k_ms_, k_bytes_;
+  std::vector<i64> k_launches_[2];
+  std::vector<double> k_ms_[2], k_work_[2];
 };
 
 // operator-level helpers (capi.cu)
