@@ -55,6 +55,7 @@ struct ModeView {
   int kept;                  // N-1
   const int* rows[kMaxOrder];      // per kept mode c: S row indices (ascending mode order)
   const double* fac[kMaxOrder];    // per kept mode c: factor (row-major, ld R) used for Z
+  const double* nrm[kMaxOrder];    // per kept mode c: column norms the factor is divided by (or null)
   const i64* base;                 // S base offsets sum_{k!=n} i_k stride_k
 };
 

@@ -18,15 +18,14 @@ void launch_base_offsets(const int* rows, int kept, int s, const i64* kstride_ho
 // ---- per-mode update --------------------------------------------------------
 // Chain per mode (stream s1 unless noted):
 //   gather_rows (side stream, ahead)  X_S rows from the tensor       tensor.hpp:188
-//   skr_gram                          Z_S [S][RT] + Gram partials    sampling.hpp:74
-//   gram_inverse (stream s2)          pinv(Z_S^T Z_S)                kr_linalg.hpp:105
+//   z                                 Z_S [S][RT]                    sampling.hpp:74
+//   gram, gram_inverse (stream s2)    pinv(Z_S^T Z_S)                kr_linalg.hpp:105
 //   rhs_gemm                          split-K Z_S^T X_S^T partials
-//   mode_apply                        A = RHS * Ginv, column norms, lambda
-//   normalize                         A /= norms                     kruskal.hpp:51
+//   mode_apply                        A_un = RHS * Ginv, norms, lambda kruskal.hpp:51
 struct ModeWork {
   double* z;           // [S][RT] sampled Khatri-Rao rows (zero padded)
   double* part_gram;   // [gram_parts][RT][RT]
-  int gram_parts;
+  int gram_parts;      // split-K partials of the Gram
   double* part_rhs;    // [ks][I_n][R]
   double* ginv;        // [R][R]
   int* info;           // [0] = numerical rank of the Gram
@@ -34,7 +33,7 @@ struct ModeWork {
   double* ssq;         // [grid][R] column sum-of-squares partials
   double* norms;       // [R]
   double* lambda;      // [R]
-  double* a;           // I_n x R row-major factor (output)
+  double* a;           // I_n x R row-major factor, unnormalized (A_un; factor = A_un / norms)
   const int* stop;     // device stop flag (kernels return early when set), may be null
   int ks;              // sample splits of the RHS GEMM
   int ks_len;          // samples per split (multiple of the K tile)
@@ -43,23 +42,21 @@ struct ModeWork {
 
 int rank_bucket(int r);  // 16 / 32 / 64
 void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms);
-int skr_gram_parts(int s);
+void gram_splits(int s, int* parts, int* klen);
 
 void launch_gather_rows(const double* x, i64 in, i64 stride, const i64* base, int s, double* xs,
                         i64 ld, cudaStream_t st);
-void launch_skr_gram(const ModeView& v, double* z, double* part_gram, const int* stop,
-                     cudaStream_t st);
+void launch_z(const ModeView& v, double* z, const int* stop, cudaStream_t st);
+void launch_gram(const double* z, int s, int r, double* part, const int* stop, cudaStream_t st);
 void launch_gram_inverse(const double* part_gram, int nparts, int r, double tol, double* ginv,
                          int* info, const int* stop, cudaStream_t st);
 void launch_rhs_gemm(const double* xs, i64 ld, const double* z, i64 in, int s, int r, int ks,
                      int ks_len, double* part, const int* stop, cudaStream_t st);
 // rhs_override != null: use it (I_n x R row-major, already reduced) instead of
-// summing part_rhs (the MIX path unmixes the RHS first).
-void launch_mode_apply(const ModeView& v, const ModeWork& w, const double* rhs_override,
-                       int first_of_pass, cudaStream_t st);
-// A /= norms (column-wise), zero columns refilled from the device normalize RNG.
-void launch_normalize(const ModeWork& w, i64 in, int r, unsigned long long* norm_rng_state,
-                      cudaStream_t st);
+// summing part_rhs (the MIX path unmixes the RHS first). Writes A_un, norms,
+// lambda; zero columns refilled from the device normalize RNG.
+void launch_mode_apply(i64 in, int r, const ModeWork& w, const double* rhs_override,
+                       int first_of_pass, unsigned long long* rng_state, cudaStream_t st);
 
 // ---- fit estimator ----------------------------------------------------------
 void launch_gather_values(const double* x, const i64* offsets, i64 n, double* out,
@@ -87,7 +84,8 @@ struct FitArgs {
   int r;
   i64 phat;
   const int* idx[kMaxOrder];     // per mode: P_hat row indices
-  const double* fac[kMaxOrder];  // row-major factors (normalized)
+  const double* fac[kMaxOrder];  // row-major factors (A_un)
+  const double* nrm[kMaxOrder];  // column norms (factor = A_un / nrm), or null
   const double* lambda;
   const double* values;          // x at the sampled entries
   double x_norm;
@@ -126,8 +124,10 @@ void free_dct_plan(DctPlan& p);
 // Applies sign-then-DCT-II (forward) or DCT-III-then-sign (adjoint) along a
 // mode: fiber f = (hi, lo) with element i at hi*st*n + lo + i*st, f < nfib.
 // in and out may alias (in place).
+// col_div (nullable): fiber f's elements are divided by col_div[f] on load
+// (lazily normalized factor columns).
 void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 st, i64 nfib,
-                           const double* sign, int forward, const double* col_scale,
+                           const double* sign, int forward, const double* col_div,
                            cudaStream_t st_);
 // MIX path: RHS (I_n x R row-major) = D_n C^T (sum_ks part_rhs) per column
 void launch_reduce_rhs(const double* part_rhs, int ks, i64 in, int r, double* out,

@@ -146,7 +146,8 @@ __device__ __forceinline__ i64 fib_addr(i64 f, i64 i, i64 st, int n) {
 __global__ void __launch_bounds__(kMixThreads) mode_transform_kernel(PlanArgs p, const double* in,
                                                                     double* out, i64 st, i64 nfib,
                                                                     int F, const double* sign,
-                                                                    int forward) {
+                                                                    int forward,
+                                                                    const double* col_div) {
   extern __shared__ __align__(16) double2 sbuf[];
   const int n = p.n, np = F / 2;
   double2* b0 = sbuf;
@@ -166,7 +167,10 @@ __global__ void __launch_bounds__(kMixThreads) mode_transform_kernel(PlanArgs p,
     }
     const i64 f = f0 + fl;
     double v = 0.0;
-    if (f < nfib) v = in[fib_addr(f, i, st, n)];
+    if (f < nfib) {
+      v = in[fib_addr(f, i, st, n)];
+      if (col_div) v = v / col_div[f];  // lazily normalized factor column
+    }
     const int q = fl >> 1;
     if (forward) {
       v *= sign[i];  // D_n first (mixing.hpp:148)
@@ -292,9 +296,8 @@ void free_dct_plan(DctPlan& p) {
 }
 
 void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 st, i64 nfib,
-                           const double* sign, int forward, const double* col_scale,
+                           const double* sign, int forward, const double* col_div,
                            cudaStream_t stream) {
-  (void)col_scale;
   if (nfib <= 0) return;
   PlanArgs a;
   a.n = p.n;
@@ -321,7 +324,7 @@ void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 
   const i64 blocks = (nfib + F - 1) / F;
   if (blocks > 0x7fffffffLL) throw Unsupported("too many fibers for one launch");
   mode_transform_kernel<<<static_cast<unsigned>(blocks), kMixThreads, smem, stream>>>(
-      a, in, out, st, nfib, F, sign, forward);
+      a, in, out, st, nfib, F, sign, forward, col_div);
   CPB_LAUNCH_CHECK();
 }
 

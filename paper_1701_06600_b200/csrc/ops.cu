@@ -195,7 +195,8 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
   int ks, len;
   const int rt = rank_bucket(r);
   mode_splits(in, static_cast<int>(s), rt, &ks, &len, sms);
-  const int gp = skr_gram_parts(static_cast<int>(s));
+  int gp, glen;
+  gram_splits(static_cast<int>(s), &gp, &glen);
   const i64 ld = (in + 1) & ~i64{1};
   DBuf prhs(static_cast<size_t>(ks) * in * r * sizeof(double)), pgram(static_cast<size_t>(gp) * rt * rt * sizeof(double));
   DBuf ginv(static_cast<size_t>(r * r) * sizeof(double)), info(4 * sizeof(int)), tickets(8 * sizeof(unsigned));
@@ -223,23 +224,25 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
   w.ks_len = len;
   w.tol = static_cast<double>(std::max<i64>(s, r)) * 2.220446049250313e-16;
   launch_gather_rows(v.x, in, v.stride, v.base, static_cast<int>(s), xs.as<double>(), ld, stream);
-  launch_skr_gram(v, w.z, w.part_gram, nullptr, stream);
+  launch_z(v, w.z, nullptr, stream);
+  launch_gram(w.z, static_cast<int>(s), r, w.part_gram, nullptr, stream);
   launch_gram_inverse(w.part_gram, gp, r, w.tol, w.ginv, w.info, nullptr, stream);
   launch_rhs_gemm(xs.as<double>(), ld, w.z, in, static_cast<int>(s), r, ks, len, w.part_rhs, nullptr, stream);
+  const double* rhsp = nullptr;
   if (mix) {
     launch_reduce_rhs(prhs.as<double>(), ks, in, r, rhs.as<double>(), stream);
     launch_mode_transform(plans[static_cast<size_t>(mode)], rhs.as<double>(), rhs.as<double>(), r, r,
                           dsigns[static_cast<size_t>(mode)]->as<double>(), 0, nullptr, stream);
-    launch_mode_apply(v, w, rhs.as<double>(), first, stream);
-  } else {
-    launch_mode_apply(v, w, nullptr, first, stream);
+    rhsp = rhs.as<double>();
   }
-  launch_normalize(w, in, r, rng.as<unsigned long long>(), stream);
+  launch_mode_apply(in, r, w, rhsp, first, rng.as<unsigned long long>(), stream);
   CPB_CUDA(cudaDeviceSynchronize());
-  std::vector<double> rm(static_cast<size_t>(in * r));
+  std::vector<double> rm(static_cast<size_t>(in * r)), nv(static_cast<size_t>(r));
   d2h(rm.data(), da.p, rm.size());
+  d2h(nv.data(), norms.p, nv.size());
+  // normalized factor = A_un / norm (kruskal.hpp:65)
   for (int q = 0; q < r; ++q)
-    for (i64 i = 0; i < in; ++i) out_factor[i + q * in] = rm[static_cast<size_t>(i * r + q)];
+    for (i64 i = 0; i < in; ++i) out_factor[i + q * in] = rm[static_cast<size_t>(i * r + q)] / nv[static_cast<size_t>(q)];
   d2h(lambda, dlam.p, static_cast<size_t>(r));
   int k = 0;
   d2h(&k, info.p, 1);

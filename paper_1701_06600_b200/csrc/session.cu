@@ -364,6 +364,12 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   lambda_ = dalloc<double>(static_cast<size_t>(r_));
   CPB_CUDA(cudaMemcpyAsync(lambda_, m.lambda.data(), sizeof(double) * r_, cudaMemcpyHostToDevice, stream_));
   norms_ = dalloc<double>(static_cast<size_t>(order_ * r_));
+  {
+    // factors are kept as A_un with per-column norms; the init model is used as is
+    std::vector<double> ones(static_cast<size_t>(order_ * r_), 1.0);
+    CPB_CUDA(cudaMemcpyAsync(norms_, ones.data(), ones.size() * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+  }
   rng_state_ = dalloc<unsigned long long>(313);
   launch_rng_seed(rng_state_, seeded_engine_seed_value(o_.rng_seed, kInitStream + 7), stream_);
 
@@ -397,7 +403,9 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
     max_in = std::max(max_in, dims_[static_cast<size_t>(n)]);
     max_apply = std::max<i64>(max_apply, ceil_div(dims_[static_cast<size_t>(n)], 16));
     max_s = std::max<i64>(max_s, sn);
-    max_gp = std::max(max_gp, skr_gram_parts(sn));
+    int gp, glen;
+    gram_splits(sn, &gp, &glen);
+    max_gp = std::max(max_gp, gp);
   }
   z_ = dalloc<double>(static_cast<size_t>(max_s * rt_));
   part_rhs_ = dalloc<double>(static_cast<size_t>(max_part));
@@ -584,6 +592,7 @@ ModeView Session::view(int it, int n) const {
     if (m == n) continue;
     v.rows[c] = rb + static_cast<i64>(c) * sn;
     v.fac[c] = mix_ ? mixed_[static_cast<size_t>(m)] : fac_[static_cast<size_t>(m)];
+    v.nrm[c] = mix_ ? nullptr : norms_ + static_cast<i64>(m) * r_;
     ++c;
   }
   v.base = base_ptr(it, n);
@@ -594,7 +603,8 @@ ModeWork Session::work(int n) const {
   ModeWork w{};
   w.z = z_;
   w.part_gram = part_gram_;
-  w.gram_parts = skr_gram_parts(s_mode_[static_cast<size_t>(n)]);
+  int glen = 0;
+  gram_splits(s_mode_[static_cast<size_t>(n)], &w.gram_parts, &glen);
   w.part_rhs = part_rhs_;
   w.ginv = ginv_;
   w.info = info_;
@@ -684,10 +694,11 @@ void Session::enqueue_iteration() {
     const ModeView v = view(it, n);
     const ModeWork w = work(n);
     const size_t slot = static_cast<size_t>(((it - 1) % depth_) * order_ + n);
-    // Z_S + Gram partials; the pseudo-inverse runs on s2 beside the GEMM
-    launch_skr_gram(v, w.z, w.part_gram, stop, stream_);
+    // Z_S; the Gram and its pseudo-inverse run on s2 beside the RHS GEMM
+    launch_z(v, w.z, stop, stream_);
     CPB_CUDA(cudaEventRecord(ev_z_, stream_));
     CPB_CUDA(cudaStreamWaitEvent(stream2_, ev_z_, 0));
+    launch_gram(w.z, v.s, r_, w.part_gram, stop, stream2_);
     launch_gram_inverse(w.part_gram, w.gram_parts, r_, w.tol, w.ginv, w.info, stop, stream2_);
     CPB_CUDA(cudaEventRecord(ev_inv_, stream2_));
     // RHS GEMM on the gathered X_S rows
@@ -706,18 +717,17 @@ void Session::enqueue_iteration() {
     }
     CPB_CUDA(cudaEventRecord(ev_consumed_[slot], stream_));
     CPB_CUDA(cudaStreamWaitEvent(stream_, ev_inv_, 0));
+    const double* rhs = nullptr;
     if (mix_) {
       launch_reduce_rhs(part_rhs_, w.ks, v.in, r_, rhs_full_, stream_);
       launch_mode_transform(plans_[static_cast<size_t>(n)], rhs_full_, rhs_full_, r_, r_,
                             signs_[static_cast<size_t>(n)], 0, nullptr, stream_);
-      launch_mode_apply(v, w, rhs_full_, n == 0, stream_);
-    } else {
-      launch_mode_apply(v, w, nullptr, n == 0, stream_);
+      rhs = rhs_full_;
     }
-    launch_normalize(w, v.in, r_, rng_state_, stream_);
-    if (mix_)
+    launch_mode_apply(v.in, r_, w, rhs, n == 0, rng_state_, stream_);
+    if (mix_)  // mixed image of the new (normalized) factor (mixing.hpp:297-298)
       launch_mode_transform(plans_[static_cast<size_t>(n)], fac_[static_cast<size_t>(n)], mixed_[static_cast<size_t>(n)], r_,
-                            r_, signs_[static_cast<size_t>(n)], 1, nullptr, stream_);
+                            r_, signs_[static_cast<size_t>(n)], 1, w.norms, stream_);
   }
   if (has_fit_) {
     FitArgs a{};
@@ -727,6 +737,7 @@ void Session::enqueue_iteration() {
     for (int n = 0; n < order_; ++n) {
       a.idx[n] = fit_idx_[static_cast<size_t>(n)];
       a.fac[n] = fac_[static_cast<size_t>(n)];
+      a.nrm[n] = norms_ + static_cast<i64>(n) * r_;
     }
     a.lambda = lambda_;
     a.values = fit_vals_;
@@ -859,10 +870,15 @@ void Session::download_model(HostModel& m) {
   m.lambda.resize(static_cast<size_t>(r_));
   CPB_CUDA(cudaMemcpy(m.lambda.data(), lambda_, sizeof(double) * r_, cudaMemcpyDeviceToHost));
   m.factors.clear();
+  std::vector<double> nrm(static_cast<size_t>(order_ * r_));
+  CPB_CUDA(cudaMemcpy(nrm.data(), norms_, nrm.size() * sizeof(double), cudaMemcpyDeviceToHost));
   for (int n = 0; n < order_; ++n) {
     const i64 rows = dims_[static_cast<size_t>(n)];
     std::vector<double> rm(static_cast<size_t>(rows * r_));
     CPB_CUDA(cudaMemcpy(rm.data(), fac_[static_cast<size_t>(n)], rm.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    // factor = A_un / norm, the same IEEE division as the reference's col /= norm
+    for (i64 i = 0; i < rows; ++i)
+      for (int c = 0; c < r_; ++c) rm[static_cast<size_t>(i * r_ + c)] /= nrm[static_cast<size_t>(n * r_ + c)];
     std::vector<double> cm(rm.size());
     from_row_major(rm, rows, r_, cm.data());
     m.factors.push_back(std::move(cm));
