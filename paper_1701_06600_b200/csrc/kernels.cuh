@@ -43,6 +43,7 @@ struct ModeWork {
 int rank_bucket(int r);  // 16 / 32 / 64
 void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms);
 void gram_splits(int s, int* parts, int* klen);
+int apply_grid(i64 in, int r);  // CTAs of mode_apply (sizes the ssq partials)
 
 void launch_gather_rows(const double* x, i64 in, i64 stride, const i64* base, int s, double* xs,
                         i64 ld, cudaStream_t st);

@@ -200,7 +200,7 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
   const i64 ld = (in + 1) & ~i64{1};
   DBuf prhs(static_cast<size_t>(ks) * in * r * sizeof(double)), pgram(static_cast<size_t>(gp) * rt * rt * sizeof(double));
   DBuf ginv(static_cast<size_t>(r * r) * sizeof(double)), info(4 * sizeof(int)), tickets(8 * sizeof(unsigned));
-  DBuf ssq(static_cast<size_t>(ceil_div(in, 16)) * r * sizeof(double)), norms(r * sizeof(double));
+  DBuf ssq(static_cast<size_t>(apply_grid(in, r)) * r * sizeof(double)), norms(r * sizeof(double));
   DBuf dlam(r * sizeof(double)), da(static_cast<size_t>(in * r) * sizeof(double)), rng(313 * sizeof(unsigned long long));
   DBuf rhs(static_cast<size_t>(in * r) * sizeof(double)), dz(static_cast<size_t>(s * rt) * sizeof(double));
   DBuf xs(static_cast<size_t>(s * ld + 2) * sizeof(double));

@@ -401,7 +401,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
     ks_len_.push_back(len);
     max_part = std::max(max_part, static_cast<i64>(ks) * dims_[static_cast<size_t>(n)] * r_);
     max_in = std::max(max_in, dims_[static_cast<size_t>(n)]);
-    max_apply = std::max<i64>(max_apply, ceil_div(dims_[static_cast<size_t>(n)], 16));
+    max_apply = std::max<i64>(max_apply, apply_grid(dims_[static_cast<size_t>(n)], r_));
     max_s = std::max<i64>(max_s, sn);
     int gp, glen;
     gram_splits(sn, &gp, &glen);

@@ -51,33 +51,64 @@ __global__ void __launch_bounds__(kThreads) z_kernel(ModeView v, double* __restr
 }
 
 // ------------------------------------------------------------------ Gram
-// G(a, b) = sum_s Z(s, a) Z(s, b): 16 x 16 output tile per CTA (one
-// output per thread), K split over blockIdx.y, K staged 32 rows at a time.
-constexpr int GT = 16, GKC = 32;
+// G = sum over chunks of Z_chunk^T Z_chunk: one CTA per chunk of GS samples
+// computes the whole RT x RT partial (a 4 x RT/16 register tile per thread
+// for RT = 64), loading its chunk in one shot.
+constexpr int GS = 64;
 
 template <int RT>
 __global__ void __launch_bounds__(kThreads) gram_kernel(const double* __restrict__ z, int s_total,
                                                         int klen, double* __restrict__ part,
                                                         const int* stop) {
   if (stop && *stop) return;
-  __shared__ double za[GKC][GT], zb[GKC][GT];
-  constexpr int TPR = RT / GT;
-  const int ta = blockIdx.x / TPR, tb = blockIdx.x % TPR;
-  const int tid = threadIdx.x, la = tid / GT, lb = tid % GT;
-  const int k0 = blockIdx.y * klen, k1 = min(s_total, k0 + klen);
-  double acc = 0.0;
-  for (int kc = k0; kc < k1; kc += GKC) {
-    for (int e = tid; e < GKC * GT; e += kThreads) {
-      const int sl = e / GT, c = e % GT, s = kc + sl;
-      za[sl][c] = (s < k1) ? z[static_cast<i64>(s) * RT + ta * GT + c] : 0.0;
-      zb[sl][c] = (s < k1) ? z[static_cast<i64>(s) * RT + tb * GT + c] : 0.0;
+  constexpr int GPT = RT * RT / kThreads;  // outputs per thread (16 / 4 / 1)
+  constexpr int TA = RT >= 32 ? 4 : 1;     // rows of the thread tile
+  constexpr int TB = GPT / TA;             // cols of the thread tile
+  constexpr int NA = RT / TA;              // thread rows
+  __shared__ double zs[GS][RT];
+  const int tid = threadIdx.x;
+  const int s0 = blockIdx.x * klen;
+  const int s1 = min(s_total, s0 + klen);
+  const int ra = (tid / (RT / TB)) * TA, cb = tid % (RT / TB);
+  double acc[TA][TB];
+#pragma unroll
+  for (int x = 0; x < TA; ++x)
+#pragma unroll
+    for (int y = 0; y < TB; ++y) acc[x][y] = 0.0;
+  for (int sc = s0; sc < s1; sc += GS) {
+    constexpr int PER = GS * RT / kThreads;
+    double v[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * kThreads, sl = e / RT, c = e % RT, s = sc + sl;
+      v[q] = (s < s1) ? z[static_cast<i64>(s) * RT + c] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * kThreads;
+      zs[e / RT][e % RT] = v[q];
     }
     __syncthreads();
-#pragma unroll 8
-    for (int sl = 0; sl < GKC; ++sl) acc = fma(za[sl][la], zb[sl][lb], acc);
+#pragma unroll 4
+    for (int sl = 0; sl < GS; ++sl) {
+      double xa[TA], xb[TB];
+#pragma unroll
+      for (int x = 0; x < TA; ++x) xa[x] = zs[sl][ra + x];
+#pragma unroll
+      for (int y = 0; y < TB; ++y) xb[y] = zs[sl][cb + (RT / TB) * y];
+#pragma unroll
+      for (int x = 0; x < TA; ++x)
+#pragma unroll
+        for (int y = 0; y < TB; ++y) acc[x][y] = fma(xa[x], xb[y], acc[x][y]);
+    }
     __syncthreads();
   }
-  part[static_cast<i64>(blockIdx.y) * RT * RT + (ta * GT + la) * RT + tb * GT + lb] = acc;
+  (void)NA;
+  double* pg = part + static_cast<i64>(blockIdx.x) * RT * RT;
+#pragma unroll
+  for (int x = 0; x < TA; ++x)
+#pragma unroll
+    for (int y = 0; y < TB; ++y) pg[(ra + x) * RT + cb + (RT / TB) * y] = acc[x][y];
 }
 
 // Pivoted Cholesky of the R x R Gram in shared memory (warp 0), then its
@@ -245,6 +276,10 @@ __device__ void gram_pinv(double* g, double* w, int* perm, int r, double tol, do
 
 
 // ------------------------------------------------------ Gram inverse
+// In-place Gauss-Jordan on the SPD Gram, one CTA of 1024 threads; thread
+// (i, jq) keeps a(i, jq + 16 q) in registers. Step k needs column k and row
+// k of the current matrix, which the owners of column/row k+1 publish into
+// double-buffered shared vectors during step k: one barrier per step.
 constexpr int kInvThreads = 1024;
 
 template <int RT>
@@ -256,88 +291,84 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
   constexpr int LD = RT + 1;
   constexpr int QN = RT / 16;  // columns per thread
   extern __shared__ __align__(16) double sm[];
-  double* a = sm;             // [RT][LD] in-place inverse
-  double* g0 = sm + RT * LD;  // original G (fallback)
-  double* wk = g0 + RT * LD;  // fallback scratch
+  double* g0 = sm;            // original G (fallback)
+  double* wk = g0 + RT * LD;  // fallback scratch [RT][LD] + 2 RT
+  double* a2 = wk + RT * LD + 2 * RT;  // fallback working copy [RT][LD]
   __shared__ double colb[2][RT], rowb[2][RT];
   __shared__ int perm[RT];
-  __shared__ int s_fail;
   __shared__ double s_thr;
   const int tid = threadIdx.x, i = tid / 16, jq = tid % 16;
-  const bool live = i < RT;
+  const bool live = i < r;
+  double a[QN];
   // G = sum of the split partials, in split order
-  if (live) {
 #pragma unroll
-    for (int q = 0; q < QN; ++q) {
-      const int j = jq + 16 * q;
-      double s0 = 0.0;
+  for (int q = 0; q < QN; ++q) {
+    const int j = jq + 16 * q;
+    double s0 = 0.0;
+    if (live && j < r) {
+      const double* p = part + i * RT + j;
       int k = 0;
       for (; k + 4 <= nparts; k += 4) {
-        const double v0 = part[static_cast<i64>(k) * RT * RT + i * RT + j];
-        const double v1 = part[static_cast<i64>(k + 1) * RT * RT + i * RT + j];
-        const double v2 = part[static_cast<i64>(k + 2) * RT * RT + i * RT + j];
-        const double v3 = part[static_cast<i64>(k + 3) * RT * RT + i * RT + j];
+        const double v0 = p[static_cast<i64>(k) * RT * RT], v1 = p[static_cast<i64>(k + 1) * RT * RT];
+        const double v2 = p[static_cast<i64>(k + 2) * RT * RT], v3 = p[static_cast<i64>(k + 3) * RT * RT];
         s0 = (((s0 + v0) + v1) + v2) + v3;
       }
-      for (; k < nparts; ++k) s0 += part[static_cast<i64>(k) * RT * RT + i * RT + j];
-      const double v = (i < r && j < r) ? s0 : 0.0;
-      a[i * LD + j] = v;
-      g0[i * LD + j] = v;
-      if (j == 0) colb[0][i] = v;
-      if (i == 0) rowb[0][j] = v;
+      for (; k < nparts; ++k) s0 += p[static_cast<i64>(k) * RT * RT];
     }
+    a[q] = s0;
+    if (i < RT) g0[i * LD + j] = s0;
+    if (j == 0 && i < RT) colb[0][i] = s0;
+    if (i == 0) rowb[0][j] = s0;
   }
-  if (tid == 0) s_fail = 0;
   __syncthreads();
   if (tid < 32) {
     double d = 0.0;
-    for (int t = tid; t < r; t += 32) d = fmax(d, a[t * LD + t]);
+    for (int t = tid; t < r; t += 32) d = fmax(d, g0[t * LD + t]);
     for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
     if (tid == 0) s_thr = tol * d;
   }
   __syncthreads();
   const double thr = s_thr;
+  bool fail = false;
   for (int k = 0; k < r; ++k) {
     const int b = k & 1;
     const double piv = colb[b][k];
     if (!(piv > thr) || !(piv > 0.0)) {
-      if (tid == 0) s_fail = 1;
-      break;  // uniform: every thread read the same pivot
+      fail = true;  // uniform: every thread read the same pivot
+      break;
     }
     const double p = 1.0 / piv;
-    if (live && i < r) {
-      const double cik = colb[b][i];
+    const double cik = live ? colb[b][i] : 0.0;
+    const bool row_k = (i == k);
 #pragma unroll
-      for (int q = 0; q < QN; ++q) {
-        const int j = jq + 16 * q;
-        if (j >= r) continue;
-        const double rkj = rowb[b][j] * p;
-        double v;
-        if (i == k) v = (j == k) ? p : rkj;
-        else if (j == k) v = -cik * p;
-        else v = a[i * LD + j] - cik * rkj;
-        a[i * LD + j] = v;
+    for (int q = 0; q < QN; ++q) {
+      const int j = jq + 16 * q;
+      const double rkj = rowb[b][j] * p;
+      double v = row_k ? rkj : fma(-cik, rkj, a[q]);
+      if (j == k) v = row_k ? p : -cik * p;
+      a[q] = v;
+      if (live && j < r) {
         if (j == k + 1) colb[b ^ 1][i] = v;
         if (i == k + 1) rowb[b ^ 1][j] = v;
       }
     }
     __syncthreads();
   }
-  __syncthreads();
-  if (!s_fail) {
-    if (live && i < r)
+  if (!fail) {
+    if (live)
 #pragma unroll
       for (int q = 0; q < QN; ++q) {
         const int j = jq + 16 * q;
-        if (j < r) ginv[i * r + j] = a[i * LD + j];
+        if (j < r) ginv[i * r + j] = a[q];
       }
     if (tid == 0) info[0] = r;
     return;
   }
   // numerically rank-deficient Gram: pivoted Cholesky pseudo-inverse
-  for (int e = tid; e < RT * LD; e += blockDim.x) a[e] = g0[e];
   __syncthreads();
-  gram_pinv<RT>(a, wk, perm, r, tol, ginv, info);
+  for (int e = tid; e < RT * LD; e += blockDim.x) a2[e] = g0[e];
+  __syncthreads();
+  gram_pinv<RT>(a2, wk, perm, r, tol, ginv, info);
 }
 
 // ------------------------------------------------------------ RHS GEMM
@@ -407,7 +438,7 @@ __global__ void __launch_bounds__(kThreads) rhs_gemm_kernel(const double* __rest
 #pragma unroll
       for (int a = 0; a < TM; ++a) af[a] = ab[kk * GBM + ty * TM + a];
 #pragma unroll
-      for (int b = 0; b < TN; ++b) bf[b] = bb[kk * RT + tx * TN + b];
+      for (int b = 0; b < TN; ++b) bf[b] = bb[kk * RT + tx + 16 * b];  // conflict-free
 #pragma unroll
       for (int a = 0; a < TM; ++a)
 #pragma unroll
@@ -421,112 +452,93 @@ __global__ void __launch_bounds__(kThreads) rhs_gemm_kernel(const double* __rest
     if (i >= in) continue;
 #pragma unroll
     for (int b = 0; b < TN; ++b) {
-      const int rr = tx * TN + b;
+      const int rr = tx + 16 * b;
       if (rr < r) pr[i * r + rr] = acc[a][b];
     }
   }
 }
 
 // --------------------------------------------------------- apply + norms
-// A_un(i, :) = (sum_ks part(ks, i, :)) * Ginv for BI rows per CTA; column
-// sum-of-squares partials; the last CTA forms the norms (fixed order), the
-// lambda rule, and refills zero columns. The factor is kept unnormalized:
-// consumers read A_un / norm, the exact value the reference stores.
-constexpr int BI = 16;
+// A_un(i, c) = sum_c' RHS(i, c') Ginv(c', c): one output per thread,
+// 1024 / RT rows per CTA; the split-K partials are summed in split order.
+// Column sum-of-squares partials per CTA; the last CTA forms the norms
+// (fixed order), the lambda rule (kruskal.hpp:57-66) and refills zero
+// columns. The factor stays unnormalized: consumers read A_un / norm, the
+// value the reference stores after col /= norm.
+constexpr int kApplyThreads = 1024;
 
 template <int RT>
-__global__ void __launch_bounds__(kThreads) mode_apply_kernel(i64 in, int r, ModeWork w,
-                                                              const double* __restrict__ rhs_full,
-                                                              int first_of_pass,
-                                                              unsigned long long* rng_state) {
+__global__ void __launch_bounds__(kApplyThreads) mode_apply_kernel(i64 in, int r, ModeWork w,
+                                                                   const double* __restrict__ rhs_full,
+                                                                   int first_of_pass,
+                                                                   unsigned long long* rng_state) {
   if (w.stop && *w.stop) return;
-  constexpr int TN = RT / 16;
+  constexpr int BI = kApplyThreads / RT;
+  constexpr int NP = kApplyThreads / RT;  // interleaved parts in the final reduction
   __shared__ double gi[RT][RT + 1];
   __shared__ double rh[BI][RT + 1];
-  __shared__ double red[4][RT];
   __shared__ bool s_last;
+  __shared__ int s_zero;
   const int tid = threadIdx.x;
-  const i64 i0 = static_cast<i64>(blockIdx.x) * BI;
-  for (int e = tid; e < RT * RT; e += kThreads) {
-    const int a = e / RT, b = e % RT;
-    gi[a][b] = (a < r && b < r) ? w.ginv[a * r + b] : 0.0;
+  const int il = tid / RT, c = tid % RT;
+  const i64 i = static_cast<i64>(blockIdx.x) * BI + il;
+  for (int e = tid; e < RT * RT; e += kApplyThreads) {
+    const int x = e / RT, y = e % RT;
+    gi[x][y] = (x < r && y < r) ? w.ginv[x * r + y] : 0.0;
   }
-#pragma unroll
-  for (int q = 0; q < BI * RT / kThreads; ++q) {
-    const int e = tid + q * kThreads;
-    const int il = e / RT, c = e % RT;
-    const i64 i = i0 + il;
-    double s = 0.0;
-    if (i < in && c < r) {
-      if (rhs_full) {
-        s = rhs_full[i * r + c];
-      } else {
-        const double* p = w.part_rhs + i * r + c;
-        const i64 step = in * r;
-        int k = 0;
-        for (; k + 4 <= w.ks; k += 4) {
-          const double v0 = p[k * step], v1 = p[(k + 1) * step], v2 = p[(k + 2) * step],
-                       v3 = p[(k + 3) * step];
-          s = (((s + v0) + v1) + v2) + v3;
-        }
-        for (; k < w.ks; ++k) s += p[k * step];
+  double s = 0.0;
+  if (i < in && c < r) {
+    if (rhs_full) {
+      s = rhs_full[i * r + c];
+    } else {
+      const double* p = w.part_rhs + i * r + c;
+      const i64 step = in * r;
+      int k = 0;
+      for (; k + 6 <= w.ks; k += 6) {
+        const double v0 = p[k * step], v1 = p[(k + 1) * step], v2 = p[(k + 2) * step];
+        const double v3 = p[(k + 3) * step], v4 = p[(k + 4) * step], v5 = p[(k + 5) * step];
+        s = (((((s + v0) + v1) + v2) + v3) + v4) + v5;
       }
+      for (; k < w.ks; ++k) s += p[k * step];
     }
-    rh[il][c] = s;
   }
+  rh[il][c] = s;
   __syncthreads();
-  const int il = tid / 16, tx = tid % 16;
-  const i64 i = i0 + il;
-  double out[TN];
-#pragma unroll
-  for (int b = 0; b < TN; ++b) out[b] = 0.0;
-  for (int c = 0; c < r; ++c) {
-    const double rv = rh[il][c];
-#pragma unroll
-    for (int b = 0; b < TN; ++b) out[b] = fma(rv, gi[c][tx * TN + b], out[b]);
-  }
-  __syncthreads();  // rh is reused for the squares
-#pragma unroll
-  for (int b = 0; b < TN; ++b) {
-    const int cc = tx * TN + b;
-    const bool ok = (i < in && cc < r);
-    if (ok) w.a[i * r + cc] = out[b];
-    rh[il][cc] = ok ? out[b] * out[b] : 0.0;
-  }
+  double out = 0.0;
+  for (int cc = 0; cc < r; ++cc) out = fma(rh[il][cc], gi[cc][c], out);
+  const bool ok = (i < in && c < r);
+  if (ok) w.a[i * r + c] = out;
+  __syncthreads();  // rh reused for the squares
+  rh[il][c] = ok ? out * out : 0.0;
   __syncthreads();
   if (tid < RT) {
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < BI; ++q) s += rh[q][tid];
-    if (tid < r) w.ssq[static_cast<i64>(blockIdx.x) * r + tid] = s;
+    double q = 0.0;
+#pragma unroll 8
+    for (int x = 0; x < BI; ++x) q += rh[x][tid];
+    if (tid < r) w.ssq[static_cast<i64>(blockIdx.x) * r + tid] = q;
   }
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(&w.ticket[1], 1u) == gridDim.x - 1u);
+  if (tid == 0) {
+    s_last = (atomicAdd(&w.ticket[1], 1u) == gridDim.x - 1u);
+    s_zero = 0;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // column norms: 4 interleaved partial sums per column, combined in order
+  // column norms: NP interleaved partial sums per column, combined in order
   {
-    const int c = tid % RT, part = tid / RT;  // RT * 4 <= 256
-    double s = 0.0;
-    if (c < r && part < 4) {
-      unsigned b = part;
-      for (; b + 12 < gridDim.x; b += 16) {
-        const double v0 = w.ssq[static_cast<i64>(b) * r + c], v1 = w.ssq[static_cast<i64>(b + 4) * r + c];
-        const double v2 = w.ssq[static_cast<i64>(b + 8) * r + c], v3 = w.ssq[static_cast<i64>(b + 12) * r + c];
-        s = (((s + v0) + v1) + v2) + v3;
-      }
-      for (; b < gridDim.x; b += 4) s += w.ssq[static_cast<i64>(b) * r + c];
-    }
-    if (part < 4) red[part][c] = s;
+    const int part = tid / RT;
+    double q = 0.0;
+    if (c < r)
+      for (unsigned b = part; b < gridDim.x; b += NP) q += w.ssq[static_cast<i64>(b) * r + c];
+    rh[part][c] = q;
   }
   __syncthreads();
-  __shared__ int s_zero;
-  if (tid == 0) s_zero = 0;
-  __syncthreads();
   if (tid < r) {
-    const double nrm = sqrt(((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid]);
+    double t = 0.0;
+    for (int x = 0; x < NP; ++x) t += rh[x][tid];
+    const double nrm = sqrt(t);
     w.norms[tid] = nrm;
     // kruskal.hpp:57-66: lambda multiplied on the first mode of a pass, else overwritten
     if (nrm == 0.0) {
@@ -544,10 +556,10 @@ __global__ void __launch_bounds__(kThreads) mode_apply_kernel(i64 in, int r, Mod
       // stream, one distribution object per call, columns in order
       DevMt g{rng_state};
       DevNormal gauss;
-      for (int c = 0; c < r; ++c) {
-        if (w.norms[c] != 0.0) continue;
-        for (i64 t = 0; t < in; ++t) w.a[t * r + c] = gauss(g);
-        w.norms[c] = dev_stable_norm(w.a + c, in, r);
+      for (int col = 0; col < r; ++col) {
+        if (w.norms[col] != 0.0) continue;
+        for (i64 t = 0; t < in; ++t) w.a[t * r + col] = gauss(g);
+        w.norms[col] = dev_stable_norm(w.a + col, in, r);
       }
     }
   }
@@ -578,10 +590,11 @@ void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms) {
 }
 
 void gram_splits(int s, int* parts, int* klen) {
-  int k = ceil_div(s, 256);
-  if (k > 16) k = 16;
+  // one CTA per GS-sample chunk, at most 64 partials (longer chunks beyond)
+  int k = ceil_div(s, GS);
+  if (k > 64) k = 64;
   if (k < 1) k = 1;
-  const int len = ceil_div(ceil_div(s, k), GKC) * GKC;
+  const int len = ceil_div(ceil_div(s, k), GS) * GS;
   *parts = ceil_div(s, len);
   *klen = len;
 }
@@ -605,7 +618,7 @@ template <int RT>
 static void gram_t(const double* z, int s, double* part, const int* stop, cudaStream_t st) {
   int parts, klen;
   gram_splits(s, &parts, &klen);
-  gram_kernel<RT><<<dim3((RT / GT) * (RT / GT), parts), kThreads, 0, st>>>(z, s, klen, part, stop);
+  gram_kernel<RT><<<parts, kThreads, 0, st>>>(z, s, klen, part, stop);
   CPB_LAUNCH_CHECK();
 }
 
@@ -620,7 +633,7 @@ void launch_gram(const double* z, int s, int r, double* part, const int* stop, c
 template <int RT>
 static void inverse_t(const double* pg, int nparts, int r, double tol, double* ginv, int* info,
                       const int* stop, cudaStream_t st) {
-  const size_t sm = static_cast<size_t>(3 * RT * (RT + 1) + 2 * RT) * sizeof(double);
+  const size_t sm = static_cast<size_t>(3 * RT * (RT + 1) + 2 * RT) * sizeof(double);  // g0, wk(+2RT), a2
   static bool configured = false;
   if (!configured) {
     CPB_CUDA(cudaFuncSetAttribute(gram_inverse_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -664,13 +677,16 @@ void launch_rhs_gemm(const double* xs, i64 ld, const double* z, i64 in, int s, i
   }
 }
 
+int apply_grid(i64 in, int r) { return ceil_div(in, kApplyThreads / rank_bucket(r)); }
+
 void launch_mode_apply(i64 in, int r, const ModeWork& w, const double* rhs_override,
                        int first_of_pass, unsigned long long* rng_state, cudaStream_t st) {
-  const int grid = ceil_div(in, BI);
-  switch (rank_bucket(r)) {
-    case 16: mode_apply_kernel<16><<<grid, kThreads, 0, st>>>(in, r, w, rhs_override, first_of_pass, rng_state); break;
-    case 32: mode_apply_kernel<32><<<grid, kThreads, 0, st>>>(in, r, w, rhs_override, first_of_pass, rng_state); break;
-    default: mode_apply_kernel<64><<<grid, kThreads, 0, st>>>(in, r, w, rhs_override, first_of_pass, rng_state); break;
+  const int rt = rank_bucket(r);
+  const int grid = ceil_div(in, kApplyThreads / rt);
+  switch (rt) {
+    case 16: mode_apply_kernel<16><<<grid, kApplyThreads, 0, st>>>(in, r, w, rhs_override, first_of_pass, rng_state); break;
+    case 32: mode_apply_kernel<32><<<grid, kApplyThreads, 0, st>>>(in, r, w, rhs_override, first_of_pass, rng_state); break;
+    default: mode_apply_kernel<64><<<grid, kApplyThreads, 0, st>>>(in, r, w, rhs_override, first_of_pass, rng_state); break;
   }
   CPB_LAUNCH_CHECK();
 }
