@@ -264,9 +264,13 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
   CPB_CUDA(cudaSetDevice(x->device));
   CPB_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, x->device));
   rt_ = rank_bucket(r);
-  CPB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  CPB_CUDA(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
-  CPB_CUDA(cudaStreamCreateWithFlags(&gstream_, cudaStreamNonBlocking));
+  // The solve chain (s1, s2) is latency-critical; the gather ring producer
+  // only has to stay ahead, so its CTAs yield SM slots to the chain.
+  int prio_lo = 0, prio_hi = 0;
+  CPB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CPB_CUDA(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_hi));
+  CPB_CUDA(cudaStreamCreateWithPriority(&stream2_, cudaStreamNonBlocking, prio_hi));
+  CPB_CUDA(cudaStreamCreateWithPriority(&gstream_, cudaStreamNonBlocking, prio_lo));
   CPB_CUDA(cudaEventCreate(&ev_loop0_));
   CPB_CUDA(cudaEventCreate(&ev_loop1_));
   CPB_CUDA(cudaEventCreateWithFlags(&ev_z_, cudaEventDisableTiming));

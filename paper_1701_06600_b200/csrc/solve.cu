@@ -300,21 +300,33 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
   const int tid = threadIdx.x, i = tid / 16, jq = tid % 16;
   const bool live = i < r;
   double a[QN];
-  // G = sum of the split partials, in split order
+  // G = sum of the split partials, in split order; all QN x 8 loads of a
+  // batch are independent, so they are in flight together
+  double acc0[QN];
+#pragma unroll
+  for (int q = 0; q < QN; ++q) acc0[q] = 0.0;
+  if (live) {
+    const double* p = part + i * RT + jq;
+    int k = 0;
+    for (; k + 8 <= nparts; k += 8) {
+      double v[8][QN];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int q = 0; q < QN; ++q) v[u][q] = p[static_cast<i64>(k + u) * RT * RT + 16 * q];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int q = 0; q < QN; ++q) acc0[q] += v[u][q];
+    }
+    for (; k < nparts; ++k)
+#pragma unroll
+      for (int q = 0; q < QN; ++q) acc0[q] += p[static_cast<i64>(k) * RT * RT + 16 * q];
+  }
 #pragma unroll
   for (int q = 0; q < QN; ++q) {
     const int j = jq + 16 * q;
-    double s0 = 0.0;
-    if (live && j < r) {
-      const double* p = part + i * RT + j;
-      int k = 0;
-      for (; k + 4 <= nparts; k += 4) {
-        const double v0 = p[static_cast<i64>(k) * RT * RT], v1 = p[static_cast<i64>(k + 1) * RT * RT];
-        const double v2 = p[static_cast<i64>(k + 2) * RT * RT], v3 = p[static_cast<i64>(k + 3) * RT * RT];
-        s0 = (((s0 + v0) + v1) + v2) + v3;
-      }
-      for (; k < nparts; ++k) s0 += p[static_cast<i64>(k) * RT * RT];
-    }
+    const double s0 = (live && j < r) ? acc0[q] : 0.0;
     a[q] = s0;
     if (i < RT) g0[i * LD + j] = s0;
     if (j == 0 && i < RT) colb[0][i] = s0;
@@ -590,9 +602,9 @@ void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms) {
 }
 
 void gram_splits(int s, int* parts, int* klen) {
-  // one CTA per GS-sample chunk, at most 64 partials (longer chunks beyond)
+  // one CTA per chunk of >= GS samples, at most 8 partials for the inverse to sum
   int k = ceil_div(s, GS);
-  if (k > 64) k = 64;
+  if (k > 8) k = 8;
   if (k < 1) k = 1;
   const int len = ceil_div(ceil_div(s, k), GS) * GS;
   *parts = ceil_div(s, len);
