@@ -276,11 +276,15 @@ __device__ void gram_pinv(double* g, double* w, int* perm, int r, double tol, do
 
 
 // ------------------------------------------------------ Gram inverse
-// In-place Gauss-Jordan on the SPD Gram, one CTA of 1024 threads; thread
-// (i, jq) keeps a(i, jq + 16 q) in registers. Step k needs column k and row
-// k of the current matrix, which the owners of column/row k+1 publish into
-// double-buffered shared vectors during step k: one barrier per step.
-constexpr int kInvThreads = 1024;
+// In-place Gauss-Jordan on the SPD Gram in one CTA of 512 threads. Warp w
+// owns rows w + 16 t, lane l owns columns l + 32 u; the elements live in
+// registers. Step k needs column k, row k and 1/pivot of the current
+// matrix; the owners of column / row / pivot k+1 publish them into
+// double-buffered shared vectors during step k, so each step costs one
+// barrier and no per-thread division. Every pivot is tested against
+// tol * max diag; a failure (numerical rank < R) switches to the pivoted
+// Cholesky pseudo-inverse (gram_pinv).
+constexpr int kInvThreads = 512;
 
 template <int RT>
 __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double* __restrict__ part,
@@ -289,55 +293,70 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
                                                                    int* info, const int* stop) {
   if (stop && *stop) return;
   constexpr int LD = RT + 1;
-  constexpr int QN = RT / 16;  // columns per thread
+  constexpr int TR = RT / 16;                 // rows per warp
+  constexpr int TC = RT >= 32 ? RT / 32 : 1;  // columns per lane
   extern __shared__ __align__(16) double sm[];
-  double* g0 = sm;            // original G (fallback)
-  double* wk = g0 + RT * LD;  // fallback scratch [RT][LD] + 2 RT
+  double* g0 = sm;                     // original G (fallback)
+  double* wk = g0 + RT * LD;           // fallback scratch [RT][LD] + 2 RT
   double* a2 = wk + RT * LD + 2 * RT;  // fallback working copy [RT][LD]
-  __shared__ double colb[2][RT], rowb[2][RT];
+  __shared__ double colb[2][RT], rowb[2][RT], prcp[2];
   __shared__ int perm[RT];
   __shared__ double s_thr;
-  const int tid = threadIdx.x, i = tid / 16, jq = tid % 16;
-  const bool live = i < r;
-  double a[QN];
-  // G = sum of the split partials, in split order; all QN x 8 loads of a
-  // batch are independent, so they are in flight together
-  double acc0[QN];
+  const int tid = threadIdx.x, w = tid / 32, l = tid % 32;
+  double a[TR][TC];
+  int row[TR], col[TC];
 #pragma unroll
-  for (int q = 0; q < QN; ++q) acc0[q] = 0.0;
-  if (live) {
-    const double* p = part + i * RT + jq;
+  for (int t = 0; t < TR; ++t) row[t] = w + 16 * t;
+#pragma unroll
+  for (int u = 0; u < TC; ++u) col[u] = l + 32 * u;
+  // G = sum of the split partials in split order; loads of a batch in flight together
+#pragma unroll
+  for (int t = 0; t < TR; ++t)
+#pragma unroll
+    for (int u = 0; u < TC; ++u) a[t][u] = 0.0;
+  {
     int k = 0;
-    for (; k + 8 <= nparts; k += 8) {
-      double v[8][QN];
+    for (; k + 4 <= nparts; k += 4) {
+      double v[4][TR][TC];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int q = 0; q < QN; ++q) v[u][q] = p[static_cast<i64>(k + u) * RT * RT + 16 * q];
+        for (int t = 0; t < TR; ++t)
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+          for (int u = 0; u < TC; ++u)
+            v[x][t][u] = (row[t] < r && col[u] < r) ? part[static_cast<i64>(k + x) * RT * RT + row[t] * RT + col[u]] : 0.0;
 #pragma unroll
-        for (int q = 0; q < QN; ++q) acc0[q] += v[u][q];
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int t = 0; t < TR; ++t)
+#pragma unroll
+          for (int u = 0; u < TC; ++u) a[t][u] += v[x][t][u];
     }
     for (; k < nparts; ++k)
 #pragma unroll
-      for (int q = 0; q < QN; ++q) acc0[q] += p[static_cast<i64>(k) * RT * RT + 16 * q];
+      for (int t = 0; t < TR; ++t)
+#pragma unroll
+        for (int u = 0; u < TC; ++u)
+          if (row[t] < r && col[u] < r) a[t][u] += part[static_cast<i64>(k) * RT * RT + row[t] * RT + col[u]];
   }
 #pragma unroll
-  for (int q = 0; q < QN; ++q) {
-    const int j = jq + 16 * q;
-    const double s0 = (live && j < r) ? acc0[q] : 0.0;
-    a[q] = s0;
-    if (i < RT) g0[i * LD + j] = s0;
-    if (j == 0 && i < RT) colb[0][i] = s0;
-    if (i == 0) rowb[0][j] = s0;
-  }
+  for (int t = 0; t < TR; ++t)
+#pragma unroll
+    for (int u = 0; u < TC; ++u) {
+      if (col[u] >= RT) continue;
+      g0[row[t] * LD + col[u]] = a[t][u];
+      if (col[u] == 0) colb[0][row[t]] = a[t][u];
+      if (row[t] == 0) rowb[0][col[u]] = a[t][u];
+    }
   __syncthreads();
   if (tid < 32) {
     double d = 0.0;
-    for (int t = tid; t < r; t += 32) d = fmax(d, g0[t * LD + t]);
+    for (int x = tid; x < r; x += 32) d = fmax(d, g0[x * LD + x]);
     for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
-    if (tid == 0) s_thr = tol * d;
+    if (tid == 0) {
+      s_thr = tol * d;
+      prcp[0] = 1.0 / g0[0];
+    }
   }
   __syncthreads();
   const double thr = s_thr;
@@ -349,30 +368,35 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
       fail = true;  // uniform: every thread read the same pivot
       break;
     }
-    const double p = 1.0 / piv;
-    const double cik = live ? colb[b][i] : 0.0;
-    const bool row_k = (i == k);
+    const double p = prcp[b];
+    double rk[TC];
 #pragma unroll
-    for (int q = 0; q < QN; ++q) {
-      const int j = jq + 16 * q;
-      const double rkj = rowb[b][j] * p;
-      double v = row_k ? rkj : fma(-cik, rkj, a[q]);
-      if (j == k) v = row_k ? p : -cik * p;
-      a[q] = v;
-      if (live && j < r) {
-        if (j == k + 1) colb[b ^ 1][i] = v;
-        if (i == k + 1) rowb[b ^ 1][j] = v;
+    for (int u = 0; u < TC; ++u) rk[u] = rowb[b][col[u] < RT ? col[u] : 0] * p;
+#pragma unroll
+    for (int t = 0; t < TR; ++t) {
+      const double cik = colb[b][row[t]];
+      const bool is_k = (row[t] == k);
+      const bool is_k1 = (row[t] == k + 1);
+#pragma unroll
+      for (int u = 0; u < TC; ++u) {
+        double v = is_k ? rk[u] : fma(-cik, rk[u], a[t][u]);
+        if (col[u] == k) v = is_k ? p : -cik * p;
+        a[t][u] = v;
+        if (col[u] == k + 1 && row[t] < r) {
+          colb[b ^ 1][row[t]] = v;
+          if (is_k1) prcp[b ^ 1] = 1.0 / v;
+        }
+        if (is_k1 && col[u] < r) rowb[b ^ 1][col[u]] = v;
       }
     }
     __syncthreads();
   }
   if (!fail) {
-    if (live)
 #pragma unroll
-      for (int q = 0; q < QN; ++q) {
-        const int j = jq + 16 * q;
-        if (j < r) ginv[i * r + j] = a[q];
-      }
+    for (int t = 0; t < TR; ++t)
+#pragma unroll
+      for (int u = 0; u < TC; ++u)
+        if (row[t] < r && col[u] < r) ginv[row[t] * r + col[u]] = a[t][u];
     if (tid == 0) info[0] = r;
     return;
   }
@@ -384,7 +408,7 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
 }
 
 // ------------------------------------------------------------ RHS GEMM
-constexpr int GBM = 64, GBK = 16, GSTAGES = 4;
+constexpr int GBM = 128, GBK = 16, GSTAGES = 3;
 
 template <int RT>
 __global__ void __launch_bounds__(kThreads) rhs_gemm_kernel(const double* __restrict__ xs, i64 ld,
@@ -409,9 +433,9 @@ __global__ void __launch_bounds__(kThreads) rhs_gemm_kernel(const double* __rest
     double* ab = as + st * GBK * GBM;
     double* bb = bs + st * GBK * RT;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {  // A: GBK x 64 doubles = 512 chunks of 16 B
+    for (int q = 0; q < GBK * GBM / 2 / kThreads; ++q) {  // A: GBK x GBM doubles in 16 B chunks
       const int c = tid + q * kThreads;
-      const int sl = c / 32, ic = (c % 32) * 2;
+      const int sl = c / (GBM / 2), ic = (c % (GBM / 2)) * 2;
       const int s = sbase + sl;
       const i64 i = i0 + ic;
       const bool ok = (s < s_end) && (i < ld);
@@ -602,9 +626,9 @@ void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms) {
 }
 
 void gram_splits(int s, int* parts, int* klen) {
-  // one CTA per chunk of >= GS samples, at most 8 partials for the inverse to sum
+  // one CTA per chunk of >= GS samples, at most 32 partials for the inverse to sum
   int k = ceil_div(s, GS);
-  if (k > 8) k = 8;
+  if (k > 32) k = 32;
   if (k < 1) k = 1;
   const int len = ceil_div(ceil_div(s, k), GS) * GS;
   *parts = ceil_div(s, len);
