@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
   double* g0 = sm;                     // original G (fallback)
   double* wk = g0 + RT * LD;           // fallback scratch [RT][LD] + 2 RT
   double* a2 = wk + RT * LD + 2 * RT;  // fallback working copy [RT][LD]
-  __shared__ double colb[2][RT], rowb[2][RT], prcp[2];
+  __shared__ double colb[2][RT], rowb[2][RT];
   __shared__ int perm[RT];
   __shared__ double s_thr;
   const int tid = threadIdx.x, w = tid / 32, l = tid % 32;
@@ -348,19 +348,23 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
       if (col[u] == 0) colb[0][row[t]] = a[t][u];
       if (row[t] == 0) rowb[0][col[u]] = a[t][u];
     }
+  if (tid < RT) {
+    colb[1][tid] = 0.0;
+    rowb[1][tid] = 0.0;
+  }
   __syncthreads();
   if (tid < 32) {
     double d = 0.0;
     for (int x = tid; x < r; x += 32) d = fmax(d, g0[x * LD + x]);
     for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
-    if (tid == 0) {
-      s_thr = tol * d;
-      prcp[0] = 1.0 / g0[0];
-    }
+    if (tid == 0) s_thr = tol * d;
   }
   __syncthreads();
   const double thr = s_thr;
   bool fail = false;
+  // Branch-free step: with x = a (0 on row k and column k), c = a(i, k)
+  // (-1 on row k) and rk = a(k, j) / piv (1 / piv on column k),
+  // a' = x - c * rk reproduces all four Gauss-Jordan update rules.
   for (int k = 0; k < r; ++k) {
     const int b = k & 1;
     const double piv = colb[b][k];
@@ -368,27 +372,34 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
       fail = true;  // uniform: every thread read the same pivot
       break;
     }
-    const double p = prcp[b];
+    const double p = __drcp_rn(piv);
     double rk[TC];
 #pragma unroll
-    for (int u = 0; u < TC; ++u) rk[u] = rowb[b][col[u] < RT ? col[u] : 0] * p;
+    for (int u = 0; u < TC; ++u) {
+      const double rv = rowb[b][col[u] < RT ? col[u] : 0] * p;
+      rk[u] = (col[u] == k) ? p : rv;
+    }
 #pragma unroll
     for (int t = 0; t < TR; ++t) {
-      const double cik = colb[b][row[t]];
       const bool is_k = (row[t] == k);
-      const bool is_k1 = (row[t] == k + 1);
+      const double c = is_k ? -1.0 : colb[b][row[t]];
 #pragma unroll
       for (int u = 0; u < TC; ++u) {
-        double v = is_k ? rk[u] : fma(-cik, rk[u], a[t][u]);
-        if (col[u] == k) v = is_k ? p : -cik * p;
-        a[t][u] = v;
-        if (col[u] == k + 1 && row[t] < r) {
-          colb[b ^ 1][row[t]] = v;
-          if (is_k1) prcp[b ^ 1] = 1.0 / v;
-        }
-        if (is_k1 && col[u] < r) rowb[b ^ 1][col[u]] = v;
+        const double x = (is_k || col[u] == k) ? 0.0 : a[t][u];
+        a[t][u] = fma(-c, rk[u], x);
       }
     }
+#pragma unroll
+    for (int u = 0; u < TC; ++u)
+      if (col[u] == k + 1)
+#pragma unroll
+        for (int t = 0; t < TR; ++t) colb[b ^ 1][row[t]] = a[t][u];
+#pragma unroll
+    for (int t = 0; t < TR; ++t)
+      if (row[t] == k + 1)
+#pragma unroll
+        for (int u = 0; u < TC; ++u)
+          if (col[u] < RT) rowb[b ^ 1][col[u]] = a[t][u];
     __syncthreads();
   }
   if (!fail) {
