@@ -264,6 +264,12 @@ def main() -> int:
     achieved = (kbytes / launches) / (kms / launches * 1e-3) / 1e9
     share = (kms / timing_iters) / (ms / args.steps)
     gemm_tflops = sum(g[2] for g in gemm) / (sum(g[1] for g in gemm) * 1e-3) / 1e12
+    kinds = ["gather", "rhs_gemm", "z", "gram", "gram_inverse", "apply", "mix_factor"]
+    breakdown = {}
+    for k, name in enumerate(kinds):
+        st = [s.kernel_stats(m, k) for m in range(n_modes)]
+        if sum(x[0] for x in st):
+            breakdown[name] = [round(x[1] / max(x[0], 1) * 1e3, 2) for x in st]
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tpath):
@@ -321,7 +327,8 @@ def main() -> int:
                          "per_mode_gbs": [p[2] / (p[1] * 1e-3) / 1e9 for p in per_mode],
                          "share_of_step": share, "peak_source": peak_src,
                          "rhs_gemm_fp64_tflops": gemm_tflops,
-                         "rhs_gemm_per_mode_us": [g[1] / g[0] * 1e3 for g in gemm]},
+                         "rhs_gemm_per_mode_us": [g[1] / g[0] * 1e3 for g in gemm],
+                         "per_kernel_us_by_mode": breakdown},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches_per_iter(cfg) * args.steps,
         }

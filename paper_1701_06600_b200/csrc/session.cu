@@ -279,7 +279,7 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
   // reuse: cap the L2 fetch granularity so DRAM moves only that sector.
   cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
   cudaGetLastError();
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kKinds; ++k) {
     k_launches_[k].assign(static_cast<size_t>(order_), 0);
     k_ms_[k].assign(static_cast<size_t>(order_), 0.0);
     k_work_[k].assign(static_cast<size_t>(order_), 0.0);
@@ -661,22 +661,27 @@ cudaEvent_t Session::timing_event() {
   return e;
 }
 
+template <class F>
+void Session::timed(int mode, int kind, cudaStream_t st, F&& launch) {
+  if (!timing_) {
+    launch();
+    return;
+  }
+  cudaEvent_t ea = timing_event(), eb = timing_event();
+  CPB_CUDA(cudaEventRecord(ea, st));
+  launch();
+  CPB_CUDA(cudaEventRecord(eb, st));
+  pending_.push_back({mode, kind, ea, eb});
+}
+
 void Session::enqueue_gather(int git) {
   for (int n = 0; n < order_; ++n) {
     const size_t slot = static_cast<size_t>(((git - 1) % depth_) * order_ + n);
     if (slot_used_[slot]) CPB_CUDA(cudaStreamWaitEvent(gstream_, ev_consumed_[slot], 0));
-    cudaEvent_t ea = nullptr, eb = nullptr;
-    if (timing_) {
-      ea = timing_event();
-      eb = timing_event();
-      CPB_CUDA(cudaEventRecord(ea, gstream_));
-    }
-    launch_gather_rows(xsolve_, dims_[static_cast<size_t>(n)], strides_[static_cast<size_t>(n)], base_ptr(git, n),
-                       s_mode_[static_cast<size_t>(n)], ring_[slot], ld_[static_cast<size_t>(n)], gstream_);
-    if (timing_) {
-      CPB_CUDA(cudaEventRecord(eb, gstream_));
-      pending_.push_back({n, 0, ea, eb});
-    }
+    timed(n, 0, gstream_, [&] {
+      launch_gather_rows(xsolve_, dims_[static_cast<size_t>(n)], strides_[static_cast<size_t>(n)], base_ptr(git, n),
+                         s_mode_[static_cast<size_t>(n)], ring_[slot], ld_[static_cast<size_t>(n)], gstream_);
+    });
     CPB_CUDA(cudaEventRecord(ev_gathered_[slot], gstream_));
     slot_used_[slot] = 1;
   }
@@ -699,39 +704,38 @@ void Session::enqueue_iteration() {
     const ModeWork w = work(n);
     const size_t slot = static_cast<size_t>(((it - 1) % depth_) * order_ + n);
     // Z_S; the Gram and its pseudo-inverse run on s2 beside the RHS GEMM
-    launch_z(v, w.z, stop, stream_);
+    timed(n, 2, stream_, [&] { launch_z(v, w.z, stop, stream_); });
     CPB_CUDA(cudaEventRecord(ev_z_, stream_));
     CPB_CUDA(cudaStreamWaitEvent(stream2_, ev_z_, 0));
-    launch_gram(w.z, v.s, r_, w.part_gram, stop, stream2_);
-    launch_gram_inverse(w.part_gram, w.gram_parts, r_, w.tol, w.ginv, w.info, stop, stream2_);
+    timed(n, 3, stream2_, [&] { launch_gram(w.z, v.s, r_, w.part_gram, stop, stream2_); });
+    timed(n, 4, stream2_, [&] {
+      launch_gram_inverse(w.part_gram, w.gram_parts, r_, w.tol, w.ginv, w.info, stop, stream2_);
+    });
     CPB_CUDA(cudaEventRecord(ev_inv_, stream2_));
     // RHS GEMM on the gathered X_S rows
     CPB_CUDA(cudaStreamWaitEvent(stream_, ev_gathered_[slot], 0));
-    cudaEvent_t ea = nullptr, eb = nullptr;
-    if (timing_) {
-      ea = timing_event();
-      eb = timing_event();
-      CPB_CUDA(cudaEventRecord(ea, stream_));
-    }
-    launch_rhs_gemm(ring_[slot], ld_[static_cast<size_t>(n)], w.z, v.in, v.s, r_, w.ks, w.ks_len, w.part_rhs, stop,
-                    stream_);
-    if (timing_) {
-      CPB_CUDA(cudaEventRecord(eb, stream_));
-      pending_.push_back({n, 1, ea, eb});
-    }
+    timed(n, 1, stream_, [&] {
+      launch_rhs_gemm(ring_[slot], ld_[static_cast<size_t>(n)], w.z, v.in, v.s, r_, w.ks, w.ks_len, w.part_rhs,
+                      stop, stream_);
+    });
     CPB_CUDA(cudaEventRecord(ev_consumed_[slot], stream_));
     CPB_CUDA(cudaStreamWaitEvent(stream_, ev_inv_, 0));
-    const double* rhs = nullptr;
-    if (mix_) {
-      launch_reduce_rhs(part_rhs_, w.ks, v.in, r_, rhs_full_, stream_);
-      launch_mode_transform(plans_[static_cast<size_t>(n)], rhs_full_, rhs_full_, r_, r_,
-                            signs_[static_cast<size_t>(n)], 0, nullptr, stream_);
-      rhs = rhs_full_;
-    }
-    launch_mode_apply(v.in, r_, w, rhs, n == 0, rng_state_, stream_);
+    timed(n, 5, stream_, [&] {
+      const double* rhs = nullptr;
+      if (mix_) {
+        launch_reduce_rhs(part_rhs_, w.ks, v.in, r_, rhs_full_, stream_);
+        launch_mode_transform(plans_[static_cast<size_t>(n)], rhs_full_, rhs_full_, r_, r_,
+                              signs_[static_cast<size_t>(n)], 0, nullptr, stream_);
+        rhs = rhs_full_;
+      }
+      launch_mode_apply(v.in, r_, w, rhs, n == 0, rng_state_, stream_);
+    });
     if (mix_)  // mixed image of the new (normalized) factor (mixing.hpp:297-298)
-      launch_mode_transform(plans_[static_cast<size_t>(n)], fac_[static_cast<size_t>(n)], mixed_[static_cast<size_t>(n)], r_,
-                            r_, signs_[static_cast<size_t>(n)], 1, w.norms, stream_);
+      timed(n, 6, stream_, [&] {
+        launch_mode_transform(plans_[static_cast<size_t>(n)], fac_[static_cast<size_t>(n)],
+                              mixed_[static_cast<size_t>(n)], r_, r_, signs_[static_cast<size_t>(n)], 1, w.norms,
+                              stream_);
+      });
   }
   if (has_fit_) {
     FitArgs a{};
@@ -852,7 +856,7 @@ void Session::collect_kernel_times() {
       // B_min accounting: 8 B per element for mode 1's
       // contiguous fibers, one 32 B sector per element for strided modes.
       k_work_[k][m] += elems * (m == 0 ? 8.0 : 32.0);
-    } else {
+    } else if (k == 1) {
       k_work_[k][m] += 2.0 * elems * static_cast<double>(r_);  // RHS flops
     }
     ev_pool_.push_back(p.a);
@@ -863,7 +867,7 @@ void Session::collect_kernel_times() {
 
 void Session::kernel_stats(int mode, int kind, i64* launches, double* ms, double* work) {
   if (mode < 0 || mode >= order_) throw InvalidArgument("mode out of range");
-  if (kind < 0 || kind > 1) throw InvalidArgument("kernel kind must be 0 (gather) or 1 (gemm)");
+  if (kind < 0 || kind >= kKinds) throw InvalidArgument("kernel kind out of range");
   sync();
   *launches = k_launches_[kind][static_cast<size_t>(mode)];
   *ms = k_ms_[kind][static_cast<size_t>(mode)];

@@ -78,8 +78,10 @@ class Session {
   void sync();
   cudaStream_t stream() const { return stream_; }
   void set_timing(bool on) { timing_ = on; }
-  // kind 0: sampled-fiber gather (bytes = B_min); kind 1: RHS GEMM (flops)
+  // kind 0: sampled-fiber gather (work = B_min bytes); 1: RHS GEMM (flops);
+  // 2: Z_S; 3: Gram; 4: Gram inverse; 5: apply (+ MIX unmix); 6: MIX factor
   void kernel_stats(int mode, int kind, i64* launches, double* ms, double* work);
+  static constexpr int kKinds = 7;
   void result(double* out_lambda, double* const* out_factors, std::vector<Trace>& trace,
               int* iterations, int* reason, double* setup_s, double* total_s, double* loop_dev_s);
 
@@ -178,8 +180,10 @@ class Session {
   };
   std::vector<Pending> pending_;
   std::vector<cudaEvent_t> ev_pool_;
-  std::vector<i64> k_launches_[2];
-  std::vector<double> k_ms_[2], k_work_[2];
+  std::vector<i64> k_launches_[kKinds];
+  std::vector<double> k_ms_[kKinds], k_work_[kKinds];
+  template <class F>
+  void timed(int mode, int kind, cudaStream_t st, F&& launch);
 };
 
 // operator-level helpers (capi.cu)
