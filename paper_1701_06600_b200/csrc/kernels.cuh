@@ -28,6 +28,7 @@ struct ModeWork {
   int gram_parts;      // split-K partials of the Gram
   double* part_rhs;    // [ks][I_n][R]
   double* ginv;        // [R][R]
+  double* gfull;       // [R][R] reduced Gram (fallback input)
   int* info;           // [0] = numerical rank of the Gram
   unsigned* ticket;    // [1] norm ticket (self-resetting)
   double* ssq;         // [grid][R] column sum-of-squares partials
@@ -44,13 +45,15 @@ int rank_bucket(int r);  // 16 / 32 / 64
 void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms);
 void gram_splits(int s, int* parts, int* klen);
 int apply_grid(i64 in, int r);  // CTAs of mode_apply (sizes the ssq partials)
+i64 gram_scratch_doubles(int r);
 
 void launch_gather_rows(const double* x, i64 in, i64 stride, const i64* base, int s, double* xs,
                         i64 ld, cudaStream_t st);
 void launch_z(const ModeView& v, double* z, const int* stop, cudaStream_t st);
 void launch_gram(const double* z, int s, int r, double* part, const int* stop, cudaStream_t st);
+// gfull: gram_scratch_doubles(r) of global scratch (the reduced Gram + fallback work)
 void launch_gram_inverse(const double* part_gram, int nparts, int r, double tol, double* ginv,
-                         int* info, const int* stop, cudaStream_t st);
+                         double* gfull, int* info, const int* stop, cudaStream_t st);
 void launch_rhs_gemm(const double* xs, i64 ld, const double* z, i64 in, int s, int r, int ks,
                      int ks_len, double* part, const int* stop, cudaStream_t st);
 // rhs_override != null: use it (I_n x R row-major, already reduced) instead of

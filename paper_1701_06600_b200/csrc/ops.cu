@@ -200,6 +200,7 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
   const i64 ld = (in + 1) & ~i64{1};
   DBuf prhs(static_cast<size_t>(ks) * in * r * sizeof(double)), pgram(static_cast<size_t>(gp) * rt * rt * sizeof(double));
   DBuf ginv(static_cast<size_t>(r * r) * sizeof(double)), info(4 * sizeof(int)), tickets(8 * sizeof(unsigned));
+  DBuf gfull(static_cast<size_t>(gram_scratch_doubles(r)) * sizeof(double));
   DBuf ssq(static_cast<size_t>(apply_grid(in, r)) * r * sizeof(double)), norms(r * sizeof(double));
   DBuf dlam(r * sizeof(double)), da(static_cast<size_t>(in * r) * sizeof(double)), rng(313 * sizeof(unsigned long long));
   DBuf rhs(static_cast<size_t>(in * r) * sizeof(double)), dz(static_cast<size_t>(s * rt) * sizeof(double));
@@ -213,6 +214,7 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
   w.gram_parts = gp;
   w.part_rhs = prhs.as<double>();
   w.ginv = ginv.as<double>();
+  w.gfull = gfull.as<double>();
   w.info = info.as<int>();
   w.ticket = tickets.as<unsigned>();
   w.ssq = ssq.as<double>();
@@ -226,7 +228,7 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
   launch_gather_rows(v.x, in, v.stride, v.base, static_cast<int>(s), xs.as<double>(), ld, stream);
   launch_z(v, w.z, nullptr, stream);
   launch_gram(w.z, static_cast<int>(s), r, w.part_gram, nullptr, stream);
-  launch_gram_inverse(w.part_gram, gp, r, w.tol, w.ginv, w.info, nullptr, stream);
+  launch_gram_inverse(w.part_gram, gp, r, w.tol, w.ginv, w.gfull, w.info, nullptr, stream);
   launch_rhs_gemm(xs.as<double>(), ld, w.z, in, static_cast<int>(s), r, ks, len, w.part_rhs, nullptr, stream);
   const double* rhsp = nullptr;
   if (mix) {

@@ -309,6 +309,7 @@ Session::~Session() {
   dfree(part_rhs_);
   dfree(part_gram_);
   dfree(ginv_);
+  dfree(gfull_);
   dfree(info_);
   dfree(tickets_);
   dfree(ssq_);
@@ -416,6 +417,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   part_gram_ = dalloc<double>(static_cast<size_t>(max_gp) * rt_ * rt_);
   alloc_ring();
   ginv_ = dalloc<double>(static_cast<size_t>(r_ * r_));
+  gfull_ = dalloc<double>(static_cast<size_t>(gram_scratch_doubles(r_)));
   info_ = dalloc<int>(4);
   tickets_ = dalloc<unsigned>(8);
   CPB_CUDA(cudaMemsetAsync(tickets_, 0, 8 * sizeof(unsigned), stream_));
@@ -611,6 +613,7 @@ ModeWork Session::work(int n) const {
   gram_splits(s_mode_[static_cast<size_t>(n)], &w.gram_parts, &glen);
   w.part_rhs = part_rhs_;
   w.ginv = ginv_;
+  w.gfull = gfull_;
   w.info = info_;
   w.ticket = tickets_;
   w.ssq = ssq_;
@@ -709,7 +712,7 @@ void Session::enqueue_iteration() {
     CPB_CUDA(cudaStreamWaitEvent(stream2_, ev_z_, 0));
     timed(n, 3, stream2_, [&] { launch_gram(w.z, v.s, r_, w.part_gram, stop, stream2_); });
     timed(n, 4, stream2_, [&] {
-      launch_gram_inverse(w.part_gram, w.gram_parts, r_, w.tol, w.ginv, w.info, stop, stream2_);
+      launch_gram_inverse(w.part_gram, w.gram_parts, r_, w.tol, w.ginv, w.gfull, w.info, stop, stream2_);
     });
     CPB_CUDA(cudaEventRecord(ev_inv_, stream2_));
     // RHS GEMM on the gathered X_S rows

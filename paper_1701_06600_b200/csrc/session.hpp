@@ -141,6 +141,7 @@ class Session {
   double* part_rhs_ = nullptr;
   double* part_gram_ = nullptr;
   double* ginv_ = nullptr;
+  double* gfull_ = nullptr;
   int* info_ = nullptr;
   unsigned* tickets_ = nullptr;
   double* ssq_ = nullptr;

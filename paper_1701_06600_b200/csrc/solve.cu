@@ -290,17 +290,12 @@ template <int RT>
 __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double* __restrict__ part,
                                                                    int nparts, int r, double tol,
                                                                    double* __restrict__ ginv,
+                                                                   double* __restrict__ gfull,
                                                                    int* info, const int* stop) {
   if (stop && *stop) return;
-  constexpr int LD = RT + 1;
   constexpr int TR = RT / 16;                 // rows per warp
   constexpr int TC = RT >= 32 ? RT / 32 : 1;  // columns per lane
-  extern __shared__ __align__(16) double sm[];
-  double* g0 = sm;                     // original G (fallback)
-  double* wk = g0 + RT * LD;           // fallback scratch [RT][LD] + 2 RT
-  double* a2 = wk + RT * LD + 2 * RT;  // fallback working copy [RT][LD]
-  __shared__ double colb[2][RT], rowb[2][RT];
-  __shared__ int perm[RT];
+  __shared__ double colb[2][RT], rowb[2][RT], diag[RT];
   __shared__ double s_thr;
   const int tid = threadIdx.x, w = tid / 32, l = tid % 32;
   double a[TR][TC];
@@ -344,9 +339,10 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
 #pragma unroll
     for (int u = 0; u < TC; ++u) {
       if (col[u] >= RT) continue;
-      g0[row[t] * LD + col[u]] = a[t][u];
+      if (row[t] < r && col[u] < r) gfull[row[t] * r + col[u]] = a[t][u];  // for the fallback
       if (col[u] == 0) colb[0][row[t]] = a[t][u];
       if (row[t] == 0) rowb[0][col[u]] = a[t][u];
+      if (row[t] == col[u]) diag[row[t]] = a[t][u];
     }
   if (tid < RT) {
     colb[1][tid] = 0.0;
@@ -355,7 +351,7 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
   __syncthreads();
   if (tid < 32) {
     double d = 0.0;
-    for (int x = tid; x < r; x += 32) d = fmax(d, g0[x * LD + x]);
+    for (int x = tid; x < r; x += 32) d = fmax(d, diag[x]);
     for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
     if (tid == 0) s_thr = tol * d;
   }
@@ -408,14 +404,31 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
 #pragma unroll
       for (int u = 0; u < TC; ++u)
         if (row[t] < r && col[u] < r) ginv[row[t] * r + col[u]] = a[t][u];
-    if (tid == 0) info[0] = r;
-    return;
   }
-  // numerically rank-deficient Gram: pivoted Cholesky pseudo-inverse
+  if (tid == 0) info[0] = fail ? -1 : r;
+}
+
+// Rank-deficient Gram (rare): pivoted Cholesky pseudo-inverse of gfull.
+// Launched after every inverse and exits at once unless the inverse flagged
+// failure; its working matrices live in global scratch (gfull + R*R), so
+// the launch reserves almost no shared memory.
+template <int RT>
+__global__ void __launch_bounds__(kThreads) gram_pinv_fallback_kernel(const double* __restrict__ gfull,
+                                                                      int r, double tol,
+                                                                      double* __restrict__ ginv,
+                                                                      int* info, const int* stop) {
+  if (stop && *stop) return;
+  if (info[0] >= 0) return;
+  constexpr int LD = RT + 1;
+  double* g = const_cast<double*>(gfull) + r * r;  // scratch: [RT][LD] + [RT][LD] + 2 RT
+  double* wk = g + RT * LD;
+  __shared__ int perm[RT];
+  for (int e = threadIdx.x; e < RT * LD; e += blockDim.x) {
+    const int x = e / LD, y = e % LD;
+    g[e] = (x < r && y < r) ? gfull[x * r + y] : 0.0;
+  }
   __syncthreads();
-  for (int e = tid; e < RT * LD; e += blockDim.x) a2[e] = g0[e];
-  __syncthreads();
-  gram_pinv<RT>(a2, wk, perm, r, tol, ginv, info);
+  gram_pinv<RT>(g, wk, perm, r, tol, ginv, info);
 }
 
 // ------------------------------------------------------------ RHS GEMM
@@ -625,7 +638,7 @@ int rank_bucket(int r) {
 void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms) {
   (void)rt;
   const int mtiles = ceil_div(in, GBM);
-  const int want = 2 * sms;  // ~2 CTAs per SM
+  const int want = sms;  // ~1 CTA per SM (each holds 2 CTA slots): fewer partials for apply
   int k = ceil_div(want, mtiles);
   const int tiles = ceil_div(s, GBK);
   if (k > tiles) k = tiles;
@@ -678,25 +691,20 @@ void launch_gram(const double* z, int s, int r, double* part, const int* stop, c
 }
 
 template <int RT>
-static void inverse_t(const double* pg, int nparts, int r, double tol, double* ginv, int* info,
-                      const int* stop, cudaStream_t st) {
-  const size_t sm = static_cast<size_t>(3 * RT * (RT + 1) + 2 * RT) * sizeof(double);  // g0, wk(+2RT), a2
-  static bool configured = false;
-  if (!configured) {
-    CPB_CUDA(cudaFuncSetAttribute(gram_inverse_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sm)));
-    configured = true;
-  }
-  gram_inverse_kernel<RT><<<1, kInvThreads, sm, st>>>(pg, nparts, r, tol, ginv, info, stop);
+static void inverse_t(const double* pg, int nparts, int r, double tol, double* ginv, double* gfull,
+                      int* info, const int* stop, cudaStream_t st) {
+  gram_inverse_kernel<RT><<<1, kInvThreads, 0, st>>>(pg, nparts, r, tol, ginv, gfull, info, stop);
+  CPB_LAUNCH_CHECK();
+  gram_pinv_fallback_kernel<RT><<<1, kThreads, 0, st>>>(gfull, r, tol, ginv, info, stop);
   CPB_LAUNCH_CHECK();
 }
 
 void launch_gram_inverse(const double* part_gram, int nparts, int r, double tol, double* ginv,
-                         int* info, const int* stop, cudaStream_t st) {
+                         double* gfull, int* info, const int* stop, cudaStream_t st) {
   switch (rank_bucket(r)) {
-    case 16: inverse_t<16>(part_gram, nparts, r, tol, ginv, info, stop, st); break;
-    case 32: inverse_t<32>(part_gram, nparts, r, tol, ginv, info, stop, st); break;
-    default: inverse_t<64>(part_gram, nparts, r, tol, ginv, info, stop, st); break;
+    case 16: inverse_t<16>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st); break;
+    case 32: inverse_t<32>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st); break;
+    default: inverse_t<64>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st); break;
   }
 }
 
@@ -722,6 +730,11 @@ void launch_rhs_gemm(const double* xs, i64 ld, const double* z, i64 in, int s, i
     case 32: gemm_t<32>(xs, ld, z, in, s, r, ks, ks_len, part, stop, st); break;
     default: gemm_t<64>(xs, ld, z, in, s, r, ks, ks_len, part, stop, st); break;
   }
+}
+
+i64 gram_scratch_doubles(int r) {
+  const i64 rt = rank_bucket(r);
+  return static_cast<i64>(r) * r + 2 * rt * (rt + 1) + 2 * rt;
 }
 
 int apply_grid(i64 in, int r) { return ceil_div(in, kApplyThreads / rank_bucket(r)); }
