@@ -41,6 +41,7 @@ CONFIGS = {
 }
 METRIC = "CPRAND iters/sec"
 SEED = 1
+DFMA_PEAK_TF = 33.5  # FP64 FMA throughput measured on this pool's B200 (tests/micro/probe.cu)
 
 
 def peaks():
@@ -150,7 +151,8 @@ def barrier(dist):
 
 def launches_per_iter(cfg) -> int:
     n = len(cfg["dims"])
-    # gather, skr_gram, gram_inverse, rhs_gemm, mode_apply, normalize
+    # z, gram, gram_inverse (+ fallback check), rhs_gemm, mode_apply; the gather
+    # kernel only for modes without in-place reads
     per_mode = 6 + (3 if cfg["method"] == "mix" and cfg["transform"] == "dct" else 0)
     return n * per_mode
 
@@ -251,25 +253,40 @@ def main() -> int:
     barrier(dist)
     value = ws * args.steps / (ms * 1e-3)
 
-    # ---- roofline: the fused gather/SKR/Gram/RHS kernel, per-launch CUDA events
+    # ---- roofline: per-launch CUDA events on each kernel's own stream
     s.set_kernel_timing(True)
     s.enqueue(timing_iters)
     s.sync()
     n_modes = len(cfg["dims"])
-    per_mode = [s.kernel_stats(m, 0) for m in range(n_modes)]
-    gemm = [s.kernel_stats(m, 1) for m in range(n_modes)]
-    launches = sum(p[0] for p in per_mode)
-    kms = sum(p[1] for p in per_mode)
-    kbytes = sum(p[2] for p in per_mode)
+    kinds = ["gather", "rhs_gemm", "z", "gram", "gram_inverse", "apply", "mix_factor"]
+    stats = {k: [s.kernel_stats(m, i) for m in range(n_modes)] for i, k in enumerate(kinds)}
+    breakdown = {k: [round(x[1] / x[0] * 1e3, 2) for x in st] for k, st in stats.items()
+                 if sum(x[0] for x in st)}
+    elems = [cfg["s"] * d for d in cfg["dims"]]
+    gather = stats["gather"]
+    gemm = stats["rhs_gemm"]
+    gemm_ms = sum(g[1] for g in gemm)
+    gemm_tflops = sum(g[2] for g in gemm) / (gemm_ms * 1e-3) / 1e12
+    if sum(g[0] for g in gather):
+        # sampled-fiber gather kernel: B_min bytes (8 B/elem mode 1, 32 B/elem strided)
+        kname = "gather_rows_kernel (sampled-fiber gather)"
+        launches = sum(g[0] for g in gather)
+        kms = sum(g[1] for g in gather)
+        kbytes = sum(g[2] for g in gather)
+        per_mode = [g[2] / (g[1] * 1e-3) / 1e9 if g[0] else None for g in gather]
+        bytes_model = "B_min: 8 B/elem mode 1, 32 B/elem strided modes"
+    else:
+        # every mode reads its sampled fibers in place (mode 1 / mode-major
+        # replicas): the dominant kernel is the RHS GEMM, whose algorithmic
+        # bytes are the sampled fibers (8 B/elem, contiguous rows) + Z_S
+        kname = "rhs_gemm_kernel (in-place fiber reads + Z_S^T X_S^T)"
+        launches = sum(g[0] for g in gemm)
+        kms = gemm_ms
+        kbytes = sum((e * 8 + cfg["s"] * cfg["r"] * 8) * g[0] for e, g in zip(elems, gemm))
+        per_mode = [(e * 8 + cfg["s"] * cfg["r"] * 8) / (g[1] / g[0] * 1e-3) / 1e9 for e, g in zip(elems, gemm)]
+        bytes_model = "fibers 8 B/elem (contiguous rows) + Z_S 8 B/entry"
     achieved = (kbytes / launches) / (kms / launches * 1e-3) / 1e9
     share = (kms / timing_iters) / (ms / args.steps)
-    gemm_tflops = sum(g[2] for g in gemm) / (sum(g[1] for g in gemm) * 1e-3) / 1e12
-    kinds = ["gather", "rhs_gemm", "z", "gram", "gram_inverse", "apply", "mix_factor"]
-    breakdown = {}
-    for k, name in enumerate(kinds):
-        st = [s.kernel_stats(m, k) for m in range(n_modes)]
-        if sum(x[0] for x in st):
-            breakdown[name] = [round(x[1] / max(x[0], 1) * 1e3, 2) for x in st]
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tpath):
@@ -321,13 +338,11 @@ def main() -> int:
                        "parallelism": "replicas" if ws > 1 else "single",
                        "l2": "inputs larger than L2 (8 GB tensor, fresh random samples per step)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": "gather_rows_kernel (sampled-fiber gather, all modes)",
-                         "bytes_model": "B_min: 8 B/elem mode 1, 32 B/elem strided modes",
-                         "per_mode_gbs": [p[2] / (p[1] * 1e-3) / 1e9 for p in per_mode],
+                         "frac": achieved / hbm_peak, "traffic": traffic, "kernel": kname,
+                         "bytes_model": bytes_model, "per_mode_gbs": per_mode,
                          "share_of_step": share, "peak_source": peak_src,
                          "rhs_gemm_fp64_tflops": gemm_tflops,
-                         "rhs_gemm_per_mode_us": [g[1] / g[0] * 1e3 for g in gemm],
+                         "rhs_gemm_fp64_frac_of_dfma": gemm_tflops / DFMA_PEAK_TF,
                          "per_kernel_us_by_mode": breakdown},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches_per_iter(cfg) * args.steps,

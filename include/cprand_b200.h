@@ -93,6 +93,8 @@ typedef struct cprand_options {
   int32_t x_is_device;        /* cprand_solve: x is a device pointer */
   int32_t x_mutable;          /* device x may be mixed in place (MIX/PREMIX) */
   void* comm;                 /* cprand_comm_t for slab-sharded runs, NULL = 1 GPU */
+  int32_t replicas;           /* mode-major copies of strided modes: -1 auto (fit in
+                                 free HBM), 0 off (gather ring), 1 on */
 } cprand_options_t;
 
 typedef struct cprand_trace_record {

@@ -41,6 +41,7 @@ class SolveOptions:
     exact_fit_trace: bool = False
     device: int = -1
     x_mutable: bool = False
+    replicas: int = -1  # mode-major replicas of strided modes: -1 auto, 0 off, 1 on
 
     def to_c(self) -> Options:
         o = Options()
@@ -59,6 +60,7 @@ class SolveOptions:
         o.exact_fit_trace = int(self.exact_fit_trace)
         o.device = self.device
         o.x_mutable = int(self.x_mutable)
+        o.replicas = self.replicas
         return o
 
 

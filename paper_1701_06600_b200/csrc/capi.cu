@@ -58,6 +58,7 @@ Options opts_of(const cprand_options_t* o) {
   r.exact_fit_trace = o->exact_fit_trace != 0;
   r.device = o->device;
   r.x_mutable = o->x_mutable != 0;
+  r.replicas = o->replicas;
   if (o->comm != nullptr) throw Unsupported("slab-sharded sessions are not enabled in this build");
   return r;
 }
@@ -120,6 +121,7 @@ void cprand_options_init(cprand_options_t* o) {
   o->stall_limit = 10;
   o->transform = CPRAND_TRANSFORM_UNSET;
   o->device = -1;
+  o->replicas = -1;
 }
 
 const char* cprand_last_error(void) { return g_err.c_str(); }

@@ -54,8 +54,13 @@ void launch_gram(const double* z, int s, int r, double* part, const int* stop, c
 // gfull: gram_scratch_doubles(r) of global scratch (the reduced Gram + fallback work)
 void launch_gram_inverse(const double* part_gram, int nparts, int r, double tol, double* ginv,
                          double* gfull, int* info, const int* stop, cudaStream_t st);
-void launch_rhs_gemm(const double* xs, i64 ld, const double* z, i64 in, int s, int r, int ks,
-                     int ks_len, double* part, const int* stop, cudaStream_t st);
+// A rows at xs + row_off[s] (fibers read in place) or xs + s * ld (gathered
+// X_S, zero padded to ld); vec16 requires 16 B aligned row starts.
+void launch_rhs_gemm(const double* xs, i64 ld, const i64* row_off, bool vec16, const double* z, i64 in,
+                     int s, int r, int ks, int ks_len, double* part, const int* stop, cudaStream_t st);
+// Mode-major replica y = X_(n) (column-major I_n x P/I_n) of a tensor whose
+// mode n has length in and stride st.
+void launch_replica(const double* x, i64 in, i64 st, i64 p, double* y, cudaStream_t stream);
 // rhs_override != null: use it (I_n x R row-major, already reduced) instead of
 // summing part_rhs (the MIX path unmixes the RHS first). Writes A_un, norms,
 // lambda; zero columns refilled from the device normalize RNG.

@@ -229,7 +229,8 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
   launch_z(v, w.z, nullptr, stream);
   launch_gram(w.z, static_cast<int>(s), r, w.part_gram, nullptr, stream);
   launch_gram_inverse(w.part_gram, gp, r, w.tol, w.ginv, w.gfull, w.info, nullptr, stream);
-  launch_rhs_gemm(xs.as<double>(), ld, w.z, in, static_cast<int>(s), r, ks, len, w.part_rhs, nullptr, stream);
+  launch_rhs_gemm(xs.as<double>(), ld, nullptr, true, w.z, in, static_cast<int>(s), r, ks, len, w.part_rhs, nullptr,
+                  stream);
   const double* rhsp = nullptr;
   if (mix) {
     launch_reduce_rhs(prhs.as<double>(), ks, in, r, rhs.as<double>(), stream);

@@ -292,6 +292,8 @@ Session::~Session() {
   if (stream2_) cudaStreamSynchronize(stream2_);
   if (gstream_) cudaStreamSynchronize(gstream_);
   for (auto& b : ring_) dfree(b);
+  for (auto& b : rep_) dfree(b);
+  dfree(dbase_);
   for (auto& e : ev_gathered_) cudaEventDestroy(e);
   for (auto& e : ev_consumed_) cudaEventDestroy(e);
   if (ev_z_) cudaEventDestroy(ev_z_);
@@ -378,6 +380,8 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   rng_state_ = dalloc<unsigned long long>(313);
   launch_rng_seed(rng_state_, seeded_engine_seed_value(o_.rng_seed, kInitStream + 7), stream_);
 
+  // ---- which modes read their fibers in place (mode 1, or a mode-major replica)
+  plan_replicas();
   // ---- sample tables (data independent: all drawn up front)
   build_tables();
 
@@ -394,6 +398,8 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
     x_norm_ = std::sqrt(ss);
     build_fit_estimator(xsolve_);
   }
+
+  build_replicas();
 
   // ---- per-mode work buffers
   i64 max_part = 1, max_in = 1, max_apply = 1, max_s = 1;
@@ -470,45 +476,62 @@ void Session::build_tables() {
     }
   std::vector<int> rows(static_cast<size_t>(std::max<i64>(rows_total, 1)));
   std::vector<i64> base(static_cast<size_t>(std::max<i64>(base_total, 1)), 0);
+  std::vector<i64> dbase(static_cast<size_t>(std::max<i64>(base_total, 1)), 0);
   auto rng = seeded_engine(o_.rng_seed, kSamplingStream);
   for (int it = 0; it < table_iters_; ++it)
     for (int n = 0; n < N; ++n) {
       const int sn = s_mode_[static_cast<size_t>(n)];
       int* rb = rows.data() + row_off_[static_cast<size_t>(it * N + n)];
       i64* bb = base.data() + base_off_[static_cast<size_t>(it * N + n)];
+      i64* db = dbase.data() + base_off_[static_cast<size_t>(it * N + n)];
       std::vector<int> km;
-      for (int k = 0; k < N; ++k)
-        if (k != n) km.push_back(k);
+      std::vector<i64> jk;  // unfolding column weights J_k (tensor.hpp:92-106)
+      {
+        i64 jw = 1;
+        for (int k = 0; k < N; ++k)
+          if (k != n) {
+            km.push_back(k);
+            jk.push_back(jw);
+            jw *= dims_[static_cast<size_t>(k)];
+          }
+      }
+      const i64 in_n = dims_[static_cast<size_t>(n)];
       if (o_.exhaustive_samples) {
         // sampling.hpp:54-69: unfolding column order
         for (int j = 0; j < sn; ++j) {
-          i64 rem = j, b = 0;
+          i64 rem = j, b = 0, col = 0;
           for (int c = 0; c < N - 1; ++c) {
             const i64 d = dims_[static_cast<size_t>(km[static_cast<size_t>(c)])];
             const i64 idx = rem % d;
             rem /= d;
             rb[static_cast<i64>(c) * sn + j] = static_cast<int>(idx);
             b += idx * strides_[static_cast<size_t>(km[static_cast<size_t>(c)])];
+            col += idx * jk[static_cast<size_t>(c)];
           }
           bb[j] = b;
+          db[j] = (n == 0) ? b : in_n * col;
         }
       } else {
         // sampling.hpp:35-51: one uniform_int per kept mode, row by row
         std::vector<std::uniform_int_distribution<long>> dist;
         for (int k : km) dist.emplace_back(0L, static_cast<long>(dims_[static_cast<size_t>(k)] - 1));
         for (int j = 0; j < sn; ++j) {
-          i64 b = 0;
+          i64 b = 0, col = 0;
           for (int c = 0; c < N - 1; ++c) {
             const long idx = dist[static_cast<size_t>(c)](rng);
             rb[static_cast<i64>(c) * sn + j] = static_cast<int>(idx);
             b += static_cast<i64>(idx) * strides_[static_cast<size_t>(km[static_cast<size_t>(c)])];
+            col += static_cast<i64>(idx) * jk[static_cast<size_t>(c)];
           }
           bb[j] = b;
+          db[j] = (n == 0) ? b : in_n * col;  // row of X_(n) in the mode-major replica
         }
       }
     }
   rows_ = dalloc<int>(rows.size());
   base_ = dalloc<i64>(base.size());
+  dbase_ = dalloc<i64>(dbase.size());
+  CPB_CUDA(cudaMemcpyAsync(dbase_, dbase.data(), dbase.size() * sizeof(i64), cudaMemcpyHostToDevice, stream_));
   CPB_CUDA(cudaMemcpyAsync(rows_, rows.data(), rows.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
   CPB_CUDA(cudaMemcpyAsync(base_, base.data(), base.size() * sizeof(i64), cudaMemcpyHostToDevice, stream_));
   CPB_CUDA(cudaStreamSynchronize(stream_));  // host vectors die here
@@ -576,6 +599,46 @@ void Session::mix_setup() {
   mix_seconds_ = seconds_since(tm);
 }
 
+const i64* Session::dbase_ptr(int it, int n) const {
+  const int ti = o_.exhaustive_samples ? 0 : it - 1;
+  return dbase_ + base_off_[static_cast<size_t>(ti * order_ + n)];
+}
+
+void Session::plan_replicas() {
+  // Mode 1 fibers are contiguous in the tensor. A strided mode n reads one
+  // 32 B sector per useful element at ~40 G random accesses/s (measured);
+  // a mode-major copy X_(n) turns each sampled fiber into a contiguous row
+  // the GEMM streams at full bandwidth. Memory: one tensor per replica.
+  direct_.assign(static_cast<size_t>(order_), 0);
+  vec16_.assign(static_cast<size_t>(order_), 0);
+  rep_.assign(static_cast<size_t>(order_), nullptr);
+  direct_[0] = 1;
+  vec16_[0] = (order_ == 1) || (dims_[0] % 2 == 0);
+  if (o_.replicas == 0) return;
+  size_t free_b = 0, total_b = 0;
+  CPB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const i64 bytes = p_ * 8;
+  i64 budget = static_cast<i64>(free_b) - (i64{6} << 30);  // keep 6 GB for work buffers
+  if ((mix_ || premix_) && !o_.x_mutable) budget -= bytes;  // the private mixed copy comes first
+  // widest strides first: they gain the most
+  for (int n = order_ - 1; n >= 1; --n) {
+    if (budget < bytes) break;
+    direct_[static_cast<size_t>(n)] = 1;
+    vec16_[static_cast<size_t>(n)] = dims_[static_cast<size_t>(n)] % 2 == 0;
+    budget -= bytes;
+  }
+}
+
+void Session::build_replicas() {
+  for (int n = 1; n < order_; ++n) {
+    if (!direct_[static_cast<size_t>(n)]) continue;
+    rep_[static_cast<size_t>(n)] = dalloc<double>(static_cast<size_t>(p_));
+    launch_replica(xsolve_, dims_[static_cast<size_t>(n)], strides_[static_cast<size_t>(n)], p_,
+                   rep_[static_cast<size_t>(n)], stream_);
+  }
+  CPB_CUDA(cudaStreamSynchronize(stream_));
+}
+
 const i64* Session::base_ptr(int it, int n) const {
   const int ti = o_.exhaustive_samples ? 0 : it - 1;
   return base_ + base_off_[static_cast<size_t>(ti * order_ + n)];
@@ -636,14 +699,16 @@ void Session::alloc_ring() {
   for (int n = 0; n < order_; ++n) {
     const i64 ld = (dims_[static_cast<size_t>(n)] + 1) & ~i64{1};  // 16 B rows for cp.async
     ld_.push_back(ld);
-    per_iter += static_cast<i64>(s_mode_[static_cast<size_t>(n)]) * ld;
+    if (!direct_[static_cast<size_t>(n)]) per_iter += static_cast<i64>(s_mode_[static_cast<size_t>(n)]) * ld;
   }
   const i64 budget = i64{3} << 30;  // bytes
   depth_ = (2 * per_iter * 8 <= budget) ? 2 : 1;
   for (int d = 0; d < depth_; ++d)
     for (int n = 0; n < order_; ++n) {
       // +2 doubles of slack: the GEMM's 16 B chunks may read one element past I_n
-      ring_.push_back(dalloc<double>(static_cast<size_t>(s_mode_[static_cast<size_t>(n)] * ld_[static_cast<size_t>(n)] + 2)));
+      ring_.push_back(direct_[static_cast<size_t>(n)]
+                          ? nullptr
+                          : dalloc<double>(static_cast<size_t>(s_mode_[static_cast<size_t>(n)] * ld_[static_cast<size_t>(n)] + 2)));
       cudaEvent_t e1, e2;
       CPB_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
       CPB_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
@@ -679,6 +744,7 @@ void Session::timed(int mode, int kind, cudaStream_t st, F&& launch) {
 
 void Session::enqueue_gather(int git) {
   for (int n = 0; n < order_; ++n) {
+    if (direct_[static_cast<size_t>(n)]) continue;
     const size_t slot = static_cast<size_t>(((git - 1) % depth_) * order_ + n);
     if (slot_used_[slot]) CPB_CUDA(cudaStreamWaitEvent(gstream_, ev_consumed_[slot], 0));
     timed(n, 0, gstream_, [&] {
@@ -715,13 +781,18 @@ void Session::enqueue_iteration() {
       launch_gram_inverse(w.part_gram, w.gram_parts, r_, w.tol, w.ginv, w.gfull, w.info, stop, stream2_);
     });
     CPB_CUDA(cudaEventRecord(ev_inv_, stream2_));
-    // RHS GEMM on the gathered X_S rows
-    CPB_CUDA(cudaStreamWaitEvent(stream_, ev_gathered_[slot], 0));
+    // RHS GEMM: fibers read in place (mode 1 / replica) or from the gather ring
+    const bool direct = direct_[static_cast<size_t>(n)];
+    if (!direct) CPB_CUDA(cudaStreamWaitEvent(stream_, ev_gathered_[slot], 0));
     timed(n, 1, stream_, [&] {
-      launch_rhs_gemm(ring_[slot], ld_[static_cast<size_t>(n)], w.z, v.in, v.s, r_, w.ks, w.ks_len, w.part_rhs,
-                      stop, stream_);
+      if (direct)
+        launch_rhs_gemm(n == 0 ? xsolve_ : rep_[static_cast<size_t>(n)], 0, dbase_ptr(it, n),
+                        vec16_[static_cast<size_t>(n)], w.z, v.in, v.s, r_, w.ks, w.ks_len, w.part_rhs, stop, stream_);
+      else
+        launch_rhs_gemm(ring_[slot], ld_[static_cast<size_t>(n)], nullptr, true, w.z, v.in, v.s, r_, w.ks, w.ks_len,
+                        w.part_rhs, stop, stream_);
     });
-    CPB_CUDA(cudaEventRecord(ev_consumed_[slot], stream_));
+    if (!direct) CPB_CUDA(cudaEventRecord(ev_consumed_[slot], stream_));
     CPB_CUDA(cudaStreamWaitEvent(stream_, ev_inv_, 0));
     timed(n, 5, stream_, [&] {
       const double* rhs = nullptr;

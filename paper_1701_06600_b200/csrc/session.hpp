@@ -31,6 +31,7 @@ struct Options {  // SolveOptions (solver.hpp:40-64) + device extensions
   bool exact_fit_trace = false;
   int device = -1;
   bool x_mutable = false;
+  int replicas = -1;  // mode-major replicas for strided modes: -1 auto, 0 off, 1 on
   void validate() const;
 };
 
@@ -97,6 +98,7 @@ class Session {
   ModeView view(int it, int n) const;
   ModeWork work(int n) const;
   const i64* base_ptr(int it, int n) const;
+  const i64* dbase_ptr(int it, int n) const;
   void download_model(HostModel& m);
   void collect_kernel_times();
   cudaEvent_t timing_event();
@@ -125,6 +127,12 @@ class Session {
   int table_iters_ = 0;
   int* rows_ = nullptr;             // [iter][mode] blocks of (N-1) x S_n
   i64* base_ = nullptr;             // [iter][mode] blocks of S_n
+  i64* dbase_ = nullptr;            // same layout: row offsets the GEMM reads in place
+  std::vector<double*> rep_;        // per mode: mode-major replica X_(n) (or null)
+  std::vector<char> direct_;        // per mode: GEMM reads fibers in place
+  std::vector<char> vec16_;         // per mode: in-place rows are 16 B aligned
+  void plan_replicas();
+  void build_replicas();
   std::vector<i64> row_off_, base_off_;  // block offsets per (iter, mode)
   // gather ring: depth_ iterations x N modes of X_S rows
   int depth_ = 2;

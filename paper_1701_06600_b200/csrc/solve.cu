@@ -434,8 +434,14 @@ __global__ void __launch_bounds__(kThreads) gram_pinv_fallback_kernel(const doub
 // ------------------------------------------------------------ RHS GEMM
 constexpr int GBM = 128, GBK = 16, GSTAGES = 3;
 
-template <int RT>
+// A operand rows: row s starts at xs + (row_off ? row_off[s] : s * ld) and
+// holds I_n contiguous doubles. With row_off the kernel reads the sampled
+// fibers in place (mode-1 fibers of the tensor, or rows of a mode-major
+// replica); without it, rows of a gathered X_S buffer. VEC16: every row
+// start is 16 B aligned (16 B async copies), else 8 B copies.
+template <int RT, bool VEC16>
 __global__ void __launch_bounds__(kThreads) rhs_gemm_kernel(const double* __restrict__ xs, i64 ld,
+                                                            const i64* __restrict__ row_off,
                                                             const double* __restrict__ z, i64 in,
                                                             int s_total, int r, int ks_len,
                                                             double* __restrict__ part,
@@ -456,14 +462,31 @@ __global__ void __launch_bounds__(kThreads) rhs_gemm_kernel(const double* __rest
     const int sbase = s_begin + t * GBK;
     double* ab = as + st * GBK * GBM;
     double* bb = bs + st * GBK * RT;
+    if constexpr (VEC16) {
 #pragma unroll
-    for (int q = 0; q < GBK * GBM / 2 / kThreads; ++q) {  // A: GBK x GBM doubles in 16 B chunks
-      const int c = tid + q * kThreads;
-      const int sl = c / (GBM / 2), ic = (c % (GBM / 2)) * 2;
-      const int s = sbase + sl;
-      const i64 i = i0 + ic;
-      const bool ok = (s < s_end) && (i < ld);
-      cp_async16(ab + sl * GBM + ic, ok ? xs + static_cast<i64>(s) * ld + i : xs, ok ? 16 : 0);
+      for (int q = 0; q < GBK * GBM / 2 / kThreads; ++q) {  // A: GBK x GBM doubles in 16 B chunks
+        const int c = tid + q * kThreads;
+        const int sl = c / (GBM / 2), ic = (c % (GBM / 2)) * 2;
+        const int s = sbase + sl;
+        const i64 i = i0 + ic;
+        const i64 lim = row_off ? in : ld;  // gathered rows are zero padded to ld
+        const bool ok = (s < s_end) && (i < lim);
+        const i64 ro = (s < s_end) ? (row_off ? row_off[s] : static_cast<i64>(s) * ld) : 0;
+        // a row of odd length: the chunk straddling I_n copies only its first element
+        const int bytes = !ok ? 0 : (i + 1 < lim ? 16 : 8);
+        cp_async16(ab + sl * GBM + ic, ok ? xs + ro + i : xs, bytes);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < GBK * GBM / kThreads; ++q) {  // 8 B chunks
+        const int c = tid + q * kThreads;
+        const int sl = c / GBM, ic = c % GBM;
+        const int s = sbase + sl;
+        const i64 i = i0 + ic;
+        const bool ok = (s < s_end) && (i < in);
+        const i64 ro = (s < s_end) ? (row_off ? row_off[s] : static_cast<i64>(s) * ld) : 0;
+        cp_async8(ab + sl * GBM + ic, ok ? xs + ro + i : xs, ok ? 8 : 0);
+      }
     }
     for (int c = tid; c < GBK * RT / 2; c += kThreads) {  // B: GBK x RT doubles
       const int sl = c / (RT / 2), rc = (c % (RT / 2)) * 2;
@@ -625,7 +648,43 @@ __global__ void __launch_bounds__(kApplyThreads) mode_apply_kernel(i64 in, int r
   }
 }
 
+// ------------------------------------------------------- mode-n replica
+// y = X_(n) stored column-major (I_n x P/I_n): for every hi-slab the
+// [i_n][lo] block (I_n x st_n, lo fastest) becomes [lo][i_n] (i_n fastest),
+// through 32 x 32 shared-memory tiles (coalesced reads and writes). Column j
+// of the unfolding (unfold_column_index, tensor.hpp:92-106) = lo + st_n hi,
+// so a sampled fiber becomes the contiguous row y + I_n * j.
+__global__ void __launch_bounds__(256) replica_kernel(const double* __restrict__ x, i64 in, i64 st,
+                                                      i64 nhi, double* __restrict__ y) {
+  __shared__ double tile[32][33];
+  const i64 tiles_lo = (st + 31) / 32, tiles_i = (in + 31) / 32;
+  const i64 per_hi = tiles_lo * tiles_i;
+  for (i64 blk = blockIdx.x; blk < nhi * per_hi; blk += gridDim.x) {
+    const i64 hi = blk / per_hi, rem = blk % per_hi;
+    const i64 ti = rem / tiles_lo, tl = rem % tiles_lo;
+    const double* src = x + hi * st * in;
+    double* dst = y + hi * st * in;
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
+    for (int k = ty; k < 32; k += 8) {
+      const i64 i = ti * 32 + k, lo = tl * 32 + tx;
+      tile[k][tx] = (i < in && lo < st) ? __ldcs(src + i * st + lo) : 0.0;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+      const i64 lo = tl * 32 + k, i = ti * 32 + tx;
+      if (i < in && lo < st) dst[lo * in + i] = tile[tx][k];
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+void launch_replica(const double* x, i64 in, i64 st, i64 p, double* y, cudaStream_t stream) {
+  const i64 nhi = p / (st * in);
+  replica_kernel<<<148 * 8, 256, 0, stream>>>(x, in, st, nhi, y);
+  CPB_LAUNCH_CHECK();
+}
 
 // ------------------------------------------------------------ launchers
 int rank_bucket(int r) {
@@ -708,27 +767,36 @@ void launch_gram_inverse(const double* part_gram, int nparts, int r, double tol,
   }
 }
 
-template <int RT>
-static void gemm_t(const double* xs, i64 ld, const double* z, i64 in, int s, int r, int ks, int ks_len,
-                   double* part, const int* stop, cudaStream_t st) {
+template <int RT, bool V>
+static void gemm_t(const double* xs, i64 ld, const i64* row_off, const double* z, i64 in, int s, int r,
+                   int ks, int ks_len, double* part, const int* stop, cudaStream_t st) {
   const size_t sm = static_cast<size_t>(GSTAGES * GBK * (GBM + RT)) * sizeof(double);
   static bool configured = false;
   if (!configured) {
-    CPB_CUDA(cudaFuncSetAttribute(rhs_gemm_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CPB_CUDA(cudaFuncSetAttribute(rhs_gemm_kernel<RT, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sm)));
     configured = true;
   }
-  rhs_gemm_kernel<RT><<<dim3(ceil_div(in, GBM), ks), kThreads, sm, st>>>(xs, ld, z, in, s, r, ks_len, part,
-                                                                         stop);
+  rhs_gemm_kernel<RT, V><<<dim3(ceil_div(in, GBM), ks), kThreads, sm, st>>>(xs, ld, row_off, z, in, s, r,
+                                                                            ks_len, part, stop);
   CPB_LAUNCH_CHECK();
 }
 
-void launch_rhs_gemm(const double* xs, i64 ld, const double* z, i64 in, int s, int r, int ks,
-                     int ks_len, double* part, const int* stop, cudaStream_t st) {
+void launch_rhs_gemm(const double* xs, i64 ld, const i64* row_off, bool vec16, const double* z, i64 in,
+                     int s, int r, int ks, int ks_len, double* part, const int* stop, cudaStream_t st) {
   switch (rank_bucket(r)) {
-    case 16: gemm_t<16>(xs, ld, z, in, s, r, ks, ks_len, part, stop, st); break;
-    case 32: gemm_t<32>(xs, ld, z, in, s, r, ks, ks_len, part, stop, st); break;
-    default: gemm_t<64>(xs, ld, z, in, s, r, ks, ks_len, part, stop, st); break;
+    case 16:
+      vec16 ? gemm_t<16, true>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st)
+            : gemm_t<16, false>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st);
+      break;
+    case 32:
+      vec16 ? gemm_t<32, true>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st)
+            : gemm_t<32, false>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st);
+      break;
+    default:
+      vec16 ? gemm_t<64, true>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st)
+            : gemm_t<64, false>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st);
+      break;
   }
 }
 
