@@ -320,13 +320,17 @@ def test_session_bench_mode_and_kernel_stats(pb, orc):
     t = pb.DeviceTensor(dims)
     t.synth(5, 0.5, 0.01, 11)
     x = t.download()
-    s = pb.Session("rand", t, 5, 80, pb.SolveOptions(rng_seed=11, max_iters=30, bench_mode=True))
+    s = pb.Session("rand", t, 5, 80, pb.SolveOptions(rng_seed=11, max_iters=30, bench_mode=True,
+                                                     replicas=0))
     s.set_kernel_timing(True)
     s.enqueue(10)
     s.sync()
     assert s.run(20) == 20
     for m in range(3):
-        n, ms, b = s.kernel_stats(m)
+        n, ms, b = s.kernel_stats(m, 1)  # RHS GEMM, every mode
+        assert n == 30 and ms > 0 and b > 0
+    for m in (1, 2):  # strided modes go through the gather ring when replicas are off
+        n, ms, b = s.kernel_stats(m, 0)
         assert n == 30 and ms > 0 and b > 0
     res = s.result()
     assert res.iterations == 30 and res.reason == "bench_complete" and res.trace == []
