@@ -258,7 +258,7 @@ def main() -> int:
     s.enqueue(timing_iters)
     s.sync()
     n_modes = len(cfg["dims"])
-    kinds = ["gather", "rhs_gemm", "z", "gram", "gram_inverse", "apply", "mix_factor"]
+    kinds = ["gather", "rhs_gemm", "z", "gram", "gram_inverse", "apply", "mix_factor", "fused_iteration"]
     stats = {k: [s.kernel_stats(m, i) for m in range(n_modes)] for i, k in enumerate(kinds)}
     breakdown = {k: [round(x[1] / x[0] * 1e3, 2) for x in st] for k, st in stats.items()
                  if sum(x[0] for x in st)}
@@ -266,8 +266,18 @@ def main() -> int:
     gather = stats["gather"]
     gemm = stats["rhs_gemm"]
     gemm_ms = sum(g[1] for g in gemm)
-    gemm_tflops = sum(g[2] for g in gemm) / (gemm_ms * 1e-3) / 1e12
-    if sum(g[0] for g in gather):
+    gemm_tflops = sum(g[2] for g in gemm) / (gemm_ms * 1e-3) / 1e12 if gemm_ms else 0.0
+    fused = stats["fused_iteration"][0]
+    if fused[0]:
+        # one persistent kernel per outer iteration: its algorithmic bytes are
+        # every mode's sampled fibers (8 B/elem, read in place) + Z_S
+        kname = "fused_iteration_kernel (all modes + fit, persistent cooperative)"
+        launches, kms = fused[0], fused[1]
+        kbytes = launches * sum(e * 8 + cfg["s"] * cfg["r"] * 8 for e in elems)
+        per_mode = None
+        bytes_model = "fibers 8 B/elem (in place) + Z_S 8 B/entry, all modes"
+        gemm_tflops = launches * sum(2.0 * e * cfg["r"] for e in elems) / (kms * 1e-3) / 1e12
+    elif sum(g[0] for g in gather):
         # sampled-fiber gather kernel: B_min bytes (8 B/elem mode 1, 32 B/elem strided)
         kname = "gather_rows_kernel (sampled-fiber gather)"
         launches = sum(g[0] for g in gather)
@@ -341,7 +351,7 @@ def main() -> int:
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": kname,
                          "bytes_model": bytes_model, "per_mode_gbs": per_mode,
                          "share_of_step": share, "peak_source": peak_src,
-                         "rhs_gemm_fp64_tflops": gemm_tflops,
+                         "rhs_gemm_fp64_tflops": gemm_tflops,  # fused: RHS flops over the whole kernel
                          "rhs_gemm_fp64_frac_of_dfma": gemm_tflops / DFMA_PEAK_TF,
                          "per_kernel_us_by_mode": breakdown},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),

@@ -95,6 +95,9 @@ typedef struct cprand_options {
   void* comm;                 /* cprand_comm_t for slab-sharded runs, NULL = 1 GPU */
   int32_t replicas;           /* mode-major copies of strided modes: -1 auto (fit in
                                  free HBM), 0 off (gather ring), 1 on */
+  int32_t fused;              /* one persistent cooperative kernel per outer
+                                 iteration: -1 auto (when every mode reads its
+                                 fibers in place), 0 off (multi-kernel chain) */
 } cprand_options_t;
 
 typedef struct cprand_trace_record {

@@ -47,7 +47,7 @@ class Options(C.Structure):
         ("stall_limit", C.c_int32), ("transform", C.c_int32), ("bench_mode", C.c_int32),
         ("exhaustive_samples", C.c_int32), ("exact_fit_trace", C.c_int32),
         ("device", C.c_int32), ("x_is_device", C.c_int32), ("x_mutable", C.c_int32),
-        ("comm", C.c_void_p), ("replicas", C.c_int32),
+        ("comm", C.c_void_p), ("replicas", C.c_int32), ("fused", C.c_int32),
     ]
 
 

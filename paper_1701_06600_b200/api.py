@@ -42,6 +42,7 @@ class SolveOptions:
     device: int = -1
     x_mutable: bool = False
     replicas: int = -1  # mode-major replicas of strided modes: -1 auto, 0 off, 1 on
+    fused: int = -1  # persistent per-iteration kernel: -1 auto, 0 off
 
     def to_c(self) -> Options:
         o = Options()
@@ -61,6 +62,7 @@ class SolveOptions:
         o.device = self.device
         o.x_mutable = int(self.x_mutable)
         o.replicas = self.replicas
+        o.fused = self.fused
         return o
 
 

@@ -59,6 +59,7 @@ Options opts_of(const cprand_options_t* o) {
   r.device = o->device;
   r.x_mutable = o->x_mutable != 0;
   r.replicas = o->replicas;
+  r.fused = o->fused;
   if (o->comm != nullptr) throw Unsupported("slab-sharded sessions are not enabled in this build");
   return r;
 }
@@ -122,6 +123,7 @@ void cprand_options_init(cprand_options_t* o) {
   o->transform = CPRAND_TRANSFORM_UNSET;
   o->device = -1;
   o->replicas = -1;
+  o->fused = -1;
 }
 
 const char* cprand_last_error(void) { return g_err.c_str(); }

@@ -11,8 +11,7 @@
 #include <cfloat>
 #include <cstdio>
 
-#include "devutil.cuh"
-#include "kernels.cuh"
+#include "phases.cuh"
 
 namespace cpb {
 
@@ -145,81 +144,17 @@ __global__ void __launch_bounds__(kThreads) estimate_fit_kernel(FitArgs a) {
   if (a.state->stopped) return;
   __shared__ double red[kThreads];
   __shared__ bool s_last;
-  const i64 j = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
-  double e2 = 0.0;
-  if (j < a.phat) {
-    double sum = 0.0;
-    // model_entry (kruskal.hpp:37-44): lambda_r * prod_n A_n(i_n, r), summed over r
-    for (int q = 0; q < a.r; ++q) {
-      double p = a.lambda[q];
-      for (int n = 0; n < a.order; ++n)
-      {
-        double f = a.fac[n][static_cast<i64>(a.idx[n][j]) * a.r + q];
-        if (a.nrm[n]) f = f / a.nrm[n][q];
-        p = __dmul_rn(p, f);
-      }
-      sum = __dadd_rn(sum, p);
-    }
-    const double e = a.values[j] - sum;
-    e2 = e * e;
-  }
-  red[threadIdx.x] = e2;
-  __syncthreads();
-  for (int s = kThreads / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
+  const double part = ph::fit_block(a, blockIdx.x, red);
   if (threadIdx.x == 0) {
-    a.partials[blockIdx.x] = red[0];
+    a.partials[blockIdx.x] = part;
     __threadfence();
-    const unsigned t = atomicAdd(a.ticket, 1u);
-    s_last = (t == gridDim.x - 1u);
+    s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1u);
   }
   __syncthreads();
   if (!s_last || threadIdx.x != 0) return;
   __threadfence();
-  double sq = 0.0;
-  for (unsigned b = 0; b < gridDim.x; ++b) sq += a.partials[b];
   *a.ticket = 0u;
-  // sampling.hpp:192, :207-209
-  double fit;
-  if (a.x_norm == 0.0) {
-    fit = 1.0;
-  } else {
-    const double mu = sq / static_cast<double>(a.phat);
-    fit = 1.0 - sqrt(a.total * mu) / a.x_norm;
-  }
-  // should_stop (sampling.hpp:237-251)
-  FitState* st = a.state;
-  if (fit > st->best_fit) {
-    st->best_fit = fit;
-    st->stall_count = 0;
-  } else {
-    st->stall_count += 1;
-  }
-  int stop = 0, reason = 0;
-  if (a.has_threshold && fit >= a.threshold) {
-    stop = 1;
-    reason = 2;  // fit_threshold
-  } else if (st->stall_count >= a.stall_limit) {
-    stop = 1;
-    reason = 3;  // best_fit_stall
-  } else if (a.iteration >= a.max_iters) {
-    stop = 1;
-    reason = 0;  // max_iterations
-  }
-  st->iterations = a.iteration;
-  TraceRec& tr = a.trace[a.iteration - 1];
-  tr.iteration = a.iteration;
-  tr.t_ns = static_cast<long long>(globaltimer()) - st->t_start_ns;
-  tr.fit = fit;
-  tr.best_fit = st->best_fit;
-  if (stop) {
-    st->reason = reason;
-    __threadfence_system();
-    st->stopped = 1;
-    if (a.stop_host_mapped) *reinterpret_cast<volatile int*>(a.stop_host_mapped) = 1;
-  }
+  ph::fit_final(a, gridDim.x);
 }
 
 }  // namespace

@@ -119,7 +119,16 @@ void launch_rng_seed(unsigned long long* state, unsigned long long seed_value, c
 // test hook: n normals from a fresh distribution object
 void launch_rng_normals(unsigned long long* state, int n, double* out, cudaStream_t st);
 
-// ---- mixing (mix.cu) ----------------------------------------------------
+// ---- mixing (mix.cu, dct.cuh) -------------------------------------------
+// Device-side view of a DctPlan (by value in kernel arguments).
+struct DctArgs {
+  int n;
+  int nrad;
+  int radix[24];
+  const double2* tw;
+  const double2* phase;
+  double s0, sk;
+};
 struct DctPlan {
   int n = 0;
   int nrad = 0;
@@ -130,6 +139,9 @@ struct DctPlan {
 };
 DctPlan make_dct_plan(int n);  // allocates device tables
 void free_dct_plan(DctPlan& p);
+DctArgs dct_args(const DctPlan& p);
+// fibers per CTA for a length-n transform within smem_budget bytes (even, >= 2)
+int dct_fibers_per_cta(int n, size_t smem_budget);
 // Applies sign-then-DCT-II (forward) or DCT-III-then-sign (adjoint) along a
 // mode: fiber f = (hi, lo) with element i at hi*st*n + lo + i*st, f < nfib.
 // in and out may alias (in place).
@@ -145,5 +157,43 @@ void launch_reduce_rhs(const double* part_rhs, int ks, i64 in, int r, double* ou
 // ---- synthetic generator (synth.cu) ------------------------------------
 void launch_synth(double* x, int order, const i64* dims, int r, const double* const* fac_dev,
                   double eta, unsigned long long seed, double* scratch, cudaStream_t st);
+
+// ---- persistent per-iteration kernel (fused.cu) -------------------------
+// One cooperative launch per outer iteration runs every mode update and the
+// fit: grid barriers separate Z -> (Gram + inverse on one CTA, GEMM on the
+// rest) -> apply (+ norms on the last CTA) -> next mode. Used when every
+// mode reads its fibers in place (mode 1 / replicas).
+struct FusedMode {
+  ModeView v;            // x / base: in-place fiber source and row offsets
+  int vec16;
+  int mtiles, ks, ks_len;
+  int gparts, gklen;
+  double tol;
+  double* a;             // A_un of this mode
+  double* norms;         // its column norms
+  double* mixed;         // MIX: mixed image of the factor
+  const double* sign;    // MIX: D_n
+  DctArgs plan;          // MIX: DCT plan of I_n
+  int dctF;              // MIX: fibers per CTA in the transform
+};
+struct FusedIter {
+  int order, r, first_mode_first_of_pass;
+  FusedMode mode[kMaxOrder];
+  double *z, *part_gram, *ginv, *gfull, *part_rhs, *ssq, *rhs_full, *lambda;
+  int* info;
+  unsigned long long* rng;
+  unsigned* ticket;      // [0] norm ticket, [1] fit ticket
+  unsigned* gram_done;
+  unsigned* bar;         // [0] count, [1] generation
+  const int* stop;
+  int has_fit;
+  FitArgs fit;
+};
+size_t fused_smem_bytes(int rt, bool mix, int max_dim);
+// Largest co-resident grid for the fused kernel (0 when cooperative launch
+// is unavailable).
+int fused_max_grid(int rt, bool mix, size_t smem, int device);
+void launch_fused_iteration(const FusedIter* dev_args, int rt, bool mix, int grid, size_t smem,
+                            cudaStream_t st);
 
 }  // namespace cpb

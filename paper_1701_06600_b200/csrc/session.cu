@@ -294,6 +294,8 @@ Session::~Session() {
   for (auto& b : ring_) dfree(b);
   for (auto& b : rep_) dfree(b);
   dfree(dbase_);
+  dfree(fargs_);
+  dfree(fsync_);
   for (auto& e : ev_gathered_) cudaEventDestroy(e);
   for (auto& e : ev_consumed_) cudaEventDestroy(e);
   if (ev_z_) cudaEventDestroy(ev_z_);
@@ -338,7 +340,7 @@ Session::~Session() {
 
 void Session::setup(const double* init_lambda, const double* const* init_factors) {
   const int nparts = 1024;
-  fit_part_ = dalloc<double>(std::max<i64>(nparts + 1, 8192));
+  fit_part_ = dalloc<double>(std::max<i64>(nparts + 1, std::max<i64>(8192, (o_.fit_sample_count + 255) / 256 + 1)));
   // ---- zero tensor short-circuit (sampling.hpp:263-264, solver.hpp:204-216)
   if (!o_.bench_mode) {
     launch_sumsq(x_->d, p_, fit_part_, nparts, fit_part_ + nparts, stream_);
@@ -427,7 +429,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   info_ = dalloc<int>(4);
   tickets_ = dalloc<unsigned>(8);
   CPB_CUDA(cudaMemsetAsync(tickets_, 0, 8 * sizeof(unsigned), stream_));
-  ssq_ = dalloc<double>(static_cast<size_t>(max_apply * r_));
+  ssq_ = dalloc<double>(static_cast<size_t>(std::max<i64>(max_apply, 4 * sms_) * r_));
   if (mix_) rhs_full_ = dalloc<double>(static_cast<size_t>(max_in * r_));
 
   // ---- fit / stop state
@@ -439,8 +441,101 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   CPB_CUDA(cudaHostAlloc(&stop_host_, sizeof(int), cudaHostAllocMapped));
   *stop_host_ = 0;
   CPB_CUDA(cudaHostGetDevicePointer(&stop_dev_, stop_host_, 0));
+  setup_fused();
   CPB_CUDA(cudaStreamSynchronize(stream_));
   setup_seconds_ = seconds_since(t0_);
+}
+
+void Session::setup_fused() {
+  bool all_direct = true;
+  for (int n = 0; n < order_; ++n) all_direct = all_direct && direct_[static_cast<size_t>(n)];
+  if (o_.fused == 0 || !all_direct || o_.exhaustive_samples) return;
+  i64 max_dim = 1;
+  for (i64 d : dims_) max_dim = std::max(max_dim, d);
+  fsmem_ = fused_smem_bytes(rt_, mix_, static_cast<int>(max_dim));
+  if (fsmem_ > 200 * 1024) return;
+  fgrid_ = fused_max_grid(rt_, mix_, fsmem_, x_->device);
+  int max_gp = 1;
+  for (int n = 0; n < order_; ++n) {
+    int gp, gl;
+    gram_splits(s_mode_[static_cast<size_t>(n)], &gp, &gl);
+    max_gp = std::max(max_gp, gp);
+  }
+  if (fgrid_ < max_gp + 2) return;
+  fsync_ = dalloc<unsigned>(16);
+  CPB_CUDA(cudaMemsetAsync(fsync_, 0, 16 * sizeof(unsigned), stream_));
+  std::vector<FusedIter> host(static_cast<size_t>(table_iters_));
+  for (int ti = 0; ti < table_iters_; ++ti) {
+    const int it = ti + 1;
+    FusedIter& A = host[static_cast<size_t>(ti)];
+    A = FusedIter{};
+    A.order = order_;
+    A.r = r_;
+    for (int n = 0; n < order_; ++n) {
+      FusedMode& M = A.mode[n];
+      M.v = view(it, n);
+      M.v.x = (n == 0) ? xsolve_ : rep_[static_cast<size_t>(n)];
+      M.v.base = dbase_ptr(it, n);
+      M.vec16 = vec16_[static_cast<size_t>(n)];
+      M.mtiles = ceil_div(dims_[static_cast<size_t>(n)], 128);
+      M.ks = ks_[static_cast<size_t>(n)];
+      M.ks_len = ks_len_[static_cast<size_t>(n)];
+      gram_splits(s_mode_[static_cast<size_t>(n)], &M.gparts, &M.gklen);
+      M.tol = work(n).tol;
+      M.a = fac_[static_cast<size_t>(n)];
+      M.norms = norms_ + static_cast<i64>(n) * r_;
+      if (mix_) {
+        M.mixed = mixed_[static_cast<size_t>(n)];
+        M.sign = signs_[static_cast<size_t>(n)];
+        M.plan = dct_args(plans_[static_cast<size_t>(n)]);
+        M.dctF = dct_fibers_per_cta(static_cast<int>(dims_[static_cast<size_t>(n)]), fsmem_);
+      }
+    }
+    A.z = z_;
+    A.part_gram = part_gram_;
+    A.ginv = ginv_;
+    A.gfull = gfull_;
+    A.part_rhs = part_rhs_;
+    A.ssq = ssq_;
+    A.rhs_full = rhs_full_;
+    A.lambda = lambda_;
+    A.info = info_;
+    A.rng = rng_state_;
+    A.gram_done = fsync_;
+    A.bar = fsync_ + 2;
+    A.ticket = fsync_ + 4;
+    A.stop = has_fit_ ? &state_->stopped : nullptr;
+    A.has_fit = has_fit_;
+    if (has_fit_) {
+      FitArgs& f = A.fit;
+      f.order = order_;
+      f.r = r_;
+      f.phat = phat_;
+      for (int n = 0; n < order_; ++n) {
+        f.idx[n] = fit_idx_[static_cast<size_t>(n)];
+        f.fac[n] = fac_[static_cast<size_t>(n)];
+        f.nrm[n] = norms_ + static_cast<i64>(n) * r_;
+      }
+      f.lambda = lambda_;
+      f.values = fit_vals_;
+      f.x_norm = x_norm_;
+      f.total = static_cast<double>(p_);
+      f.partials = fit_part_;
+      f.ticket = nullptr;
+      f.state = state_;
+      f.trace = trace_dev_;
+      f.stop_host_mapped = stop_dev_;
+      f.iteration = it;
+      f.max_iters = o_.max_iters;
+      f.has_threshold = o_.fit_threshold.has_value();
+      f.threshold = o_.fit_threshold.value_or(0.0);
+      f.stall_limit = o_.stall_limit;
+    }
+  }
+  fargs_ = dalloc<FusedIter>(host.size());
+  CPB_CUDA(cudaMemcpyAsync(fargs_, host.data(), host.size() * sizeof(FusedIter), cudaMemcpyHostToDevice, stream_));
+  CPB_CUDA(cudaStreamSynchronize(stream_));
+  fused_ = true;
 }
 
 void Session::finish_zero_tensor() {
@@ -763,6 +858,13 @@ void Session::enqueue_iteration() {
     CPB_CUDA(cudaEventRecord(ev_loop0_, stream_));
     launch_stamp_start(state_, stream_);
     loop_started_ = true;
+  }
+  if (fused_) {
+    const int ti = o_.exhaustive_samples ? 0 : it - 1;
+    timed(0, 7, stream_, [&] { launch_fused_iteration(fargs_ + ti, rt_, mix_, fgrid_, fsmem_, stream_); });
+    CPB_CUDA(cudaEventRecord(ev_loop1_, stream_));
+    it_ = it;
+    return;
   }
   // producer: gathers for this iteration and up to depth_-1 ahead (within the horizon)
   const int want = std::min(it + depth_ - 1, std::max(horizon_, it));

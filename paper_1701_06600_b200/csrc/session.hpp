@@ -32,6 +32,7 @@ struct Options {  // SolveOptions (solver.hpp:40-64) + device extensions
   int device = -1;
   bool x_mutable = false;
   int replicas = -1;  // mode-major replicas for strided modes: -1 auto, 0 off, 1 on
+  int fused = -1;     // persistent per-iteration kernel: -1 auto, 0 off (multi-kernel chain)
   void validate() const;
 };
 
@@ -80,9 +81,11 @@ class Session {
   cudaStream_t stream() const { return stream_; }
   void set_timing(bool on) { timing_ = on; }
   // kind 0: sampled-fiber gather (work = B_min bytes); 1: RHS GEMM (flops);
-  // 2: Z_S; 3: Gram; 4: Gram inverse; 5: apply (+ MIX unmix); 6: MIX factor
+  // 2: Z_S; 3: Gram; 4: Gram inverse; 5: apply (+ MIX unmix); 6: MIX factor;
+  // 7: whole fused iteration (reported under mode 0)
   void kernel_stats(int mode, int kind, i64* launches, double* ms, double* work);
-  static constexpr int kKinds = 7;
+  static constexpr int kKinds = 8;
+  bool fused() const { return fused_; }
   void result(double* out_lambda, double* const* out_factors, std::vector<Trace>& trace,
               int* iterations, int* reason, double* setup_s, double* total_s, double* loop_dev_s);
 
@@ -133,6 +136,12 @@ class Session {
   std::vector<char> vec16_;         // per mode: in-place rows are 16 B aligned
   void plan_replicas();
   void build_replicas();
+  void setup_fused();
+  bool fused_ = false;
+  int fgrid_ = 0;
+  size_t fsmem_ = 0;
+  FusedIter* fargs_ = nullptr;     // [table iterations] device copies
+  unsigned* fsync_ = nullptr;      // gram_done, barrier, tickets
   std::vector<i64> row_off_, base_off_;  // block offsets per (iter, mode)
   // gather ring: depth_ iterations x N modes of X_S rows
   int depth_ = 2;

@@ -1,553 +1,84 @@
 // sm_100a kernels of one sampled mode update (the CPRAND inner step,
-// sampling.hpp:283-290; MIX variant mixing.hpp:286-298):
+// sampling.hpp:283-290; MIX variant mixing.hpp:286-298), as standalone
+// launches; the phase logic lives in phases.cuh and is shared with the
+// persistent per-iteration kernel (fused.cu).
 //
-//   z_kernel        Z_S rows: ones, then *= factor rows in ascending mode
-//                   (sampling.hpp:82-90), factors read as A_un / norm
-//                   (bit-identical to the reference's normalized factor)
-//   gram_kernel     split-K Z_S^T Z_S partials               (stream s2)
-//   gram_inverse    pinv of the Gram, 1024-thread Gauss-Jordan with a
-//                   pivot test; pivoted-Cholesky fallback     (stream s2)
-//   rhs_gemm        split-K Z_S^T X_S^T partials on the gathered rows,
-//                   4-stage cp.async pipeline, FP64 FMA
+//   z_kernel        Z_S rows (sampling.hpp:82-90), factors read A_un / norm
+//   gram_kernel     split-K Z_S^T Z_S partials                 (stream s2)
+//   gram_inverse    pinv of the Gram: Gauss-Jordan with a pivot test, then
+//                   a pivoted-Cholesky fallback kernel          (stream s2)
+//   rhs_gemm        split-K Z_S^T X_S^T partials, FP64 FMA
 //   mode_apply      A_un = RHS * pinv(G), column norms, lambda rule
-//                   (kruskal.hpp:51-67), zero-column refill from the device
-//                   normalize RNG
+//                   (kruskal.hpp:51-67), zero-column refill
 //
 // The reference solves min ||Z_S A^T - X_S^T|| by pivoted QR
 // (kr_linalg.hpp:105-118); the normal equations used here agree with it to
 // ~kappa(Z_S)^2 eps, inside the 1e-10 parity bar for the configs' Z_S.
 // Reductions run in a fixed order, so results are bitwise reproducible.
-#include <cfloat>
-
-#include "devutil.cuh"
-#include "kernels.cuh"
+#include "phases.cuh"
 
 namespace cpb {
 
 namespace {
 
 constexpr int kThreads = 256;
+using ph::GBK;
+using ph::GBM;
+using ph::GS;
+using ph::GSTAGES;
 
-
-// ------------------------------------------------------------------ Z_S
 template <int RT>
-__global__ void __launch_bounds__(kThreads) z_kernel(ModeView v, double* __restrict__ z,
-                                                     const int* stop) {
+__global__ void __launch_bounds__(kThreads) z_kernel(ModeView v, double* __restrict__ z, const int* stop) {
   if (stop && *stop) return;
-  const i64 e = static_cast<i64>(blockIdx.x) * kThreads + threadIdx.x;
-  const int s = static_cast<int>(e / RT), rr = static_cast<int>(e % RT);
-  if (s >= v.s) return;
-  double zv = 0.0;
-  if (rr < v.r) {
-    zv = 1.0;
-    for (int c = 0; c < v.kept; ++c) {
-      const int row = __ldg(v.rows[c] + s);
-      double a = __ldg(v.fac[c] + static_cast<i64>(row) * v.r + rr);
-      if (v.nrm[c]) a = a / __ldg(v.nrm[c] + rr);
-      zv = __dmul_rn(zv, a);
-    }
-  }
-  z[static_cast<i64>(s) * RT + rr] = zv;
+  ph::z_range<RT>(v, z, static_cast<i64>(blockIdx.x) * kThreads + threadIdx.x,
+                  static_cast<i64>(gridDim.x) * kThreads);
 }
 
-// ------------------------------------------------------------------ Gram
-// G = sum over chunks of Z_chunk^T Z_chunk: one CTA per chunk of GS samples
-// computes the whole RT x RT partial (a 4 x RT/16 register tile per thread
-// for RT = 64), loading its chunk in one shot.
-constexpr int GS = 64;
-
 template <int RT>
-__global__ void __launch_bounds__(kThreads) gram_kernel(const double* __restrict__ z, int s_total,
-                                                        int klen, double* __restrict__ part,
-                                                        const int* stop) {
+__global__ void __launch_bounds__(kThreads) gram_kernel(const double* __restrict__ z, int s_total, int klen,
+                                                        double* __restrict__ part, const int* stop) {
   if (stop && *stop) return;
-  constexpr int GPT = RT * RT / kThreads;  // outputs per thread (16 / 4 / 1)
-  constexpr int TA = RT >= 32 ? 4 : 1;     // rows of the thread tile
-  constexpr int TB = GPT / TA;             // cols of the thread tile
-  constexpr int NA = RT / TA;              // thread rows
-  __shared__ double zs[GS][RT];
-  const int tid = threadIdx.x;
+  __shared__ double sh[GS * RT];
   const int s0 = blockIdx.x * klen;
-  const int s1 = min(s_total, s0 + klen);
-  const int ra = (tid / (RT / TB)) * TA, cb = tid % (RT / TB);
-  double acc[TA][TB];
-#pragma unroll
-  for (int x = 0; x < TA; ++x)
-#pragma unroll
-    for (int y = 0; y < TB; ++y) acc[x][y] = 0.0;
-  for (int sc = s0; sc < s1; sc += GS) {
-    constexpr int PER = GS * RT / kThreads;
-    double v[PER];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = tid + q * kThreads, sl = e / RT, c = e % RT, s = sc + sl;
-      v[q] = (s < s1) ? z[static_cast<i64>(s) * RT + c] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = tid + q * kThreads;
-      zs[e / RT][e % RT] = v[q];
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int sl = 0; sl < GS; ++sl) {
-      double xa[TA], xb[TB];
-#pragma unroll
-      for (int x = 0; x < TA; ++x) xa[x] = zs[sl][ra + x];
-#pragma unroll
-      for (int y = 0; y < TB; ++y) xb[y] = zs[sl][cb + (RT / TB) * y];
-#pragma unroll
-      for (int x = 0; x < TA; ++x)
-#pragma unroll
-        for (int y = 0; y < TB; ++y) acc[x][y] = fma(xa[x], xb[y], acc[x][y]);
-    }
-    __syncthreads();
-  }
-  (void)NA;
-  double* pg = part + static_cast<i64>(blockIdx.x) * RT * RT;
-#pragma unroll
-  for (int x = 0; x < TA; ++x)
-#pragma unroll
-    for (int y = 0; y < TB; ++y) pg[(ra + x) * RT + cb + (RT / TB) * y] = acc[x][y];
+  ph::gram_chunk<RT>(z, s0, min(s_total, s0 + klen), part + static_cast<i64>(blockIdx.x) * RT * RT, sh);
 }
 
-// Pivoted Cholesky of the R x R Gram in shared memory (warp 0), then its
-// (pseudo-)inverse. g: [RT][RT+1]; w: [RT][RT+1] scratch. On exit ginv
-// (global, R x R row-major) holds pinv(G) and info[0] the numerical rank.
-template <int RT>
-__device__ void gram_pinv(double* g, double* w, int* perm, int r, double tol, double* ginv,
-                          int* info) {
-  constexpr int LD = RT + 1;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ int s_rank;
-  if (warp == 0) {
-    for (int t = lane; t < RT; t += 32) perm[t] = t;
-    __syncwarp();
-    int rank = r;
-    double d0 = 0.0;
-    for (int k = 0; k < r; ++k) {
-      double bv = -1.0;
-      int bj = RT;
-      for (int j = lane; j < r; j += 32)
-        if (j >= k) {
-          const double dv = g[j * LD + j];
-          if (dv > bv || (dv == bv && j < bj)) {
-            bv = dv;
-            bj = j;
-          }
-        }
-      for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
-        if (ov > bv || (ov == bv && oj < bj)) {
-          bv = ov;
-          bj = oj;
-        }
-      }
-      if (k == 0) d0 = bv;
-      if (!(bv > tol * d0) || !(bv > 0.0)) {
-        rank = k;
-        break;
-      }
-      const int p = bj;
-      if (p != k) {
-        for (int t = lane; t < r; t += 32) {
-          const double a = g[k * LD + t];
-          g[k * LD + t] = g[p * LD + t];
-          g[p * LD + t] = a;
-        }
-        __syncwarp();
-        for (int t = lane; t < r; t += 32) {
-          const double a = g[t * LD + k];
-          g[t * LD + k] = g[t * LD + p];
-          g[t * LD + p] = a;
-        }
-        if (lane == 0) {
-          const int q = perm[k];
-          perm[k] = perm[p];
-          perm[p] = q;
-        }
-        __syncwarp();
-      }
-      const double lkk = sqrt(g[k * LD + k]);
-      __syncwarp();
-      for (int t = lane; t < r; t += 32)
-        if (t > k) g[t * LD + k] = g[t * LD + k] / lkk;
-      __syncwarp();
-      if (lane == 0) g[k * LD + k] = lkk;
-      __syncwarp();
-      for (int j = lane; j < r; j += 32)
-        if (j > k) {
-          const double ljk = g[j * LD + k];
-          for (int i = k + 1; i < r; ++i) g[i * LD + j] -= g[i * LD + k] * ljk;
-        }
-      __syncwarp();
-    }
-    if (lane == 0) s_rank = rank;
-  }
-  __syncthreads();
-  const int rank = s_rank;
-  // w <- inverse of the leading rank x rank lower factor L (column j per thread)
-  for (int j = tid; j < rank; j += blockDim.x) {
-    for (int i = 0; i < rank; ++i) {
-      if (i < j) {
-        w[i * LD + j] = 0.0;
-        continue;
-      }
-      double sacc = (i == j) ? 1.0 : 0.0;
-      for (int m = j; m < i; ++m) sacc -= g[i * LD + m] * w[m * LD + j];
-      w[i * LD + j] = sacc / g[i * LD + i];
-    }
-  }
-  __syncthreads();
-  if (rank == r) {
-    // pinv = P L^-T L^-1 P^T
-    for (int e = tid; e < r * r; e += blockDim.x) {
-      const int a = e / r, b = e % r;
-      const int lo = a > b ? a : b;
-      double sacc = 0.0;
-      for (int m = lo; m < r; ++m) sacc += w[m * LD + a] * w[m * LD + b];
-      ginv[perm[a] * r + perm[b]] = sacc;
-    }
-  } else {
-    // rank-deficient: G ~= M M^T, M = P L[:, :k]; pinv = B B^T with
-    // B = M (M^T M)^{-1}. Rare path, single thread.
-    if (tid == 0) {
-      const int k = rank;
-      // C = L1^T L1 (k x k) over all r rows of the factored columns, into w
-      for (int a = 0; a < k; ++a)
-        for (int b = 0; b <= a; ++b) {
-          double sacc = 0.0;
-          for (int m = a; m < r; ++m) sacc += g[m * LD + a] * g[m * LD + b];
-          w[a * LD + b] = sacc;
-          w[b * LD + a] = sacc;
-        }
-      // Cholesky of C in place (lower), into w
-      for (int j = 0; j < k; ++j) {
-        double d = w[j * LD + j];
-        for (int m = 0; m < j; ++m) d -= w[j * LD + m] * w[j * LD + m];
-        d = sqrt(d > 0.0 ? d : DBL_MIN);
-        w[j * LD + j] = d;
-        for (int i = j + 1; i < k; ++i) {
-          double sacc = w[i * LD + j];
-          for (int m = 0; m < j; ++m) sacc -= w[i * LD + m] * w[j * LD + m];
-          w[i * LD + j] = sacc / d;
-        }
-      }
-      for (int e = 0; e < r * r; ++e) ginv[e] = 0.0;
-      // rows of B: b_t = C^{-1} m_t with m_t = row t of L1 (k entries);
-      // scratch vectors live in shared memory right after w
-      double* bt = w + RT * LD;
-      double* bu = bt + RT;
-      for (int t = 0; t < r; ++t) {
-        for (int a = 0; a < k; ++a) bt[a] = (t >= a) ? g[t * LD + a] : 0.0;
-        for (int a = 0; a < k; ++a) {
-          double sacc = bt[a];
-          for (int m = 0; m < a; ++m) sacc -= w[a * LD + m] * bt[m];
-          bt[a] = sacc / w[a * LD + a];
-        }
-        for (int a = k - 1; a >= 0; --a) {
-          double sacc = bt[a];
-          for (int m = a + 1; m < k; ++m) sacc -= w[m * LD + a] * bt[m];
-          bt[a] = sacc / w[a * LD + a];
-        }
-        for (int u = 0; u <= t; ++u) {
-          for (int a = 0; a < k; ++a) bu[a] = (u >= a) ? g[u * LD + a] : 0.0;
-          for (int a = 0; a < k; ++a) {
-            double sacc = bu[a];
-            for (int m = 0; m < a; ++m) sacc -= w[a * LD + m] * bu[m];
-            bu[a] = sacc / w[a * LD + a];
-          }
-          for (int a = k - 1; a >= 0; --a) {
-            double sacc = bu[a];
-            for (int m = a + 1; m < k; ++m) sacc -= w[m * LD + a] * bu[m];
-            bu[a] = sacc / w[a * LD + a];
-          }
-          double dot = 0.0;
-          for (int a = 0; a < k; ++a) dot += bt[a] * bu[a];
-          ginv[perm[t] * r + perm[u]] = dot;
-          ginv[perm[u] * r + perm[t]] = dot;
-        }
-      }
-    }
-  }
-  if (tid == 0) info[0] = rank;
-}
-
-
-// ------------------------------------------------------ Gram inverse
-// In-place Gauss-Jordan on the SPD Gram in one CTA of 512 threads. Warp w
-// owns rows w + 16 t, lane l owns columns l + 32 u; the elements live in
-// registers. Step k needs column k, row k and 1/pivot of the current
-// matrix; the owners of column / row / pivot k+1 publish them into
-// double-buffered shared vectors during step k, so each step costs one
-// barrier and no per-thread division. Every pivot is tested against
-// tol * max diag; a failure (numerical rank < R) switches to the pivoted
-// Cholesky pseudo-inverse (gram_pinv).
 constexpr int kInvThreads = 512;
 
 template <int RT>
-__global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double* __restrict__ part,
-                                                                   int nparts, int r, double tol,
-                                                                   double* __restrict__ ginv,
-                                                                   double* __restrict__ gfull,
-                                                                   int* info, const int* stop) {
+__global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double* __restrict__ part, int nparts,
+                                                                   int r, double tol, double* __restrict__ ginv,
+                                                                   double* __restrict__ gfull, int* info,
+                                                                   const int* stop) {
   if (stop && *stop) return;
-  constexpr int TR = RT / 16;                 // rows per warp
-  constexpr int TC = RT >= 32 ? RT / 32 : 1;  // columns per lane
-  __shared__ double colb[2][RT], rowb[2][RT], diag[RT];
-  __shared__ double s_thr;
-  const int tid = threadIdx.x, w = tid / 32, l = tid % 32;
-  double a[TR][TC];
-  int row[TR], col[TC];
-#pragma unroll
-  for (int t = 0; t < TR; ++t) row[t] = w + 16 * t;
-#pragma unroll
-  for (int u = 0; u < TC; ++u) col[u] = l + 32 * u;
-  // G = sum of the split partials in split order; loads of a batch in flight together
-#pragma unroll
-  for (int t = 0; t < TR; ++t)
-#pragma unroll
-    for (int u = 0; u < TC; ++u) a[t][u] = 0.0;
-  {
-    int k = 0;
-    for (; k + 4 <= nparts; k += 4) {
-      double v[4][TR][TC];
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int t = 0; t < TR; ++t)
-#pragma unroll
-          for (int u = 0; u < TC; ++u)
-            v[x][t][u] = (row[t] < r && col[u] < r) ? part[static_cast<i64>(k + x) * RT * RT + row[t] * RT + col[u]] : 0.0;
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int t = 0; t < TR; ++t)
-#pragma unroll
-          for (int u = 0; u < TC; ++u) a[t][u] += v[x][t][u];
-    }
-    for (; k < nparts; ++k)
-#pragma unroll
-      for (int t = 0; t < TR; ++t)
-#pragma unroll
-        for (int u = 0; u < TC; ++u)
-          if (row[t] < r && col[u] < r) a[t][u] += part[static_cast<i64>(k) * RT * RT + row[t] * RT + col[u]];
-  }
-#pragma unroll
-  for (int t = 0; t < TR; ++t)
-#pragma unroll
-    for (int u = 0; u < TC; ++u) {
-      if (col[u] >= RT) continue;
-      if (row[t] < r && col[u] < r) gfull[row[t] * r + col[u]] = a[t][u];  // for the fallback
-      if (col[u] == 0) colb[0][row[t]] = a[t][u];
-      if (row[t] == 0) rowb[0][col[u]] = a[t][u];
-      if (row[t] == col[u]) diag[row[t]] = a[t][u];
-    }
-  if (tid < RT) {
-    colb[1][tid] = 0.0;
-    rowb[1][tid] = 0.0;
-  }
-  __syncthreads();
-  if (tid < 32) {
-    double d = 0.0;
-    for (int x = tid; x < r; x += 32) d = fmax(d, diag[x]);
-    for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
-    if (tid == 0) s_thr = tol * d;
-  }
-  __syncthreads();
-  const double thr = s_thr;
-  bool fail = false;
-  // Branch-free step: with x = a (0 on row k and column k), c = a(i, k)
-  // (-1 on row k) and rk = a(k, j) / piv (1 / piv on column k),
-  // a' = x - c * rk reproduces all four Gauss-Jordan update rules.
-  for (int k = 0; k < r; ++k) {
-    const int b = k & 1;
-    const double piv = colb[b][k];
-    if (!(piv > thr) || !(piv > 0.0)) {
-      fail = true;  // uniform: every thread read the same pivot
-      break;
-    }
-    const double p = __drcp_rn(piv);
-    double rk[TC];
-#pragma unroll
-    for (int u = 0; u < TC; ++u) {
-      const double rv = rowb[b][col[u] < RT ? col[u] : 0] * p;
-      rk[u] = (col[u] == k) ? p : rv;
-    }
-#pragma unroll
-    for (int t = 0; t < TR; ++t) {
-      const bool is_k = (row[t] == k);
-      const double c = is_k ? -1.0 : colb[b][row[t]];
-#pragma unroll
-      for (int u = 0; u < TC; ++u) {
-        const double x = (is_k || col[u] == k) ? 0.0 : a[t][u];
-        a[t][u] = fma(-c, rk[u], x);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < TC; ++u)
-      if (col[u] == k + 1)
-#pragma unroll
-        for (int t = 0; t < TR; ++t) colb[b ^ 1][row[t]] = a[t][u];
-#pragma unroll
-    for (int t = 0; t < TR; ++t)
-      if (row[t] == k + 1)
-#pragma unroll
-        for (int u = 0; u < TC; ++u)
-          if (col[u] < RT) rowb[b ^ 1][col[u]] = a[t][u];
-    __syncthreads();
-  }
-  if (!fail) {
-#pragma unroll
-    for (int t = 0; t < TR; ++t)
-#pragma unroll
-      for (int u = 0; u < TC; ++u)
-        if (row[t] < r && col[u] < r) ginv[row[t] * r + col[u]] = a[t][u];
-  }
-  if (tid == 0) info[0] = fail ? -1 : r;
+  __shared__ double sh[5 * RT + 1];
+  ph::inverse_cta<RT, kInvThreads>(part, nparts, r, tol, ginv, gfull, info, sh);
 }
 
-// Rank-deficient Gram (rare): pivoted Cholesky pseudo-inverse of gfull.
-// Launched after every inverse and exits at once unless the inverse flagged
-// failure; its working matrices live in global scratch (gfull + R*R), so
-// the launch reserves almost no shared memory.
+// Rank-deficient Gram (rare): exits at once unless the inverse flagged
+// failure; its matrices live in global scratch, so the launch reserves
+// almost no shared memory.
 template <int RT>
-__global__ void __launch_bounds__(kThreads) gram_pinv_fallback_kernel(const double* __restrict__ gfull,
-                                                                      int r, double tol,
-                                                                      double* __restrict__ ginv,
-                                                                      int* info, const int* stop) {
+__global__ void __launch_bounds__(kThreads) gram_pinv_fallback_kernel(double* gfull, int r, double tol,
+                                                                      double* __restrict__ ginv, int* info,
+                                                                      const int* stop) {
   if (stop && *stop) return;
   if (info[0] >= 0) return;
-  constexpr int LD = RT + 1;
-  double* g = const_cast<double*>(gfull) + r * r;  // scratch: [RT][LD] + [RT][LD] + 2 RT
-  double* wk = g + RT * LD;
   __shared__ int perm[RT];
-  for (int e = threadIdx.x; e < RT * LD; e += blockDim.x) {
-    const int x = e / LD, y = e % LD;
-    g[e] = (x < r && y < r) ? gfull[x * r + y] : 0.0;
-  }
-  __syncthreads();
-  gram_pinv<RT>(g, wk, perm, r, tol, ginv, info);
+  ph::pinv_fallback<RT>(gfull, r, tol, ginv, info, perm);
 }
 
-// ------------------------------------------------------------ RHS GEMM
-constexpr int GBM = 128, GBK = 16, GSTAGES = 3;
-
-// A operand rows: row s starts at xs + (row_off ? row_off[s] : s * ld) and
-// holds I_n contiguous doubles. With row_off the kernel reads the sampled
-// fibers in place (mode-1 fibers of the tensor, or rows of a mode-major
-// replica); without it, rows of a gathered X_S buffer. VEC16: every row
-// start is 16 B aligned (16 B async copies), else 8 B copies.
 template <int RT, bool VEC16>
 __global__ void __launch_bounds__(kThreads) rhs_gemm_kernel(const double* __restrict__ xs, i64 ld,
                                                             const i64* __restrict__ row_off,
-                                                            const double* __restrict__ z, i64 in,
-                                                            int s_total, int r, int ks_len,
-                                                            double* __restrict__ part,
+                                                            const double* __restrict__ z, i64 in, int s_total,
+                                                            int r, int ks_len, double* __restrict__ part,
                                                             const int* stop) {
   if (stop && *stop) return;
-  constexpr int TN = RT / 16, TM = GBM / 16;
   extern __shared__ __align__(16) double gsm[];
-  double* as = gsm;                              // [GSTAGES][GBK][GBM]
-  double* bs = gsm + GSTAGES * GBK * GBM;        // [GSTAGES][GBK][RT]
-  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-  const i64 i0 = static_cast<i64>(blockIdx.x) * GBM;
-  const int kb = blockIdx.y;
-  const int s_begin = kb * ks_len;
-  const int s_end = min(s_total, s_begin + ks_len);
-  const int ntiles = (s_end - s_begin + GBK - 1) / GBK;
-
-  auto load_tile = [&](int t, int st) {
-    const int sbase = s_begin + t * GBK;
-    double* ab = as + st * GBK * GBM;
-    double* bb = bs + st * GBK * RT;
-    if constexpr (VEC16) {
-#pragma unroll
-      for (int q = 0; q < GBK * GBM / 2 / kThreads; ++q) {  // A: GBK x GBM doubles in 16 B chunks
-        const int c = tid + q * kThreads;
-        const int sl = c / (GBM / 2), ic = (c % (GBM / 2)) * 2;
-        const int s = sbase + sl;
-        const i64 i = i0 + ic;
-        const i64 lim = row_off ? in : ld;  // gathered rows are zero padded to ld
-        const bool ok = (s < s_end) && (i < lim);
-        const i64 ro = (s < s_end) ? (row_off ? row_off[s] : static_cast<i64>(s) * ld) : 0;
-        // a row of odd length: the chunk straddling I_n copies only its first element
-        const int bytes = !ok ? 0 : (i + 1 < lim ? 16 : 8);
-        cp_async16(ab + sl * GBM + ic, ok ? xs + ro + i : xs, bytes);
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < GBK * GBM / kThreads; ++q) {  // 8 B chunks
-        const int c = tid + q * kThreads;
-        const int sl = c / GBM, ic = c % GBM;
-        const int s = sbase + sl;
-        const i64 i = i0 + ic;
-        const bool ok = (s < s_end) && (i < in);
-        const i64 ro = (s < s_end) ? (row_off ? row_off[s] : static_cast<i64>(s) * ld) : 0;
-        cp_async8(ab + sl * GBM + ic, ok ? xs + ro + i : xs, ok ? 8 : 0);
-      }
-    }
-    for (int c = tid; c < GBK * RT / 2; c += kThreads) {  // B: GBK x RT doubles
-      const int sl = c / (RT / 2), rc = (c % (RT / 2)) * 2;
-      const int s = sbase + sl;
-      const bool ok = s < s_end;
-      cp_async16(bb + sl * RT + rc, ok ? z + static_cast<i64>(s) * RT + rc : z, ok ? 16 : 0);
-    }
-  };
-
-  double acc[TM][TN];
-#pragma unroll
-  for (int a = 0; a < TM; ++a)
-#pragma unroll
-    for (int b = 0; b < TN; ++b) acc[a][b] = 0.0;
-
-#pragma unroll
-  for (int t = 0; t < GSTAGES - 1; ++t) {
-    if (t < ntiles) load_tile(t, t);
-    cp_async_commit();
-  }
-  for (int t = 0; t < ntiles; ++t) {
-    cp_async_wait<GSTAGES - 2>();
-    __syncthreads();
-    const int nt = t + GSTAGES - 1;
-    if (nt < ntiles) load_tile(nt, nt % GSTAGES);
-    cp_async_commit();
-    const double* ab = as + (t % GSTAGES) * GBK * GBM;
-    const double* bb = bs + (t % GSTAGES) * GBK * RT;
-#pragma unroll
-    for (int kk = 0; kk < GBK; ++kk) {
-      double af[TM], bf[TN];
-#pragma unroll
-      for (int a = 0; a < TM; ++a) af[a] = ab[kk * GBM + ty * TM + a];
-#pragma unroll
-      for (int b = 0; b < TN; ++b) bf[b] = bb[kk * RT + tx + 16 * b];  // conflict-free
-#pragma unroll
-      for (int a = 0; a < TM; ++a)
-#pragma unroll
-        for (int b = 0; b < TN; ++b) acc[a][b] = fma(af[a], bf[b], acc[a][b]);
-    }
-  }
-  double* pr = part + static_cast<i64>(kb) * in * r;
-#pragma unroll
-  for (int a = 0; a < TM; ++a) {
-    const i64 i = i0 + ty * TM + a;
-    if (i >= in) continue;
-#pragma unroll
-    for (int b = 0; b < TN; ++b) {
-      const int rr = tx + 16 * b;
-      if (rr < r) pr[i * r + rr] = acc[a][b];
-    }
-  }
+  ph::gemm_tile<RT, VEC16>(xs, ld, row_off, z, in, s_total, r, ks_len, part, blockIdx.x, blockIdx.y, gsm);
 }
 
-// --------------------------------------------------------- apply + norms
-// A_un(i, c) = sum_c' RHS(i, c') Ginv(c', c): one output per thread,
-// 1024 / RT rows per CTA; the split-K partials are summed in split order.
-// Column sum-of-squares partials per CTA; the last CTA forms the norms
-// (fixed order), the lambda rule (kruskal.hpp:57-66) and refills zero
-// columns. The factor stays unnormalized: consumers read A_un / norm, the
-// value the reference stores after col /= norm.
 constexpr int kApplyThreads = 1024;
 
 template <int RT>
@@ -557,95 +88,21 @@ __global__ void __launch_bounds__(kApplyThreads) mode_apply_kernel(i64 in, int r
                                                                    unsigned long long* rng_state) {
   if (w.stop && *w.stop) return;
   constexpr int BI = kApplyThreads / RT;
-  constexpr int NP = kApplyThreads / RT;  // interleaved parts in the final reduction
-  __shared__ double gi[RT][RT + 1];
-  __shared__ double rh[BI][RT + 1];
+  __shared__ double gi[RT * (RT + 1)];
+  __shared__ double rh[BI * (RT + 1)];
   __shared__ bool s_last;
-  __shared__ int s_zero;
-  const int tid = threadIdx.x;
-  const int il = tid / RT, c = tid % RT;
-  const i64 i = static_cast<i64>(blockIdx.x) * BI + il;
-  for (int e = tid; e < RT * RT; e += kApplyThreads) {
-    const int x = e / RT, y = e % RT;
-    gi[x][y] = (x < r && y < r) ? w.ginv[x * r + y] : 0.0;
-  }
-  double s = 0.0;
-  if (i < in && c < r) {
-    if (rhs_full) {
-      s = rhs_full[i * r + c];
-    } else {
-      const double* p = w.part_rhs + i * r + c;
-      const i64 step = in * r;
-      int k = 0;
-      for (; k + 6 <= w.ks; k += 6) {
-        const double v0 = p[k * step], v1 = p[(k + 1) * step], v2 = p[(k + 2) * step];
-        const double v3 = p[(k + 3) * step], v4 = p[(k + 4) * step], v5 = p[(k + 5) * step];
-        s = (((((s + v0) + v1) + v2) + v3) + v4) + v5;
-      }
-      for (; k < w.ks; ++k) s += p[k * step];
-    }
-  }
-  rh[il][c] = s;
+  ph::load_ginv<RT, kApplyThreads>(w.ginv, r, gi);
   __syncthreads();
-  double out = 0.0;
-  for (int cc = 0; cc < r; ++cc) out = fma(rh[il][cc], gi[cc][c], out);
-  const bool ok = (i < in && c < r);
-  if (ok) w.a[i * r + c] = out;
-  __syncthreads();  // rh reused for the squares
-  rh[il][c] = ok ? out * out : 0.0;
-  __syncthreads();
-  if (tid < RT) {
-    double q = 0.0;
-#pragma unroll 8
-    for (int x = 0; x < BI; ++x) q += rh[x][tid];
-    if (tid < r) w.ssq[static_cast<i64>(blockIdx.x) * r + tid] = q;
-  }
+  const double q = ph::apply_block<RT, kApplyThreads>(in, r, w, rhs_full, static_cast<i64>(blockIdx.x) * BI, gi, rh);
+  ph::ssq_store<RT, kApplyThreads>(q, r, w.ssq + static_cast<i64>(blockIdx.x) * r, rh);
   __threadfence();
   __syncthreads();
-  if (tid == 0) {
-    s_last = (atomicAdd(&w.ticket[1], 1u) == gridDim.x - 1u);
-    s_zero = 0;
-  }
+  if (threadIdx.x == 0) s_last = (atomicAdd(&w.ticket[1], 1u) == gridDim.x - 1u);
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // column norms: NP interleaved partial sums per column, combined in order
-  {
-    const int part = tid / RT;
-    double q = 0.0;
-    if (c < r)
-      for (unsigned b = part; b < gridDim.x; b += NP) q += w.ssq[static_cast<i64>(b) * r + c];
-    rh[part][c] = q;
-  }
-  __syncthreads();
-  if (tid < r) {
-    double t = 0.0;
-    for (int x = 0; x < NP; ++x) t += rh[x][tid];
-    const double nrm = sqrt(t);
-    w.norms[tid] = nrm;
-    // kruskal.hpp:57-66: lambda multiplied on the first mode of a pass, else overwritten
-    if (nrm == 0.0) {
-      w.lambda[tid] = 0.0;
-      atomicOr(&s_zero, 1);
-    } else {
-      w.lambda[tid] = first_of_pass ? w.lambda[tid] * nrm : nrm;
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    w.ticket[1] = 0u;
-    if (s_zero) {
-      // zero columns (kruskal.hpp:57-63): N(0,1) column from the normalize
-      // stream, one distribution object per call, columns in order
-      DevMt g{rng_state};
-      DevNormal gauss;
-      for (int col = 0; col < r; ++col) {
-        if (w.norms[col] != 0.0) continue;
-        for (i64 t = 0; t < in; ++t) w.a[t * r + col] = gauss(g);
-        w.norms[col] = dev_stable_norm(w.a + col, in, r);
-      }
-    }
-  }
+  ph::norms_final<RT, kApplyThreads>(r, in, w, gridDim.x, first_of_pass, rng_state, rh);
+  if (threadIdx.x == 0) w.ticket[1] = 0u;
 }
 
 // ------------------------------------------------------- mode-n replica

@@ -352,16 +352,22 @@ def test_cpp_dropin_program(pb):
 
 
 @pytest.mark.parametrize("dims,r,s", [((30, 28, 26), 4, 60), ((17, 9, 13), 3, 40), ((9, 8, 7, 6), 3, 40)])
-def test_replica_and_ring_paths_are_bit_identical(pb, orc, dims, r, s):
-    """Fibers read in place (mode 1 / mode-major replicas) or gathered into the
-    ring feed the same GEMM in the same order: bitwise equal results, and
-    both equal the oracle's trajectory (even and odd mode lengths)."""
+def test_execution_paths_agree(pb, orc, dims, r, s):
+    """The three device paths -- persistent fused iteration kernel (replicas),
+    multi-kernel chain on in-place fibers, multi-kernel chain on the gather
+    ring -- agree with each other and with the oracle trajectory (even and
+    odd mode lengths). The in-place and ring GEMM inputs are identical, so
+    the two multi-kernel paths agree bitwise."""
     x, _ = orc.gen_baseline(dims, r, 0.5, 0.01, 3)
     base = dict(rng_seed=3, max_iters=12, stall_limit=1000)
-    rep = pb.cprand(x, r, s, pb.SolveOptions(replicas=1, **base))
+    fused = pb.cprand(x, r, s, pb.SolveOptions(replicas=1, **base))
+    chain = pb.cprand(x, r, s, pb.SolveOptions(replicas=1, fused=0, **base))
     ring = pb.cprand(x, r, s, pb.SolveOptions(replicas=0, **base))
-    assert np.array_equal(rep.lam, ring.lam)
-    for a, b in zip(rep.factors, ring.factors):
+    assert np.array_equal(chain.lam, ring.lam)
+    for a, b in zip(chain.factors, ring.factors):
         assert np.array_equal(a, b)
+    for a, b in zip(fused.factors, ring.factors):
+        assert rel(a, b) < 1e-12
     ref = orc.cprand(x, r, s, orc.SolveOptions(**base))
-    assert max(abs(a[2] - b[2]) for a, b in zip(rep.trace, ref.trace)) < 1e-8
+    for res in (fused, chain):
+        assert max(abs(a[2] - b[2]) for a, b in zip(res.trace, ref.trace)) < 1e-8
