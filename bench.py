@@ -260,8 +260,8 @@ def main() -> int:
     n_modes = len(cfg["dims"])
     kinds = ["gather", "rhs_gemm", "z", "gram", "gram_inverse", "apply", "mix_factor", "fused_iteration"]
     stats = {k: [s.kernel_stats(m, i) for m in range(n_modes)] for i, k in enumerate(kinds)}
-    breakdown = {k: [round(x[1] / x[0] * 1e3, 2) for x in st] for k, st in stats.items()
-                 if sum(x[0] for x in st)}
+    breakdown = {k: [round(x[1] / x[0] * 1e3, 2) if x[0] else None for x in st]
+                 for k, st in stats.items() if sum(x[0] for x in st)}
     elems = [cfg["s"] * d for d in cfg["dims"]]
     gather = stats["gather"]
     gemm = stats["rhs_gemm"]
