@@ -258,6 +258,7 @@ def main() -> int:
     s.enqueue(timing_iters)
     s.sync()
     n_modes = len(cfg["dims"])
+    phases = s.phase_us()
     kinds = ["gather", "rhs_gemm", "z", "gram", "gram_inverse", "apply", "mix_factor", "fused_iteration"]
     stats = {k: [s.kernel_stats(m, i) for m in range(n_modes)] for i, k in enumerate(kinds)}
     breakdown = {k: [round(x[1] / x[0] * 1e3, 2) if x[0] else None for x in st]
@@ -353,7 +354,10 @@ def main() -> int:
                          "share_of_step": share, "peak_source": peak_src,
                          "rhs_gemm_fp64_tflops": gemm_tflops,  # fused: RHS flops over the whole kernel
                          "rhs_gemm_fp64_frac_of_dfma": gemm_tflops / DFMA_PEAK_TF,
-                         "per_kernel_us_by_mode": breakdown},
+                         "per_kernel_us_by_mode": breakdown,
+                         "fused_phase_us_per_mode": dict(zip(
+                             ["z", "z_barrier", "phaseB_cta0", "B_barrier", "apply", "apply_barrier",
+                              "inverse_done_after_z_barrier"], [round(x, 2) for x in phases])) if phases else None},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches_per_iter(cfg) * args.steps,
         }

@@ -250,6 +250,12 @@ class Session:
                                                 C.byref(b)))
         return n.value, ms.value, b.value
 
+    def phase_us(self) -> list:
+        out = (C.c_double * 16)()
+        n = C.c_int32()
+        check(lib().cprand_session_phase_us(self.h, out, 16, C.byref(n)))
+        return [out[i] for i in range(min(n.value, 16))]
+
     def result(self) -> SolveResult:
         lam = np.empty(self.r, dtype=np.float64)
         fs = [np.empty((d, self.r), dtype=np.float64, order="F") for d in self.dims]

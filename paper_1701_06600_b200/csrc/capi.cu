@@ -273,6 +273,14 @@ int cprand_session_kernel_stats(cprand_session_t s, int32_t mode, int32_t kind, 
   });
 }
 
+int cprand_session_phase_us(cprand_session_t s, double* out, int32_t cap, int32_t* n) {
+  return guarded([&] {
+    const auto v = s->s->phase_us();
+    *n = static_cast<int32_t>(v.size());
+    for (size_t i = 0; i < v.size() && static_cast<int32_t>(i) < cap; ++i) out[i] = v[i];
+  });
+}
+
 int cprand_session_result(cprand_session_t s, double* out_lambda, double* const* out_factors,
                           cprand_trace_record_t* trace, int32_t trace_cap, cprand_result_t* res) {
   return guarded([&] { fill_result(*s->s, out_lambda, out_factors, trace, trace_cap, res); });

@@ -76,12 +76,18 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
   const unsigned G = gridDim.x, b = blockIdx.x;
   const int tid = threadIdx.x;
   const int r = A.r;
+  auto stamp = [&](int n, int k) {
+    if (A.phase_t && b == 0 && tid == 0) A.phase_t[n * 8 + k] = globaltimer();
+  };
   for (int n = 0; n < A.order; ++n) {
     const FusedMode& M = A.mode[n];
     const ModeWork w = work_of(A, M);
+    stamp(n, 0);
     // ---- Z_S
     ph::z_range<RT>(M.v, A.z, static_cast<i64>(b) * kFusedThreads + tid, static_cast<i64>(G) * kFusedThreads);
+    stamp(n, 1);
     grid_sync(A.bar);
+    stamp(n, 2);
     // ---- Gram + inverse (last CTA) beside the split-K GEMM (all others)
     if (b == G - 1) {
       if (tid == 0)
@@ -91,6 +97,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
       const bool fail = ph::inverse_cta<RT, kFusedThreads>(A.part_gram, M.gparts, r, M.tol, A.ginv, A.gfull, A.info, fsm);
       if (fail) ph::pinv_fallback<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
       if (tid == 0) *A.gram_done = 0u;
+      if (A.phase_t && tid == 0) A.phase_t[n * 8 + 7] = globaltimer();  // inverse done
     } else {
       if (static_cast<int>(b) < M.gparts) {
         const int s0 = b * M.gklen;
@@ -109,7 +116,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
                                    t / M.mtiles, fsm);
       }
     }
+    stamp(n, 3);
     grid_sync(A.bar);
+    stamp(n, 4);
     const double* rhs = nullptr;
     if constexpr (MIX) {
       // unmix the summed RHS along I_n (linear, so equal to unmixing each fiber)
@@ -148,7 +157,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
         if (tid == 0) A.ticket[0] = 0u;
       }
     }
+    stamp(n, 5);
     grid_sync(A.bar);
+    stamp(n, 6);
     if constexpr (MIX) {
       for (int g = b; g * M.dctF < r; g += G)
         dct::transform_group(M.plan, M.a, M.mixed, r, r, static_cast<i64>(g) * M.dctF, M.dctF, M.sign, 1, M.norms,

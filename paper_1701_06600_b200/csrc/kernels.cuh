@@ -188,6 +188,7 @@ struct FusedIter {
   const int* stop;
   int has_fit;
   FitArgs fit;
+  unsigned long long* phase_t;  // optional: CTA 0 stamps globaltimer at phase edges [order][8]
 };
 size_t fused_smem_bytes(int rt, bool mix, int max_dim);
 // Largest co-resident grid for the fused kernel (0 when cooperative launch

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <cstddef>
 #include <unordered_set>
 
 namespace cpb {
@@ -295,6 +296,7 @@ Session::~Session() {
   for (auto& b : rep_) dfree(b);
   dfree(dbase_);
   dfree(fargs_);
+  dfree(phase_t_);
   dfree(fsync_);
   for (auto& e : ev_gathered_) cudaEventDestroy(e);
   for (auto& e : ev_consumed_) cudaEventDestroy(e);
@@ -861,7 +863,27 @@ void Session::enqueue_iteration() {
   }
   if (fused_) {
     const int ti = o_.exhaustive_samples ? 0 : it - 1;
+    if (timing_ && !phase_t_) {
+      phase_t_ = dalloc<unsigned long long>(static_cast<size_t>(order_ * 8));
+      for (int t = 0; t < table_iters_; ++t)  // point every iteration's args at the stamp buffer
+        CPB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(fargs_ + t) + offsetof(FusedIter, phase_t), &phase_t_,
+                                 sizeof(phase_t_), cudaMemcpyHostToDevice, stream_));
+    }
     timed(0, 7, stream_, [&] { launch_fused_iteration(fargs_ + ti, rt_, mix_, fgrid_, fsmem_, stream_); });
+    if (timing_) {
+      // collect this launch's phase stamps (timing mode only: synchronizes)
+      std::vector<unsigned long long> t(static_cast<size_t>(order_ * 8));
+      CPB_CUDA(cudaMemcpyAsync(t.data(), phase_t_, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               stream_));
+      CPB_CUDA(cudaStreamSynchronize(stream_));
+      if (phase_acc_.empty()) phase_acc_.assign(7, 0.0);
+      for (int n = 0; n < order_; ++n) {
+        const unsigned long long* q = t.data() + n * 8;
+        for (int k = 0; k < 6; ++k) phase_acc_[static_cast<size_t>(k)] += 1e-3 * static_cast<double>(q[k + 1] - q[k]) / order_;
+        phase_acc_[6] += 1e-3 * static_cast<double>(q[7] - q[2]) / order_;
+      }
+      ++phase_acc_n_;
+    }
     CPB_CUDA(cudaEventRecord(ev_loop1_, stream_));
     it_ = it;
     return;

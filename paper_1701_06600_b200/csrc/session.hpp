@@ -142,6 +142,14 @@ class Session {
   size_t fsmem_ = 0;
   FusedIter* fargs_ = nullptr;     // [table iterations] device copies
   unsigned* fsync_ = nullptr;      // gram_done, barrier, tickets
+  unsigned long long* phase_t_ = nullptr;  // fused phase timestamps [order][8] (timing mode)
+ public:
+  // fused path: mean per-mode phase durations (us) over the timed launches:
+  // z, z-barrier, phaseB(gemm CTA 0), B-barrier, apply, apply-barrier, inverse-done
+  std::vector<double> phase_us() const { return phase_acc_n_ ? phase_acc_ : std::vector<double>(); }
+ private:
+  std::vector<double> phase_acc_;
+  int phase_acc_n_ = 0;
   std::vector<i64> row_off_, base_off_;  // block offsets per (iter, mode)
   // gather ring: depth_ iterations x N modes of X_S rows
   int depth_ = 2;
