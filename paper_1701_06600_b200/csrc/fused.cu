@@ -207,7 +207,7 @@ size_t fused_smem_bytes(int rt, bool mix, int max_dim) {
   size_t need = static_cast<size_t>(ph::GSTAGES * ph::GBK * (ph::GBM + rt)) * sizeof(double);
   need = std::max(need, static_cast<size_t>(ph::GS * rt) * sizeof(double));
   need = std::max(need, static_cast<size_t>(rt * (rt + 1) + (kFusedThreads / rt) * (rt + 1)) * sizeof(double));
-  need = std::max(need, static_cast<size_t>(5 * rt + 1) * sizeof(double));
+  need = std::max(need, static_cast<size_t>(16 * rt + 40) * sizeof(double));
   need = std::max(need, static_cast<size_t>(256) * sizeof(double));
   if (mix) need = std::max(need, static_cast<size_t>(2) * 16 * static_cast<size_t>(max_dim));
   return need;

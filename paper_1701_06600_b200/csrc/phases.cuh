@@ -267,16 +267,18 @@ __device__ void pinv_fallback(double* gfull, int r, double tol, double* ginv, in
 }
 
 // ------------------------------------------------------ Gram inverse
-// In-place Gauss-Jordan on the SPD Gram by one CTA of NTH threads. Warp w
-// owns rows w + W t, lane l owns columns l + 32 u, elements in registers.
-// Step k needs column k and row k of the current matrix; their owners
-// publish column/row k+1 into double-buffered shared vectors during step
-// k: one barrier per step. Branch-free update: with x = a (0 on row and
-// column k), c = a(i,k) (-1 on row k), rk = a(k,j)/piv (1/piv on column
-// k), a' = x - c rk covers all four Gauss-Jordan rules. Every pivot is
-// tested against tol * max diag; returns true (uniformly) on failure, after
-// writing the reduced Gram to gfull for the pivoted fallback.
-// sh: 5 RT + 1 doubles.
+// In-place block Gauss-Jordan (4 x 4 pivot blocks, no pivoting: the Gram
+// is SPD) by one CTA of NTH threads. Warp w owns rows w + W t, lane l owns
+// columns l + 32 u; elements live in registers. The matrix is padded to a
+// multiple of 4 with d_max on the padding diagonal. Step s (K = [4s,4s+4)):
+// with P^-1 the inverse of the current pivot block, X = a with rows and
+// columns K zeroed, C(i) = a(i,K) (-e on rows K) and M(j) = P^-1 a(K,j)
+// (column j - 4s of P^-1 on columns K), a' = X - C M covers all four
+// Gauss-Jordan block rules with 4 FMAs per element. The owners of the next
+// block's rows/columns publish them (double-buffered); thread 0 inverts the
+// next pivot block (scalar pivots tested against tol * d_max). Returns true
+// (uniformly) on failure, after writing the reduced Gram to gfull for the
+// pivoted fallback. sh: 16 RT + 40 doubles.
 template <int RT, int NTH>
 __device__ bool inverse_cta(const double* __restrict__ part, int nparts, int r, double tol,
                             double* __restrict__ ginv, double* __restrict__ gfull, int* info,
@@ -284,11 +286,12 @@ __device__ bool inverse_cta(const double* __restrict__ part, int nparts, int r, 
   constexpr int W = NTH / 32;
   constexpr int TR = RT / W > 0 ? RT / W : 1;  // rows per warp
   constexpr int TC = RT >= 32 ? RT / 32 : 1;   // columns per lane
-  double* colb = sh;            // [2][RT]
-  double* rowb = sh + 2 * RT;   // [2][RT]
-  double* diag = sh + 4 * RT;   // [RT]
-  double* sthr = sh + 5 * RT;   // [1]
+  double* colB = sh;              // [2][RT][4]  column block of the next step
+  double* rowB = sh + 8 * RT;     // [2][4][RT]  row block of the next step
+  double* pinv = sh + 16 * RT;    // [2][16]
+  double* misc = pinv + 32;       // [0] d_max, [1] thr, [2..3] fail flags
   const int tid = threadIdx.x, w = tid / 32, l = tid % 32;
+  const int r4 = (r + 3) & ~3;
   double a[TR][TC];
   int row[TR], col[TC];
 #pragma unroll
@@ -325,67 +328,113 @@ __device__ bool inverse_cta(const double* __restrict__ part, int nparts, int r, 
         for (int u = 0; u < TC; ++u)
           if (row[t] < r && col[u] < r) a[t][u] += part[static_cast<i64>(k) * RT * RT + row[t] * RT + col[u]];
   }
+  // d_max for the threshold and the padding diagonal
+  if (tid == 0) misc[0] = 0.0;
+  __syncthreads();
 #pragma unroll
   for (int t = 0; t < TR; ++t)
 #pragma unroll
     for (int u = 0; u < TC; ++u) {
-      if (col[u] >= RT || row[t] >= RT) continue;
       if (row[t] < r && col[u] < r) gfull[row[t] * r + col[u]] = a[t][u];
-      if (col[u] == 0) colb[row[t]] = a[t][u];
-      if (row[t] == 0) rowb[col[u]] = a[t][u];
-      if (row[t] == col[u]) diag[row[t]] = a[t][u];
+      if (row[t] == col[u] && row[t] < r)
+        atomicMax(reinterpret_cast<unsigned long long*>(misc), __double_as_longlong(fmax(a[t][u], 0.0)));
     }
-  if (tid < RT) {
-    colb[RT + tid] = 0.0;
-    rowb[RT + tid] = 0.0;
-  }
   __syncthreads();
-  if (tid < 32) {
-    double d = 0.0;
-    for (int x = tid; x < r; x += 32) d = fmax(d, diag[x]);
-    for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
-    if (tid == 0) sthr[0] = tol * d;
-  }
-  __syncthreads();
-  const double thr = sthr[0];
-  bool fail = false;
-  for (int k = 0; k < r; ++k) {
-    const int b = (k & 1) * RT, nb = RT - b;
-    const double piv = colb[b + k];
-    if (!(piv > thr) || !(piv > 0.0)) {
-      fail = true;  // uniform: every thread read the same pivot
-      break;
-    }
-    const double p = __drcp_rn(piv);
-    double rk[TC];
+  const double dmax = misc[0];
+  const double thr = tol * dmax;
+#pragma unroll
+  for (int t = 0; t < TR; ++t)
 #pragma unroll
     for (int u = 0; u < TC; ++u) {
-      const double rv = rowb[b + (col[u] < RT ? col[u] : 0)] * p;
-      rk[u] = (col[u] == k) ? p : rv;
+      if (row[t] >= r && row[t] < r4 && row[t] == col[u]) a[t][u] = dmax;  // padding diagonal
+      if (row[t] < 4 && col[u] < RT) rowB[row[t] * RT + col[u]] = a[t][u];
+      if (col[u] < 4 && row[t] < RT) colB[row[t] * 4 + col[u]] = a[t][u];
     }
+  __syncthreads();
+  auto invert_block = [&](const double* cb, int k0, double* out, double* failp) {
+    // unpivoted 4 x 4 Gauss-Jordan of rows/cols K of the current matrix
+    double p[4][4];
+    for (int x = 0; x < 4; ++x)
+      for (int y = 0; y < 4; ++y) p[x][y] = cb[(k0 + x) * 4 + y];
+    bool bad = false;
+    for (int k = 0; k < 4; ++k) {
+      const double piv = p[k][k];
+      if (!(piv > thr) || !(piv > 0.0)) bad = true;
+      const double q = 1.0 / piv;
+      double rk[4], ck[4];
+      for (int y = 0; y < 4; ++y) rk[y] = (y == k) ? q : p[k][y] * q;
+      for (int x = 0; x < 4; ++x) ck[x] = (x == k) ? -1.0 : p[x][k];
+      for (int x = 0; x < 4; ++x)
+        for (int y = 0; y < 4; ++y) {
+          const double xv = (x == k || y == k) ? 0.0 : p[x][y];
+          p[x][y] = fma(-ck[x], rk[y], xv);
+        }
+    }
+    for (int x = 0; x < 4; ++x)
+      for (int y = 0; y < 4; ++y) out[x * 4 + y] = p[x][y];
+    *failp = bad ? 1.0 : 0.0;
+  };
+  if (tid == 0) invert_block(colB, 0, pinv, misc + 2);
+  __syncthreads();
+  bool fail = false;
+  for (int k0 = 0; k0 < r4; k0 += 4) {
+    const int b = (k0 >> 2) & 1, nb = b ^ 1;
+    if (misc[2 + b] != 0.0) {
+      fail = true;  // uniform
+      break;
+    }
+    const double* P = pinv + 16 * b;
+    const double* cb = colB + b * RT * 4;
+    const double* rb = rowB + b * 4 * RT;
+    double m[TC][4];
 #pragma unroll
-    for (int t = 0; t < TR; ++t) {
-      const bool is_k = (row[t] == k);
-      const double c = is_k ? -1.0 : colb[b + (row[t] < RT ? row[t] : 0)];
+    for (int u = 0; u < TC; ++u) {
+      const int j = col[u];
+      const bool jk = (j >= k0 && j < k0 + 4);
+      double rv[4];
 #pragma unroll
-      for (int u = 0; u < TC; ++u) {
-        const double x = (is_k || col[u] == k) ? 0.0 : a[t][u];
-        a[t][u] = fma(-c, rk[u], x);
+      for (int q = 0; q < 4; ++q) rv[q] = rb[q * RT + (j < RT ? j : 0)];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const double mv = P[x * 4 + 0] * rv[0] + P[x * 4 + 1] * rv[1] + P[x * 4 + 2] * rv[2] + P[x * 4 + 3] * rv[3];
+        m[u][x] = jk ? P[x * 4 + (j - k0)] : mv;
       }
     }
 #pragma unroll
-    for (int u = 0; u < TC; ++u)
-      if (col[u] == k + 1)
+    for (int t = 0; t < TR; ++t) {
+      const int i = row[t];
+      const bool ik = (i >= k0 && i < k0 + 4);
+      double c[4];
 #pragma unroll
-        for (int t = 0; t < TR; ++t)
-          if (row[t] < RT) colb[nb + row[t]] = a[t][u];
+      for (int q = 0; q < 4; ++q) c[q] = ik ? (i - k0 == q ? -1.0 : 0.0) : cb[(i < RT ? i : 0) * 4 + q];
 #pragma unroll
-    for (int t = 0; t < TR; ++t)
-      if (row[t] == k + 1)
+      for (int u = 0; u < TC; ++u) {
+        const bool jk = (col[u] >= k0 && col[u] < k0 + 4);
+        double v = (ik || jk) ? 0.0 : a[t][u];
+        v = fma(-c[0], m[u][0], v);
+        v = fma(-c[1], m[u][1], v);
+        v = fma(-c[2], m[u][2], v);
+        v = fma(-c[3], m[u][3], v);
+        a[t][u] = v;
+      }
+    }
+    // publish the next step's row and column blocks
+    const int n0 = k0 + 4;
+    if (n0 < r4) {
 #pragma unroll
-        for (int u = 0; u < TC; ++u)
-          if (col[u] < RT) rowb[nb + col[u]] = a[t][u];
+      for (int t = 0; t < TR; ++t)
+#pragma unroll
+        for (int u = 0; u < TC; ++u) {
+          const int i = row[t], j = col[u];
+          if (j >= n0 && j < n0 + 4 && i < RT) colB[nb * RT * 4 + i * 4 + (j - n0)] = a[t][u];
+          if (i >= n0 && i < n0 + 4 && j < RT) rowB[nb * 4 * RT + (i - n0) * RT + j] = a[t][u];
+        }
+    }
     __syncthreads();
+    if (n0 < r4) {
+      if (tid == 0) invert_block(colB + nb * RT * 4, n0, pinv + 16 * nb, misc + 2 + nb);
+      __syncthreads();
+    }
   }
   if (!fail) {
 #pragma unroll

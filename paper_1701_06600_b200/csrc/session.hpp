@@ -146,7 +146,11 @@ class Session {
  public:
   // fused path: mean per-mode phase durations (us) over the timed launches:
   // z, z-barrier, phaseB(gemm CTA 0), B-barrier, apply, apply-barrier, inverse-done
-  std::vector<double> phase_us() const { return phase_acc_n_ ? phase_acc_ : std::vector<double>(); }
+  std::vector<double> phase_us() const {
+    std::vector<double> v = phase_acc_;
+    for (auto& x : v) x /= (phase_acc_n_ ? phase_acc_n_ : 1);
+    return v;
+  }
  private:
   std::vector<double> phase_acc_;
   int phase_acc_n_ = 0;

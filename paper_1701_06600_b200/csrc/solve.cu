@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kInvThreads) gram_inverse_kernel(const double*
                                                                    double* __restrict__ gfull, int* info,
                                                                    const int* stop) {
   if (stop && *stop) return;
-  __shared__ double sh[5 * RT + 1];
+  __shared__ double sh[16 * RT + 40];
   ph::inverse_cta<RT, kInvThreads>(part, nparts, r, tol, ginv, gfull, info, sh);
 }
 
