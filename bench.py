@@ -303,6 +303,7 @@ def main() -> int:
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get("traffic_bytes_per_launch")
+    fallbacks = s.gram_fallbacks()
     s.close()
 
     # ---- e2e through the public one-shot call with host buffers
@@ -356,8 +357,12 @@ def main() -> int:
                          "rhs_gemm_fp64_frac_of_dfma": gemm_tflops / DFMA_PEAK_TF,
                          "per_kernel_us_by_mode": breakdown,
                          "fused_phase_us_per_mode": dict(zip(
-                             ["z", "z_barrier", "phaseB_cta0", "B_barrier", "apply", "apply_barrier",
-                              "inverse_done_after_z_barrier"], [round(x, 2) for x in phases])) if phases else None},
+                             (["z", "z_barrier", "phaseB_cta0", "B_barrier", "apply", "apply_barrier",
+                               "inverse_done_after_z_barrier"] if cfg["method"] == "mix" else
+                              ["z_tile", "gram_blocks", "rhs_tiles", "apply_share", "ssq", "release",
+                               "inverse_done_after_mode_start"]),
+                             [round(x, 2) for x in phases])) if phases else None,
+                         "gram_fallbacks": fallbacks},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches_per_iter(cfg) * args.steps,
         }

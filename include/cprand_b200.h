@@ -173,6 +173,8 @@ int cprand_session_kernel_stats(cprand_session_t s, int32_t mode, int32_t kind, 
  * (z, z-barrier, phase B on CTA 0, B-barrier, apply, apply-barrier,
  * inverse completion after the Z barrier); *n = 0 when unavailable. */
 int cprand_session_phase_us(cprand_session_t s, double* out, int32_t cap, int32_t* n);
+/* Diagnostics: Gram solves that took the pivoted-Cholesky (min-norm) path. */
+int cprand_session_gram_fallbacks(cprand_session_t s, int64_t* out);
 int cprand_session_result(cprand_session_t s, double* out_lambda, double* const* out_factors,
                           cprand_trace_record_t* trace, int32_t trace_cap, cprand_result_t* res);
 void cprand_session_destroy(cprand_session_t s);

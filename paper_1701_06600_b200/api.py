@@ -256,6 +256,12 @@ class Session:
         check(lib().cprand_session_phase_us(self.h, out, 16, C.byref(n)))
         return [out[i] for i in range(min(n.value, 16))]
 
+    def gram_fallbacks(self) -> int:
+        """Gram solves so far that took the pivoted-Cholesky min-norm path."""
+        n = C.c_int64()
+        check(lib().cprand_session_gram_fallbacks(self.h, C.byref(n)))
+        return n.value
+
     def result(self) -> SolveResult:
         lam = np.empty(self.r, dtype=np.float64)
         fs = [np.empty((d, self.r), dtype=np.float64, order="F") for d in self.dims]

@@ -17,6 +17,10 @@ namespace {
 
 thread_local std::string g_err;
 
+void need(const void* h) {
+  if (!h) throw InvalidArgument("null (or destroyed) handle");
+}
+
 template <class F>
 int guarded(F&& f) {
   try {
@@ -184,6 +188,7 @@ int cprand_tensor_create(const int64_t* dims, int32_t order, int32_t device, cpr
 
 int cprand_tensor_upload(cprand_tensor_t t, const double* host) {
   return guarded([&] {
+    need(t);
     CPB_CUDA(cudaSetDevice(t->t->device));
     CPB_CUDA(cudaMemcpy(t->t->d, host, sizeof(double) * t->t->p, cudaMemcpyHostToDevice));
   });
@@ -191,6 +196,7 @@ int cprand_tensor_upload(cprand_tensor_t t, const double* host) {
 
 int cprand_tensor_download(cprand_tensor_t t, double* host) {
   return guarded([&] {
+    need(t);
     CPB_CUDA(cudaSetDevice(t->t->device));
     CPB_CUDA(cudaMemcpy(host, t->t->d, sizeof(double) * t->t->p, cudaMemcpyDeviceToHost));
   });
@@ -199,6 +205,7 @@ int cprand_tensor_download(cprand_tensor_t t, double* host) {
 int cprand_tensor_synth(cprand_tensor_t t, int64_t r, double c, double eta, uint64_t seed,
                         double* const* out_factors) {
   return guarded([&] {
+    need(t);
     if (r < 1) throw InvalidArgument("rank must be >= 1");
     op_synth(t->t.get(), static_cast<int>(r), c, eta, seed, out_factors);
   });
@@ -227,21 +234,22 @@ int cprand_session_create(int32_t method, cprand_tensor_t t, int64_t r, int64_t 
 
 int cprand_session_run(cprand_session_t s, int32_t n, int32_t* ran) {
   return guarded([&] {
+    need(s);
     const int k = s->s->run(n);
     if (ran) *ran = k;
   });
 }
 
 int cprand_session_enqueue(cprand_session_t s, int32_t n) {
-  return guarded([&] { s->s->enqueue(n); });
+  return guarded([&] { need(s); s->s->enqueue(n); });
 }
 
 int cprand_session_sync(cprand_session_t s) {
-  return guarded([&] { s->s->sync(); });
+  return guarded([&] { need(s); s->s->sync(); });
 }
 
 int cprand_session_timed_enqueue(cprand_session_t s, int32_t n, double* ms) {
-  return guarded([&] { *ms = s->s->timed_enqueue(n); });
+  return guarded([&] { need(s); *ms = s->s->timed_enqueue(n); });
 }
 
 void* cprand_host_alloc_pinned(uint64_t bytes) {
@@ -261,12 +269,13 @@ void cprand_host_free_pinned(void* p) {
 void* cprand_session_stream(cprand_session_t s) { return s ? static_cast<void*>(s->s->stream()) : nullptr; }
 
 int cprand_session_set_kernel_timing(cprand_session_t s, int32_t on) {
-  return guarded([&] { s->s->set_timing(on != 0); });
+  return guarded([&] { need(s); s->s->set_timing(on != 0); });
 }
 
 int cprand_session_kernel_stats(cprand_session_t s, int32_t mode, int32_t kind, int64_t* launches,
                                 double* total_ms, double* work) {
   return guarded([&] {
+    need(s);
     i64 l = 0;
     s->s->kernel_stats(mode, kind, &l, total_ms, work);
     *launches = l;
@@ -275,15 +284,20 @@ int cprand_session_kernel_stats(cprand_session_t s, int32_t mode, int32_t kind, 
 
 int cprand_session_phase_us(cprand_session_t s, double* out, int32_t cap, int32_t* n) {
   return guarded([&] {
+    need(s);
     const auto v = s->s->phase_us();
     *n = static_cast<int32_t>(v.size());
     for (size_t i = 0; i < v.size() && static_cast<int32_t>(i) < cap; ++i) out[i] = v[i];
   });
 }
 
+int cprand_session_gram_fallbacks(cprand_session_t s, int64_t* out) {
+  return guarded([&] { need(s); *out = s->s->gram_fallbacks(); });
+}
+
 int cprand_session_result(cprand_session_t s, double* out_lambda, double* const* out_factors,
                           cprand_trace_record_t* trace, int32_t trace_cap, cprand_result_t* res) {
-  return guarded([&] { fill_result(*s->s, out_lambda, out_factors, trace, trace_cap, res); });
+  return guarded([&] { need(s); fill_result(*s->s, out_lambda, out_factors, trace, trace_cap, res); });
 }
 
 void cprand_session_destroy(cprand_session_t s) { delete s; }

@@ -18,6 +18,7 @@
 // kernels use (phases.cuh, dct.cuh), with the same reduction orders.
 #include "dct.cuh"
 #include "phases.cuh"
+#include "tile.cuh"
 
 namespace cpb {
 
@@ -188,20 +189,281 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
   }
 }
 
-template <int RT, bool MIX>
-void* fused_fn() {
-  return reinterpret_cast<void*>(&fused_iteration_kernel<RT, MIX>);
+// ---------------------------------------------------------------------------
+// CPRAND (no mixing): tile-owned mode updates, one grid-wide rendezvous per mode.
+//
+// CTAs [0, G-1) own (64-row block mt, sample split kb) tiles; CTA G-1 owns the
+// Gram inverse. Per mode n, with no grid barrier between the phases:
+//   tile CTA   Z_S rows of split kb -> shared memory (z_tile)
+//              Gram blocks q = mt (mod tm) of split kb -> gpart; the last of
+//              the tk splits to arrive sums block q into gsum (both triangles)
+//              RHS partial (mt, kb) -> part_rhs, then arrive mt_cnt[mt]
+//   inverse    waits for every Gram block, block Gauss-Jordan -> ginv, flag
+//   tile CTA   waits mt_cnt[mt] == tk, sums its share of the rows of mt over
+//              the splits, waits for ginv, A_un rows = RHS * Ginv, column
+//              sums of squares
+//   all        ticket; the last CTA forms norms + lambda (kruskal.hpp:51-67)
+//              and releases the next mode (sense-reversing generation).
+// Counters of mode n are reset by CTA 0 during mode n+1, when no CTA can
+// still be waiting on them.
+template <int RT>
+__global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const FusedIter* __restrict__ args) {
+  using namespace tl;
+  const FusedIter& A = *args;
+  if (A.stop && *A.stop) return;  // uniform: the flag only changes in a previous launch
+  extern __shared__ __align__(16) double fsm[];
+  __shared__ int perm[RT];
+  __shared__ unsigned s_old;
+  __shared__ int s_lastq[64];
+  __shared__ int s_nlast;
+  __shared__ bool s_last;
+  const unsigned G = gridDim.x, b = blockIdx.x;
+  const unsigned Gw = G - 1;
+  const int tid = threadIdx.x;
+  const int r = A.r;
+  const int nfr = (r + 7) / 8;
+  auto stamp = [&](int n, int k) {
+    if (A.phase_t && b == 0 && tid == 0) A.phase_t[n * 8 + k] = globaltimer();
+  };
+  for (int n = 0; n < A.order; ++n) {
+    const FusedMode& M = A.mode[n];
+    const ModeWork w = work_of(A, M);
+    const i64 in = M.v.in;
+    stamp(n, 0);
+    if (b == 0) {
+      const FusedMode& P = A.mode[(n + A.order - 1) % A.order];
+      for (int e = tid; e < P.tm; e += kFusedThreads) P.mt_cnt[e] = 0u;
+      for (int e = tid; e < P.tk; e += kFusedThreads) P.kb_cnt[e] = 0u;
+      if (tid < 64) P.gbt[tid] = 0u;
+      if (tid < 2) P.gready[tid] = 0u;
+    }
+    if (b == G - 1) {
+      // ---- Gram inverse (pivoted-Cholesky min-norm fallback when rank deficient)
+      wait_geq(M.gready, static_cast<unsigned>(M.nblk));
+      __threadfence();
+      const bool fail = ph::inverse_la<RT>(A.gsum, r, M.tol, A.ginv, A.gfull, A.info, fsm);
+      if (fail) ph::pinv_fallback<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
+      release_add(M.gready + 1, 1u, &s_old);
+      if (A.phase_t && tid == 0) A.phase_t[n * 8 + 7] = globaltimer();
+      if (tid < r) A.ssq[static_cast<i64>(b) * r + tid] = 0.0;
+    } else {
+      const int ntiles = M.tm * M.tk;
+      const TileSmem t = tile_smem<RT>(fsm, M.zcap);
+      // this CTA's share of every one of its splits' Z rows, then arrive
+      // (no waiting here, so CTAs with several tiles cannot deadlock)
+      for (int tt = b; tt < ntiles; tt += Gw) {
+        const int mt = tt % M.tm, kb = tt / M.tm;
+        const int s0 = kb * M.tklen;
+        const int cnt = min(M.v.s - s0, M.tklen);
+        const int zr = (cnt + M.tm - 1) / M.tm;
+        const int z0 = s0 + mt * zr, z1 = min(s0 + cnt, z0 + zr);
+        if (z0 < z1) z_share<RT>(M.v, z0, z1, A.z);
+        release_add(M.kb_cnt + kb, 1u, &s_old);
+      }
+      for (int tt = b; tt < ntiles; tt += Gw) {
+        const int mt = tt % M.tm, kb = tt / M.tm;
+        const int s0 = kb * M.tklen;
+        const int cnt = min(M.v.s - s0, M.tklen);
+        const int kpad = (cnt + BK - 1) / BK * BK;
+        wait_geq(M.kb_cnt + kb, static_cast<unsigned>(M.tm));
+        z_load<RT>(M.v, A.z, s0, cnt, kpad, t);
+        if (tt == static_cast<int>(b)) stamp(n, 1);
+        // Gram blocks q = mt, mt + tm, ... of this split; the last split to
+        // arrive on a block reduces it (fixed split order)
+        gram_blocks<RT>(t, kpad, nfr, mt, M.tm, kb, M.tk, A.gpart);
+        __syncthreads();
+        if (tid == 0) s_nlast = 0;
+        __syncthreads();
+        for (int q = mt + tid * M.tm; q < M.nblk; q += kFusedThreads * M.tm) {
+          __threadfence();
+          if (atomicAdd(M.gbt + q, 1u) == static_cast<unsigned>(M.tk - 1)) s_lastq[atomicAdd(&s_nlast, 1)] = q;
+        }
+        __syncthreads();
+        const int nl = s_nlast;
+        if (nl > 0) {
+          __threadfence();
+          for (int e = tid; e < nl * 64; e += kFusedThreads) {
+            const int q = s_lastq[e / 64], el = e % 64;
+            const double* src = A.gpart + static_cast<i64>(q) * M.tk * 64 + el;
+            double sum = 0.0;
+            for (int k = 0; k < M.tk; ++k) sum += __ldcg(src + k * 64);
+            int bi, bj;
+            gram_block_coords(q, nfr, &bi, &bj);
+            const int gi = bi * 8 + el / 8, gj = bj * 8 + el % 8;
+            A.gsum[gi * RT + gj] = sum;
+            A.gsum[gj * RT + gi] = sum;
+          }
+          release_add(M.gready, static_cast<unsigned>(nl), &s_old);
+        }
+        if (tt == static_cast<int>(b)) stamp(n, 2);
+        gemm_tile<RT>(M.v.x, M.vec16 != 0, in, static_cast<i64>(mt) * BM, r, cnt, kpad, t,
+                      A.part_rhs + static_cast<i64>(kb) * in * r);
+        release_add(M.mt_cnt + mt, 1u, &s_old);
+      }
+      stamp(n, 3);
+      // ---- apply: this CTA's share of the rows of each of its tiles
+      double q2 = 0.0;  // thread c < r: column sum of squares over this CTA's rows
+      constexpr int LD = RT + 1;
+      double* gi = fsm;             // RT x LD
+      double* rh = gi + RT * LD;    // rows_per x LD
+      const int rows_per = (BM + M.tk - 1) / M.tk;
+      double* ob = rh + rows_per * LD;
+      bool have_ginv = false;
+      for (int tt = b; tt < ntiles; tt += Gw) {
+        const int mt = tt % M.tm, kb = tt / M.tm;
+        const i64 r0 = static_cast<i64>(mt) * BM + static_cast<i64>(kb) * rows_per;
+        const i64 r1 = min(min(static_cast<i64>(mt) * BM + BM, in), r0 + rows_per);
+        if (r0 >= r1) continue;
+        const int nrow = static_cast<int>(r1 - r0);
+        wait_geq(M.mt_cnt + mt, static_cast<unsigned>(M.tk));
+        __threadfence();
+        const i64 step = in * r;
+        for (int e = tid; e < nrow * r; e += kFusedThreads) {
+          const int il = e / r, c = e - il * r;
+          const double* p = A.part_rhs + (r0 + il) * r + c;
+          double sum = 0.0;
+          int k = 0;
+          for (; k + 4 <= M.tk; k += 4) {
+            const double v0 = __ldcg(p + k * step), v1 = __ldcg(p + (k + 1) * step);
+            const double v2 = __ldcg(p + (k + 2) * step), v3 = __ldcg(p + (k + 3) * step);
+            sum = (((sum + v0) + v1) + v2) + v3;
+          }
+          for (; k < M.tk; ++k) sum += __ldcg(p + k * step);
+          rh[il * LD + c] = sum;
+        }
+        if (!have_ginv) {
+          wait_geq(M.gready + 1, 1u);
+          __threadfence();
+          for (int e = tid; e < r * r; e += kFusedThreads) {
+            const int x = e / r, y = e - x * r;
+            gi[x * LD + y] = __ldcg(A.ginv + e);
+          }
+          have_ginv = true;
+        }
+        __syncthreads();
+        for (int e = tid; e < nrow * r; e += kFusedThreads) {
+          const int il = e / r, c = e - il * r;
+          double o = 0.0;
+          for (int cc = 0; cc < r; ++cc) o = fma(rh[il * LD + cc], gi[cc * LD + c], o);
+          M.a[(r0 + il) * r + c] = o;
+          ob[il * LD + c] = o;
+        }
+        __syncthreads();
+        if (tid < r)
+          for (int il = 0; il < nrow; ++il) q2 += ob[il * LD + tid] * ob[il * LD + tid];
+        __syncthreads();
+      }
+      if (tid < r) A.ssq[static_cast<i64>(b) * r + tid] = q2;
+    }
+    stamp(n, 4);
+    // ---- ticket: the last CTA forms the norms and releases the next mode
+    {
+      volatile unsigned* gen = A.bar + 1;
+      __syncthreads();
+      unsigned g0 = 0;
+      if (tid == 0) {
+        g0 = *gen;
+        __threadfence();
+        s_last = (atomicAdd(&A.ticket[0], 1u) == G - 1u);
+      }
+      __syncthreads();
+      stamp(n, 5);
+      if (s_last) {
+        __threadfence();
+        ph::norms_final<RT, kFusedThreads>(r, in, w, G, n == 0, A.rng, fsm);
+        if (tid == 0) {
+          A.ticket[0] = 0u;
+          __threadfence();
+          atomicAdd(A.bar + 1, 1u);
+        }
+      } else if (tid == 0) {
+        while (ld_acquire(A.bar + 1) == g0) __nanosleep(32);
+      }
+      __syncthreads();
+    }
+    stamp(n, 6);
+  }
+  // ---- sampled fit + stop rule (sampling.hpp:191-210, :237-251)
+  if (A.has_fit) {
+    const FitArgs& f = A.fit;
+    const i64 nvb = (f.phat + 255) / 256;
+    double* red = fsm;
+    for (i64 vb = b; vb < nvb; vb += G) {
+      const double part = ph::fit_block(f, vb, red);
+      if (tid == 0) f.partials[vb] = part;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(&A.ticket[1], 1u) == G - 1u);
+    __syncthreads();
+    if (s_last && tid == 0) {
+      __threadfence();
+      A.ticket[1] = 0u;
+      ph::fit_final(f, nvb);
+    }
+  }
+}
+
+template <int RT>
+void* mix_fn() {
+  return reinterpret_cast<void*>(&fused_iteration_kernel<RT, true>);
+}
+template <int RT>
+void* rand_fn() {
+  return reinterpret_cast<void*>(&fused_rand_kernel<RT>);
 }
 
 void* pick(int rt, bool mix) {
   switch (rt) {
-    case 16: return mix ? fused_fn<16, true>() : fused_fn<16, false>();
-    case 32: return mix ? fused_fn<32, true>() : fused_fn<32, false>();
-    default: return mix ? fused_fn<64, true>() : fused_fn<64, false>();
+    case 16: return mix ? mix_fn<16>() : rand_fn<16>();
+    case 32: return mix ? mix_fn<32>() : rand_fn<32>();
+    default: return mix ? mix_fn<64>() : rand_fn<64>();
   }
 }
 
+template <int RT>
+size_t rand_smem_for(int zcap) {
+  i64 need = tl::tile_smem_doubles<RT>(zcap);
+  need = std::max<i64>(need, static_cast<i64>(RT) * (RT + 1) + 2 * static_cast<i64>(tl::BM) * (RT + 1));
+  need = std::max<i64>(need, 24 * RT + 64);
+  need = std::max<i64>(need, static_cast<i64>(kFusedThreads / RT) * (RT + 1));
+  need = std::max<i64>(need, 256);
+  return static_cast<size_t>(need) * sizeof(double);
+}
+
 }  // namespace
+
+int fused_rand_zcap(int rt) {
+  // two CTAs per SM: keep the dynamic shared memory of one CTA near 110 KB
+  const i64 budget = 110 * 1024 / 8;
+  const i64 sb = rt + 8;
+  const i64 fixed = static_cast<i64>(tl::STAGES) * tl::BK * tl::SA + 2 * kMaxOrder * rt + 1;
+  const i64 per = sb + 1 + kMaxOrder / 2;
+  i64 z = (budget - fixed) / per;
+  z &= ~static_cast<i64>(tl::BK - 1);
+  return static_cast<int>(std::max<i64>(z, tl::BK));
+}
+
+size_t fused_rand_smem(int rt, int zcap) {
+  switch (rt) {
+    case 16: return rand_smem_for<16>(zcap);
+    case 32: return rand_smem_for<32>(zcap);
+    default: return rand_smem_for<64>(zcap);
+  }
+}
+
+void fused_rand_tiles(i64 in, int s, int gw, int zcap, int* tm, int* tk, int* tklen) {
+  const int m = ceil_div(in, tl::BM);
+  int k = std::max(1, gw / m);
+  k = std::max(k, ceil_div(s, zcap));
+  int len = ceil_div(s, k);
+  len = std::max(32, (len + 3) / 4 * 4);
+  len = std::min(len, zcap);
+  k = ceil_div(s, len);
+  *tm = m;
+  *tk = k;
+  *tklen = len;
+}
 
 size_t fused_smem_bytes(int rt, bool mix, int max_dim) {
   size_t need = static_cast<size_t>(ph::GSTAGES * ph::GBK * (ph::GBM + rt)) * sizeof(double);

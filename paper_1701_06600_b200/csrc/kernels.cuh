@@ -175,11 +175,20 @@ struct FusedMode {
   const double* sign;    // MIX: D_n
   DctArgs plan;          // MIX: DCT plan of I_n
   int dctF;              // MIX: fibers per CTA in the transform
+  // CPRAND kernel (fused_rand_kernel): 64-row x tklen-sample tiles
+  int tm, tk, tklen;     // row blocks, sample splits, samples per split
+  int nblk;              // upper 8 x 8 Gram blocks
+  int zcap;              // Z rows the tile's shared memory holds
+  unsigned* mt_cnt;      // [tm] splits finished per row block
+  unsigned* gbt;         // [64] splits finished per Gram block
+  unsigned* gready;      // [0] Gram blocks reduced, [1] Gram inverse ready
+  unsigned* kb_cnt;      // [tk] CTAs that wrote their share of split kb's Z rows
 };
 struct FusedIter {
   int order, r, first_mode_first_of_pass;
   FusedMode mode[kMaxOrder];
   double *z, *part_gram, *ginv, *gfull, *part_rhs, *ssq, *rhs_full, *lambda;
+  double *gpart, *gsum;  // CPRAND kernel: Gram block partials [nblk][tk][64], reduced Gram [RT][RT]
   int* info;
   unsigned long long* rng;
   unsigned* ticket;      // [0] norm ticket, [1] fit ticket
@@ -191,6 +200,11 @@ struct FusedIter {
   unsigned long long* phase_t;  // optional: CTA 0 stamps globaltimer at phase edges [order][8]
 };
 size_t fused_smem_bytes(int rt, bool mix, int max_dim);
+// CPRAND kernel: Z rows per tile, its dynamic shared memory, and the tiling
+// of one mode over gw tile CTAs.
+int fused_rand_zcap(int rt);
+size_t fused_rand_smem(int rt, int zcap);
+void fused_rand_tiles(i64 in, int s, int gw, int zcap, int* tm, int* tk, int* tklen);
 // Largest co-resident grid for the fused kernel (0 when cooperative launch
 // is unavailable).
 int fused_max_grid(int rt, bool mix, size_t smem, int device);

@@ -14,6 +14,11 @@
 #include "devutil.cuh"
 #include "kernels.cuh"
 
+#ifndef CPB_INV_STAMP
+#define CPB_INV_STAMP(k)  // micro-benchmark hooks (tests/micro/inv_bench.cu)
+#define CPB_INV_STAMP_AT(k, s, lane0)
+#endif
+
 namespace cpb {
 namespace ph {
 
@@ -25,8 +30,8 @@ __device__ __forceinline__ double z_entry(const ModeView& v, int s, int rr) {
   double zv = 1.0;
   for (int c = 0; c < v.kept; ++c) {
     const int row = __ldg(v.rows[c] + s);
-    double a = __ldg(v.fac[c] + static_cast<i64>(row) * v.r + rr);
-    if (v.nrm[c]) a = a / __ldg(v.nrm[c] + rr);
+    double a = __ldcg(v.fac[c] + static_cast<i64>(row) * v.r + rr);  // written earlier in a persistent launch
+    if (v.nrm[c]) a = a / __ldcg(v.nrm[c] + rr);
     zv = __dmul_rn(zv, a);
   }
   return zv;
@@ -248,7 +253,10 @@ __device__ void gram_pinv(double* g, double* w, int* perm, int r, double tol, do
       }
     }
   }
-  if (tid == 0) info[0] = rank;
+  if (tid == 0) {
+    info[0] = rank;
+    info[1] += 1;  // fallback count (diagnostics)
+  }
 }
 
 // Fallback driver: G from gfull, working matrices in global scratch after it.
@@ -312,8 +320,9 @@ __device__ bool inverse_cta(const double* __restrict__ part, int nparts, int r, 
         for (int t = 0; t < TR; ++t)
 #pragma unroll
           for (int u = 0; u < TC; ++u)
-            v[x][t][u] = (row[t] < r && col[u] < r) ? part[static_cast<i64>(k + x) * RT * RT + row[t] * RT + col[u]]
-                                                    : 0.0;
+            v[x][t][u] = (row[t] < r && col[u] < r)
+                             ? __ldcg(part + static_cast<i64>(k + x) * RT * RT + row[t] * RT + col[u])
+                             : 0.0;
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -326,7 +335,7 @@ __device__ bool inverse_cta(const double* __restrict__ part, int nparts, int r, 
       for (int t = 0; t < TR; ++t)
 #pragma unroll
         for (int u = 0; u < TC; ++u)
-          if (row[t] < r && col[u] < r) a[t][u] += part[static_cast<i64>(k) * RT * RT + row[t] * RT + col[u]];
+          if (row[t] < r && col[u] < r) a[t][u] += __ldcg(part + static_cast<i64>(k) * RT * RT + row[t] * RT + col[u]);
   }
   // d_max for the threshold and the padding diagonal
   if (tid == 0) misc[0] = 0.0;
@@ -436,6 +445,7 @@ __device__ bool inverse_cta(const double* __restrict__ part, int nparts, int r, 
       __syncthreads();
     }
   }
+  CPB_INV_STAMP(30);
   if (!fail) {
 #pragma unroll
     for (int t = 0; t < TR; ++t)
@@ -445,6 +455,287 @@ __device__ bool inverse_cta(const double* __restrict__ part, int nparts, int r, 
   }
   if (tid == 0) info[0] = fail ? -1 : r;
   __syncthreads();
+  CPB_INV_STAMP(31);
+  return fail;
+}
+
+// ---------------------------------------------- 4 x 4 pivot inverse
+// 1/d to full precision: hardware approximation + two Newton steps (the
+// inverse is not a bit-parity quantity; 1e-16 relative is what matters).
+__device__ __forceinline__ double rcp_nr(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;\n" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+// Unpivoted 4 x 4 Gauss-Jordan inverse by lanes 0..15 of a warp (lane
+// 4 x + y holds p(x, y) in and p^-1(x, y) out); all 32 lanes must call.
+// ok = false when a pivot is <= thr (or not positive).
+__device__ __forceinline__ double invert4_lanes(double p, double thr, bool& ok) {
+  const int l = threadIdx.x & 31, x = (l >> 2) & 3, y = l & 3;
+  ok = true;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double pkk = __shfl_sync(0xffffffffu, p, k * 5);
+    const double pky = __shfl_sync(0xffffffffu, p, k * 4 + y);
+    const double pxk = __shfl_sync(0xffffffffu, p, x * 4 + k);
+    if (!(pkk > thr) || !(pkk > 0.0)) ok = false;
+    const double q = rcp_nr(pkk);
+    const double rk = (y == k) ? q : pky * q;
+    const double ck = (x == k) ? -1.0 : pxk;
+    const double xv = (x == k || y == k) ? 0.0 : p;
+    p = fma(-ck, rk, xv);
+  }
+  return p;
+}
+
+// ------------------------------------------- Gram inverse, look-ahead
+// 4 x 4 inverse by the 2 x 2-minor (Laplace) expansion: every entry is a
+// short independent expression, so the latency is ~6 dependent FP64 ops and
+// one reciprocal instead of four chained pivot divisions. The unpivoted
+// Gauss-Jordan pivots are d_k / d_{k-1} (leading principal minors), so the
+// rank test pivot_k > thr becomes d_k > thr d_{k-1} without divisions.
+__device__ __forceinline__ bool inv4_minors(const double* a, double* out, double thr) {
+  const double a00 = a[0], a01 = a[1], a02 = a[2], a03 = a[3];
+  const double a10 = a[4], a11 = a[5], a12 = a[6], a13 = a[7];
+  const double a20 = a[8], a21 = a[9], a22 = a[10], a23 = a[11];
+  const double a30 = a[12], a31 = a[13], a32 = a[14], a33 = a[15];
+  const double s0 = fma(a00, a11, -a10 * a01), s1 = fma(a00, a12, -a10 * a02);
+  const double s2 = fma(a00, a13, -a10 * a03), s3 = fma(a01, a12, -a11 * a02);
+  const double s4 = fma(a01, a13, -a11 * a03), s5 = fma(a02, a13, -a12 * a03);
+  const double c5 = fma(a22, a33, -a32 * a23), c4 = fma(a21, a33, -a31 * a23);
+  const double c3 = fma(a21, a32, -a31 * a22), c2 = fma(a20, a33, -a30 * a23);
+  const double c1 = fma(a20, a32, -a30 * a22), c0 = fma(a20, a31, -a30 * a21);
+  const double det = (fma(s0, c5, -s1 * c4) + fma(s2, c3, s3 * c2)) + fma(-s4, c1, s5 * c0);
+  // leading principal minors d1 = a00, d2 = s0, d3 = det(a[0..2][0..2])
+  const double d3 = fma(a20, s3, fma(-a21, s1, a22 * s0));
+  const bool ok = (a00 > thr) && (s0 > thr * a00) && (d3 > thr * s0) && (det > thr * d3) && (a00 > 0.0) &&
+                  (s0 > 0.0) && (d3 > 0.0) && (det > 0.0);
+  const double id = 1.0 / det;
+  out[0] = (fma(a11, c5, -a12 * c4) + a13 * c3) * id;
+  out[1] = (fma(-a01, c5, a02 * c4) - a03 * c3) * id;
+  out[2] = (fma(a31, s5, -a32 * s4) + a33 * s3) * id;
+  out[3] = (fma(-a21, s5, a22 * s4) - a23 * s3) * id;
+  out[4] = (fma(-a10, c5, a12 * c2) - a13 * c1) * id;
+  out[5] = (fma(a00, c5, -a02 * c2) + a03 * c1) * id;
+  out[6] = (fma(-a30, s5, a32 * s2) - a33 * s1) * id;
+  out[7] = (fma(a20, s5, -a22 * s2) + a23 * s1) * id;
+  out[8] = (fma(a10, c4, -a11 * c2) + a13 * c0) * id;
+  out[9] = (fma(-a00, c4, a01 * c2) - a03 * c0) * id;
+  out[10] = (fma(a30, s4, -a31 * s2) + a33 * s0) * id;
+  out[11] = (fma(-a20, s4, a21 * s2) - a23 * s0) * id;
+  out[12] = (fma(-a10, c3, a11 * c1) - a12 * c0) * id;
+  out[13] = (fma(a00, c3, -a01 * c1) + a02 * c0) * id;
+  out[14] = (fma(-a30, s3, a31 * s1) - a32 * s0) * id;
+  out[15] = (fma(a20, s3, -a21 * s1) + a22 * s0) * id;
+  return ok;
+}
+
+// Block Gauss-Jordan inverse (4 x 4 pivot blocks, no pivoting: the Gram is
+// SPD) by one CTA of 256 threads, one barrier per step.
+//  * Warps 0-6 hold the matrix as FP64 MMA accumulator fragments (warp w:
+//    8-column tiles w and w + 7, every 8-row tile) and do step s as one
+//    m8n8k4 MMA per tile: a' = X + (-C) M, where X = a with rows/columns K
+//    zeroed, -C(i) = -a(i, K) (+e on rows K) comes from the published column
+//    block and M(j) = P^-1 a(K, j) from the published row block, whose K
+//    columns hold the identity (so M = P^-1 e_j there): the four
+//    Gauss-Jordan block rules in one form.
+//  * After the MMAs the owners publish step s+1's row/column blocks and
+//    zero rows/columns K_{s+1} (X of the next step). The step loop is fully
+//    unrolled, so every tile index is a compile-time constant.
+//  * Warp 7 meanwhile forms the NEXT pivot block (rows/columns K_{s+1} after
+//    step s, from the raw rows K_s, K_{s+1}) and inverts it (inv4_minors):
+//    the pivot inversion is off the workers' critical path.
+// g: RT x RT Gram (ld RT; entries outside [0, r) ignored). Returns true
+// (uniformly) on a pivot <= tol * d_max, after writing the Gram to gfull
+// (r x r) for the pivoted fallback. sh: 24 RT + 64 doubles.
+template <int RT>
+__device__ bool inverse_la(const double* __restrict__ g, int r, double tol, double* __restrict__ ginv,
+                           double* __restrict__ gfull, int* info, double* sh) {
+  constexpr int NTI = RT / 8;
+  constexpr int NSMAX = RT / 4;
+  static_assert(NTI <= 8, "one 8-column tile per warp");
+  double* rbs = sh;              // [2][8][RT] rows K_s (identity on K_s columns), raw rows K_{s+1}
+  double* cbs = rbs + 16 * RT;   // [2][RT][4] -a(i, K_s), +e on rows K_s
+  double* pin = cbs + 8 * RT;    // [2][16]    inverse of the pivot block of step s
+  double* misc = pin + 32;       // [2..3] fail flags, [4..5] warp maxima
+  double* tmp = misc + 8;        // [16] next pivot block
+  const int tid = threadIdx.x, w = tid / 32, l = tid % 32;
+  const int lr = l >> 2, lc = (l & 3) * 2, lk = l & 3;
+  const int r4 = (r + 3) & ~3;
+  const int nt = (r + 7) / 8;
+  const int nsteps = r4 / 4;
+  const bool worker = w < nt;  // warp w owns 8-column tile w
+  const int ct = w;
+  double acc[NTI][2];
+#pragma unroll
+  for (int mt = 0; mt < NTI; ++mt) {
+    const int row = mt * 8 + lr, col = ct * 8 + lc;
+    const bool ok = worker && row < r;
+    acc[mt][0] = (ok && col < r) ? __ldcg(g + row * RT + col) : 0.0;
+    acc[mt][1] = (ok && col + 1 < r) ? __ldcg(g + row * RT + col + 1) : 0.0;
+  }
+  {  // d_max: largest (clamped) diagonal entry
+    double dv = (tid < r) ? fmax(__ldcg(g + tid * (RT + 1)), 0.0) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dv = fmax(dv, __shfl_xor_sync(0xffffffffu, dv, o));
+    if (l == 0 && w < 2) misc[4 + w] = dv;
+  }
+  __syncthreads();
+  const double dmax = RT > 32 ? fmax(misc[4], misc[5]) : misc[4];
+  const double thr = tol * dmax;
+#pragma unroll
+  for (int mt = 0; mt < NTI; ++mt) {
+    const int row = mt * 8 + lr;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int col = ct * 8 + lc + e;
+      if (!worker) continue;
+      if (row < r && col < r) gfull[row * r + col] = acc[mt][e];
+      if (row == col && row >= r && row < r4) acc[mt][e] = dmax;  // padding diagonal
+    }
+  }
+  CPB_INV_STAMP(1);
+  // Publish rows K = [n0, n0+4) (identity on K x K) and raw rows [n0+4, n0+8)
+  // into rb, -a(., K) (+e on rows K) into cb; zero rows/columns K. n0 is a
+  // compile-time constant at every call site (unrolled step loop).
+  auto publish = [&](const int n0, double* rb, double* cb, const bool first) {
+    const int tk = n0 / 8, tn = (n0 + 4) / 8;
+    if (!worker) return;  // warp-uniform
+    const int col = ct * 8 + lc;
+    const bool ck0 = static_cast<unsigned>(col - n0) < 4u, ck1 = static_cast<unsigned>(col + 1 - n0) < 4u;
+    if (tk < NTI) {
+      const int qi = tk * 8 + lr - n0;
+      if (static_cast<unsigned>(qi) < 4u) {
+        const double v0 = acc[tk][0], v1 = acc[tk][1];
+        if (first) {
+          if (ck0) tmp[qi * 4 + col - n0] = v0;
+          if (ck1) tmp[qi * 4 + col + 1 - n0] = v1;
+        }
+        double2 o;
+        o.x = ck0 ? (qi == col - n0 ? 1.0 : 0.0) : v0;
+        o.y = ck1 ? (qi == col + 1 - n0 ? 1.0 : 0.0) : v1;
+        *reinterpret_cast<double2*>(rb + qi * RT + col) = o;
+      }
+    }
+    if (tn < NTI) {
+      const int qi = tn * 8 + lr - n0;
+      if (qi >= 4 && qi < 8 && tn * 8 + lr < r4)
+        *reinterpret_cast<double2*>(rb + qi * RT + col) = make_double2(acc[tn][0], acc[tn][1]);
+    }
+    if (ct == tk) {  // warp-uniform: this warp owns columns K
+#pragma unroll
+      for (int mt = 0; mt < NTI; ++mt) {
+        const int row = mt * 8 + lr;
+        const bool rk = static_cast<unsigned>(row - n0) < 4u;
+        if (ck0) {
+          cb[row * 4 + col - n0] = rk ? (row == col ? 1.0 : 0.0) : -acc[mt][0];
+          acc[mt][0] = 0.0;
+        }
+        if (ck1) {
+          cb[row * 4 + col + 1 - n0] = rk ? (row == col + 1 ? 1.0 : 0.0) : -acc[mt][1];
+          acc[mt][1] = 0.0;
+        }
+      }
+    }
+    if (tk < NTI && static_cast<unsigned>(tk * 8 + lr - n0) < 4u) {  // zero rows K
+      acc[tk][0] = 0.0;
+      acc[tk][1] = 0.0;
+    }
+  };
+  publish(0, rbs, cbs, true);
+  __syncthreads();
+  if (w == 7 && l == 0) {
+    double p[16], o[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) p[e] = tmp[e];
+    const bool ok = inv4_minors(p, o, thr);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) pin[e] = o[e];
+    misc[2] = ok ? 0.0 : 1.0;
+  }
+  __syncthreads();
+  CPB_INV_STAMP(2);
+  bool fail = false;
+#pragma unroll
+  for (int s = 0; s < NSMAX; ++s) {
+    if (s >= nsteps) break;  // uniform
+    CPB_INV_STAMP(3 + s);
+    const int pb = s & 1, k0 = 4 * s;
+    if (misc[2 + pb] != 0.0) {
+      fail = true;  // uniform
+      break;
+    }
+    const double* P = pin + 16 * pb;
+    const double* rb = rbs + pb * 8 * RT;
+    const double* cb = cbs + pb * RT * 4;
+    if (w == 7 && k0 + 4 < r4) {
+      // warp 7: pivot block of step s+1 = rows/columns K_{s+1} after step s
+      if (l < 16) {
+        const int x = l >> 2, y = l & 3;
+        const int jj = k0 + 4 + y;
+        const double* rn = rb + (4 + x) * RT;  // raw row k0 + 4 + x
+        double mv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          mv[q] = fma(P[q * 4], rb[jj], P[q * 4 + 1] * rb[RT + jj]) +
+                  fma(P[q * 4 + 2], rb[2 * RT + jj], P[q * 4 + 3] * rb[3 * RT + jj]);
+        tmp[l] = (rn[jj] - fma(rn[k0], mv[0], rn[k0 + 1] * mv[1])) - fma(rn[k0 + 2], mv[2], rn[k0 + 3] * mv[3]);
+      }
+      __syncwarp();
+      CPB_INV_STAMP_AT(43, s, l == 0);
+      if (l == 0) {
+        double p[16], o[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) p[e] = tmp[e];
+        const bool ok = inv4_minors(p, o, thr);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pin[16 * (pb ^ 1) + e] = o[e];
+        misc[2 + (pb ^ 1)] = ok ? 0.0 : 1.0;
+      }
+      __syncwarp();
+      CPB_INV_STAMP_AT(44, s, l == 0);
+    }
+    if (worker) {
+      // all fragment operands are loaded before the first MMA
+      const double2 p01 = *reinterpret_cast<const double2*>(P + lk * 4);
+      const double2 p23 = *reinterpret_cast<const double2*>(P + lk * 4 + 2);
+      double am[NTI];
+#pragma unroll
+      for (int mt = 0; mt < NTI; ++mt) am[mt] = cb[(mt * 8 + lr) * 4 + lk];  // rows >= r4 hold zeros
+      const int j = ct * 8 + lr;  // B fragment (k = l % 4, n = l / 4)
+      const double bm = fma(p01.x, rb[j], p01.y * rb[RT + j]) + fma(p23.x, rb[2 * RT + j], p23.y * rb[3 * RT + j]);
+#pragma unroll
+      for (int mt = 0; mt < NTI; ++mt)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[mt][0]), "+d"(acc[mt][1])
+                     : "d"(am[mt]), "d"(bm));
+      CPB_INV_STAMP_AT(41, s, tid == 0);
+      if (k0 + 4 < r4) publish(k0 + 4, rbs + (pb ^ 1) * 8 * RT, cbs + (pb ^ 1) * RT * 4, false);
+    }
+    CPB_INV_STAMP_AT(42, s, tid == 0);
+    CPB_INV_STAMP_AT(45, s, tid == 224);
+    __syncthreads();
+  }
+  CPB_INV_STAMP(30);
+  if (!fail && worker) {
+#pragma unroll
+    for (int mt = 0; mt < NTI; ++mt) {
+      const int row = mt * 8 + lr, col = ct * 8 + lc;
+      if (mt >= nt || row >= r) continue;
+      if (col + 1 < r && !(r & 1))
+        *reinterpret_cast<double2*>(ginv + row * r + col) = make_double2(acc[mt][0], acc[mt][1]);
+      else {
+        if (col < r) ginv[row * r + col] = acc[mt][0];
+        if (col + 1 < r) ginv[row * r + col + 1] = acc[mt][1];
+      }
+    }
+  }
+  if (tid == 0) info[0] = fail ? -1 : r;
+  __syncthreads();
+  CPB_INV_STAMP(31);
   return fail;
 }
 
@@ -562,7 +853,7 @@ template <int RT, int NTH>
 __device__ void load_ginv(const double* __restrict__ ginv, int r, double* gi) {
   for (int e = threadIdx.x; e < RT * RT; e += NTH) {
     const int x = e / RT, y = e % RT;
-    gi[x * (RT + 1) + y] = (x < r && y < r) ? ginv[x * r + y] : 0.0;
+    gi[x * (RT + 1) + y] = (x < r && y < r) ? __ldcg(ginv + x * r + y) : 0.0;
   }
 }
 
@@ -576,17 +867,17 @@ __device__ double apply_block(i64 in, int r, const ModeWork& w, const double* __
   double s = 0.0;
   if (i < in && c < r) {
     if (rhs_full) {
-      s = rhs_full[i * r + c];
+      s = __ldcg(rhs_full + i * r + c);
     } else {
       const double* p = w.part_rhs + i * r + c;
       const i64 step = in * r;
       int k = 0;
       for (; k + 6 <= w.ks; k += 6) {
-        const double v0 = p[k * step], v1 = p[(k + 1) * step], v2 = p[(k + 2) * step];
-        const double v3 = p[(k + 3) * step], v4 = p[(k + 4) * step], v5 = p[(k + 5) * step];
+        const double v0 = __ldcg(p + k * step), v1 = __ldcg(p + (k + 1) * step), v2 = __ldcg(p + (k + 2) * step);
+        const double v3 = __ldcg(p + (k + 3) * step), v4 = __ldcg(p + (k + 4) * step), v5 = __ldcg(p + (k + 5) * step);
         s = (((((s + v0) + v1) + v2) + v3) + v4) + v5;
       }
-      for (; k < w.ks; ++k) s += p[k * step];
+      for (; k < w.ks; ++k) s += __ldcg(p + k * step);
     }
   }
   rh[il * LD + c] = s;
@@ -627,7 +918,7 @@ __device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int fi
   __shared__ int s_zero;
   double q = 0.0;
   if (c < r)
-    for (int b = part; b < nparts; b += NP) q += w.ssq[static_cast<i64>(b) * r + c];
+    for (int b = part; b < nparts; b += NP) q += __ldcg(w.ssq + static_cast<i64>(b) * r + c);
   red[part * (RT + 1) + c] = q;
   if (tid == 0) s_zero = 0;
   __syncthreads();
@@ -640,7 +931,7 @@ __device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int fi
       w.lambda[tid] = 0.0;
       atomicOr(&s_zero, 1);
     } else {
-      w.lambda[tid] = first_of_pass ? w.lambda[tid] * nrm : nrm;
+      w.lambda[tid] = first_of_pass ? __ldcg(w.lambda + tid) * nrm : nrm;
     }
   }
   __syncthreads();
@@ -668,10 +959,10 @@ __device__ inline double fit_block(const FitArgs& a, i64 vb, double* red) {
   if (j < a.phat) {
     double sum = 0.0;
     for (int q = 0; q < a.r; ++q) {
-      double p = a.lambda[q];
+      double p = __ldcg(a.lambda + q);
       for (int n = 0; n < a.order; ++n) {
-        double f = a.fac[n][static_cast<i64>(a.idx[n][j]) * a.r + q];
-        if (a.nrm[n]) f = f / a.nrm[n][q];
+        double f = __ldcg(a.fac[n] + static_cast<i64>(a.idx[n][j]) * a.r + q);
+        if (a.nrm[n]) f = f / __ldcg(a.nrm[n] + q);
         p = __dmul_rn(p, f);
       }
       sum = __dadd_rn(sum, p);

@@ -298,6 +298,9 @@ Session::~Session() {
   dfree(fargs_);
   dfree(phase_t_);
   dfree(fsync_);
+  dfree(fcnt_);
+  dfree(gpart_);
+  dfree(gsum_);
   for (auto& e : ev_gathered_) cudaEventDestroy(e);
   for (auto& e : ev_consumed_) cudaEventDestroy(e);
   if (ev_z_) cudaEventDestroy(ev_z_);
@@ -429,6 +432,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   ginv_ = dalloc<double>(static_cast<size_t>(r_ * r_));
   gfull_ = dalloc<double>(static_cast<size_t>(gram_scratch_doubles(r_)));
   info_ = dalloc<int>(4);
+  CPB_CUDA(cudaMemsetAsync(info_, 0, 4 * sizeof(int), stream_));
   tickets_ = dalloc<unsigned>(8);
   CPB_CUDA(cudaMemsetAsync(tickets_, 0, 8 * sizeof(unsigned), stream_));
   ssq_ = dalloc<double>(static_cast<size_t>(std::max<i64>(max_apply, 4 * sms_) * r_));
@@ -454,7 +458,13 @@ void Session::setup_fused() {
   if (o_.fused == 0 || !all_direct || o_.exhaustive_samples) return;
   i64 max_dim = 1;
   for (i64 d : dims_) max_dim = std::max(max_dim, d);
-  fsmem_ = fused_smem_bytes(rt_, mix_, static_cast<int>(max_dim));
+  int zcap = 0;
+  if (mix_) {
+    fsmem_ = fused_smem_bytes(rt_, mix_, static_cast<int>(max_dim));
+  } else {
+    zcap = fused_rand_zcap(rt_);
+    fsmem_ = fused_rand_smem(rt_, zcap);
+  }
   if (fsmem_ > 200 * 1024) return;
   fgrid_ = fused_max_grid(rt_, mix_, fsmem_, x_->device);
   int max_gp = 1;
@@ -464,6 +474,34 @@ void Session::setup_fused() {
     max_gp = std::max(max_gp, gp);
   }
   if (fgrid_ < max_gp + 2) return;
+  // CPRAND kernel tiling per mode
+  std::vector<int> tm(static_cast<size_t>(order_)), tk(tm), tkl(tm);
+  const int nfr = (r_ + 7) / 8, nblk = nfr * (nfr + 1) / 2;
+  int tm_max = 1;
+  if (!mix_) {
+    i64 max_part = 1;
+    int& tk_max = tk_max_;
+    for (int n = 0; n < order_; ++n) {
+      const size_t k = static_cast<size_t>(n);
+      fused_rand_tiles(dims_[k], s_mode_[k], fgrid_ - 1, zcap, &tm[k], &tk[k], &tkl[k]);
+      tm_max = std::max(tm_max, tm[k]);
+      tk_max = std::max(tk_max, tk[k]);
+      max_part = std::max(max_part, static_cast<i64>(tk[k]) * dims_[k] * r_);
+    }
+    i64 have = 1;
+    for (int n = 0; n < order_; ++n)
+      have = std::max(have, static_cast<i64>(ks_[static_cast<size_t>(n)]) * dims_[static_cast<size_t>(n)] * r_);
+    if (max_part > have) {
+      dfree(part_rhs_);
+      part_rhs_ = dalloc<double>(static_cast<size_t>(max_part));
+    }
+    gpart_ = dalloc<double>(static_cast<size_t>(nblk) * tk_max * 64);
+    gsum_ = dalloc<double>(static_cast<size_t>(rt_) * rt_);
+    CPB_CUDA(cudaMemsetAsync(gsum_, 0, sizeof(double) * rt_ * rt_, stream_));
+    const size_t per = static_cast<size_t>(tm_max) + 64 + 2 + static_cast<size_t>(tk_max);
+    fcnt_ = dalloc<unsigned>(per * order_);
+    CPB_CUDA(cudaMemsetAsync(fcnt_, 0, per * order_ * sizeof(unsigned), stream_));
+  }
   fsync_ = dalloc<unsigned>(16);
   CPB_CUDA(cudaMemsetAsync(fsync_, 0, 16 * sizeof(unsigned), stream_));
   std::vector<FusedIter> host(static_cast<size_t>(table_iters_));
@@ -491,6 +529,18 @@ void Session::setup_fused() {
         M.sign = signs_[static_cast<size_t>(n)];
         M.plan = dct_args(plans_[static_cast<size_t>(n)]);
         M.dctF = dct_fibers_per_cta(static_cast<int>(dims_[static_cast<size_t>(n)]), fsmem_);
+      } else {
+        const size_t k = static_cast<size_t>(n);
+        M.tm = tm[k];
+        M.tk = tk[k];
+        M.tklen = tkl[k];
+        M.nblk = nblk;
+        M.zcap = zcap;
+        unsigned* c = fcnt_ + (static_cast<size_t>(tm_max) + 66 + tk_max_) * k;
+        M.mt_cnt = c;
+        M.gbt = c + tm_max;
+        M.gready = c + tm_max + 64;
+        M.kb_cnt = c + tm_max + 66;
       }
     }
     A.z = z_;
@@ -498,6 +548,8 @@ void Session::setup_fused() {
     A.ginv = ginv_;
     A.gfull = gfull_;
     A.part_rhs = part_rhs_;
+    A.gpart = gpart_;
+    A.gsum = gsum_;
     A.ssq = ssq_;
     A.rhs_full = rhs_full_;
     A.lambda = lambda_;
@@ -538,6 +590,15 @@ void Session::setup_fused() {
   CPB_CUDA(cudaMemcpyAsync(fargs_, host.data(), host.size() * sizeof(FusedIter), cudaMemcpyHostToDevice, stream_));
   CPB_CUDA(cudaStreamSynchronize(stream_));
   fused_ = true;
+}
+
+long long Session::gram_fallbacks() {
+  if (!info_) return 0;
+  CPB_CUDA(cudaStreamSynchronize(stream_));
+  CPB_CUDA(cudaStreamSynchronize(stream2_));
+  int v[4];
+  CPB_CUDA(cudaMemcpy(v, info_, sizeof(v), cudaMemcpyDeviceToHost));
+  return v[1];
 }
 
 void Session::finish_zero_tensor() {
@@ -880,7 +941,8 @@ void Session::enqueue_iteration() {
       for (int n = 0; n < order_; ++n) {
         const unsigned long long* q = t.data() + n * 8;
         for (int k = 0; k < 6; ++k) phase_acc_[static_cast<size_t>(k)] += 1e-3 * static_cast<double>(q[k + 1] - q[k]) / order_;
-        phase_acc_[6] += 1e-3 * static_cast<double>(q[7] - q[2]) / order_;
+        // MIX kernel: inverse done after the Z barrier; CPRAND kernel: after the mode start
+        phase_acc_[6] += 1e-3 * static_cast<double>(q[7] - q[mix_ ? 2 : 0]) / order_;
       }
       ++phase_acc_n_;
     }

@@ -142,6 +142,10 @@ class Session {
   size_t fsmem_ = 0;
   FusedIter* fargs_ = nullptr;     // [table iterations] device copies
   unsigned* fsync_ = nullptr;      // gram_done, barrier, tickets
+  unsigned* fcnt_ = nullptr;       // CPRAND kernel counters [order][tm_max + 64 + 2 + tk_max]
+  int tk_max_ = 1;
+  double* gpart_ = nullptr;        // CPRAND kernel Gram block partials
+  double* gsum_ = nullptr;         // CPRAND kernel reduced Gram [RT][RT]
   unsigned long long* phase_t_ = nullptr;  // fused phase timestamps [order][8] (timing mode)
  public:
   // fused path: mean per-mode phase durations (us) over the timed launches:
@@ -151,6 +155,8 @@ class Session {
     for (auto& x : v) x /= (phase_acc_n_ ? phase_acc_n_ : 1);
     return v;
   }
+  // Gram inverses that took the pivoted-Cholesky fallback so far (waits)
+  long long gram_fallbacks();
  private:
   std::vector<double> phase_acc_;
   int phase_acc_n_ = 0;
