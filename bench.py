@@ -360,7 +360,10 @@ def main() -> int:
                              (["z", "z_barrier", "phaseB_cta0", "B_barrier", "apply", "apply_barrier",
                                "inverse_done_after_z_barrier"] if cfg["method"] == "mix" else
                               ["z_tile", "gram_blocks", "rhs_tiles", "apply_share", "ssq", "release",
-                               "inverse_done_after_mode_start"]),
+                               "inverse_done_after_mode_start", "gram_ready_after_mode_start",
+                               "z_share_done_after_mode_start", "z_split_ready_after_mode_start",
+                               "inverse_prologue", "inverse_steps", "norms_done_after_mode_start",
+                               "gram_reduce"]),
                              [round(x, 2) for x in phases])) if phases else None,
                          "gram_fallbacks": fallbacks},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
   const int tid = threadIdx.x;
   const int r = A.r;
   auto stamp = [&](int n, int k) {
-    if (A.phase_t && b == 0 && tid == 0) A.phase_t[n * 8 + k] = globaltimer();
+    if (A.phase_t && b == 0 && tid == 0) A.phase_t[n * 16 + k] = globaltimer();
   };
   for (int n = 0; n < A.order; ++n) {
     const FusedMode& M = A.mode[n];
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
       const bool fail = ph::inverse_cta<RT, kFusedThreads>(A.part_gram, M.gparts, r, M.tol, A.ginv, A.gfull, A.info, fsm);
       if (fail) ph::pinv_fallback<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
       if (tid == 0) *A.gram_done = 0u;
-      if (A.phase_t && tid == 0) A.phase_t[n * 8 + 7] = globaltimer();  // inverse done
+      if (A.phase_t && tid == 0) A.phase_t[n * 16 + 7] = globaltimer();  // inverse done
     } else {
       if (static_cast<int>(b) < M.gparts) {
         const int s0 = b * M.gklen;
@@ -206,6 +206,46 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
 //              and releases the next mode (sense-reversing generation).
 // Counters of mode n are reset by CTA 0 during mode n+1, when no CTA can
 // still be waiting on them.
+// sum_{k < n} p[k * step] in order k = 0, 1, ... (16 loads in flight per batch)
+__device__ __forceinline__ double sum_strided(const double* __restrict__ p, i64 step, int n) {
+  double sum = 0.0;
+  int k = 0;
+  for (; k + 16 <= n; k += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldcg(p + (k + u) * step);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) sum += v[u];
+  }
+  if (k < n) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = (k + u < n) ? __ldcg(p + (k + u) * step) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (k + u < n) sum += v[u];
+  }
+  return sum;
+}
+
+// L2 prefetch of one iteration's sample tables (all modes): global thread g
+// prefetches 128-byte line g of the concatenated tables.
+__device__ __forceinline__ void prefetch_tables(const FusedIter& A, unsigned b) {
+  i64 line = static_cast<i64>(b) * blockDim.x + threadIdx.x;
+  for (int n = 0; n < A.order; ++n) {
+    const ModeView& v = A.mode[n].v;
+    for (int c = 0; c <= v.kept; ++c) {
+      const char* base = c < v.kept ? reinterpret_cast<const char*>(v.rows[c]) : reinterpret_cast<const char*>(v.base);
+      const i64 nl = ((c < v.kept ? 4LL : 8LL) * v.s + 127) / 128;
+      if (line < nl) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + line * 128));
+        return;
+      }
+      line -= nl;
+    }
+  }
+}
+
 template <int RT>
 __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const FusedIter* __restrict__ args) {
   using namespace tl;
@@ -213,92 +253,150 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
   if (A.stop && *A.stop) return;  // uniform: the flag only changes in a previous launch
   extern __shared__ __align__(16) double fsm[];
   __shared__ int perm[RT];
-  __shared__ unsigned s_old;
-  __shared__ int s_lastq[64];
-  __shared__ int s_nlast;
   __shared__ bool s_last;
   const unsigned G = gridDim.x, b = blockIdx.x;
-  const unsigned Gw = G - 1;
   const int tid = threadIdx.x;
+  if (A.census) {
+    if (tid == 0) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      A.census[b] = static_cast<int>(sm);
+    }
+    return;
+  }
+  // roles: CTA inv_cta inverts the Gram and reduces the norms; idle_cta (its
+  // SM partner, if any) stays off the FP64 pipe; the rest own tiles in rank order
+  const int inv = A.inv_cta >= 0 ? A.inv_cta : static_cast<int>(G) - 1;
+  const int idle = A.idle_cta;
+  const bool is_inv = static_cast<int>(b) == inv, is_idle = static_cast<int>(b) == idle;
+  const unsigned Gw = G - 1 - (idle >= 0 ? 1u : 0u);
+  const unsigned rank = b - (static_cast<int>(b) > inv ? 1u : 0u) - (idle >= 0 && static_cast<int>(b) > idle ? 1u : 0u);
   const int r = A.r;
   const int nfr = (r + 7) / 8;
+  unsigned* gen = A.bar + 1;  // release generation: +1 per mode
+  const unsigned gen0 = ld_acquire(gen);  // no release of this launch can precede every CTA's first signal
+  prefetch_tables(A, b);
+  if (A.cta_t && tid == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    A.cta_t[b * 16 + 14] = sm;
+  }
   auto stamp = [&](int n, int k) {
-    if (A.phase_t && b == 0 && tid == 0) A.phase_t[n * 8 + k] = globaltimer();
+    if (A.phase_t && rank == 0 && !is_inv && !is_idle && tid == 0) A.phase_t[n * 16 + k] = globaltimer();
+    if (A.cta_t && n == 1 && tid == 0) A.cta_t[b * 16 + k] = globaltimer();
   };
   for (int n = 0; n < A.order; ++n) {
     const FusedMode& M = A.mode[n];
     const ModeWork w = work_of(A, M);
     const i64 in = M.v.in;
+    const int ntiles = M.tm * M.tk;
     stamp(n, 0);
-    if (b == 0) {
+    if (b == 0) {  // reset the previous mode's counters: every wait on them is over
       const FusedMode& P = A.mode[(n + A.order - 1) % A.order];
-      for (int e = tid; e < P.tm; e += kFusedThreads) P.mt_cnt[e] = 0u;
-      for (int e = tid; e < P.tk; e += kFusedThreads) P.kb_cnt[e] = 0u;
-      if (tid < 64) P.gbt[tid] = 0u;
-      if (tid < 2) P.gready[tid] = 0u;
+      for (int e = tid; e < P.tm; e += kFusedThreads) P.mt_cnt[e * kCS] = 0u;
+      for (int e = tid; e < P.tk; e += kFusedThreads) P.kb_cnt[e * kCS] = 0u;
+      if (tid < 3) P.mcnt[tid * kCS] = 0u;
+      for (int e = tid; e < P.tm; e += kFusedThreads) P.gm_cnt[e * kCS] = 0u;
     }
-    if (b == G - 1) {
-      // ---- Gram inverse (pivoted-Cholesky min-norm fallback when rank deficient)
-      wait_geq(M.gready, static_cast<unsigned>(M.nblk));
-      __threadfence();
-      const bool fail = ph::inverse_la<RT>(A.gsum, r, M.tol, A.ginv, A.gfull, A.info, fsm);
+    if (is_inv) {
+      // ---- Gram: the row-block reducers summed it (dist_gram), or sum the
+      // split partials of every 8 x 8 block here (split order)
+      wait_geq(M.mcnt, static_cast<unsigned>(M.dist_gram ? M.nblk : ntiles));
+      if (A.phase_t && tid == 0) A.phase_t[n * 16 + 8] = globaltimer();
+      if (!M.dist_gram) {
+        constexpr int PER = 8, KC = 5;
+        const int ne = M.nblk * 64;
+        double sum[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) sum[u] = 0.0;
+        for (int k0 = 0; k0 < M.tk; k0 += KC) {
+          double v[PER][KC];
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const int e = tid + u * kFusedThreads;
+            const double* src = A.gpart + static_cast<i64>(e / 64) * M.tk * 64 + (e % 64);
+#pragma unroll
+            for (int k = 0; k < KC; ++k) v[u][k] = (e < ne && k0 + k < M.tk) ? __ldcg(src + (k0 + k) * 64) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < PER; ++u)
+#pragma unroll
+            for (int k = 0; k < KC; ++k)
+              if (k0 + k < M.tk) sum[u] += v[u][k];
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int e = tid + u * kFusedThreads;
+          if (e >= ne) continue;
+          int bi, bj;
+          gram_block_coords(e / 64, nfr, &bi, &bj);
+          const int el = e % 64, gi = bi * 8 + el / 8, gj = bj * 8 + el % 8;
+          A.gsum[gi * RT + gj] = sum[u];
+          A.gsum[gj * RT + gi] = sum[u];
+        }
+      }
+      __syncthreads();
+      if (A.phase_t && tid == 0) A.phase_t[n * 16 + 15] = globaltimer();
+      // ---- inverse (pivoted-Cholesky min-norm fallback when rank deficient)
+      const bool fail = ph::inverse_la<RT>(A.gsum, r, M.tol, A.ginv, A.gfull, A.info, fsm,
+                                           A.phase_t ? A.phase_t + n * 16 + 11 : nullptr);
       if (fail) ph::pinv_fallback<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
-      release_add(M.gready + 1, 1u, &s_old);
-      if (A.phase_t && tid == 0) A.phase_t[n * 8 + 7] = globaltimer();
-      if (tid < r) A.ssq[static_cast<i64>(b) * r + tid] = 0.0;
-    } else {
-      const int ntiles = M.tm * M.tk;
+      signal_add(M.mcnt + kCS, 1u);
+      if (A.phase_t && tid == 0) A.phase_t[n * 16 + 7] = globaltimer();
+      // ---- norms + lambda from the tile CTAs' column sums of squares
+      wait_geq(M.mcnt + 2 * kCS, Gw);
+      ph::norms_final<RT, kFusedThreads>(r, in, w, static_cast<int>(Gw), n == 0, A.rng, fsm);
+      if (A.phase_t && tid == 0) A.phase_t[n * 16 + 13] = globaltimer();
+      signal_add(gen, 1u);
+    } else if (!is_idle) {
       const TileSmem t = tile_smem<RT>(fsm, M.zcap);
-      // this CTA's share of every one of its splits' Z rows, then arrive
+      // this CTA's share of every one of its splits' Z rows, then signal
       // (no waiting here, so CTAs with several tiles cannot deadlock)
-      for (int tt = b; tt < ntiles; tt += Gw) {
+      for (int tt = rank; tt < ntiles; tt += Gw) {
         const int mt = tt % M.tm, kb = tt / M.tm;
         const int s0 = kb * M.tklen;
         const int cnt = min(M.v.s - s0, M.tklen);
         const int zr = (cnt + M.tm - 1) / M.tm;
         const int z0 = s0 + mt * zr, z1 = min(s0 + cnt, z0 + zr);
         if (z0 < z1) z_share<RT>(M.v, z0, z1, A.z);
-        release_add(M.kb_cnt + kb, 1u, &s_old);
+        signal_add(M.kb_cnt + kb * kCS, 1u);
       }
-      for (int tt = b; tt < ntiles; tt += Gw) {
+      stamp(n, 9);
+      for (int tt = rank; tt < ntiles; tt += Gw) {
         const int mt = tt % M.tm, kb = tt / M.tm;
         const int s0 = kb * M.tklen;
         const int cnt = min(M.v.s - s0, M.tklen);
         const int kpad = (cnt + BK - 1) / BK * BK;
-        wait_geq(M.kb_cnt + kb, static_cast<unsigned>(M.tm));
+        wait_geq(M.kb_cnt + kb * kCS, static_cast<unsigned>(M.tm));
+        if (tt == static_cast<int>(rank)) stamp(n, 10);
         z_load<RT>(M.v, A.z, s0, cnt, kpad, t);
-        if (tt == static_cast<int>(b)) stamp(n, 1);
-        // Gram blocks q = mt, mt + tm, ... of this split; the last split to
-        // arrive on a block reduces it (fixed split order)
+        if (tt == static_cast<int>(rank)) stamp(n, 1);
+        // Gram blocks q = mt, mt + tm, ... of this split (the inverse CTA sums them)
         gram_blocks<RT>(t, kpad, nfr, mt, M.tm, kb, M.tk, A.gpart);
-        __syncthreads();
-        if (tid == 0) s_nlast = 0;
-        __syncthreads();
-        for (int q = mt + tid * M.tm; q < M.nblk; q += kFusedThreads * M.tm) {
-          __threadfence();
-          if (atomicAdd(M.gbt + q, 1u) == static_cast<unsigned>(M.tk - 1)) s_lastq[atomicAdd(&s_nlast, 1)] = q;
-        }
-        __syncthreads();
-        const int nl = s_nlast;
-        if (nl > 0) {
-          __threadfence();
-          for (int e = tid; e < nl * 64; e += kFusedThreads) {
-            const int q = s_lastq[e / 64], el = e % 64;
-            const double* src = A.gpart + static_cast<i64>(q) * M.tk * 64 + el;
-            double sum = 0.0;
-            for (int k = 0; k < M.tk; ++k) sum += __ldcg(src + k * 64);
-            int bi, bj;
-            gram_block_coords(q, nfr, &bi, &bj);
-            const int gi = bi * 8 + el / 8, gj = bj * 8 + el % 8;
-            A.gsum[gi * RT + gj] = sum;
-            A.gsum[gj * RT + gi] = sum;
+        if (!M.dist_gram) {
+          signal_add(M.mcnt, 1u);
+        } else {
+          signal_add(M.gm_cnt + mt * kCS, 1u);
+          if (kb == M.tk - 1 && mt < M.nblk) {
+            // row-block reducer: sum blocks q = mt, mt + tm, ... over the splits
+            wait_geq(M.gm_cnt + mt * kCS, static_cast<unsigned>(M.tk));
+            const int nq = (M.nblk - mt + M.tm - 1) / M.tm;
+            for (int e = tid; e < nq * 64; e += kFusedThreads) {
+              const int q = mt + (e / 64) * M.tm, el = e % 64;
+              const double sum = sum_strided(A.gpart + static_cast<i64>(q) * M.tk * 64 + el, 64, M.tk);
+              int bi, bj;
+              gram_block_coords(q, nfr, &bi, &bj);
+              const int gi = bi * 8 + el / 8, gj = bj * 8 + el % 8;
+              A.gsum[gi * RT + gj] = sum;
+              A.gsum[gj * RT + gi] = sum;
+            }
+            signal_add(M.mcnt, static_cast<unsigned>(nq));
           }
-          release_add(M.gready, static_cast<unsigned>(nl), &s_old);
         }
-        if (tt == static_cast<int>(b)) stamp(n, 2);
+        if (tt == static_cast<int>(rank)) stamp(n, 2);
         gemm_tile<RT>(M.v.x, M.vec16 != 0, in, static_cast<i64>(mt) * BM, r, cnt, kpad, t,
                       A.part_rhs + static_cast<i64>(kb) * in * r);
-        release_add(M.mt_cnt + mt, 1u, &s_old);
+        signal_add(M.mt_cnt + mt * kCS, 1u);
       }
       stamp(n, 3);
       // ---- apply: this CTA's share of the rows of each of its tiles
@@ -309,31 +407,21 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       const int rows_per = (BM + M.tk - 1) / M.tk;
       double* ob = rh + rows_per * LD;
       bool have_ginv = false;
-      for (int tt = b; tt < ntiles; tt += Gw) {
+      for (int tt = rank; tt < ntiles; tt += Gw) {
         const int mt = tt % M.tm, kb = tt / M.tm;
         const i64 r0 = static_cast<i64>(mt) * BM + static_cast<i64>(kb) * rows_per;
         const i64 r1 = min(min(static_cast<i64>(mt) * BM + BM, in), r0 + rows_per);
         if (r0 >= r1) continue;
         const int nrow = static_cast<int>(r1 - r0);
-        wait_geq(M.mt_cnt + mt, static_cast<unsigned>(M.tk));
-        __threadfence();
+        wait_geq(M.mt_cnt + mt * kCS, static_cast<unsigned>(M.tk));
         const i64 step = in * r;
         for (int e = tid; e < nrow * r; e += kFusedThreads) {
           const int il = e / r, c = e - il * r;
           const double* p = A.part_rhs + (r0 + il) * r + c;
-          double sum = 0.0;
-          int k = 0;
-          for (; k + 4 <= M.tk; k += 4) {
-            const double v0 = __ldcg(p + k * step), v1 = __ldcg(p + (k + 1) * step);
-            const double v2 = __ldcg(p + (k + 2) * step), v3 = __ldcg(p + (k + 3) * step);
-            sum = (((sum + v0) + v1) + v2) + v3;
-          }
-          for (; k < M.tk; ++k) sum += __ldcg(p + k * step);
-          rh[il * LD + c] = sum;
+          rh[il * LD + c] = sum_strided(p, step, M.tk);
         }
         if (!have_ginv) {
-          wait_geq(M.gready + 1, 1u);
-          __threadfence();
+          wait_geq(M.mcnt + kCS, 1u);
           for (int e = tid; e < r * r; e += kFusedThreads) {
             const int x = e / r, y = e - x * r;
             gi[x * LD + y] = __ldcg(A.ginv + e);
@@ -353,36 +441,20 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
           for (int il = 0; il < nrow; ++il) q2 += ob[il * LD + tid] * ob[il * LD + tid];
         __syncthreads();
       }
-      if (tid < r) A.ssq[static_cast<i64>(b) * r + tid] = q2;
-    }
-    stamp(n, 4);
-    // ---- ticket: the last CTA forms the norms and releases the next mode
-    {
-      volatile unsigned* gen = A.bar + 1;
-      __syncthreads();
-      unsigned g0 = 0;
-      if (tid == 0) {
-        g0 = *gen;
-        __threadfence();
-        s_last = (atomicAdd(&A.ticket[0], 1u) == G - 1u);
-      }
-      __syncthreads();
+      stamp(n, 4);
+      if (tid < r) A.ssq[static_cast<i64>(rank) * r + tid] = q2;
+      signal_add(M.mcnt + 2 * kCS, 1u);
       stamp(n, 5);
-      if (s_last) {
-        __threadfence();
-        ph::norms_final<RT, kFusedThreads>(r, in, w, G, n == 0, A.rng, fsm);
-        if (tid == 0) {
-          A.ticket[0] = 0u;
-          __threadfence();
-          atomicAdd(A.bar + 1, 1u);
-        }
-      } else if (tid == 0) {
-        while (ld_acquire(A.bar + 1) == g0) __nanosleep(32);
-      }
+    }
+    // ---- wait for the release of mode n (the inverse CTA formed the norms)
+    if (!is_inv) {
+      if (tid == 0)
+        while (static_cast<int>(ld_acquire(gen) - (gen0 + n + 1)) < 0) __nanosleep(32);
       __syncthreads();
     }
     stamp(n, 6);
   }
+  if (A.next) prefetch_tables(*A.next, b);
   // ---- sampled fit + stop rule (sampling.hpp:191-210, :237-251)
   if (A.has_fit) {
     const FitArgs& f = A.fit;
@@ -425,7 +497,7 @@ template <int RT>
 size_t rand_smem_for(int zcap) {
   i64 need = tl::tile_smem_doubles<RT>(zcap);
   need = std::max<i64>(need, static_cast<i64>(RT) * (RT + 1) + 2 * static_cast<i64>(tl::BM) * (RT + 1));
-  need = std::max<i64>(need, 24 * RT + 64);
+  need = std::max<i64>(need, 48 * RT + 256);
   need = std::max<i64>(need, static_cast<i64>(kFusedThreads / RT) * (RT + 1));
   need = std::max<i64>(need, 256);
   return static_cast<size_t>(need) * sizeof(double);

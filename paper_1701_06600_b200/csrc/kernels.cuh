@@ -179,11 +179,18 @@ struct FusedMode {
   int tm, tk, tklen;     // row blocks, sample splits, samples per split
   int nblk;              // upper 8 x 8 Gram blocks
   int zcap;              // Z rows the tile's shared memory holds
-  unsigned* mt_cnt;      // [tm] splits finished per row block
-  unsigned* gbt;         // [64] splits finished per Gram block
-  unsigned* gready;      // [0] Gram blocks reduced, [1] Gram inverse ready
-  unsigned* kb_cnt;      // [tk] CTAs that wrote their share of split kb's Z rows
+  unsigned* mt_cnt;      // [tm] splits finished per row block                      (stride kCS)
+  unsigned* kb_cnt;      // [tk] CTAs that wrote their share of split kb's Z rows   (stride kCS)
+  unsigned* gm_cnt;      // [tm] splits whose Gram blocks of row block mt are written  (stride kCS)
+  int dist_gram;         // 1: tile (mt, tk-1) sums row block mt's Gram blocks (one tile per CTA)
+  unsigned* mcnt;        // [0] Gram blocks summed (or tiles written), [1] inverse ready,
+                         // [2] tile CTAs whose sums of squares are written        (stride kCS)
 };
+// Inter-CTA counters live one per 128-byte line (atomics and polling on a
+// shared line serialize): kCS words apart.
+constexpr int kCS = 32;
+constexpr int kSyncWords = 3 * kCS + 128 * kCS;  // gram_done, barrier, tickets, ssq group tickets
+struct FusedIter;
 struct FusedIter {
   int order, r, first_mode_first_of_pass;
   FusedMode mode[kMaxOrder];
@@ -197,7 +204,15 @@ struct FusedIter {
   const int* stop;
   int has_fit;
   FitArgs fit;
-  unsigned long long* phase_t;  // optional: CTA 0 stamps globaltimer at phase edges [order][8]
+  unsigned long long* phase_t;  // optional: CTA 0 stamps globaltimer at phase edges [order][16]
+  // CPRAND kernel roles: the Gram-inverse CTA and an idle CTA sharing its SM
+  // (-1: none), chosen from a census launch (census != null: every CTA writes
+  // its SM id to census[blockIdx] and returns).
+  int inv_cta, idle_cta;
+  int* census;
+  unsigned* grp_cnt;             // CPRAND kernel: ssq group tickets [grid / 16] (stride kCS)
+  const FusedIter* next;         // next iteration's arguments (L2 prefetch of its tables)
+  unsigned long long* cta_t;  // debug: per-CTA stamps of mode 1 [grid][16] (CPRAND_DEBUG_CTA)
 };
 size_t fused_smem_bytes(int rt, bool mix, int max_dim);
 // CPRAND kernel: Z rows per tile, its dynamic shared memory, and the tiling

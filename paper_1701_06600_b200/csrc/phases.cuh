@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cfloat>
+#include <type_traits>
 
 #include "devutil.cuh"
 #include "kernels.cuh"
@@ -533,6 +534,32 @@ __device__ __forceinline__ bool inv4_minors(const double* a, double* out, double
   return ok;
 }
 
+// 4 x 4 inverse by cofactors, one entry per lane (lanes 0..15; all 32 lanes
+// must call): lane 4 i + j forms the 3 x 3 minor of P without row j and
+// column i from p (row-major, shared memory), det P from the row-0
+// cofactors (shuffles), and returns P^-1(i, j) = C_ji / det. The rank test
+// uses the leading principal minors d_k (pivot_k = d_k / d_{k-1}) without
+// divisions; ok is uniform over the warp.
+__device__ __forceinline__ double inv4_cofactor(const double* p, double thr, bool& ok) {
+  const int l = threadIdx.x & 31, i = (l >> 2) & 3, j = l & 3;
+  const int r0 = (0 >= j) ? 1 : 0, r1 = (1 >= j) ? 2 : 1, r2 = (2 >= j) ? 3 : 2;
+  const int c0 = (0 >= i) ? 1 : 0, c1 = (1 >= i) ? 2 : 1, c2 = (2 >= i) ? 3 : 2;
+  const double m00 = p[r0 * 4 + c0], m01 = p[r0 * 4 + c1], m02 = p[r0 * 4 + c2];
+  const double m10 = p[r1 * 4 + c0], m11 = p[r1 * 4 + c1], m12 = p[r1 * 4 + c2];
+  const double m20 = p[r2 * 4 + c0], m21 = p[r2 * 4 + c1], m22 = p[r2 * 4 + c2];
+  const double det3 = fma(m00, fma(m11, m22, -m12 * m21), fma(-m01, fma(m10, m22, -m12 * m20), m02 * fma(m10, m21, -m11 * m20)));
+  const double cof = ((i + j) & 1) ? -det3 : det3;  // C_ji
+  // det P = sum_k P(0, k) C_0k (C_0k lives on lane 4 k)
+  const double q0 = __shfl_sync(0xffffffffu, cof, 0), q1 = __shfl_sync(0xffffffffu, cof, 4);
+  const double q2 = __shfl_sync(0xffffffffu, cof, 8), q3 = __shfl_sync(0xffffffffu, cof, 12);
+  const double d3 = __shfl_sync(0xffffffffu, cof, 15);  // C_33 = det P[0..2][0..2]
+  const double det = fma(p[0], q0, p[1] * q1) + fma(p[2], q2, p[3] * q3);
+  const double d1 = p[0], d2 = fma(p[0], p[5], -p[1] * p[4]);
+  ok = (d1 > thr) && (d2 > thr * d1) && (d3 > thr * d2) && (det > thr * d3) && (d1 > 0.0) && (d2 > 0.0) &&
+       (d3 > 0.0) && (det > 0.0);
+  return cof * rcp_nr(det);
+}
+
 // Block Gauss-Jordan inverse (4 x 4 pivot blocks, no pivoting: the Gram is
 // SPD) by one CTA of 256 threads, one barrier per step.
 //  * Warps 0-6 hold the matrix as FP64 MMA accumulator fragments (warp w:
@@ -553,7 +580,8 @@ __device__ __forceinline__ bool inv4_minors(const double* a, double* out, double
 // (r x r) for the pivoted fallback. sh: 24 RT + 64 doubles.
 template <int RT>
 __device__ bool inverse_la(const double* __restrict__ g, int r, double tol, double* __restrict__ ginv,
-                           double* __restrict__ gfull, int* info, double* sh) {
+                           double* __restrict__ gfull, int* info, double* sh,
+                           unsigned long long* stamps = nullptr) {
   constexpr int NTI = RT / 8;
   constexpr int NSMAX = RT / 4;
   static_assert(NTI <= 8, "one 8-column tile per warp");
@@ -598,132 +626,402 @@ __device__ bool inverse_la(const double* __restrict__ g, int r, double tol, doub
     }
   }
   CPB_INV_STAMP(1);
-  // Publish rows K = [n0, n0+4) (identity on K x K) and raw rows [n0+4, n0+8)
-  // into rb, -a(., K) (+e on rows K) into cb; zero rows/columns K. n0 is a
-  // compile-time constant at every call site (unrolled step loop).
-  auto publish = [&](const int n0, double* rb, double* cb, const bool first) {
-    const int tk = n0 / 8, tn = (n0 + 4) / 8;
+  // Publish rows K (identity on K x K) and the raw rows K+ after them into
+  // rb, -a(., K) (+e on rows K) into cb (owner warp of the K columns), and
+  // zero rows/columns K. Fragment slot p holds row tile (T + p) % NTI (the
+  // slots rotate once per tile), so every slot index here is compile-time:
+  // rows K are local rows RK..RK+3 of slot PK, rows K+ local rows RKK.. of
+  // slot PKK, columns K local columns 4 CH..4 CH+3 of the owner.
+  auto publish = [&](auto pk, auto rk0, auto pkk, auto rkk0, auto ch, int T, bool own, double* rb, double* cb,
+                     bool first) {
+    constexpr int PK = decltype(pk)::value, RK = decltype(rk0)::value;
+    constexpr int PKK = decltype(pkk)::value, RKK = decltype(rkk0)::value, CH = decltype(ch)::value;
     if (!worker) return;  // warp-uniform
     const int col = ct * 8 + lc;
-    const bool ck0 = static_cast<unsigned>(col - n0) < 4u, ck1 = static_cast<unsigned>(col + 1 - n0) < 4u;
-    if (tk < NTI) {
-      const int qi = tk * 8 + lr - n0;
-      if (static_cast<unsigned>(qi) < 4u) {
-        const double v0 = acc[tk][0], v1 = acc[tk][1];
-        if (first) {
-          if (ck0) tmp[qi * 4 + col - n0] = v0;
-          if (ck1) tmp[qi * 4 + col + 1 - n0] = v1;
+    const bool inK = (lr >= RK && lr < RK + 4);
+    const bool inKK = (lr >= RKK && lr < RKK + 4) && (((T + PKK) % NTI) * 8 + lr < r4);
+    const bool ck = (lk >> 1) == CH;  // my two columns are in K (owner warp only)
+    {  // rows K (slot PK)
+      const int qi = lr - RK;
+      if (inK) {
+        const double v0 = acc[PK][0], v1 = acc[PK][1];
+        if (first && own && ck) {
+          tmp[qi * 4 + (lc & 3)] = v0;
+          tmp[qi * 4 + (lc & 3) + 1] = v1;
         }
         double2 o;
-        o.x = ck0 ? (qi == col - n0 ? 1.0 : 0.0) : v0;
-        o.y = ck1 ? (qi == col + 1 - n0 ? 1.0 : 0.0) : v1;
+        o.x = (own && ck) ? (qi == (lc & 3) ? 1.0 : 0.0) : v0;
+        o.y = (own && ck) ? (qi == (lc & 3) + 1 ? 1.0 : 0.0) : v1;
         *reinterpret_cast<double2*>(rb + qi * RT + col) = o;
       }
     }
-    if (tn < NTI) {
-      const int qi = tn * 8 + lr - n0;
-      if (qi >= 4 && qi < 8 && tn * 8 + lr < r4)
-        *reinterpret_cast<double2*>(rb + qi * RT + col) = make_double2(acc[tn][0], acc[tn][1]);
-    }
-    if (ct == tk) {  // warp-uniform: this warp owns columns K
+    if (inKK)  // raw rows K+ (slot PKK)
+      *reinterpret_cast<double2*>(rb + (4 + lr - RKK) * RT + col) = make_double2(acc[PKK][0], acc[PKK][1]);
+    if (own && ck) {  // column block K, every slot
 #pragma unroll
-      for (int mt = 0; mt < NTI; ++mt) {
-        const int row = mt * 8 + lr;
-        const bool rk = static_cast<unsigned>(row - n0) < 4u;
-        if (ck0) {
-          cb[row * 4 + col - n0] = rk ? (row == col ? 1.0 : 0.0) : -acc[mt][0];
-          acc[mt][0] = 0.0;
-        }
-        if (ck1) {
-          cb[row * 4 + col + 1 - n0] = rk ? (row == col + 1 ? 1.0 : 0.0) : -acc[mt][1];
-          acc[mt][1] = 0.0;
-        }
+      for (int p = 0; p < NTI; ++p) {
+        const int row = ((T + p) % NTI) * 8 + lr;
+        const bool rkk = (p == PK) && inK;
+        const int q0 = (lc & 3);
+        double2 o;
+        o.x = rkk ? ((lr - RK) == q0 ? 1.0 : 0.0) : -acc[p][0];
+        o.y = rkk ? ((lr - RK) == q0 + 1 ? 1.0 : 0.0) : -acc[p][1];
+        *reinterpret_cast<double2*>(cb + row * 4 + q0) = o;
+        acc[p][0] = 0.0;
+        acc[p][1] = 0.0;
       }
     }
-    if (tk < NTI && static_cast<unsigned>(tk * 8 + lr - n0) < 4u) {  // zero rows K
-      acc[tk][0] = 0.0;
-      acc[tk][1] = 0.0;
+    if (inK) {
+      acc[PK][0] = 0.0;
+      acc[PK][1] = 0.0;
     }
   };
-  publish(0, rbs, cbs, true);
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  using I4 = std::integral_constant<int, 4>;
+  publish(I0{}, I0{}, I0{}, I4{}, I0{}, 0, ct == 0, rbs, cbs, true);
   __syncthreads();
-  if (w == 7 && l == 0) {
-    double p[16], o[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) p[e] = tmp[e];
-    const bool ok = inv4_minors(p, o, thr);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) pin[e] = o[e];
-    misc[2] = ok ? 0.0 : 1.0;
+  if (w == 7) {
+    bool ok;
+    const double v = inv4_cofactor(tmp, thr, ok);
+    if (l < 16) pin[l] = v;
+    if (l == 0) misc[2] = ok ? 0.0 : 1.0;
   }
   __syncthreads();
   CPB_INV_STAMP(2);
+  if (stamps && tid == 0) stamps[0] = globaltimer();
   bool fail = false;
+  int T = 0;
+#pragma unroll 1
+  for (; T < nt && !fail; ++T) {
 #pragma unroll
-  for (int s = 0; s < NSMAX; ++s) {
-    if (s >= nsteps) break;  // uniform
+    for (int h = 0; h < 2; ++h) {
+      const int s = 2 * T + h;
+      if (s >= nsteps) break;  // uniform
+      CPB_INV_STAMP(3 + s);
+      const int pb = s & 1, k0 = 4 * s;
+      if (misc[2 + pb] != 0.0) {
+        fail = true;  // uniform
+        break;
+      }
+      const double* P = pin + 16 * pb;
+      const double* rb = rbs + pb * 8 * RT;
+      const double* cb = cbs + pb * RT * 4;
+      if (w == 7 && k0 + 4 < r4) {
+        // warp 7: pivot block of step s+1 = rows/columns K_{s+1} after step s
+        if (l < 16) {
+          const int x = l >> 2, y = l & 3;
+          const int jj = k0 + 4 + y;
+          const double* rn = rb + (4 + x) * RT;  // raw row k0 + 4 + x
+          double mv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            mv[q] = fma(P[q * 4], rb[jj], P[q * 4 + 1] * rb[RT + jj]) +
+                    fma(P[q * 4 + 2], rb[2 * RT + jj], P[q * 4 + 3] * rb[3 * RT + jj]);
+          tmp[l] = (rn[jj] - fma(rn[k0], mv[0], rn[k0 + 1] * mv[1])) - fma(rn[k0 + 2], mv[2], rn[k0 + 3] * mv[3]);
+        }
+        __syncwarp();
+        CPB_INV_STAMP_AT(43, s, l == 0);
+        {
+          bool ok;
+          const double v = inv4_cofactor(tmp, thr, ok);
+          if (l < 16) pin[16 * (pb ^ 1) + l] = v;
+          if (l == 0) misc[2 + (pb ^ 1)] = ok ? 0.0 : 1.0;
+        }
+        CPB_INV_STAMP_AT(44, s, l == 0);
+      }
+      if (worker) {
+        // all fragment operands are loaded before the first MMA
+        const double2 p01 = *reinterpret_cast<const double2*>(P + lk * 4);
+        const double2 p23 = *reinterpret_cast<const double2*>(P + lk * 4 + 2);
+        double am[NTI];
+#pragma unroll
+        for (int p = 0; p < NTI; ++p) am[p] = cb[(((T + p) % NTI) * 8 + lr) * 4 + lk];  // rows >= r4 hold zeros
+        const int j = ct * 8 + lr;  // B fragment (k = l % 4, n = l / 4)
+        const double bm = fma(p01.x, rb[j], p01.y * rb[RT + j]) + fma(p23.x, rb[2 * RT + j], p23.y * rb[3 * RT + j]);
+#pragma unroll
+        for (int p = 0; p < NTI; ++p)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[p][0]), "+d"(acc[p][1])
+                       : "d"(am[p]), "d"(bm));
+        CPB_INV_STAMP_AT(41, s, tid == 0);
+        if (k0 + 4 < r4) {
+          double* rbn = rbs + (pb ^ 1) * 8 * RT;
+          double* cbn = cbs + (pb ^ 1) * RT * 4;
+          if (h == 0)  // K' = rows 4..7 of tile T (slot 0), K'' = rows 0..3 of tile T+1 (slot 1)
+            publish(I0{}, I4{}, I1{}, I0{}, I1{}, T, ct == T, rbn, cbn, false);
+          else  // K' = rows 0..3 of tile T+1 (slot 1), K'' = rows 4..7 of tile T+1
+            publish(I1{}, I0{}, I1{}, I4{}, I0{}, T, ct == T + 1, rbn, cbn, false);
+        }
+      }
+      CPB_INV_STAMP_AT(42, s, tid == 0);
+      CPB_INV_STAMP_AT(45, s, tid == 224);
+      __syncthreads();
+    }
+    // rotate the slots: slot 0 <- tile T + 1
+    double f0 = acc[0][0], f1 = acc[0][1];
+#pragma unroll
+    for (int p = 0; p + 1 < NTI; ++p) {
+      acc[p][0] = acc[p + 1][0];
+      acc[p][1] = acc[p + 1][1];
+    }
+    acc[NTI - 1][0] = f0;
+    acc[NTI - 1][1] = f1;
+  }
+  CPB_INV_STAMP(30);
+  if (stamps && tid == 0) stamps[1] = globaltimer();
+  if (!fail && worker) {
+#pragma unroll
+    for (int p = 0; p < NTI; ++p) {
+      const int mt = (T + p) % NTI;
+      const int row = mt * 8 + lr, col = ct * 8 + lc;
+      if (mt >= nt || row >= r) continue;
+      if (col + 1 < r && !(r & 1))
+        *reinterpret_cast<double2*>(ginv + row * r + col) = make_double2(acc[p][0], acc[p][1]);
+      else {
+        if (col < r) ginv[row * r + col] = acc[p][0];
+        if (col + 1 < r) ginv[row * r + col + 1] = acc[p][1];
+      }
+    }
+  }
+  if (tid == 0) info[0] = fail ? -1 : r;
+  __syncthreads();
+  CPB_INV_STAMP(31);
+  return fail;
+}
+
+// ------------------------------------------- Gram inverse, 8-wide steps
+// Unpivoted 8 x 8 Gauss-Jordan inverse by one warp: lane l holds
+// p[0] = P(l/4, l%4) and p[1] = P(l/4, l%4 + 4), in and out. ok = false
+// when a pivot is <= thr (or not positive).
+__device__ __forceinline__ void inv8_warp(double (&p)[2], double thr, bool& ok) {
+  const int l = threadIdx.x & 31, x = l >> 2, y = l & 3;
+  ok = true;
+#pragma unroll 1
+  for (int k = 0; k < 8; ++k) {
+    const int ks = k >> 2, kl = k & 3;
+    const double pk0 = __shfl_sync(0xffffffffu, p[0], k * 4 + kl);
+    const double pk1 = __shfl_sync(0xffffffffu, p[1], k * 4 + kl);
+    const double rk0 = __shfl_sync(0xffffffffu, p[0], k * 4 + y);
+    const double rk1 = __shfl_sync(0xffffffffu, p[1], k * 4 + y);
+    const double cx0 = __shfl_sync(0xffffffffu, p[0], x * 4 + kl);
+    const double cx1 = __shfl_sync(0xffffffffu, p[1], x * 4 + kl);
+    const double pkk = ks ? pk1 : pk0;
+    if (!(pkk > thr) || !(pkk > 0.0)) ok = false;
+    const double q = rcp_nr(pkk);
+    const double ck = (x == k) ? -1.0 : (ks ? cx1 : cx0);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int col = y + 4 * e;
+      const double rkv = (col == k) ? q : (e ? rk1 : rk0) * q;
+      const double xv = (x == k || col == k) ? 0.0 : p[e];
+      p[e] = fma(-ck, rkv, xv);
+    }
+  }
+}
+
+// Block Gauss-Jordan inverse with 8 x 8 pivot blocks (no pivoting: the Gram
+// is SPD, padded to a multiple of 8 with d_max on the padding diagonal) by
+// one CTA of 256 threads, one barrier per step; step s pivots on tile s.
+//  * Warp w holds 8-column tile w as FP64 MMA accumulator fragments (every
+//    8-row tile) and does step s as two m8n8k4 MMAs per tile:
+//    a' = X + (-C) M, X = a with rows/columns K zeroed, -C(i) = -a(i, K)
+//    (+e on rows K) from the published column block, M(j) = P^-1 a(K, j)
+//    from the published row block whose K columns hold the identity: the
+//    four Gauss-Jordan block rules in one form.
+//  * After its MMAs each warp publishes its part of the next row block
+//    (identity on the next K) and the raw row block after it; the owner of
+//    the next column tile publishes -C; rows/columns of the next K are
+//    zeroed in the fragments. The step loop is unrolled (compile-time tiles).
+//  * Warp 7 (first, when it also owns a tile) forms the next pivot block from
+//    the raw rows and inverts it (inv8_warp), off the workers' critical path.
+// g: RT x RT Gram (ld RT; entries outside [0, r) ignored). Returns true
+// (uniformly) on a pivot <= tol * d_max, after writing the Gram to gfull
+// (r x r) for the pivoted fallback. sh: 48 RT + 256 doubles.
+template <int RT>
+__device__ bool inverse_b8(const double* __restrict__ g, int r, double tol, double* __restrict__ ginv,
+                           double* __restrict__ gfull, int* info, double* sh,
+                           unsigned long long* stamps = nullptr) {
+  constexpr int NTI = RT / 8;
+  static_assert(NTI <= 8, "one 8-column tile per warp");
+  double* rbs = sh;              // [2][16][RT] rows K_s (identity on K_s columns), raw rows K_{s+1}
+  double* cbs = rbs + 32 * RT;   // [2][RT][8]  -a(i, K_s), +e on rows K_s
+  double* pin = cbs + 16 * RT;   // [2][64]     inverse of the pivot block of step s
+  double* mtmp = pin + 128;      // [64]        look-ahead scratch
+  double* misc = mtmp + 64;      // [2..3] fail flags, [4..5] warp maxima
+  const int tid = threadIdx.x, w = tid / 32, l = tid % 32;
+  const int lr = l >> 2, lc = (l & 3) * 2, lk = l & 3;
+  const int r8 = (r + 7) & ~7;
+  const int nt = r8 / 8;
+  const bool worker = w < nt;  // warp w owns 8-column tile w
+  double acc[NTI][2];
+#pragma unroll
+  for (int mt = 0; mt < NTI; ++mt) {
+    const int row = mt * 8 + lr, col = w * 8 + lc;
+    const bool ok = worker && row < r;
+    acc[mt][0] = (ok && col < r) ? __ldcg(g + row * RT + col) : 0.0;
+    acc[mt][1] = (ok && col + 1 < r) ? __ldcg(g + row * RT + col + 1) : 0.0;
+  }
+  {  // d_max: largest (clamped) diagonal entry
+    double dv = (tid < r) ? fmax(__ldcg(g + tid * (RT + 1)), 0.0) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dv = fmax(dv, __shfl_xor_sync(0xffffffffu, dv, o));
+    if (l == 0 && w < 2) misc[4 + w] = dv;
+  }
+  __syncthreads();
+  const double dmax = RT > 32 ? fmax(misc[4], misc[5]) : misc[4];
+  const double thr = tol * dmax;
+  CPB_INV_STAMP(1);
+  if (worker) {
+#pragma unroll
+    for (int mt = 0; mt < NTI; ++mt) {
+      const int row = mt * 8 + lr;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = w * 8 + lc + e;
+        if (row < r && col < r) gfull[row * r + col] = acc[mt][e];
+        if (row == col && row >= r && row < r8) acc[mt][e] = dmax;  // padding diagonal
+      }
+    }
+  }
+  // publish step n's blocks (tile n; runtime n, fragments selected by
+  // compile-time tile loops so nothing is indexed dynamically)
+  auto publish = [&](const int n, double* rb, double* cb) {
+    if (!worker) return;  // warp-uniform
+    const bool own = (w == n);
+#pragma unroll
+    for (int mt = 0; mt < NTI; ++mt) {
+      const int row = mt * 8 + lr;
+      if (own) {
+        double2 o;
+        o.x = (mt == n) ? (lr == lc ? 1.0 : 0.0) : -acc[mt][0];
+        o.y = (mt == n) ? (lr == lc + 1 ? 1.0 : 0.0) : -acc[mt][1];
+        *reinterpret_cast<double2*>(cb + row * 8 + lc) = o;
+      }
+      if (mt == n) {
+        double2 o;
+        o.x = own ? (lr == lc ? 1.0 : 0.0) : acc[mt][0];
+        o.y = own ? (lr == lc + 1 ? 1.0 : 0.0) : acc[mt][1];
+        *reinterpret_cast<double2*>(rb + lr * RT + w * 8 + lc) = o;
+      }
+      if (mt == n + 1 && mt < nt)
+        *reinterpret_cast<double2*>(rb + (8 + lr) * RT + w * 8 + lc) = make_double2(acc[mt][0], acc[mt][1]);
+      if (mt == n || own) acc[mt][0] = acc[mt][1] = 0.0;
+    }
+  };
+  // raw first pivot block (tile 0 of warp 0) for warp 7
+  if (w == 0) *reinterpret_cast<double2*>(mtmp + lr * 8 + lc) = make_double2(acc[0][0], acc[0][1]);
+  publish(0, rbs, cbs);
+  __syncthreads();
+  if (w == 7) {
+    double p[2] = {mtmp[lr * 8 + lk], mtmp[lr * 8 + lk + 4]};
+    bool ok;
+    inv8_warp(p, thr, ok);
+    pin[lr * 8 + lk] = p[0];
+    pin[lr * 8 + lk + 4] = p[1];
+    if (l == 0) misc[2] = ok ? 0.0 : 1.0;
+  }
+  __syncthreads();
+  CPB_INV_STAMP(2);
+  if (stamps && tid == 0) stamps[0] = globaltimer();
+  bool fail = false;
+#pragma unroll 1
+  for (int s = 0; s < nt; ++s) {
     CPB_INV_STAMP(3 + s);
-    const int pb = s & 1, k0 = 4 * s;
+    const int pb = s & 1;
     if (misc[2 + pb] != 0.0) {
       fail = true;  // uniform
       break;
     }
-    const double* P = pin + 16 * pb;
-    const double* rb = rbs + pb * 8 * RT;
-    const double* cb = cbs + pb * RT * 4;
-    if (w == 7 && k0 + 4 < r4) {
-      // warp 7: pivot block of step s+1 = rows/columns K_{s+1} after step s
-      if (l < 16) {
-        const int x = l >> 2, y = l & 3;
-        const int jj = k0 + 4 + y;
-        const double* rn = rb + (4 + x) * RT;  // raw row k0 + 4 + x
-        double mv[4];
+    const double* P = pin + 64 * pb;
+    const double* rb = rbs + pb * 16 * RT;
+    const double* cb = cbs + pb * RT * 8;
+    if (w == 7 && s + 1 < nt) {
+      // look-ahead: pivot block of step s+1 = rows/columns of tile s+1 after step s
+      const int k0 = 8 * s, k1 = 8 * (s + 1);
+      {  // M_q(j) = sum_t P(q, t) a(K_t, j) for q = l/4, j = k1 + l%4 (+4)
+        const int q = lr;
+        double m0 = 0.0, m1 = 0.0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          mv[q] = fma(P[q * 4], rb[jj], P[q * 4 + 1] * rb[RT + jj]) +
-                  fma(P[q * 4 + 2], rb[2 * RT + jj], P[q * 4 + 3] * rb[3 * RT + jj]);
-        tmp[l] = (rn[jj] - fma(rn[k0], mv[0], rn[k0 + 1] * mv[1])) - fma(rn[k0 + 2], mv[2], rn[k0 + 3] * mv[3]);
+        for (int t = 0; t < 8; ++t) {
+          const double pq = P[q * 8 + t];
+          m0 = fma(pq, rb[t * RT + k1 + lk], m0);
+          m1 = fma(pq, rb[t * RT + k1 + lk + 4], m1);
+        }
+        mtmp[q * 8 + lk] = m0;
+        mtmp[q * 8 + lk + 4] = m1;
       }
       __syncwarp();
+      double p[2];
+      {
+        const double* rn = rb + (8 + lr) * RT;  // raw row k1 + x
+        double v0 = rn[k1 + lk], v1 = rn[k1 + lk + 4];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double c = rn[k0 + q];
+          v0 = fma(-c, mtmp[q * 8 + lk], v0);
+          v1 = fma(-c, mtmp[q * 8 + lk + 4], v1);
+        }
+        p[0] = v0;
+        p[1] = v1;
+      }
+      bool ok;
       CPB_INV_STAMP_AT(43, s, l == 0);
-      if (l == 0) {
-        double p[16], o[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) p[e] = tmp[e];
-        const bool ok = inv4_minors(p, o, thr);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) pin[16 * (pb ^ 1) + e] = o[e];
-        misc[2 + (pb ^ 1)] = ok ? 0.0 : 1.0;
-      }
-      __syncwarp();
+      inv8_warp(p, thr, ok);
       CPB_INV_STAMP_AT(44, s, l == 0);
+      pin[64 * (pb ^ 1) + lr * 8 + lk] = p[0];
+      pin[64 * (pb ^ 1) + lr * 8 + lk + 4] = p[1];
+      if (l == 0) misc[2 + (pb ^ 1)] = ok ? 0.0 : 1.0;
+      __syncwarp();
     }
     if (worker) {
       // all fragment operands are loaded before the first MMA
-      const double2 p01 = *reinterpret_cast<const double2*>(P + lk * 4);
-      const double2 p23 = *reinterpret_cast<const double2*>(P + lk * 4 + 2);
-      double am[NTI];
+      double pr0[8], pr1[8];  // rows l%4 and l%4 + 4 of P^-1
 #pragma unroll
-      for (int mt = 0; mt < NTI; ++mt) am[mt] = cb[(mt * 8 + lr) * 4 + lk];  // rows >= r4 hold zeros
-      const int j = ct * 8 + lr;  // B fragment (k = l % 4, n = l / 4)
-      const double bm = fma(p01.x, rb[j], p01.y * rb[RT + j]) + fma(p23.x, rb[2 * RT + j], p23.y * rb[3 * RT + j]);
+      for (int t = 0; t < 8; t += 2) {
+        const double2 a = *reinterpret_cast<const double2*>(P + lk * 8 + t);
+        const double2 c = *reinterpret_cast<const double2*>(P + (lk + 4) * 8 + t);
+        pr0[t] = a.x;
+        pr0[t + 1] = a.y;
+        pr1[t] = c.x;
+        pr1[t + 1] = c.y;
+      }
+      const int j = w * 8 + lr;  // B fragment (k = l % 4 (+4), n = l / 4)
+      double bm0 = 0.0, bm1 = 0.0;
 #pragma unroll
-      for (int mt = 0; mt < NTI; ++mt)
+      for (int t = 0; t < 8; ++t) {
+        const double rv = rb[t * RT + j];
+        bm0 = fma(pr0[t], rv, bm0);
+        bm1 = fma(pr1[t], rv, bm1);
+      }
+      double am[NTI][2];
+#pragma unroll
+      for (int mt = 0; mt < NTI; ++mt) {
+        am[mt][0] = cb[(mt * 8 + lr) * 8 + lk];
+        am[mt][1] = cb[(mt * 8 + lr) * 8 + lk + 4];
+      }
+#pragma unroll
+      for (int mt = 0; mt < NTI; ++mt) {
         asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                      : "+d"(acc[mt][0]), "+d"(acc[mt][1])
-                     : "d"(am[mt]), "d"(bm));
+                     : "d"(am[mt][0]), "d"(bm0));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[mt][0]), "+d"(acc[mt][1])
+                     : "d"(am[mt][1]), "d"(bm1));
+      }
       CPB_INV_STAMP_AT(41, s, tid == 0);
-      if (k0 + 4 < r4) publish(k0 + 4, rbs + (pb ^ 1) * 8 * RT, cbs + (pb ^ 1) * RT * 4, false);
+      if (s + 1 < nt) publish(s + 1, rbs + (pb ^ 1) * 16 * RT, cbs + (pb ^ 1) * RT * 8);
     }
     CPB_INV_STAMP_AT(42, s, tid == 0);
     CPB_INV_STAMP_AT(45, s, tid == 224);
     __syncthreads();
   }
   CPB_INV_STAMP(30);
+  if (stamps && tid == 0) stamps[1] = globaltimer();
   if (!fail && worker) {
 #pragma unroll
     for (int mt = 0; mt < NTI; ++mt) {
-      const int row = mt * 8 + lr, col = ct * 8 + lc;
+      const int row = mt * 8 + lr, col = w * 8 + lc;
       if (mt >= nt || row >= r) continue;
       if (col + 1 < r && !(r & 1))
         *reinterpret_cast<double2*>(ginv + row * r + col) = make_double2(acc[mt][0], acc[mt][1]);
@@ -917,8 +1215,19 @@ __device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int fi
   const int tid = threadIdx.x, part = tid / RT, c = tid % RT;
   __shared__ int s_zero;
   double q = 0.0;
-  if (c < r)
-    for (int b = part; b < nparts; b += NP) q += __ldcg(w.ssq + static_cast<i64>(b) * r + c);
+  if (c < r && part < nparts) {  // partials part, part + NP, ... in order, 16 loads in flight
+    const double* p = w.ssq + static_cast<i64>(part) * r + c;
+    const i64 step = static_cast<i64>(NP) * r;
+    const int cnt = (nparts - part + NP - 1) / NP;
+    for (int k = 0; k < cnt; k += 16) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = (k + u < cnt) ? __ldcg(p + (k + u) * step) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (k + u < cnt) q += v[u];
+    }
+  }
   red[part * (RT + 1) + c] = q;
   if (tid == 0) s_zero = 0;
   __syncthreads();

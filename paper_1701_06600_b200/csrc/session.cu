@@ -1,3 +1,5 @@
+#include <cstdlib>
+#include <cstdio>
 // Host orchestration of the B200 CPRAND / CPRAND-MIX outer loop.
 //
 // Mirrors cprand() (sampling.hpp:257-310), cprand_mix_impl()
@@ -299,6 +301,7 @@ Session::~Session() {
   dfree(phase_t_);
   dfree(fsync_);
   dfree(fcnt_);
+  dfree(cta_t_);
   dfree(gpart_);
   dfree(gsum_);
   for (auto& e : ev_gathered_) cudaEventDestroy(e);
@@ -474,6 +477,30 @@ void Session::setup_fused() {
     max_gp = std::max(max_gp, gp);
   }
   if (fgrid_ < max_gp + 2) return;
+  // CPRAND kernel roles: a census launch maps CTAs to SMs; the Gram-inverse
+  // CTA gets its SM to itself (its partner CTA idles) so the serial inverse
+  // does not share the FP64 pipe with a GEMM tile. Only performance depends
+  // on the mapping staying the same across launches.
+  int inv_cta = fgrid_ - 1, idle_cta = -1;
+  if (!mix_) {
+    int* cen = dalloc<int>(static_cast<size_t>(fgrid_));
+    FusedIter* dc = dalloc<FusedIter>(1);
+    FusedIter c{};
+    c.census = cen;
+    CPB_CUDA(cudaMemcpyAsync(dc, &c, sizeof(c), cudaMemcpyHostToDevice, stream_));
+    launch_fused_iteration(dc, rt_, false, fgrid_, fsmem_, stream_);
+    std::vector<int> sm(static_cast<size_t>(fgrid_));
+    CPB_CUDA(cudaMemcpyAsync(sm.data(), cen, sm.size() * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+    for (int b = 0; b < fgrid_ - 1; ++b)
+      if (sm[static_cast<size_t>(b)] == sm[static_cast<size_t>(inv_cta)]) {
+        idle_cta = b;
+        break;
+      }
+    dfree(cen);
+    dfree(dc);
+  }
+  const int gw = fgrid_ - 1 - (idle_cta >= 0 ? 1 : 0);
   // CPRAND kernel tiling per mode
   std::vector<int> tm(static_cast<size_t>(order_)), tk(tm), tkl(tm);
   const int nfr = (r_ + 7) / 8, nblk = nfr * (nfr + 1) / 2;
@@ -483,7 +510,7 @@ void Session::setup_fused() {
     int& tk_max = tk_max_;
     for (int n = 0; n < order_; ++n) {
       const size_t k = static_cast<size_t>(n);
-      fused_rand_tiles(dims_[k], s_mode_[k], fgrid_ - 1, zcap, &tm[k], &tk[k], &tkl[k]);
+      fused_rand_tiles(dims_[k], s_mode_[k], gw, zcap, &tm[k], &tk[k], &tkl[k]);
       tm_max = std::max(tm_max, tm[k]);
       tk_max = std::max(tk_max, tk[k]);
       max_part = std::max(max_part, static_cast<i64>(tk[k]) * dims_[k] * r_);
@@ -498,13 +525,14 @@ void Session::setup_fused() {
     gpart_ = dalloc<double>(static_cast<size_t>(nblk) * tk_max * 64);
     gsum_ = dalloc<double>(static_cast<size_t>(rt_) * rt_);
     CPB_CUDA(cudaMemsetAsync(gsum_, 0, sizeof(double) * rt_ * rt_, stream_));
-    const size_t per = static_cast<size_t>(tm_max) + 64 + 2 + static_cast<size_t>(tk_max);
+    const size_t per = (2 * static_cast<size_t>(tm_max) + static_cast<size_t>(tk_max) + 3) * kCS;
     fcnt_ = dalloc<unsigned>(per * order_);
     CPB_CUDA(cudaMemsetAsync(fcnt_, 0, per * order_ * sizeof(unsigned), stream_));
   }
-  fsync_ = dalloc<unsigned>(16);
-  CPB_CUDA(cudaMemsetAsync(fsync_, 0, 16 * sizeof(unsigned), stream_));
+  fsync_ = dalloc<unsigned>(kSyncWords);
+  CPB_CUDA(cudaMemsetAsync(fsync_, 0, kSyncWords * sizeof(unsigned), stream_));
   std::vector<FusedIter> host(static_cast<size_t>(table_iters_));
+  fargs_ = dalloc<FusedIter>(host.size());
   for (int ti = 0; ti < table_iters_; ++ti) {
     const int it = ti + 1;
     FusedIter& A = host[static_cast<size_t>(ti)];
@@ -536,11 +564,12 @@ void Session::setup_fused() {
         M.tklen = tkl[k];
         M.nblk = nblk;
         M.zcap = zcap;
-        unsigned* c = fcnt_ + (static_cast<size_t>(tm_max) + 66 + tk_max_) * k;
+        unsigned* c = fcnt_ + (2 * static_cast<size_t>(tm_max) + tk_max_ + 3) * kCS * k;
         M.mt_cnt = c;
-        M.gbt = c + tm_max;
-        M.gready = c + tm_max + 64;
-        M.kb_cnt = c + tm_max + 66;
+        M.kb_cnt = c + static_cast<size_t>(tm_max) * kCS;
+        M.mcnt = c + static_cast<size_t>(tm_max + tk_max_) * kCS;
+        M.gm_cnt = c + static_cast<size_t>(tm_max + tk_max_ + 3) * kCS;
+        M.dist_gram = (tm[k] * tk[k] <= gw) ? 1 : 0;
       }
     }
     A.z = z_;
@@ -550,14 +579,19 @@ void Session::setup_fused() {
     A.part_rhs = part_rhs_;
     A.gpart = gpart_;
     A.gsum = gsum_;
+    A.grp_cnt = fsync_ + 3 * kCS;
+    A.next = (ti + 1 < table_iters_) ? fargs_ + ti + 1 : nullptr;
+    A.inv_cta = mix_ ? -1 : inv_cta;
+    A.idle_cta = mix_ ? -1 : idle_cta;
+    A.census = nullptr;
     A.ssq = ssq_;
     A.rhs_full = rhs_full_;
     A.lambda = lambda_;
     A.info = info_;
     A.rng = rng_state_;
     A.gram_done = fsync_;
-    A.bar = fsync_ + 2;
-    A.ticket = fsync_ + 4;
+    A.bar = fsync_ + kCS;
+    A.ticket = fsync_ + 2 * kCS;
     A.stop = has_fit_ ? &state_->stopped : nullptr;
     A.has_fit = has_fit_;
     if (has_fit_) {
@@ -586,7 +620,6 @@ void Session::setup_fused() {
       f.stall_limit = o_.stall_limit;
     }
   }
-  fargs_ = dalloc<FusedIter>(host.size());
   CPB_CUDA(cudaMemcpyAsync(fargs_, host.data(), host.size() * sizeof(FusedIter), cudaMemcpyHostToDevice, stream_));
   CPB_CUDA(cudaStreamSynchronize(stream_));
   fused_ = true;
@@ -924,27 +957,83 @@ void Session::enqueue_iteration() {
   }
   if (fused_) {
     const int ti = o_.exhaustive_samples ? 0 : it - 1;
+    if (timing_ && !cta_t_ && std::getenv("CPRAND_DEBUG_CTA") && !mix_) {
+      cta_t_ = dalloc<unsigned long long>(static_cast<size_t>(fgrid_) * 16);
+      CPB_CUDA(cudaMemset(cta_t_, 0, sizeof(unsigned long long) * fgrid_ * 16));
+      for (int t = 0; t < table_iters_; ++t)
+        CPB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(fargs_ + t) + offsetof(FusedIter, cta_t), &cta_t_,
+                                 sizeof(cta_t_), cudaMemcpyHostToDevice, stream_));
+    }
     if (timing_ && !phase_t_) {
-      phase_t_ = dalloc<unsigned long long>(static_cast<size_t>(order_ * 8));
+      phase_t_ = dalloc<unsigned long long>(static_cast<size_t>(order_ * 16));
+      CPB_CUDA(cudaMemset(phase_t_, 0, sizeof(unsigned long long) * order_ * 16));
       for (int t = 0; t < table_iters_; ++t)  // point every iteration's args at the stamp buffer
         CPB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(fargs_ + t) + offsetof(FusedIter, phase_t), &phase_t_,
                                  sizeof(phase_t_), cudaMemcpyHostToDevice, stream_));
     }
+    if (cta_t_) CPB_CUDA(cudaMemsetAsync(cta_t_, 0, sizeof(unsigned long long) * fgrid_ * 16, stream_));
     timed(0, 7, stream_, [&] { launch_fused_iteration(fargs_ + ti, rt_, mix_, fgrid_, fsmem_, stream_); });
     if (timing_) {
       // collect this launch's phase stamps (timing mode only: synchronizes)
-      std::vector<unsigned long long> t(static_cast<size_t>(order_ * 8));
+      std::vector<unsigned long long> t(static_cast<size_t>(order_ * 16));
       CPB_CUDA(cudaMemcpyAsync(t.data(), phase_t_, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                stream_));
       CPB_CUDA(cudaStreamSynchronize(stream_));
-      if (phase_acc_.empty()) phase_acc_.assign(7, 0.0);
+      if (phase_acc_.empty()) phase_acc_.assign(mix_ ? 7 : 14, 0.0);
       for (int n = 0; n < order_; ++n) {
-        const unsigned long long* q = t.data() + n * 8;
+        const unsigned long long* q = t.data() + n * 16;
         for (int k = 0; k < 6; ++k) phase_acc_[static_cast<size_t>(k)] += 1e-3 * static_cast<double>(q[k + 1] - q[k]) / order_;
         // MIX kernel: inverse done after the Z barrier; CPRAND kernel: after the mode start
         phase_acc_[6] += 1e-3 * static_cast<double>(q[7] - q[mix_ ? 2 : 0]) / order_;
+        if (!mix_)  // gram ready (inverse CTA), Z share done, split Z complete (CTA 0), from mode start
+          for (int k = 0; k < 3; ++k) phase_acc_[static_cast<size_t>(7 + k)] += 1e-3 * static_cast<double>(q[8 + k] - q[0]) / order_;
+        if (!mix_) {  // inverse: prologue (gram ready -> first pivot), step loop
+          phase_acc_[10] += 1e-3 * static_cast<double>(q[11] - q[8]) / order_;
+          phase_acc_[11] += 1e-3 * static_cast<double>(q[12] - q[11]) / order_;
+          phase_acc_[12] += 1e-3 * static_cast<double>(q[13] - q[0]) / order_;
+          phase_acc_[13] += 1e-3 * static_cast<double>(q[15] - q[8]) / order_;
+        }
       }
       ++phase_acc_n_;
+      if (cta_t_) {  // debug: per-CTA timeline of mode 1 (us after the earliest mode start)
+        std::vector<unsigned long long> c(static_cast<size_t>(fgrid_) * 16);
+        CPB_CUDA(cudaMemcpy(c.data(), cta_t_, c.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        unsigned long long t0 = ~0ULL;
+        for (int b = 0; b < fgrid_; ++b)
+          if (c[static_cast<size_t>(b) * 16]) t0 = std::min(t0, c[static_cast<size_t>(b) * 16]);
+        const int ks[] = {0, 9, 10, 1, 2, 3, 4, 5, 6};
+        std::fprintf(stderr, "cta timeline (mode 1):");
+        for (int k : ks) {
+          double mx = 0, sum = 0;
+          int cnt = 0, arg = -1;
+          for (int b = 0; b < fgrid_; ++b) {
+            const unsigned long long v = c[static_cast<size_t>(b) * 16 + k];
+            if (!v) continue;
+            const double us = 1e-3 * static_cast<double>(v - t0);
+            sum += us;
+            ++cnt;
+            if (us > mx) {
+              mx = us;
+              arg = b;
+            }
+          }
+          std::fprintf(stderr, " [%d mean %.2f max %.2f @cta %d kb %llu]", k, cnt ? sum / cnt : 0.0, mx, arg,
+                       arg >= 0 ? c[static_cast<size_t>(arg) * 16 + 11] : 0ULL);
+        }
+        std::fprintf(stderr, "\n");
+        {  // SM sharing of the inverse CTA in this launch
+          int inv = fgrid_ - 1;
+          FusedIter h;
+          CPB_CUDA(cudaMemcpy(&h, fargs_ + ti, sizeof(h), cudaMemcpyDeviceToHost));
+          if (h.inv_cta >= 0) inv = h.inv_cta;
+          std::fprintf(stderr, "inverse CTA %d on SM %llu (idle CTA %d); sharing:", inv,
+                       c[static_cast<size_t>(inv) * 16 + 14], h.idle_cta);
+          for (int b = 0; b < fgrid_; ++b)
+            if (b != inv && c[static_cast<size_t>(b) * 16 + 14] == c[static_cast<size_t>(inv) * 16 + 14])
+              std::fprintf(stderr, " %d", b);
+          std::fprintf(stderr, "\n");
+        }
+      }
     }
     CPB_CUDA(cudaEventRecord(ev_loop1_, stream_));
     it_ = it;

@@ -144,6 +144,7 @@ class Session {
   unsigned* fsync_ = nullptr;      // gram_done, barrier, tickets
   unsigned* fcnt_ = nullptr;       // CPRAND kernel counters [order][tm_max + 64 + 2 + tk_max]
   int tk_max_ = 1;
+  unsigned long long* cta_t_ = nullptr;  // debug per-CTA stamps (CPRAND_DEBUG_CTA)
   double* gpart_ = nullptr;        // CPRAND kernel Gram block partials
   double* gsum_ = nullptr;         // CPRAND kernel reduced Gram [RT][RT]
   unsigned long long* phase_t_ = nullptr;  // fused phase timestamps [order][8] (timing mode)

@@ -90,6 +90,12 @@ __device__ __forceinline__ void wait_geq(const unsigned* p, unsigned target) {
     while (ld_acquire(p) < target) __nanosleep(32);
   __syncthreads();
 }
+// Whole CTA: publishes this CTA's prior writes (release), then adds v to *p
+// without waiting for a reply.
+__device__ __forceinline__ void signal_add(unsigned* p, unsigned v) {
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 // Whole CTA: publishes this CTA's prior writes, then adds v to *p.
 __device__ __forceinline__ unsigned release_add(unsigned* p, unsigned v, unsigned* sh_old) {
   __syncthreads();

@@ -24,6 +24,8 @@ __global__ void __launch_bounds__(NTH) inv_kernel(const double* g, int r, double
     bool fail;
     if (KIND == 0)
       fail = ph::inverse_la<64>(g, r, 4.4e-13, ginv, gfull, info, sh);
+    else if (KIND == 2)
+      fail = ph::inverse_b8<64>(g, r, 4.4e-13, ginv, gfull, info, sh);
     else
       fail = ph::inverse_cta<64, NTH>(g, 1, r, 4.4e-13, ginv, gfull, info, sh);
     __syncthreads();
@@ -89,6 +91,19 @@ int main() {
     printf("  cycles: prologue %llu, first pivot %llu, steps:", st[1] - st[0], st[2] - st[1]);
     for (int k = 3; k < 16; ++k) printf(" %llu", st[k + 1] - st[k]);
     printf(", epilogue %llu\n", st[31] - st[30]);
+    printf("  step 5 (from step start, cycles): mma done %lld, worker end %lld | warp7 P done %lld, inverse done %lld, w7 end %lld\n",
+           (long long)(st[17] - st[8]), (long long)(st[18] - st[8]),
+           (long long)(st[19] - st[8]), (long long)(st[20] - st[8]), (long long)(st[21] - st[8]));
+  }
+  cudaFuncSetAttribute(inv_kernel<2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  inv_kernel<2, 256><<<1, 256, 100 * 1024>>>(g, r, ginv, gfull, info, t, reps);
+  report("inverse_b8 256");
+  {
+    unsigned long long st[32];
+    cudaMemcpyFromSymbol(st, g_st, sizeof(st));
+    printf("  cycles: prologue %llu, first pivot %llu, steps:", st[1] - st[0], st[2] - st[1]);
+    for (int k = 3; k < 9; ++k) printf(" %llu", st[k + 1] - st[k]);
+    printf(", last %llu, epilogue %llu\n", st[30] - st[9], st[31] - st[30]);
     printf("  step 5 (from step start, cycles): mma done %lld, worker end %lld | warp7 P done %lld, inverse done %lld, w7 end %lld\n",
            (long long)(st[17] - st[8]), (long long)(st[18] - st[8]),
            (long long)(st[19] - st[8]), (long long)(st[20] - st[8]), (long long)(st[21] - st[8]));
