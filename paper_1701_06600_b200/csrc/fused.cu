@@ -273,8 +273,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
   const unsigned rank = b - (static_cast<int>(b) > inv ? 1u : 0u) - (idle >= 0 && static_cast<int>(b) > idle ? 1u : 0u);
   const int r = A.r;
   const int nfr = (r + 7) / 8;
-  unsigned* gen = A.bar + 1;  // release generation: +1 per mode
-  const unsigned gen0 = ld_acquire(gen);  // no release of this launch can precede every CTA's first signal
+  // release generation (+1 per mode), replicated; CTA b polls replica b % kRep.
+  // No release of this launch can precede every CTA's first signal.
+  unsigned* gen = A.gen_rep + (b % kRep) * kCS;
+  const unsigned gen0 = ld_acquire(gen);
   prefetch_tables(A, b);
   if (A.cta_t && tid == 0) {
     unsigned sm;
@@ -296,6 +298,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       for (int e = tid; e < P.tm; e += kFusedThreads) P.mt_cnt[e * kCS] = 0u;
       for (int e = tid; e < P.tk; e += kFusedThreads) P.kb_cnt[e * kCS] = 0u;
       if (tid < 3) P.mcnt[tid * kCS] = 0u;
+      if (tid < kRep) P.grdy[tid * kCS] = 0u;
       for (int e = tid; e < P.tm; e += kFusedThreads) P.gm_cnt[e * kCS] = 0u;
     }
     if (is_inv) {
@@ -341,13 +344,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       const bool fail = ph::inverse_la<RT>(A.gsum, r, M.tol, A.ginv, A.gfull, A.info, fsm,
                                            A.phase_t ? A.phase_t + n * 16 + 11 : nullptr);
       if (fail) ph::pinv_fallback<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
-      signal_add(M.mcnt + kCS, 1u);
+      signal_add_rep(M.grdy, 1u, kRep);
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 7] = globaltimer();
-      // ---- norms + lambda from the tile CTAs' column sums of squares
-      wait_geq(M.mcnt + 2 * kCS, Gw);
-      ph::norms_final<RT, kFusedThreads>(r, in, w, static_cast<int>(Gw), n == 0, A.rng, fsm);
-      if (A.phase_t && tid == 0) A.phase_t[n * 16 + 13] = globaltimer();
-      signal_add(gen, 1u);
     } else if (!is_idle) {
       const TileSmem t = tile_smem<RT>(fsm, M.zcap);
       // this CTA's share of every one of its splits' Z rows, then signal
@@ -421,7 +419,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
           rh[il * LD + c] = sum_strided(p, step, M.tk);
         }
         if (!have_ginv) {
-          wait_geq(M.mcnt + kCS, 1u);
+          wait_geq(M.grdy + (rank % kRep) * kCS, 1u, 64);
           for (int e = tid; e < r * r; e += kFusedThreads) {
             const int x = e / r, y = e - x * r;
             gi[x * LD + y] = __ldcg(A.ginv + e);
@@ -445,11 +443,23 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       if (tid < r) A.ssq[static_cast<i64>(rank) * r + tid] = q2;
       signal_add(M.mcnt + 2 * kCS, 1u);
       stamp(n, 5);
+      if (rank == 0) {
+        // ---- norms + lambda from the tile CTAs' column sums of squares
+        wait_geq(M.mcnt + 2 * kCS, Gw);
+        if (A.cta_t && n == 1 && tid == 0) A.cta_t[b * 16 + 12] = globaltimer();
+        ph::norms_final<RT, kFusedThreads>(r, in, w, static_cast<int>(Gw), n == 0, A.rng, fsm,
+                                           (A.cta_t && n == 1) ? A.cta_t + b * 16 + 7 : nullptr);
+        if (A.cta_t && n == 1 && tid == 0) A.cta_t[b * 16 + 13] = globaltimer();
+        if (A.phase_t && tid == 0) A.phase_t[n * 16 + 13] = globaltimer();
+        signal_add_rep(A.gen_rep, 1u, kRep);
+      }
     }
-    // ---- wait for the release of mode n (the inverse CTA formed the norms)
-    if (!is_inv) {
-      if (tid == 0)
-        while (static_cast<int>(ld_acquire(gen) - (gen0 + n + 1)) < 0) __nanosleep(32);
+    // ---- wait for the release of mode n (tile rank 0 formed the norms)
+    {
+      if (tid == 0) {
+        while (static_cast<int>(ld_relaxed(gen) - (gen0 + n + 1)) < 0) __nanosleep(64);
+        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+      }
       __syncthreads();
     }
     stamp(n, 6);

@@ -183,13 +183,15 @@ struct FusedMode {
   unsigned* kb_cnt;      // [tk] CTAs that wrote their share of split kb's Z rows   (stride kCS)
   unsigned* gm_cnt;      // [tm] splits whose Gram blocks of row block mt are written  (stride kCS)
   int dist_gram;         // 1: tile (mt, tk-1) sums row block mt's Gram blocks (one tile per CTA)
+  unsigned* grdy;        // [kRep] replicas of the "Gram inverse ready" flag      (stride kCS)
   unsigned* mcnt;        // [0] Gram blocks summed (or tiles written), [1] inverse ready,
                          // [2] tile CTAs whose sums of squares are written        (stride kCS)
 };
 // Inter-CTA counters live one per 128-byte line (atomics and polling on a
 // shared line serialize): kCS words apart.
 constexpr int kCS = 32;
-constexpr int kSyncWords = 3 * kCS + 128 * kCS;  // gram_done, barrier, tickets, ssq group tickets
+constexpr int kRep = 16;  // replicas of widely polled flags
+constexpr int kSyncWords = 3 * kCS + 128 * kCS + kRep * kCS;  // gram_done, barrier, tickets, group tickets, gen replicas
 struct FusedIter;
 struct FusedIter {
   int order, r, first_mode_first_of_pass;
@@ -212,6 +214,7 @@ struct FusedIter {
   int* census;
   unsigned* grp_cnt;             // CPRAND kernel: ssq group tickets [grid / 16] (stride kCS)
   const FusedIter* next;         // next iteration's arguments (L2 prefetch of its tables)
+  unsigned* gen_rep;             // CPRAND kernel: [kRep] replicas of the mode-release generation
   unsigned long long* cta_t;  // debug: per-CTA stamps of mode 1 [grid][16] (CPRAND_DEBUG_CTA)
 };
 size_t fused_smem_bytes(int rt, bool mix, int max_dim);

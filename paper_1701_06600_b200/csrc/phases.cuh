@@ -1210,7 +1210,7 @@ __device__ void ssq_store(double q, int r, double* ssq_part, double* red) {
 // red: (NTH / RT) x (RT + 1) doubles.
 template <int RT, int NTH>
 __device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int first_of_pass,
-                            unsigned long long* rng_state, double* red) {
+                            unsigned long long* rng_state, double* red, unsigned long long* dbg = nullptr) {
   constexpr int NP = NTH / RT;
   const int tid = threadIdx.x, part = tid / RT, c = tid % RT;
   __shared__ int s_zero;
@@ -1230,7 +1230,9 @@ __device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int fi
   }
   red[part * (RT + 1) + c] = q;
   if (tid == 0) s_zero = 0;
+  if (dbg && tid == 0) dbg[0] = globaltimer();
   __syncthreads();
+  if (dbg && tid == 0) dbg[1] = globaltimer();
   if (tid < r) {
     double t = 0.0;
     for (int x = 0; x < NP; ++x) t += red[x * (RT + 1) + tid];
@@ -1244,6 +1246,7 @@ __device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int fi
     }
   }
   __syncthreads();
+  if (dbg && tid == 0) dbg[2] = globaltimer() | (s_zero ? (1ULL << 63) : 0ULL);
   if (tid == 0 && s_zero) {
     // zero columns (kruskal.hpp:57-63): N(0,1) column from the normalize
     // stream, one distribution object per call, columns in order

@@ -525,7 +525,7 @@ void Session::setup_fused() {
     gpart_ = dalloc<double>(static_cast<size_t>(nblk) * tk_max * 64);
     gsum_ = dalloc<double>(static_cast<size_t>(rt_) * rt_);
     CPB_CUDA(cudaMemsetAsync(gsum_, 0, sizeof(double) * rt_ * rt_, stream_));
-    const size_t per = (2 * static_cast<size_t>(tm_max) + static_cast<size_t>(tk_max) + 3) * kCS;
+    const size_t per = (2 * static_cast<size_t>(tm_max) + static_cast<size_t>(tk_max) + 3 + kRep) * kCS;
     fcnt_ = dalloc<unsigned>(per * order_);
     CPB_CUDA(cudaMemsetAsync(fcnt_, 0, per * order_ * sizeof(unsigned), stream_));
   }
@@ -564,12 +564,13 @@ void Session::setup_fused() {
         M.tklen = tkl[k];
         M.nblk = nblk;
         M.zcap = zcap;
-        unsigned* c = fcnt_ + (2 * static_cast<size_t>(tm_max) + tk_max_ + 3) * kCS * k;
+        unsigned* c = fcnt_ + (2 * static_cast<size_t>(tm_max) + tk_max_ + 3 + kRep) * kCS * k;
         M.mt_cnt = c;
         M.kb_cnt = c + static_cast<size_t>(tm_max) * kCS;
         M.mcnt = c + static_cast<size_t>(tm_max + tk_max_) * kCS;
         M.gm_cnt = c + static_cast<size_t>(tm_max + tk_max_ + 3) * kCS;
         M.dist_gram = (tm[k] * tk[k] <= gw) ? 1 : 0;
+        M.grdy = c + static_cast<size_t>(2 * tm_max + tk_max_ + 3) * kCS;
       }
     }
     A.z = z_;
@@ -580,6 +581,7 @@ void Session::setup_fused() {
     A.gpart = gpart_;
     A.gsum = gsum_;
     A.grp_cnt = fsync_ + 3 * kCS;
+    A.gen_rep = fsync_ + (3 + 128) * kCS;
     A.next = (ti + 1 < table_iters_) ? fargs_ + ti + 1 : nullptr;
     A.inv_cta = mix_ ? -1 : inv_cta;
     A.idle_cta = mix_ ? -1 : idle_cta;
@@ -1001,7 +1003,7 @@ void Session::enqueue_iteration() {
         unsigned long long t0 = ~0ULL;
         for (int b = 0; b < fgrid_; ++b)
           if (c[static_cast<size_t>(b) * 16]) t0 = std::min(t0, c[static_cast<size_t>(b) * 16]);
-        const int ks[] = {0, 9, 10, 1, 2, 3, 4, 5, 6};
+        const int ks[] = {0, 9, 10, 1, 2, 3, 4, 5, 12, 7, 8, 9, 13, 6};
         std::fprintf(stderr, "cta timeline (mode 1):");
         for (int k : ks) {
           double mx = 0, sum = 0;

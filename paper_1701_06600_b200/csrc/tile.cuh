@@ -85,9 +85,18 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 // Whole CTA: returns after *p >= target was observed (thread 0 polls).
-__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned target) {
-  if (threadIdx.x == 0)
-    while (ld_acquire(p) < target) __nanosleep(32);
+// Relaxed load for polling: an acquire load invalidates the SM's L1 on every
+// poll (stalling the co-resident CTA's loads); poll relaxed, then one fence.
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned target, unsigned sleep_ns = 32) {
+  if (threadIdx.x == 0) {
+    while (ld_relaxed(p) < target) __nanosleep(sleep_ns);
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+  }
   __syncthreads();
 }
 // Whole CTA: publishes this CTA's prior writes (release), then adds v to *p
@@ -95,6 +104,14 @@ __device__ __forceinline__ void wait_geq(const unsigned* p, unsigned target) {
 __device__ __forceinline__ void signal_add(unsigned* p, unsigned v) {
   __syncthreads();
   if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// Whole CTA: release-add v to nrep replicas p[0], p[kCS], ... (a flag that
+// many CTAs poll is replicated over cache lines so the polling spreads over
+// L2 slices); poll replica (CTA % nrep).
+__device__ __forceinline__ void signal_add_rep(unsigned* p, unsigned v, int nrep) {
+  __syncthreads();
+  if (static_cast<int>(threadIdx.x) < nrep)
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p + threadIdx.x * kCS), "r"(v) : "memory");
 }
 // Whole CTA: publishes this CTA's prior writes, then adds v to *p.
 __device__ __forceinline__ unsigned release_add(unsigned* p, unsigned v, unsigned* sh_old) {
