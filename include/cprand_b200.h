@@ -98,6 +98,8 @@ typedef struct cprand_options {
   int32_t fused;              /* one persistent cooperative kernel per outer
                                  iteration: -1 auto (when every mode reads its
                                  fibers in place), 0 off (multi-kernel chain) */
+  int64_t shard_total;        /* with comm: global length of the last mode; x is
+                                 this rank's slab, rows [rank*ceil(I/P), ...) */
 } cprand_options_t;
 
 typedef struct cprand_trace_record {
@@ -144,6 +146,9 @@ int cprand_tensor_download(cprand_tensor_t t, double* host);
 int cprand_tensor_synth(cprand_tensor_t t, int64_t r, double collinearity, double eta,
                         uint64_t seed, double* const* out_factors);
 double* cprand_tensor_device_ptr(cprand_tensor_t t);
+/* Slab of the BASELINE.json tensor with last dim shard_total (rank/nranks
+ * from comm); noise scaled by the global norms (allreduced). Declared after
+ * cprand_comm_t below. */
 void cprand_tensor_destroy(cprand_tensor_t t);
 
 /* Setup (init, sample tables, fit estimator, mixing pass). The session keeps
@@ -215,12 +220,20 @@ int cprand_unmix_rows(const double* g, int64_t s, int64_t in, const int64_t* dim
  * drawn by the device mt19937_64 + polar method. */
 int cprand_debug_normal_stream(uint64_t seed, int32_t n, double* out);
 
-/* ---- slab sharding over NCCL (one process per GPU) ---- */
+/* ---- slab sharding over NCCL (one process per GPU) ----
+ * The tensor is split along its last mode: rank p holds rows
+ * [p*ceil(I/P), min(I, (p+1)*ceil(I/P))). Sample tables, factors and the fit
+ * estimator are replicated; modes n < N-1 contract each rank's fibers and
+ * allreduce the R x I_n right-hand sides, mode N-1 forms each rank's factor
+ * rows, allreduces the column sums of squares and allgathers the slabs
+ * (SURVEY.md §8e). Method rand only. */
 typedef struct cprand_comm_s* cprand_comm_t;
 int cprand_comm_unique_id(uint8_t out[128]);
 int cprand_comm_create(const uint8_t id[128], int32_t rank, int32_t nranks, int32_t device,
                        cprand_comm_t* out);
 void cprand_comm_destroy(cprand_comm_t c);
+int cprand_tensor_synth_slab(cprand_tensor_t t, int64_t r, double collinearity, double eta, uint64_t seed,
+                             int64_t shard_total, cprand_comm_t comm, double* const* out_factors);
 
 #ifdef __cplusplus
 }

@@ -48,6 +48,7 @@ class Options(C.Structure):
         ("exhaustive_samples", C.c_int32), ("exact_fit_trace", C.c_int32),
         ("device", C.c_int32), ("x_is_device", C.c_int32), ("x_mutable", C.c_int32),
         ("comm", C.c_void_p), ("replicas", C.c_int32), ("fused", C.c_int32),
+        ("shard_total", C.c_int64),
     ]
 
 
@@ -75,7 +76,7 @@ EXPORTS = [
     "cprand_gather_fibers", "cprand_skr", "cprand_mode_update", "cprand_fit_values",
     "cprand_estimate_fit", "cprand_mix_tensor", "cprand_mix_factor", "cprand_unmix_factor",
     "cprand_unmix_rows", "cprand_debug_normal_stream", "cprand_comm_unique_id",
-    "cprand_comm_create", "cprand_comm_destroy",
+    "cprand_comm_create", "cprand_comm_destroy", "cprand_tensor_synth_slab",
 ]
 
 _lib = None

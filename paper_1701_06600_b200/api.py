@@ -43,6 +43,8 @@ class SolveOptions:
     x_mutable: bool = False
     replicas: int = -1  # mode-major replicas of strided modes: -1 auto, 0 off, 1 on
     fused: int = -1  # persistent per-iteration kernel: -1 auto, 0 off
+    comm: object | None = None  # Comm: slab-sharded run (tensor = this rank's slab)
+    shard_total: int = 0  # with comm: global length of the last mode
 
     def to_c(self) -> Options:
         o = Options()
@@ -63,6 +65,9 @@ class SolveOptions:
         o.x_mutable = int(self.x_mutable)
         o.replicas = self.replicas
         o.fused = self.fused
+        if self.comm is not None:
+            o.comm = self.comm.h
+            o.shard_total = int(self.shard_total)
         return o
 
 
@@ -192,6 +197,16 @@ class DeviceTensor:
         check(lib().cprand_tensor_synth(self.h, C.c_int64(r), C.c_double(collinearity),
                                         C.c_double(eta), C.c_uint64(seed),
                                         _ptrs(fs) if fs else None))
+        return fs
+
+    def synth_slab(self, r: int, collinearity: float, eta: float, seed: int, shard_total: int, comm,
+                   want_factors=False):
+        """This rank's slab of the BASELINE.json tensor (last dim shard_total)."""
+        gd = list(self.dims[:-1]) + [int(shard_total)]
+        fs = [np.empty((d, r), dtype=np.float64, order="F") for d in gd] if want_factors else None
+        check(lib().cprand_tensor_synth_slab(self.h, C.c_int64(r), C.c_double(collinearity), C.c_double(eta),
+                                             C.c_uint64(seed), C.c_int64(shard_total), comm.h,
+                                             _ptrs(fs) if fs else None))
         return fs
 
     def close(self):
@@ -415,3 +430,31 @@ def debug_normal_stream(seed: int, n: int) -> np.ndarray:
     out = np.empty(n, dtype=np.float64)
     check(lib().cprand_debug_normal_stream(C.c_uint64(seed), n, _p(out)))
     return out
+
+
+class Comm:
+    """NCCL communicator for slab-sharded runs (one process per GPU). Rank 0
+    creates the id (unique_id()), every rank passes it to Comm(...)."""
+
+    def __init__(self, uid: bytes, rank: int, nranks: int, device: int):
+        self.rank, self.nranks, self.device = rank, nranks, device
+        self.h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
+        check(lib().cprand_comm_create(buf, rank, nranks, device, C.byref(self.h)))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().cprand_comm_unique_id(buf))
+        return bytes(buf)
+
+    def close(self):
+        if self.h:
+            lib().cprand_comm_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -46,6 +46,15 @@ std::vector<i64> dims_of(const int64_t* dims, int32_t order) {
   return d;
 }
 
+}  // namespace
+
+struct cprand_comm_s {
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1, device = 0;
+};
+
+namespace {
+
 Options opts_of(const cprand_options_t* o) {
   Options r;
   if (!o) return r;
@@ -64,7 +73,15 @@ Options opts_of(const cprand_options_t* o) {
   r.x_mutable = o->x_mutable != 0;
   r.replicas = o->replicas;
   r.fused = o->fused;
-  if (o->comm != nullptr) throw Unsupported("slab-sharded sessions are not enabled in this build");
+  if (o->comm != nullptr) {
+    const auto* c = static_cast<const cprand_comm_s*>(o->comm);
+    r.nccl = c->comm;
+    r.nranks = c->nranks;
+    r.rank = c->rank;
+    r.shard_total = o->shard_total;
+  } else if (o->shard_total != 0) {
+    throw InvalidArgument("shard_total requires a communicator");
+  }
   return r;
 }
 
@@ -108,10 +125,7 @@ struct cprand_tensor_s {
 struct cprand_session_s {
   std::unique_ptr<Session> s;
 };
-struct cprand_comm_s {
-  ncclComm_t comm = nullptr;
-  int rank = 0, nranks = 1, device = 0;
-};
+
 
 extern "C" {
 
@@ -208,6 +222,24 @@ int cprand_tensor_synth(cprand_tensor_t t, int64_t r, double c, double eta, uint
     need(t);
     if (r < 1) throw InvalidArgument("rank must be >= 1");
     op_synth(t->t.get(), static_cast<int>(r), c, eta, seed, out_factors);
+  });
+}
+
+int cprand_tensor_synth_slab(cprand_tensor_t t, int64_t r, double c, double eta, uint64_t seed,
+                             int64_t shard_total, cprand_comm_t comm, double* const* out_factors) {
+  return guarded([&] {
+    need(t);
+    need(comm);
+    if (r < 1) throw InvalidArgument("rank must be >= 1");
+    const i64 lmax = (shard_total + comm->nranks - 1) / comm->nranks;
+    const i64 off = lmax * comm->rank;
+    const i64 len = std::max<i64>(0, std::min<i64>(shard_total, off + lmax) - off);
+    if (t->t->dims.back() != len) throw InvalidArgument("slab tensor must hold rows [rank*ceil(I/P), ...)");
+    auto reduce = [&](double* sums) {
+      const ncclResult_t e = ncclAllReduce(sums, sums, 2, ncclDouble, ncclSum, comm->comm, nullptr);
+      if (e != ncclSuccess) throw CudaError(std::string("ncclAllReduce: ") + ncclGetErrorString(e));
+    };
+    op_synth(t->t.get(), static_cast<int>(r), c, eta, seed, out_factors, off, shard_total, reduce);
   });
 }
 

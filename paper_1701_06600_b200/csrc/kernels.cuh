@@ -1,6 +1,8 @@
 // Launch wrappers for the sm_100a kernels (kernels.cu, mix.cu, synth.cu).
 #pragma once
 
+#include <functional>
+
 #include "common.cuh"
 
 namespace cpb {
@@ -154,9 +156,21 @@ void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 
 void launch_reduce_rhs(const double* part_rhs, int ks, i64 in, int r, double* out,
                        cudaStream_t st);
 
+// ---- slab sharding (shard.cu) ---------------------------------------------
+void launch_gather_z_rows(const double* z, const int* idx, int cnt, int rt, double* out, cudaStream_t st);
+int apply_rows_grid(i64 rows, int r);
+void launch_apply_rows(i64 rows, int r, const double* rhs, const double* ginv, double* a_out, double* ssq_part,
+                       cudaStream_t st);
+void launch_col_ssq(const double* part, int nparts, int r, double* out, cudaStream_t st);
+void launch_norms_from_ssq(const double* ssq, int r, i64 rows, double* a, double* norms, double* lambda,
+                           int first_of_pass, unsigned long long* rng_state, cudaStream_t st);
+// out[j] = x[loc[j]], or 0 where loc[j] < 0 (entry outside this slab)
+void launch_gather_values_masked(const double* x, const i64* loc, i64 n, double* out, cudaStream_t st);
+
 // ---- synthetic generator (synth.cu) ------------------------------------
 void launch_synth(double* x, int order, const i64* dims, int r, const double* const* fac_dev,
-                  double eta, unsigned long long seed, double* scratch, cudaStream_t st);
+                  double eta, unsigned long long seed, double* scratch, cudaStream_t st, i64 last_off = 0,
+                  i64 global_last = 0, const std::function<void(double*)>& reduce_sums = nullptr);
 
 // ---- persistent per-iteration kernel (fused.cu) -------------------------
 // One cooperative launch per outer iteration runs every mode update and the

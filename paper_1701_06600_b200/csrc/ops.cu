@@ -8,6 +8,8 @@
 #include <memory>
 #include <vector>
 
+#include <functional>
+
 #include "session.hpp"
 
 namespace cpb {
@@ -394,14 +396,17 @@ void op_debug_normals(std::uint64_t seed, int n, double* out) {
 }
 
 void op_synth(Tensor* t, int r, double c, double eta, std::uint64_t seed,
-              double* const* out_factors) {
+              double* const* out_factors, i64 last_off, i64 global_last,
+              const std::function<void(double*)>& reduce_sums) {
+  std::vector<i64> gdims = t->dims;
+  if (global_last > 0) gdims.back() = global_last;
   std::vector<std::vector<double>> f;
-  baseline_factors_host(t->dims, r, c, seed, f);
+  baseline_factors_host(gdims, r, c, seed, f);
   CPB_CUDA(cudaSetDevice(t->device));
   std::vector<std::unique_ptr<DBuf>> facs;
   std::vector<const double*> ptrs;
   for (size_t n = 0; n < t->dims.size(); ++n) {
-    auto rm = row_major(f[n].data(), t->dims[n], r);
+    auto rm = row_major(f[n].data(), gdims[n], r);
     facs.push_back(std::make_unique<DBuf>(rm.size() * sizeof(double)));
     h2d(facs.back()->p, rm.data(), rm.size());
     ptrs.push_back(facs.back()->as<double>());
@@ -409,7 +414,7 @@ void op_synth(Tensor* t, int r, double c, double eta, std::uint64_t seed,
   }
   DBuf scratch((2 * 4096 + 8) * sizeof(double));
   launch_synth(t->d, static_cast<int>(t->dims.size()), t->dims.data(), r, ptrs.data(), eta, seed,
-               scratch.as<double>(), nullptr);
+               scratch.as<double>(), nullptr, last_off, global_last, reduce_sums);
   CPB_CUDA(cudaDeviceSynchronize());
 }
 

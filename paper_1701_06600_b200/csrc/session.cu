@@ -16,6 +16,8 @@
 //    host keeps a bounded number of iterations in flight.
 #include "session.hpp"
 
+#include <nccl.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -264,6 +266,31 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
   dims_ = x->dims;
   strides_ = x->strides;
   p_ = x->p;
+  tdims_ = x->dims;
+  tstrides_ = x->strides;
+  tp_ = x->p;
+  if (o_.nccl) {
+    shard_ = true;
+    nccl_ = o_.nccl;
+    nranks_ = o_.nranks;
+    rank_ = o_.rank;
+    if (method != 1) throw Unsupported("slab sharding covers the cprand method (rand)");
+    if (o_.exhaustive_samples || o_.exact_fit_trace) throw Unsupported("exhaustive / exact-fit runs are not sharded");
+    if (order_ < 2) throw InvalidArgument("slab sharding needs a tensor of order >= 2");
+    const i64 total = o_.shard_total > 0 ? o_.shard_total : tdims_.back();
+    lmax_ = (total + nranks_ - 1) / nranks_;
+    slab_off_ = static_cast<i64>(rank_) * lmax_;
+    slab_len_ = std::max<i64>(0, std::min(total, slab_off_ + lmax_) - slab_off_);
+    if (tdims_.back() != slab_len_)
+      throw InvalidArgument("sharded tensor must hold rows [rank * ceil(I/P), ...) of the last mode");
+    dims_.back() = total;
+    i64 st = 1;
+    for (int n = 0; n < order_; ++n) {
+      strides_[static_cast<size_t>(n)] = st;
+      st *= dims_[static_cast<size_t>(n)];
+    }
+    p_ = st;
+  }
   CPB_CUDA(cudaSetDevice(x->device));
   CPB_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, x->device));
   rt_ = rank_bucket(r);
@@ -302,6 +329,10 @@ Session::~Session() {
   dfree(fsync_);
   dfree(fcnt_);
   dfree(cta_t_);
+  dfree(loc_idx_);
+  dfree(loc_dbase_);
+  dfree(zloc_);
+  dfree(sh_part_);
   dfree(gpart_);
   dfree(gsum_);
   for (auto& e : ev_gathered_) cudaEventDestroy(e);
@@ -351,7 +382,8 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   fit_part_ = dalloc<double>(std::max<i64>(nparts + 1, std::max<i64>(8192, (o_.fit_sample_count + 255) / 256 + 1)));
   // ---- zero tensor short-circuit (sampling.hpp:263-264, solver.hpp:204-216)
   if (!o_.bench_mode) {
-    launch_sumsq(x_->d, p_, fit_part_, nparts, fit_part_ + nparts, stream_);
+    launch_sumsq(x_->d, tp_, fit_part_, nparts, fit_part_ + nparts, stream_);
+    if (shard_) allreduce_sum(fit_part_ + nparts, 1);
     double ss = 0.0;
     CPB_CUDA(cudaMemcpyAsync(&ss, fit_part_ + nparts, sizeof(double), cudaMemcpyDeviceToHost, stream_));
     CPB_CUDA(cudaStreamSynchronize(stream_));
@@ -373,7 +405,8 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   }
   for (int n = 0; n < order_; ++n) {
     const i64 rows = dims_[static_cast<size_t>(n)];
-    fac_.push_back(dalloc<double>(static_cast<size_t>(rows * r_)));
+    const i64 alloc_rows = (shard_ && n == order_ - 1) ? std::max(rows, lmax_ * nranks_) : rows;
+    fac_.push_back(dalloc<double>(static_cast<size_t>(alloc_rows * r_)));
     const auto rm = to_row_major(m.factors[static_cast<size_t>(n)].data(), rows, r_);
     CPB_CUDA(cudaMemcpyAsync(fac_.back(), rm.data(), rm.size() * sizeof(double),
                              cudaMemcpyHostToDevice, stream_));
@@ -401,7 +434,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   if (mix_ || premix_) mix_setup();
   if (!o_.bench_mode && premix_) {
     // cprand(x_hat) builds its estimator and norm on the mixed tensor
-    launch_sumsq(xsolve_, p_, fit_part_, nparts, fit_part_ + nparts, stream_);
+    launch_sumsq(xsolve_, tp_, fit_part_, nparts, fit_part_ + nparts, stream_);
     double ss = 0.0;
     CPB_CUDA(cudaMemcpyAsync(&ss, fit_part_ + nparts, sizeof(double), cudaMemcpyDeviceToHost, stream_));
     CPB_CUDA(cudaStreamSynchronize(stream_));
@@ -428,6 +461,14 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
     gram_splits(sn, &gp, &glen);
     max_gp = std::max(max_gp, gp);
   }
+  if (shard_) {  // mode N-1 contracts only the slab rows: its split count may differ
+    int ks, len;
+    mode_splits(std::max<i64>(slab_len_, 1), s_mode_.back(), rt_, &ks, &len, sms_);
+    max_part = std::max(max_part, static_cast<i64>(ks) * std::max<i64>(slab_len_, 1) * r_);
+    zloc_ = dalloc<double>(static_cast<size_t>(max_s * rt_));
+    const int g = apply_rows_grid(std::max<i64>(slab_len_, 1), r_);
+    sh_part_ = dalloc<double>(static_cast<size_t>((g + 1) * r_));
+  }
   z_ = dalloc<double>(static_cast<size_t>(max_s * rt_));
   part_rhs_ = dalloc<double>(static_cast<size_t>(max_part));
   part_gram_ = dalloc<double>(static_cast<size_t>(max_gp) * rt_ * rt_);
@@ -439,7 +480,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   tickets_ = dalloc<unsigned>(8);
   CPB_CUDA(cudaMemsetAsync(tickets_, 0, 8 * sizeof(unsigned), stream_));
   ssq_ = dalloc<double>(static_cast<size_t>(std::max<i64>(max_apply, 4 * sms_) * r_));
-  if (mix_) rhs_full_ = dalloc<double>(static_cast<size_t>(max_in * r_));
+  if (mix_ || shard_) rhs_full_ = dalloc<double>(static_cast<size_t>(max_in * r_));
 
   // ---- fit / stop state
   state_ = dalloc<FitState>(1);
@@ -458,7 +499,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
 void Session::setup_fused() {
   bool all_direct = true;
   for (int n = 0; n < order_; ++n) all_direct = all_direct && direct_[static_cast<size_t>(n)];
-  if (o_.fused == 0 || !all_direct || o_.exhaustive_samples) return;
+  if (o_.fused == 0 || !all_direct || o_.exhaustive_samples || shard_) return;
   i64 max_dim = 1;
   for (i64 d : dims_) max_dim = std::max(max_dim, d);
   int zcap = 0;
@@ -627,6 +668,79 @@ void Session::setup_fused() {
   fused_ = true;
 }
 
+void Session::allreduce_sum(double* buf, i64 n) {
+  if (!shard_ || n == 0) return;
+  const ncclResult_t r = ncclAllReduce(buf, buf, static_cast<size_t>(n), ncclDouble, ncclSum,
+                                       static_cast<ncclComm_t>(nccl_), stream_);
+  if (r != ncclSuccess) throw CudaError(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+}
+
+void Session::allgather(double* buf, i64 per_rank) {
+  if (!shard_ || per_rank == 0) return;
+  const ncclResult_t r = ncclAllGather(buf + static_cast<i64>(rank_) * per_rank, buf, static_cast<size_t>(per_rank),
+                                       ncclDouble, static_cast<ncclComm_t>(nccl_), stream_);
+  if (r != ncclSuccess) throw CudaError(std::string("ncclAllGather: ") + ncclGetErrorString(r));
+}
+
+// One mode of the slab-sharded loop: Z_S, the Gram and its
+// inverse are replicated; the RHS contracts only this rank's fibers.
+//  n < N-1: fibers of the samples whose last-mode index is in the slab;
+//           RHS allreduced, then every rank applies the same solve.
+//  n = N-1: the slab rows of every fiber; the rank forms its factor rows,
+//           the column sums of squares are allreduced, the slabs allgathered.
+void Session::enqueue_mode_sharded(int it, int n, const int* stop) {
+  const int N = order_;
+  const int ti = o_.exhaustive_samples ? 0 : it - 1;
+  const ModeView v = view(it, n);
+  const ModeWork w = work(n);
+  timed(n, 2, stream_, [&] { launch_z(v, w.z, stop, stream_); });
+  CPB_CUDA(cudaEventRecord(ev_z_, stream_));
+  CPB_CUDA(cudaStreamWaitEvent(stream2_, ev_z_, 0));
+  timed(n, 3, stream2_, [&] { launch_gram(w.z, v.s, r_, w.part_gram, stop, stream2_); });
+  timed(n, 4, stream2_, [&] {
+    launch_gram_inverse(w.part_gram, w.gram_parts, r_, w.tol, w.ginv, w.gfull, w.info, stop, stream2_);
+  });
+  CPB_CUDA(cudaEventRecord(ev_inv_, stream2_));
+  const bool last = (n == N - 1);
+  const i64 in_loc = last ? slab_len_ : dims_[static_cast<size_t>(n)];
+  const int cnt = loc_cnt_[static_cast<size_t>(ti * N + n)];
+  const i64 lo = loc_off_[static_cast<size_t>(ti * N + n)];
+  const double* zsrc = w.z;
+  const i64* db = dbase_ptr(it, n);
+  if (!last) {
+    launch_gather_z_rows(w.z, loc_idx_ + lo, cnt, rt_, zloc_, stream_);
+    zsrc = zloc_;
+    db = loc_dbase_ + lo;
+  }
+  if (cnt > 0 && in_loc > 0) {
+    int ks = 1, ks_len = 16;
+    mode_splits(in_loc, cnt, rt_, &ks, &ks_len, sms_);
+    timed(n, 1, stream_, [&] {
+      launch_rhs_gemm(n == 0 ? xsolve_ : rep_[static_cast<size_t>(n)], 0, db, vec16_[static_cast<size_t>(n)], zsrc,
+                      in_loc, cnt, r_, ks, ks_len, w.part_rhs, stop, stream_);
+    });
+    launch_reduce_rhs(w.part_rhs, ks, in_loc, r_, rhs_full_, stream_);
+  } else if (in_loc > 0) {
+    CPB_CUDA(cudaMemsetAsync(rhs_full_, 0, sizeof(double) * in_loc * r_, stream_));
+  }
+  CPB_CUDA(cudaStreamWaitEvent(stream_, ev_inv_, 0));
+  if (!last) {
+    allreduce_sum(rhs_full_, dims_[static_cast<size_t>(n)] * r_);
+    timed(n, 5, stream_, [&] { launch_mode_apply(v.in, r_, w, rhs_full_, n == 0, rng_state_, stream_); });
+  } else {
+    const int g = apply_rows_grid(std::max<i64>(slab_len_, 1), r_);
+    double* ssq = sh_part_ + static_cast<i64>(g) * r_;
+    timed(n, 5, stream_, [&] {
+      launch_apply_rows(slab_len_, r_, rhs_full_, w.ginv, w.a + slab_off_ * r_, sh_part_, stream_);
+      launch_col_ssq(sh_part_, g, r_, ssq, stream_);
+    });
+    allreduce_sum(ssq, r_);
+    allgather(w.a, lmax_ * r_);
+    launch_norms_from_ssq(ssq, r_, dims_[static_cast<size_t>(n)], w.a, w.norms, w.lambda, n == 0, rng_state_,
+                          stream_);
+  }
+}
+
 long long Session::gram_fallbacks() {
   if (!info_) return 0;
   CPB_CUDA(cudaStreamSynchronize(stream_));
@@ -670,6 +784,8 @@ void Session::build_tables() {
   std::vector<int> rows(static_cast<size_t>(std::max<i64>(rows_total, 1)));
   std::vector<i64> base(static_cast<size_t>(std::max<i64>(base_total, 1)), 0);
   std::vector<i64> dbase(static_cast<size_t>(std::max<i64>(base_total, 1)), 0);
+  std::vector<int> lidx;
+  std::vector<i64> ldb;
   auto rng = seeded_engine(o_.rng_seed, kSamplingStream);
   for (int it = 0; it < table_iters_; ++it)
     for (int n = 0; n < N; ++n) {
@@ -678,49 +794,84 @@ void Session::build_tables() {
       i64* bb = base.data() + base_off_[static_cast<size_t>(it * N + n)];
       i64* db = dbase.data() + base_off_[static_cast<size_t>(it * N + n)];
       std::vector<int> km;
-      std::vector<i64> jk;  // unfolding column weights J_k (tensor.hpp:92-106)
+      std::vector<i64> jk;  // unfolding column weights J_k of the tensor read (tensor.hpp:92-106)
       {
         i64 jw = 1;
         for (int k = 0; k < N; ++k)
           if (k != n) {
             km.push_back(k);
             jk.push_back(jw);
-            jw *= dims_[static_cast<size_t>(k)];
+            jw *= tdims_[static_cast<size_t>(k)];
           }
       }
-      const i64 in_n = dims_[static_cast<size_t>(n)];
+      const i64 in_n = tdims_[static_cast<size_t>(n)];
+      std::vector<long> idx(static_cast<size_t>(N - 1));
+      // base offset (tensor the session reads) and replica row of sample j;
+      // with sharding the last mode's index is taken relative to the slab
+      auto place = [&](int j) {
+        i64 b = 0, col = 0;
+        for (int c = 0; c < N - 1; ++c) {
+          const int k = km[static_cast<size_t>(c)];
+          i64 v = idx[static_cast<size_t>(c)];
+          if (shard_ && k == N - 1) v -= slab_off_;
+          b += v * tstrides_[static_cast<size_t>(k)];
+          col += v * jk[static_cast<size_t>(c)];
+        }
+        bb[j] = b;
+        db[j] = (n == 0) ? b : in_n * col;  // row of X_(n) in the mode-major replica
+      };
       if (o_.exhaustive_samples) {
         // sampling.hpp:54-69: unfolding column order
         for (int j = 0; j < sn; ++j) {
-          i64 rem = j, b = 0, col = 0;
+          i64 rem = j;
           for (int c = 0; c < N - 1; ++c) {
             const i64 d = dims_[static_cast<size_t>(km[static_cast<size_t>(c)])];
-            const i64 idx = rem % d;
+            idx[static_cast<size_t>(c)] = static_cast<long>(rem % d);
             rem /= d;
-            rb[static_cast<i64>(c) * sn + j] = static_cast<int>(idx);
-            b += idx * strides_[static_cast<size_t>(km[static_cast<size_t>(c)])];
-            col += idx * jk[static_cast<size_t>(c)];
+            rb[static_cast<i64>(c) * sn + j] = static_cast<int>(idx[static_cast<size_t>(c)]);
           }
-          bb[j] = b;
-          db[j] = (n == 0) ? b : in_n * col;
+          place(j);
         }
       } else {
         // sampling.hpp:35-51: one uniform_int per kept mode, row by row
         std::vector<std::uniform_int_distribution<long>> dist;
         for (int k : km) dist.emplace_back(0L, static_cast<long>(dims_[static_cast<size_t>(k)] - 1));
         for (int j = 0; j < sn; ++j) {
-          i64 b = 0, col = 0;
           for (int c = 0; c < N - 1; ++c) {
-            const long idx = dist[static_cast<size_t>(c)](rng);
-            rb[static_cast<i64>(c) * sn + j] = static_cast<int>(idx);
-            b += static_cast<i64>(idx) * strides_[static_cast<size_t>(km[static_cast<size_t>(c)])];
-            col += static_cast<i64>(idx) * jk[static_cast<size_t>(c)];
+            idx[static_cast<size_t>(c)] = dist[static_cast<size_t>(c)](rng);
+            rb[static_cast<i64>(c) * sn + j] = static_cast<int>(idx[static_cast<size_t>(c)]);
           }
-          bb[j] = b;
-          db[j] = (n == 0) ? b : in_n * col;  // row of X_(n) in the mode-major replica
+          if (shard_ && n < N - 1) {  // fiber in this slab? (last kept column is mode N-1)
+            const long last = idx[static_cast<size_t>(N - 2)];
+            if (last >= slab_off_ && last < slab_off_ + slab_len_) place(j);
+          } else {
+            place(j);
+          }
         }
       }
+      if (shard_) {  // local sample lists (mode N-1: every sample)
+        loc_off_.push_back(static_cast<i64>(lidx.size()));
+        int cnt = 0;
+        for (int j = 0; j < sn; ++j) {
+          const bool local = (n == N - 1) || (rb[static_cast<i64>(N - 2) * sn + j] >= slab_off_ &&
+                                              rb[static_cast<i64>(N - 2) * sn + j] < slab_off_ + slab_len_);
+          if (!local) continue;
+          lidx.push_back(j);
+          ldb.push_back(db[j]);
+          ++cnt;
+        }
+        loc_cnt_.push_back(cnt);
+      }
     }
+  if (shard_) {
+    loc_idx_ = dalloc<int>(std::max<size_t>(lidx.size(), 1));
+    loc_dbase_ = dalloc<i64>(std::max<size_t>(ldb.size(), 1));
+    if (!lidx.empty()) {
+      CPB_CUDA(cudaMemcpyAsync(loc_idx_, lidx.data(), lidx.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
+      CPB_CUDA(cudaMemcpyAsync(loc_dbase_, ldb.data(), ldb.size() * sizeof(i64), cudaMemcpyHostToDevice, stream_));
+    }
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+  }
   rows_ = dalloc<int>(rows.size());
   base_ = dalloc<i64>(base.size());
   dbase_ = dalloc<i64>(dbase.size());
@@ -746,7 +897,29 @@ void Session::build_fit_estimator(const double* xsrc) {
   i64* d_off = dalloc<i64>(offs.size());
   CPB_CUDA(cudaMemcpyAsync(d_off, offs.data(), offs.size() * sizeof(i64), cudaMemcpyHostToDevice, stream_));
   fit_vals_ = dalloc<double>(offs.size());
-  launch_gather_values(xsrc, d_off, phat_, fit_vals_, stream_);
+  if (shard_) {
+    // entries outside this slab contribute 0; the allreduce assembles them
+    std::vector<i64> loc(offs.size());
+    for (size_t j = 0; j < offs.size(); ++j) {
+      i64 lo = 0;
+      bool mine = true;
+      for (int n = 0; n < order_; ++n) {
+        i64 v = (offs[j] / strides_[static_cast<size_t>(n)]) % dims_[static_cast<size_t>(n)];
+        if (n == order_ - 1) {
+          v -= slab_off_;
+          mine = v >= 0 && v < slab_len_;
+        }
+        lo += v * tstrides_[static_cast<size_t>(n)];
+      }
+      loc[j] = mine ? lo : -1;
+    }
+    CPB_CUDA(cudaMemcpyAsync(d_off, loc.data(), loc.size() * sizeof(i64), cudaMemcpyHostToDevice, stream_));
+    launch_gather_values_masked(xsrc, d_off, phat_, fit_vals_, stream_);
+    allreduce_sum(fit_vals_, phat_);
+    CPB_CUDA(cudaStreamSynchronize(stream_));  // loc dies here
+  } else {
+    launch_gather_values(xsrc, d_off, phat_, fit_vals_, stream_);
+  }
   std::vector<int> idx(offs.size());
   for (int n = 0; n < order_; ++n) {
     const i64 d = dims_[static_cast<size_t>(n)], st = strides_[static_cast<size_t>(n)];
@@ -806,27 +979,31 @@ void Session::plan_replicas() {
   vec16_.assign(static_cast<size_t>(order_), 0);
   rep_.assign(static_cast<size_t>(order_), nullptr);
   direct_[0] = 1;
-  vec16_[0] = (order_ == 1) || (dims_[0] % 2 == 0);
+  vec16_[0] = (order_ == 1) || (tdims_[0] % 2 == 0);
   if (o_.replicas == 0) return;
   size_t free_b = 0, total_b = 0;
   CPB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const i64 bytes = p_ * 8;
+  const i64 bytes = tp_ * 8;
   i64 budget = static_cast<i64>(free_b) - (i64{6} << 30);  // keep 6 GB for work buffers
   if ((mix_ || premix_) && !o_.x_mutable) budget -= bytes;  // the private mixed copy comes first
   // widest strides first: they gain the most
   for (int n = order_ - 1; n >= 1; --n) {
     if (budget < bytes) break;
     direct_[static_cast<size_t>(n)] = 1;
-    vec16_[static_cast<size_t>(n)] = dims_[static_cast<size_t>(n)] % 2 == 0;
+    vec16_[static_cast<size_t>(n)] = tdims_[static_cast<size_t>(n)] % 2 == 0;
     budget -= bytes;
   }
+  if (shard_)
+    for (int n = 0; n < order_; ++n)
+      if (!direct_[static_cast<size_t>(n)])
+        throw Unsupported("slab sharding needs the mode-major replicas of every strided mode to fit in HBM");
 }
 
 void Session::build_replicas() {
   for (int n = 1; n < order_; ++n) {
     if (!direct_[static_cast<size_t>(n)]) continue;
-    rep_[static_cast<size_t>(n)] = dalloc<double>(static_cast<size_t>(p_));
-    launch_replica(xsolve_, dims_[static_cast<size_t>(n)], strides_[static_cast<size_t>(n)], p_,
+    rep_[static_cast<size_t>(n)] = dalloc<double>(static_cast<size_t>(tp_));
+    launch_replica(xsolve_, tdims_[static_cast<size_t>(n)], tstrides_[static_cast<size_t>(n)], tp_,
                    rep_[static_cast<size_t>(n)], stream_);
   }
   CPB_CUDA(cudaStreamSynchronize(stream_));
@@ -844,7 +1021,7 @@ ModeView Session::view(int it, int n) const {
   ModeView v{};
   v.x = xsolve_;
   v.in = dims_[static_cast<size_t>(n)];
-  v.stride = strides_[static_cast<size_t>(n)];
+  v.stride = tstrides_[static_cast<size_t>(n)];
   v.s = sn;
   v.r = r_;
   v.kept = N - 1;
@@ -941,7 +1118,7 @@ void Session::enqueue_gather(int git) {
     const size_t slot = static_cast<size_t>(((git - 1) % depth_) * order_ + n);
     if (slot_used_[slot]) CPB_CUDA(cudaStreamWaitEvent(gstream_, ev_consumed_[slot], 0));
     timed(n, 0, gstream_, [&] {
-      launch_gather_rows(xsolve_, dims_[static_cast<size_t>(n)], strides_[static_cast<size_t>(n)], base_ptr(git, n),
+      launch_gather_rows(xsolve_, tdims_[static_cast<size_t>(n)], tstrides_[static_cast<size_t>(n)], base_ptr(git, n),
                          s_mode_[static_cast<size_t>(n)], ring_[slot], ld_[static_cast<size_t>(n)], gstream_);
     });
     CPB_CUDA(cudaEventRecord(ev_gathered_[slot], gstream_));
@@ -1046,6 +1223,10 @@ void Session::enqueue_iteration() {
   while (gathered_ < want) enqueue_gather(gathered_ + 1);
   const int* stop = has_fit_ ? &state_->stopped : nullptr;
   for (int n = 0; n < order_; ++n) {
+    if (shard_) {
+      enqueue_mode_sharded(it, n, stop);
+      continue;
+    }
     const ModeView v = view(it, n);
     const ModeWork w = work(n);
     const size_t slot = static_cast<size_t>(((it - 1) % depth_) * order_ + n);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <chrono>
+#include <functional>
 #include <cstdint>
 #include <optional>
 #include <random>
@@ -33,6 +34,11 @@ struct Options {  // SolveOptions (solver.hpp:40-64) + device extensions
   bool x_mutable = false;
   int replicas = -1;  // mode-major replicas for strided modes: -1 auto, 0 off, 1 on
   int fused = -1;     // persistent per-iteration kernel: -1 auto, 0 off (multi-kernel chain)
+  // slab sharding over NCCL: the session's tensor is this rank's slab of the
+  // last mode, rows [rank * ceil(I/P), ...) of a tensor with last dim shard_total
+  void* nccl = nullptr;  // ncclComm_t
+  int nranks = 1, rank = 0;
+  i64 shard_total = 0;
   void validate() const;
 };
 
@@ -103,6 +109,9 @@ class Session {
   const i64* base_ptr(int it, int n) const;
   const i64* dbase_ptr(int it, int n) const;
   void download_model(HostModel& m);
+  void allreduce_sum(double* buf, i64 n);
+  void allgather(double* buf, i64 per_rank);
+  void enqueue_mode_sharded(int it, int n, const int* stop);
   void collect_kernel_times();
   cudaEvent_t timing_event();
 
@@ -113,8 +122,21 @@ class Session {
   Options o_;
   int transform_ = -1;
   bool mix_ = false, premix_ = false;
-  std::vector<i64> dims_, strides_;
+  std::vector<i64> dims_, strides_;  // global (model) shape
   i64 p_ = 0;
+  std::vector<i64> tdims_, tstrides_;  // the tensor this session reads (a slab when sharded)
+  i64 tp_ = 0;
+  // slab sharding
+  bool shard_ = false;
+  void* nccl_ = nullptr;
+  int nranks_ = 1, rank_ = 0;
+  i64 slab_off_ = 0, slab_len_ = 0, lmax_ = 0;
+  std::vector<i64> loc_off_;   // [iter][mode] offset into loc_idx_ / loc_dbase_
+  std::vector<int> loc_cnt_;   // [iter][mode] samples whose fiber lies in this slab
+  int* loc_idx_ = nullptr;     // their sample indices
+  i64* loc_dbase_ = nullptr;   // their row offsets in the (slab) replica
+  double* zloc_ = nullptr;     // Z rows of the local samples
+  double* sh_part_ = nullptr;  // mode N-1: per-CTA column sums of squares, then [R] totals
   int sms_ = 148;
   cudaStream_t stream_ = nullptr;   // s1: solve chain
   cudaStream_t stream2_ = nullptr;  // s2: Gram pseudo-inverse
@@ -242,7 +264,7 @@ void op_transform_factor(const double* a, i64 rows, int r, const std::vector<i64
 void op_unmix_rows(const double* g, i64 s, i64 in, const std::vector<i64>& dims, int transform,
                    std::uint64_t seed, int mode, double* out);
 void op_debug_normals(std::uint64_t seed, int n, double* out);
-void op_synth(Tensor* t, int r, double c, double eta, std::uint64_t seed,
-              double* const* out_factors);
+void op_synth(Tensor* t, int r, double c, double eta, std::uint64_t seed, double* const* out_factors,
+              i64 last_off = 0, i64 global_last = 0, const std::function<void(double*)>& reduce_sums = nullptr);
 
 }  // namespace cpb

@@ -4,6 +4,8 @@
 // keyed by the seed (the CPU oracle draws the identical integer stream;
 // transcendental rounding may differ in the last ulp). Factors are drawn on
 // the host (normal_distribution on seeded_engine(seed, kSynthStream)).
+#include <functional>
+
 #include "kernels.cuh"
 
 namespace cpb {
@@ -15,7 +17,9 @@ constexpr int kSynthThreads = 256;
 struct SynthArgs {
   double* x;
   int order;
-  i64 dims[kMaxOrder];
+  i64 dims[kMaxOrder];   // of the tensor written (a slab of the last mode when sharded)
+  i64 gstr[kMaxOrder];   // strides of the global tensor (Philox counter = global offset)
+  i64 last_off;          // global index of the slab's first last-mode row
   int r;
   const double* fac[kMaxOrder];  // row-major I_n x R
   i64 p;
@@ -53,12 +57,14 @@ __global__ void __launch_bounds__(kSynthThreads) synth_pass1(SynthArgs a) {
   const i64 per = (a.p + gridDim.x - 1) / gridDim.x;
   const i64 lo = per * blockIdx.x, hi = min(a.p, lo + per);
   for (i64 off = lo + threadIdx.x; off < hi; off += blockDim.x) {
-    i64 rem = off;
+    i64 rem = off, goff = 0;
     i64 idx[kMaxOrder];
     for (int k = 0; k < a.order; ++k) {
       idx[k] = rem % a.dims[k];
       rem /= a.dims[k];
     }
+    idx[a.order - 1] += a.last_off;
+    for (int k = 0; k < a.order; ++k) goff += idx[k] * a.gstr[k];
     double sum = 0.0;
     for (int q = 0; q < a.r; ++q) {
       double prod = a.fac[0][idx[0] * a.r + q];
@@ -68,7 +74,7 @@ __global__ void __launch_bounds__(kSynthThreads) synth_pass1(SynthArgs a) {
     a.x[off] = sum;
     sig = fma(sum, sum, sig);
     if (a.part_noise) {
-      const double z = philox_gauss(a.seed, static_cast<unsigned long long>(off));
+      const double z = philox_gauss(a.seed, static_cast<unsigned long long>(goff));
       noi = fma(z, z, noi);
     }
   }
@@ -88,42 +94,61 @@ __global__ void __launch_bounds__(kSynthThreads) synth_pass1(SynthArgs a) {
   }
 }
 
-__global__ void synth_scale(const double* part_sig, const double* part_noise, int nb, double eta,
-                            double* scale_out) {
+__global__ void synth_sums(const double* part_sig, const double* part_noise, int nb, double* out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s = 0.0, n = 0.0;
   for (int i = 0; i < nb; ++i) {
     s += part_sig[i];
     n += part_noise[i];
   }
-  const double signal = sqrt(s), nn = sqrt(n);
-  *scale_out = (signal > 0.0 && nn > 0.0) ? eta * signal / nn : 0.0;
+  out[0] = s;
+  out[1] = n;
 }
 
-__global__ void synth_pass2(double* x, i64 p, unsigned long long seed, const double* scale) {
+__global__ void synth_scale(double* sums, double eta) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double signal = sqrt(sums[0]), nn = sqrt(sums[1]);
+  sums[2] = (signal > 0.0 && nn > 0.0) ? eta * signal / nn : 0.0;
+}
+
+__global__ void synth_pass2(SynthArgs a, const double* scale) {
   const double sc = *scale;
-  for (i64 off = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; off < p;
+  for (i64 off = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; off < a.p;
        off += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const double z = philox_gauss(seed, static_cast<unsigned long long>(off));
-    x[off] = __dadd_rn(x[off], __dmul_rn(sc, z));
+    i64 rem = off, goff = 0;
+    for (int k = 0; k < a.order; ++k) {
+      i64 v = rem % a.dims[k];
+      rem /= a.dims[k];
+      if (k == a.order - 1) v += a.last_off;
+      goff += v * a.gstr[k];
+    }
+    const double z = philox_gauss(a.seed, static_cast<unsigned long long>(goff));
+    a.x[off] = __dadd_rn(a.x[off], __dmul_rn(sc, z));
   }
 }
 
 }  // namespace
 
-// scratch: >= 2 * 4096 + 1 doubles
+// scratch: >= 2 * 4096 + 3 doubles. Slab form: dims are the slab's, the
+// last mode starts at global row last_off of a tensor whose last dim is
+// global_last; reduce_sums (nullable) sums [sig, noise] over the ranks.
 void launch_synth(double* x, int order, const i64* dims, int r, const double* const* fac_dev,
-                  double eta, unsigned long long seed, double* scratch, cudaStream_t st) {
+                  double eta, unsigned long long seed, double* scratch, cudaStream_t st, i64 last_off,
+                  i64 global_last, const std::function<void(double*)>& reduce_sums) {
   if (order > kMaxOrder) throw Unsupported("synth: order > 8");
   SynthArgs a{};
   a.x = x;
   a.order = order;
   a.p = 1;
+  i64 gs = 1;
   for (int k = 0; k < order; ++k) {
     a.dims[k] = dims[k];
     a.fac[k] = fac_dev[k];
     a.p *= dims[k];
+    a.gstr[k] = gs;
+    gs *= (k == order - 1 && global_last > 0) ? global_last : dims[k];
   }
+  a.last_off = last_off;
   a.r = r;
   a.seed = seed;
   const int nb = 4096;
@@ -132,9 +157,13 @@ void launch_synth(double* x, int order, const i64* dims, int r, const double* co
   synth_pass1<<<nb, kSynthThreads, 0, st>>>(a);
   CPB_LAUNCH_CHECK();
   if (eta > 0.0) {
-    synth_scale<<<1, 32, 0, st>>>(scratch, scratch + nb, nb, eta, scratch + 2 * nb);
+    double* sums = scratch + 2 * nb;
+    synth_sums<<<1, 32, 0, st>>>(scratch, scratch + nb, nb, sums);
     CPB_LAUNCH_CHECK();
-    synth_pass2<<<148 * 16, 256, 0, st>>>(x, a.p, seed, scratch + 2 * nb);
+    if (reduce_sums) reduce_sums(sums);
+    synth_scale<<<1, 32, 0, st>>>(sums, eta);
+    CPB_LAUNCH_CHECK();
+    synth_pass2<<<148 * 16, 256, 0, st>>>(a, sums + 2);
     CPB_LAUNCH_CHECK();
   }
 }
