@@ -230,13 +230,26 @@ def main() -> int:
     dev = local
     hbm_peak, peak_src = peaks()
 
-    # ---- inputs resident in HBM
-    t = pb.DeviceTensor(cfg["dims"], device=dev)
-    t.synth(cfg["r"], cfg["c"], cfg["eta"], SEED)
+    # ---- inputs resident in HBM: the whole tensor, or (N > 1) this rank's
+    # slab of the last mode (BASELINE.json: slab-sharded with NCCL)
+    comm = None
+    dims = list(cfg["dims"])
+    if ws > 1:
+        from paper_1701_06600_b200 import shard
+        uid = [pb.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = pb.Comm(uid[0], rank, ws, dev)
+        dims[-1] = shard.slab(cfg["dims"][-1], ws, rank)[1]
+    t = pb.DeviceTensor(dims, device=dev)
+    if comm is None:
+        t.synth(cfg["r"], cfg["c"], cfg["eta"], SEED)
+    else:
+        t.synth_slab(cfg["r"], cfg["c"], cfg["eta"], SEED, cfg["dims"][-1], comm)
     timing_iters = max(args.steps, 10)
     total_iters = args.warmup + args.steps + timing_iters + 2
     opts = pb.SolveOptions(rng_seed=SEED, max_iters=total_iters, bench_mode=True,
-                           transform=cfg["transform"], x_mutable=False, device=dev)
+                           transform=cfg["transform"], x_mutable=False, device=dev,
+                           comm=comm, shard_total=cfg["dims"][-1] if comm is not None else 0)
     s = pb.Session(cfg["method"], t, cfg["r"], cfg["s"], opts)
     clk = ClockSampler(dev).__enter__()
     s.run(args.warmup)
@@ -251,7 +264,8 @@ def main() -> int:
     clk.__exit__(None, None, None)
     ms = allreduce_max(dist, ms)
     barrier(dist)
-    value = ws * args.steps / (ms * 1e-3)
+    # one global problem: iterations of the whole (sharded) decomposition per second
+    value = args.steps / (ms * 1e-3)
 
     # ---- roofline: per-launch CUDA events on each kernel's own stream
     s.set_kernel_timing(True)
@@ -308,15 +322,16 @@ def main() -> int:
 
     # ---- e2e through the public one-shot call with host buffers
     e2e, cpu = None, None
-    if rank == 0 and (args.e2e_steps > 0 or not args.no_cpu):
-        p = int(np.prod(cfg["dims"]))
+    if (rank == 0 or comm is not None) and (args.e2e_steps > 0 or not args.no_cpu):
+        p = int(np.prod(dims))
         buf = pb.PinnedBuffer(p)
         flat = t.download().reshape(-1, order="F")
         buf.array[:] = flat
         del flat
-        xh = buf.array.reshape(cfg["dims"], order="F")
+        xh = buf.array.reshape(dims, order="F")
         eo = pb.SolveOptions(rng_seed=SEED, max_iters=args.e2e_iters, bench_mode=True,
-                             transform=cfg["transform"], device=dev)
+                             transform=cfg["transform"], device=dev, comm=comm,
+                             shard_total=cfg["dims"][-1] if comm is not None else 0)
         if args.e2e_steps > 0:
             pb.solve(cfg["method"], xh, cfg["r"], cfg["s"], eo)  # warm
             t0 = time.perf_counter()
@@ -342,12 +357,12 @@ def main() -> int:
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE.json generator in HBM, seed 1)",
             "config": {"workload": args.config, "dims": list(cfg["dims"]), "R": cfg["r"],
                        "S": cfg["s"], "P_hat": cfg["phat"], "method": cfg["method"],
                        "transform": cfg["transform"], "bench_mode": True,
-                       "parallelism": "replicas" if ws > 1 else "single",
+                       "parallelism": f"slab{ws} (last mode, NCCL allreduce/allgather)" if ws > 1 else "single",
                        "l2": "inputs larger than L2 (8 GB tensor, fresh random samples per step)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": kname,
@@ -370,6 +385,8 @@ def main() -> int:
             "gpu_launches": launches_per_iter(cfg) * args.steps,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if dist is not None:
         dist.destroy_process_group()
     return 0
