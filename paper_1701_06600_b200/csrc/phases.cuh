@@ -1214,18 +1214,20 @@ __device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int fi
   constexpr int NP = NTH / RT;
   const int tid = threadIdx.x, part = tid / RT, c = tid % RT;
   __shared__ int s_zero;
+  // thread (part, c) sums a contiguous range of partials, 32 loads in flight;
+  // the parts are then combined in order (deterministic)
   double q = 0.0;
-  if (c < r && part < nparts) {  // partials part, part + NP, ... in order, 16 loads in flight
-    const double* p = w.ssq + static_cast<i64>(part) * r + c;
-    const i64 step = static_cast<i64>(NP) * r;
-    const int cnt = (nparts - part + NP - 1) / NP;
-    for (int k = 0; k < cnt; k += 16) {
-      double v[16];
+  if (c < r && part < nparts) {
+    const int len = (nparts + NP - 1) / NP;
+    const int b0 = part * len, b1 = min(nparts, b0 + len);
+    const double* p = w.ssq + static_cast<i64>(b0) * r + c;
+    for (int k = 0; k < b1 - b0; k += 32) {
+      double v[32];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = (k + u < cnt) ? __ldcg(p + (k + u) * step) : 0.0;
+      for (int u = 0; u < 32; ++u) v[u] = (k + u < b1 - b0) ? p[static_cast<i64>(k + u) * r] : 0.0;  // after an acquire
 #pragma unroll
-      for (int u = 0; u < 16; ++u)
-        if (k + u < cnt) q += v[u];
+      for (int u = 0; u < 32; ++u)
+        if (k + u < b1 - b0) q += v[u];
     }
   }
   red[part * (RT + 1) + c] = q;
