@@ -273,10 +273,6 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
   const unsigned rank = b - (static_cast<int>(b) > inv ? 1u : 0u) - (idle >= 0 && static_cast<int>(b) > idle ? 1u : 0u);
   const int r = A.r;
   const int nfr = (r + 7) / 8;
-  // release generation (+1 per mode), replicated; CTA b polls replica b % kRep.
-  // No release of this launch can precede every CTA's first signal.
-  unsigned* gen = A.gen_rep + (b % kRep) * kCS;
-  const unsigned gen0 = ld_acquire(gen);
   prefetch_tables(A, b);
   if (A.cta_t && tid == 0) {
     unsigned sm;
@@ -287,11 +283,25 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
     if (A.phase_t && rank == 0 && !is_inv && !is_idle && tid == 0) A.phase_t[n * 16 + k] = globaltimer();
     if (A.cta_t && n == 1 && tid == 0) A.cta_t[b * 16 + k] = globaltimer();
   };
+  const unsigned seq = A.seq;
+  // norms + lambda of mode m (inverse CTA), from the tile CTAs' column sums
+  // of squares (buffer m & 1). Mode m >= 1 entered the next Z_S unnormalized,
+  // so its solution carries mode m-1's norms as a column scale (lam_scale).
+  auto form_norms = [&](int m) {
+    const FusedMode& Q = A.mode[m];
+    ModeWork wq = work_of(A, Q);
+    wq.ssq = A.ssq + static_cast<i64>(m & 1) * G * r;
+    ph::norms_final<RT, kFusedThreads>(r, Q.v.in, wq, static_cast<int>(Gw), m == 0, A.rng, fsm, nullptr,
+                                       m >= 1 ? A.mode[m - 1].norms : nullptr);
+    signal_add_rep(Q.nready, 1u, kRep);
+  };
   for (int n = 0; n < A.order; ++n) {
     const FusedMode& M = A.mode[n];
     const ModeWork w = work_of(A, M);
     const i64 in = M.v.in;
     const int ntiles = M.tm * M.tk;
+    if (n >= 1 && !is_idle)  // the previous mode's factor rows are all written
+      wait_geq(A.mode[n - 1].adone + (b % kRep) * kCS, seq * Gw, 64);
     stamp(n, 0);
     if (b == 0) {  // reset the previous mode's counters: every wait on them is over
       const FusedMode& P = A.mode[(n + A.order - 1) % A.order];
@@ -302,6 +312,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       for (int e = tid; e < P.tm; e += kFusedThreads) P.gm_cnt[e * kCS] = 0u;
     }
     if (is_inv) {
+      if (n >= 1) form_norms(n - 1);  // off the critical path: overlaps this mode's Z / Gram
+      if (A.phase_t && tid == 0) A.phase_t[n * 16 + 13] = globaltimer();
       // ---- Gram: the row-block reducers summed it (dist_gram), or sum the
       // split partials of every 8 x 8 block here (split order)
       wait_geq(M.mcnt, static_cast<unsigned>(M.dist_gram ? M.nblk : ntiles));
@@ -348,6 +360,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 7] = globaltimer();
     } else if (!is_idle) {
       const TileSmem t = tile_smem<RT>(fsm, M.zcap);
+      if (n >= 2)  // Z_S divides by the norms of the modes before n-1
+        wait_geq(A.mode[n - 2].nready + (b % kRep) * kCS, seq, 64);
       // this CTA's share of every one of its splits' Z rows, then signal
       // (no waiting here, so CTAs with several tiles cannot deadlock)
       for (int tt = rank; tt < ntiles; tt += Gw) {
@@ -440,31 +454,21 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
         __syncthreads();
       }
       stamp(n, 4);
-      if (tid < r) A.ssq[static_cast<i64>(rank) * r + tid] = q2;
-      signal_add(M.mcnt + 2 * kCS, 1u);
+      if (tid < r) A.ssq[static_cast<i64>(n & 1) * G * r + static_cast<i64>(rank) * r + tid] = q2;
+      signal_add_rep(M.adone, 1u, kRep);
       stamp(n, 5);
-      if (rank == 0) {
-        // ---- norms + lambda from the tile CTAs' column sums of squares
-        wait_geq(M.mcnt + 2 * kCS, Gw);
-        if (A.cta_t && n == 1 && tid == 0) A.cta_t[b * 16 + 12] = globaltimer();
-        ph::norms_final<RT, kFusedThreads>(r, in, w, static_cast<int>(Gw), n == 0, A.rng, fsm,
-                                           (A.cta_t && n == 1) ? A.cta_t + b * 16 + 7 : nullptr);
-        if (A.cta_t && n == 1 && tid == 0) A.cta_t[b * 16 + 13] = globaltimer();
-        if (A.phase_t && tid == 0) A.phase_t[n * 16 + 13] = globaltimer();
-        signal_add_rep(A.gen_rep, 1u, kRep);
-      }
-    }
-    // ---- wait for the release of mode n (tile rank 0 formed the norms)
-    {
-      if (tid == 0) {
-        while (static_cast<int>(ld_relaxed(gen) - (gen0 + n + 1)) < 0) __nanosleep(64);
-        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-      }
-      __syncthreads();
     }
     stamp(n, 6);
   }
   if (A.next) prefetch_tables(*A.next, b);
+  {  // norms of the last mode (the next launch's Z_S and the fit need them)
+    const FusedMode& L = A.mode[A.order - 1];
+    if (is_inv) {
+      wait_geq(L.adone + (b % kRep) * kCS, seq * Gw, 64);
+      form_norms(A.order - 1);
+    }
+    if (A.has_fit && !is_inv) wait_geq(L.nready + (b % kRep) * kCS, seq, 64);
+  }
   // ---- sampled fit + stop rule (sampling.hpp:191-210, :237-251)
   if (A.has_fit) {
     const FitArgs& f = A.fit;

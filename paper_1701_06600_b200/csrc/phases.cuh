@@ -1210,7 +1210,8 @@ __device__ void ssq_store(double q, int r, double* ssq_part, double* red) {
 // red: (NTH / RT) x (RT + 1) doubles.
 template <int RT, int NTH>
 __device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int first_of_pass,
-                            unsigned long long* rng_state, double* red, unsigned long long* dbg = nullptr) {
+                            unsigned long long* rng_state, double* red, unsigned long long* dbg = nullptr,
+                            const double* lam_scale = nullptr) {
   constexpr int NP = NTH / RT;
   const int tid = threadIdx.x, part = tid / RT, c = tid % RT;
   __shared__ int s_zero;
@@ -1244,7 +1245,10 @@ __device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int fi
       w.lambda[tid] = 0.0;
       atomicOr(&s_zero, 1);
     } else {
-      w.lambda[tid] = first_of_pass ? __ldcg(w.lambda + tid) * nrm : nrm;
+      // lam_scale: column scale the solution carried (the previous mode's norms
+      // when its factor entered Z_S unnormalized)
+      const double full = lam_scale ? nrm * __ldcg(lam_scale + tid) : nrm;
+      w.lambda[tid] = first_of_pass ? __ldcg(w.lambda + tid) * full : full;
     }
   }
   __syncthreads();
