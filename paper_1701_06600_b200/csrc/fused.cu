@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       for (int e = tid; e < P.tk; e += kFusedThreads) P.kb_cnt[e * kCS] = 0u;
       if (tid < 3) P.mcnt[tid * kCS] = 0u;
       if (tid < kRep) P.grdy[tid * kCS] = 0u;
+      if (tid < kRep) P.gdone[tid * kCS] = 0u;
       for (int e = tid; e < P.tm; e += kFusedThreads) P.gm_cnt[e * kCS] = 0u;
     }
     if (is_inv) {
@@ -316,7 +317,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 13] = globaltimer();
       // ---- Gram: the row-block reducers summed it (dist_gram), or sum the
       // split partials of every 8 x 8 block here (split order)
-      wait_geq(M.mcnt, static_cast<unsigned>(M.dist_gram ? M.nblk : ntiles));
+      if (M.dist_gram)
+        wait_geq(M.gdone + (b % kRep) * kCS, static_cast<unsigned>(M.nblk));
+      else
+        wait_geq(M.mcnt, static_cast<unsigned>(ntiles));
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 8] = globaltimer();
       if (!M.dist_gram) {
         constexpr int PER = 8, KC = 5;
@@ -402,9 +406,13 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
               A.gsum[gi * RT + gj] = sum;
               A.gsum[gj * RT + gi] = sum;
             }
-            signal_add(M.mcnt, static_cast<unsigned>(nq));
+            signal_add_rep(M.gdone, static_cast<unsigned>(nq), kRep);
           }
         }
+        // the RHS streams the fibers only after the Gram is summed, so the
+        // Gram's round trips do not queue behind the fiber traffic (the RHS
+        // has slack: it is consumed after the inverse)
+        if (M.dist_gram && A.gram_first) wait_geq(M.gdone + (b % kRep) * kCS, static_cast<unsigned>(M.nblk), 64);
         if (tt == static_cast<int>(rank)) stamp(n, 2);
         gemm_tile<RT>(M.v.x, M.vec16 != 0, in, static_cast<i64>(mt) * BM, r, cnt, kpad, t,
                       A.part_rhs + static_cast<i64>(kb) * in * r);

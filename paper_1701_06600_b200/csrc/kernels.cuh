@@ -199,6 +199,7 @@ struct FusedMode {
   int dist_gram;         // 1: tile (mt, tk-1) sums row block mt's Gram blocks (one tile per CTA)
   unsigned* grdy;        // [kRep] replicas of the "Gram inverse ready" flag      (stride kCS)
   unsigned* adone;       // [kRep] replicas: tile CTAs whose factor rows are written (epoch count)
+  unsigned* gdone;       // [kRep] replicas: Gram blocks summed (dist_gram)
   unsigned* nready;      // [kRep] replicas: this mode's norms / lambda are formed (epoch count)
   unsigned* mcnt;        // [0] Gram blocks summed (or tiles written), [1] inverse ready,
                          // [2] tile CTAs whose sums of squares are written        (stride kCS)
@@ -232,6 +233,7 @@ struct FusedIter {
   const FusedIter* next;         // next iteration's arguments (L2 prefetch of its tables)
   unsigned* gen_rep;             // CPRAND kernel: [kRep] replicas of the mode-release generation
   unsigned seq;                  // CPRAND kernel: 1-based launch sequence (epoch of adone / nready)
+  int gram_first;                // CPRAND kernel: RHS tiles wait for the summed Gram
   unsigned long long* cta_t;  // debug: per-CTA stamps of mode 1 [grid][16] (CPRAND_DEBUG_CTA)
 };
 size_t fused_smem_bytes(int rt, bool mix, int max_dim);

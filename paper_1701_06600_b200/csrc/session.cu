@@ -566,7 +566,7 @@ void Session::setup_fused() {
     gpart_ = dalloc<double>(static_cast<size_t>(nblk) * tk_max * 64);
     gsum_ = dalloc<double>(static_cast<size_t>(rt_) * rt_);
     CPB_CUDA(cudaMemsetAsync(gsum_, 0, sizeof(double) * rt_ * rt_, stream_));
-    const size_t per = (2 * static_cast<size_t>(tm_max) + static_cast<size_t>(tk_max) + 3 + 3 * kRep) * kCS;
+    const size_t per = (2 * static_cast<size_t>(tm_max) + static_cast<size_t>(tk_max) + 3 + 4 * kRep) * kCS;
     fcnt_ = dalloc<unsigned>(per * order_);
     CPB_CUDA(cudaMemsetAsync(fcnt_, 0, per * order_ * sizeof(unsigned), stream_));
   }
@@ -605,7 +605,7 @@ void Session::setup_fused() {
         M.tklen = tkl[k];
         M.nblk = nblk;
         M.zcap = zcap;
-        unsigned* c = fcnt_ + (2 * static_cast<size_t>(tm_max) + tk_max_ + 3 + 3 * kRep) * kCS * k;
+        unsigned* c = fcnt_ + (2 * static_cast<size_t>(tm_max) + tk_max_ + 3 + 4 * kRep) * kCS * k;
         M.mt_cnt = c;
         M.kb_cnt = c + static_cast<size_t>(tm_max) * kCS;
         M.mcnt = c + static_cast<size_t>(tm_max + tk_max_) * kCS;
@@ -614,6 +614,7 @@ void Session::setup_fused() {
         M.grdy = c + static_cast<size_t>(2 * tm_max + tk_max_ + 3) * kCS;
         M.adone = M.grdy + static_cast<size_t>(kRep) * kCS;
         M.nready = M.adone + static_cast<size_t>(kRep) * kCS;
+        M.gdone = M.nready + static_cast<size_t>(kRep) * kCS;
         // Z_S of mode n >= 1 uses mode n-1's rows unnormalized (its norms are
         // formed concurrently; they only rescale columns of the solution)
         if (n >= 1) {
@@ -637,6 +638,7 @@ void Session::setup_fused() {
     A.gen_rep = fsync_ + (3 + 128) * kCS;
     A.next = (ti + 1 < table_iters_) ? fargs_ + ti + 1 : nullptr;
     A.seq = static_cast<unsigned>(ti + 1);
+    A.gram_first = std::getenv("CPRAND_GRAM_FIRST") ? std::atoi(std::getenv("CPRAND_GRAM_FIRST")) : 0;
     A.inv_cta = mix_ ? -1 : inv_cta;
     A.idle_cta = mix_ ? -1 : idle_cta;
     A.census = nullptr;

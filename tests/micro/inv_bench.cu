@@ -26,6 +26,8 @@ __global__ void __launch_bounds__(NTH) inv_kernel(const double* g, int r, double
       fail = ph::inverse_la<64>(g, r, 4.4e-13, ginv, gfull, info, sh);
     else if (KIND == 2)
       fail = ph::inverse_b8<64>(g, r, 4.4e-13, ginv, gfull, info, sh);
+    else if (KIND == 3)
+      fail = ph::inverse_b8r<64>(g, r, 4.4e-13, ginv, gfull, info, sh);
     else
       fail = ph::inverse_cta<64, NTH>(g, 1, r, 4.4e-13, ginv, gfull, info, sh);
     __syncthreads();
@@ -108,6 +110,9 @@ int main() {
            (long long)(st[17] - st[8]), (long long)(st[18] - st[8]),
            (long long)(st[19] - st[8]), (long long)(st[20] - st[8]), (long long)(st[21] - st[8]));
   }
+  cudaFuncSetAttribute(inv_kernel<3, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  inv_kernel<3, 256><<<1, 256, 100 * 1024>>>(g, r, ginv, gfull, info, t, reps);
+  report("inverse_b8r 256");
   inv_kernel<1, 256><<<1, 256, 48 * 1024>>>(g, r, ginv, gfull, info, t, reps);
   report("inverse_cta 256");
   inv_kernel<1, 512><<<1, 512, 48 * 1024>>>(g, r, ginv, gfull, info, t, reps);
