@@ -385,6 +385,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
         const int kpad = (cnt + BK - 1) / BK * BK;
         wait_geq(M.kb_cnt + kb * kCS, static_cast<unsigned>(M.tm));
         if (tt == static_cast<int>(rank)) stamp(n, 10);
+        if (tt == static_cast<int>(rank) && A.cta_t && n == 1 && tid == 0)
+          A.cta_t[b * 16 + 11] = (static_cast<unsigned long long>(mt) << 8) | static_cast<unsigned long long>(kb);
         z_load<RT>(M.v, A.z, s0, cnt, kpad, t);
         if (tt == static_cast<int>(rank)) stamp(n, 1);
         // Gram blocks q = mt, mt + tm, ... of this split (the inverse CTA sums them)
@@ -393,6 +395,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
           signal_add(M.mcnt, 1u);
         } else {
           signal_add(M.gm_cnt + mt * kCS, 1u);
+          if (A.cta_t && n == 1 && tid == 0) A.cta_t[b * 16 + 12] = globaltimer();
           if (kb == M.tk - 1 && mt < M.nblk) {
             // row-block reducer: sum blocks q = mt, mt + tm, ... over the splits
             wait_geq(M.gm_cnt + mt * kCS, static_cast<unsigned>(M.tk));

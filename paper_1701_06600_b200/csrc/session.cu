@@ -1215,6 +1215,22 @@ void Session::enqueue_iteration() {
                        arg >= 0 ? c[static_cast<size_t>(arg) * 16 + 11] : 0ULL);
         }
         std::fprintf(stderr, "\n");
+        {  // Gram per row block: slowest split's blocks written vs the reducer's sum
+          std::vector<double> mx(64, 0.0), red(64, 0.0);
+          int tmx = 0;
+          for (int b = 0; b < fgrid_; ++b) {
+            const unsigned long long tag = c[static_cast<size_t>(b) * 16 + 11];
+            const unsigned long long g12 = c[static_cast<size_t>(b) * 16 + 12], g2 = c[static_cast<size_t>(b) * 16 + 2];
+            if (!g12) continue;
+            const int mt = static_cast<int>(tag >> 8) & 63;
+            tmx = std::max(tmx, mt + 1);
+            mx[static_cast<size_t>(mt)] = std::max(mx[static_cast<size_t>(mt)], 1e-3 * static_cast<double>(g12 - t0));
+            red[static_cast<size_t>(mt)] = std::max(red[static_cast<size_t>(mt)], 1e-3 * static_cast<double>(g2 - t0));
+          }
+          std::fprintf(stderr, "gram per row block (slowest split written / summed):");
+          for (int mt = 0; mt < tmx; ++mt) std::fprintf(stderr, " %.1f/%.1f", mx[static_cast<size_t>(mt)], red[static_cast<size_t>(mt)]);
+          std::fprintf(stderr, "\n");
+        }
         {  // SM sharing of the inverse CTA in this launch
           int inv = fgrid_ - 1;
           FusedIter h;
