@@ -351,6 +351,17 @@ def main() -> int:
                    "sample": f"{n_it} bench-mode outer iterations of {args.config} on the same "
                              f"tensor ({secs:.1f} s); gather on all host threads, LS single-threaded"}
         buf.close()
+    # ---- CPRAND-MIX preprocessing pass (mix_tensor, in place) on the same tensor
+    mix_pass = None
+    if rank == 0 and comm is None:
+        ms_modes = t.mix("dct", SEED)
+        pbytes = 16.0 * float(np.prod(dims))
+        gbs = [pbytes / (m * 1e-3) / 1e9 for m in ms_modes]
+        mix_pass = {"kernel": "mode_transform_kernel (sign + DCT-II per fiber, in place)",
+                    "bytes_model": "16 B per element per mode (read + write)",
+                    "ms_per_mode": [round(m, 3) for m in ms_modes],
+                    "gbs_per_mode": [round(g, 1) for g in gbs],
+                    "frac_per_mode": [round(g / hbm_peak, 3) for g in gbs]}
     t.close()
 
     if rank == 0:
@@ -380,7 +391,7 @@ def main() -> int:
                                "inverse_prologue", "inverse_steps", "norms_done_after_mode_start",
                                "gram_reduce"]),
                              [round(x, 2) for x in phases])) if phases else None,
-                         "gram_fallbacks": fallbacks},
+                         "gram_fallbacks": fallbacks, "mix_pass": mix_pass},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches_per_iter(cfg) * args.steps,
         }

@@ -146,6 +146,10 @@ int cprand_tensor_download(cprand_tensor_t t, double* host);
 int cprand_tensor_synth(cprand_tensor_t t, int64_t r, double collinearity, double eta,
                         uint64_t seed, double* const* out_factors);
 double* cprand_tensor_device_ptr(cprand_tensor_t t);
+/* mix_tensor (mixing.hpp:130-156) in place on a device tensor (dct): per
+ * mode, sign then orthonormal DCT-II; ms_per_mode[order] (nullable) receives
+ * the CUDA-event time of each mode's pass. */
+int cprand_tensor_mix(cprand_tensor_t t, int32_t transform, uint64_t seed, double* ms_per_mode);
 /* Slab of the BASELINE.json tensor with last dim shard_total (rank/nranks
  * from comm); noise scaled by the global norms (allreduced). Declared after
  * cprand_comm_t below. */

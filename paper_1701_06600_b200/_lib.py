@@ -76,7 +76,7 @@ EXPORTS = [
     "cprand_gather_fibers", "cprand_skr", "cprand_mode_update", "cprand_fit_values",
     "cprand_estimate_fit", "cprand_mix_tensor", "cprand_mix_factor", "cprand_unmix_factor",
     "cprand_unmix_rows", "cprand_debug_normal_stream", "cprand_comm_unique_id",
-    "cprand_comm_create", "cprand_comm_destroy", "cprand_tensor_synth_slab",
+    "cprand_comm_create", "cprand_comm_destroy", "cprand_tensor_synth_slab", "cprand_tensor_mix",
 ]
 
 _lib = None

@@ -199,6 +199,12 @@ class DeviceTensor:
                                         _ptrs(fs) if fs else None))
         return fs
 
+    def mix(self, transform: str = "dct", seed: int = 0) -> list:
+        """mix_tensor in place (device); returns the per-mode pass times in ms."""
+        ms = np.zeros(len(self.dims), dtype=np.float64)
+        check(lib().cprand_tensor_mix(self.h, TRANSFORMS[transform], C.c_uint64(seed), _p(ms)))
+        return [float(v) for v in ms]
+
     def synth_slab(self, r: int, collinearity: float, eta: float, seed: int, shard_total: int, comm,
                    want_factors=False):
         """This rank's slab of the BASELINE.json tensor (last dim shard_total)."""

@@ -243,6 +243,13 @@ int cprand_tensor_synth_slab(cprand_tensor_t t, int64_t r, double c, double eta,
   });
 }
 
+int cprand_tensor_mix(cprand_tensor_t t, int32_t transform, uint64_t seed, double* ms_per_mode) {
+  return guarded([&] {
+    need(t);
+    op_tensor_mix(t->t.get(), transform, seed, ms_per_mode);
+  });
+}
+
 double* cprand_tensor_device_ptr(cprand_tensor_t t) { return t ? t->t->d : nullptr; }
 
 void cprand_tensor_destroy(cprand_tensor_t t) { delete t; }

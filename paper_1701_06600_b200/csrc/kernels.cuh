@@ -152,6 +152,10 @@ int dct_fibers_per_cta(int n, size_t smem_budget);
 void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 st, i64 nfib,
                            const double* sign, int forward, const double* col_div,
                            cudaStream_t st_);
+// Whole-tensor mixing pass (mixpass.cu): persistent, pipelined, radices 2-8.
+bool mix_pass_supported(const DctPlan& p);
+void launch_mix_pass(const DctPlan& p, const double* in, double* out, i64 st, i64 nfib, const double* sign,
+                     int forward, cudaStream_t stream);
 // MIX path: RHS (I_n x R row-major) = D_n C^T (sum_ks part_rhs) per column
 void launch_reduce_rhs(const double* part_rhs, int ks, i64 in, int r, double* out,
                        cudaStream_t st);

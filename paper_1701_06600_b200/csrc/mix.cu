@@ -110,6 +110,10 @@ void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 
                            const double* sign, int forward, const double* col_div,
                            cudaStream_t stream) {
   if (nfib <= 0) return;
+  if (nfib >= 4096 && col_div == nullptr && in == out && mix_pass_supported(p)) {
+    launch_mix_pass(p, in, out, st, nfib, sign, forward, stream);  // whole-tensor pass
+    return;
+  }
   PlanArgs a;
   a.n = p.n;
   a.nrad = p.nrad;

@@ -388,6 +388,33 @@ void op_unmix_rows(const double* g, i64 s, i64 in, const std::vector<i64>& dims,
   d2h(out, dg.p, static_cast<size_t>(s * in));
 }
 
+// mix_tensor (mixing.hpp:130-156) in place on a device tensor: per mode,
+// sign then orthonormal DCT-II; ms[mode] = CUDA-event time of that pass.
+void op_tensor_mix(Tensor* t, int transform, std::uint64_t seed, double* ms) {
+  if (transform != 1) throw Unsupported("in-place device mixing supports the dct transform");
+  CPB_CUDA(cudaSetDevice(t->device));
+  const auto signs = mixing_signs(t->dims, transform, seed);
+  cudaEvent_t e0, e1;
+  CPB_CUDA(cudaEventCreate(&e0));
+  CPB_CUDA(cudaEventCreate(&e1));
+  for (size_t n = 0; n < t->dims.size(); ++n) {
+    DBuf sg(signs[n].size() * sizeof(double));
+    h2d(sg.p, signs[n].data(), signs[n].size());
+    DctPlan plan = make_dct_plan(static_cast<int>(t->dims[n]));
+    CPB_CUDA(cudaDeviceSynchronize());
+    CPB_CUDA(cudaEventRecord(e0, nullptr));
+    launch_mode_transform(plan, t->d, t->d, t->strides[n], t->p / t->dims[n], sg.as<double>(), 1, nullptr, nullptr);
+    CPB_CUDA(cudaEventRecord(e1, nullptr));
+    CPB_CUDA(cudaEventSynchronize(e1));
+    float f = 0.f;
+    CPB_CUDA(cudaEventElapsedTime(&f, e0, e1));
+    if (ms) ms[n] = f;
+    free_dct_plan(plan);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
 void op_debug_normals(std::uint64_t seed, int n, double* out) {
   DBuf st(313 * sizeof(unsigned long long)), d(static_cast<size_t>(n) * sizeof(double));
   launch_rng_seed(st.as<unsigned long long>(), seeded_engine_seed_value(seed, kInitStream + 7), nullptr);

@@ -414,3 +414,16 @@ def test_sharded_session_rejects_bad_slab(pb):
     with pytest.raises(pb.UnsupportedOnDevice):
         pb.Session("mix", t, 3, 20, pb.SolveOptions(comm=comm, shard_total=8, transform="dct"))
     comm.close()
+
+
+@pytest.mark.gpu
+def test_device_tensor_mix_matches_oracle(pb, orc):
+    dims = (24, 30, 20)
+    x = orc.random_tensor(dims, 5)
+    t = pb.DeviceTensor(dims)
+    t.upload(x)
+    ms = t.mix("dct", 7)
+    assert len(ms) == 3 and all(m > 0 for m in ms)
+    got = t.download()
+    want = orc.mix_tensor(x, "dct", 7)
+    assert rel(got, want) < 1e-12
