@@ -217,6 +217,8 @@ def main() -> int:
     ap.add_argument("--e2e-iters", type=int, default=100, help="iterations per e2e solve call")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--atomic-gram", action="store_true",
+                    help="time the loop with SolveOptions(atomic_gram=True) (not bitwise reproducible)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
@@ -249,7 +251,8 @@ def main() -> int:
     total_iters = args.warmup + args.steps + timing_iters + 2
     opts = pb.SolveOptions(rng_seed=SEED, max_iters=total_iters, bench_mode=True,
                            transform=cfg["transform"], x_mutable=False, device=dev,
-                           comm=comm, shard_total=cfg["dims"][-1] if comm is not None else 0)
+                           comm=comm, shard_total=cfg["dims"][-1] if comm is not None else 0,
+                           atomic_gram=args.atomic_gram)
     s = pb.Session(cfg["method"], t, cfg["r"], cfg["s"], opts)
     clk = ClockSampler(dev).__enter__()
     s.run(args.warmup)
@@ -320,6 +323,21 @@ def main() -> int:
     fallbacks = s.gram_fallbacks()
     s.close()
 
+    # ---- the same timed loop with the Gram summed by L2 fp64 atomics
+    # (SolveOptions.atomic_gram: one round trip fewer per mode, not bitwise
+    # reproducible; reported beside the default, reproducible, value)
+    atomic = None
+    if cfg["method"] == "rand" and not args.atomic_gram:
+        import dataclasses
+        s2 = pb.Session(cfg["method"], t, cfg["r"], cfg["s"], dataclasses.replace(opts, atomic_gram=True))
+        s2.run(args.warmup)
+        barrier(dist)
+        s2.sync()
+        ms2 = allreduce_max(dist, s2.timed_enqueue(args.steps))
+        s2.close()
+        atomic = {"value": args.steps / (ms2 * 1e-3), "unit": "iters/s", "ms_per_step": ms2 / args.steps,
+                  "option": "SolveOptions(atomic_gram=True)"}
+
     # ---- e2e through the public one-shot call with host buffers
     e2e, cpu = None, None
     if (rank == 0 or comm is not None) and (args.e2e_steps > 0 or not args.no_cpu):
@@ -373,6 +391,8 @@ def main() -> int:
             "config": {"workload": args.config, "dims": list(cfg["dims"]), "R": cfg["r"],
                        "S": cfg["s"], "P_hat": cfg["phat"], "method": cfg["method"],
                        "transform": cfg["transform"], "bench_mode": True,
+                       "gram_sum": "L2 fp64 atomics (atomic_gram)" if args.atomic_gram else
+                                   "fixed-order split partials (bitwise reproducible)",
                        "parallelism": f"slab{ws} (last mode, NCCL allreduce/allgather)" if ws > 1 else "single",
                        "l2": "inputs larger than L2 (8 GB tensor, fresh random samples per step)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -392,6 +412,7 @@ def main() -> int:
                                "gram_reduce"]),
                              [round(x, 2) for x in phases])) if phases else None,
                          "gram_fallbacks": fallbacks, "mix_pass": mix_pass},
+            "atomic_gram": atomic,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches_per_iter(cfg) * args.steps,
         }

@@ -100,6 +100,11 @@ typedef struct cprand_options {
                                  fibers in place), 0 off (multi-kernel chain) */
   int64_t shard_total;        /* with comm: global length of the last mode; x is
                                  this rank's slab, rows [rank*ceil(I/P), ...) */
+  int32_t atomic_gram;        /* 0 (default): bitwise run-to-run reproducible;
+                                 1: the fused CPRAND kernel sums the sampled
+                                 Gram with L2 fp64 atomic adds (one inter-CTA
+                                 round trip fewer per mode; the summation
+                                 order, so the last bits, vary run to run) */
 } cprand_options_t;
 
 typedef struct cprand_trace_record {

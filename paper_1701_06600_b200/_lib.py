@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcprand_b200.so")
+LIB_PATH = os.environ.get("CPRAND_LIB") or os.path.join(HERE, "libcprand_b200.so")
 
 OK, ERR_INTERNAL, ERR_INVALID, ERR_NUMERICAL, ERR_CUDA, ERR_UNSUPPORTED = 0, 1, 2, 3, 4, 5
 
@@ -49,6 +49,7 @@ class Options(C.Structure):
         ("device", C.c_int32), ("x_is_device", C.c_int32), ("x_mutable", C.c_int32),
         ("comm", C.c_void_p), ("replicas", C.c_int32), ("fused", C.c_int32),
         ("shard_total", C.c_int64),
+        ("atomic_gram", C.c_int32),
     ]
 
 

@@ -45,6 +45,7 @@ class SolveOptions:
     fused: int = -1  # persistent per-iteration kernel: -1 auto, 0 off
     comm: object | None = None  # Comm: slab-sharded run (tensor = this rank's slab)
     shard_total: int = 0  # with comm: global length of the last mode
+    atomic_gram: bool = False  # fused CPRAND kernel: Gram via L2 fp64 atomics (not bitwise reproducible)
 
     def to_c(self) -> Options:
         o = Options()
@@ -65,6 +66,7 @@ class SolveOptions:
         o.x_mutable = int(self.x_mutable)
         o.replicas = self.replicas
         o.fused = self.fused
+        o.atomic_gram = int(self.atomic_gram)
         if self.comm is not None:
             o.comm = self.comm.h
             o.shard_total = int(self.shard_total)

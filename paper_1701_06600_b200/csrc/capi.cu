@@ -73,6 +73,7 @@ Options opts_of(const cprand_options_t* o) {
   r.x_mutable = o->x_mutable != 0;
   r.replicas = o->replicas;
   r.fused = o->fused;
+  r.atomic_gram = o->atomic_gram != 0;
   if (o->comm != nullptr) {
     const auto* c = static_cast<const cprand_comm_s*>(o->comm);
     r.nccl = c->comm;

@@ -228,6 +228,20 @@ __device__ __forceinline__ double sum_strided(const double* __restrict__ p, i64 
   return sum;
 }
 
+// the same sum with all (n <= 32) loads in flight at once: one L2 round trip
+// for the row-block reducers on the Gram's critical path
+__device__ __forceinline__ double sum_strided32(const double* __restrict__ p, i64 step, int n) {
+  if (n > 32) return sum_strided(p, step, n);
+  double v[32];
+#pragma unroll
+  for (int u = 0; u < 32; ++u) v[u] = (u < n) ? __ldcg(p + u * step) : 0.0;
+  double sum = 0.0;
+#pragma unroll
+  for (int u = 0; u < 32; ++u)
+    if (u < n) sum += v[u];
+  return sum;
+}
+
 // L2 prefetch of one iteration's sample tables (all modes): global thread g
 // prefetches 128-byte line g of the concatenated tables.
 __device__ __forceinline__ void prefetch_tables(const FusedIter& A, unsigned b) {
@@ -246,7 +260,8 @@ __device__ __forceinline__ void prefetch_tables(const FusedIter& A, unsigned b) 
   }
 }
 
-template <int RT>
+// GA: the Gram is summed with L2 fp64 atomics (FusedIter::gram_atomic)
+template <int RT, bool GA>
 __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const FusedIter* __restrict__ args) {
   using namespace tl;
   const FusedIter& A = *args;
@@ -317,12 +332,18 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 13] = globaltimer();
       // ---- Gram: the row-block reducers summed it (dist_gram), or sum the
       // split partials of every 8 x 8 block here (split order)
-      if (M.dist_gram)
+      if constexpr (GA) {
+        // buffer (n-1) & 1 is next added to by mode n+1, whose tiles start
+        // after this CTA's grdy(n): zero it now
+        if (n >= 1)
+          for (int e = tid; e < RT * RT; e += kFusedThreads) A.gsum[((n - 1) & 1) * RT * RT + e] = 0.0;
+        wait_geq(M.gdone + (b % kRep) * kCS, static_cast<unsigned>(ntiles));
+      } else if (M.dist_gram)
         wait_geq(M.gdone + (b % kRep) * kCS, static_cast<unsigned>(M.nblk));
       else
         wait_geq(M.mcnt, static_cast<unsigned>(ntiles));
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 8] = globaltimer();
-      if (!M.dist_gram) {
+      if (!M.dist_gram && !GA) {
         constexpr int PER = 8, KC = 5;
         const int ne = M.nblk * 64;
         double sum[PER];
@@ -357,7 +378,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       __syncthreads();
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 15] = globaltimer();
       // ---- inverse (pivoted-Cholesky min-norm fallback when rank deficient)
-      const bool fail = ph::inverse_la<RT>(A.gsum, r, M.tol, A.ginv, A.gfull, A.info, fsm,
+      const bool fail = ph::inverse_la<RT>(A.gsum + (GA ? (n & 1) * RT * RT : 0), r, M.tol, A.ginv, A.gfull, A.info, fsm,
                                            A.phase_t ? A.phase_t + n * 16 + 11 : nullptr);
       if (fail) ph::pinv_fallback<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
       signal_add_rep(M.grdy, 1u, kRep);
@@ -390,8 +411,14 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
         z_load<RT>(M.v, A.z, s0, cnt, kpad, t);
         if (tt == static_cast<int>(rank)) stamp(n, 1);
         // Gram blocks q = mt, mt + tm, ... of this split (the inverse CTA sums them)
-        gram_blocks<RT>(t, kpad, nfr, mt, M.tm, kb, M.tk, A.gpart);
-        if (!M.dist_gram) {
+        if constexpr (GA) {
+          gram_blocks_add<RT>(t, kpad, nfr, mt, M.tm, A.gsum + (n & 1) * RT * RT);
+          signal_add(M.gdone + (inv % kRep) * kCS, 1u);
+        } else {
+          gram_blocks<RT>(t, kpad, nfr, mt, M.tm, kb, M.tk, A.gpart);
+        }
+        if constexpr (GA) {
+        } else if (!M.dist_gram) {
           signal_add(M.mcnt, 1u);
         } else {
           signal_add(M.gm_cnt + mt * kCS, 1u);
@@ -415,7 +442,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
         // the RHS streams the fibers only after the Gram is summed, so the
         // Gram's round trips do not queue behind the fiber traffic (the RHS
         // has slack: it is consumed after the inverse)
-        if (M.dist_gram && A.gram_first) wait_geq(M.gdone + (b % kRep) * kCS, static_cast<unsigned>(M.nblk), 64);
+        if (M.dist_gram && A.gram_first && !GA) wait_geq(M.gdone + (b % kRep) * kCS, static_cast<unsigned>(M.nblk), 64);
         if (tt == static_cast<int>(rank)) stamp(n, 2);
         gemm_tile<RT>(M.v.x, M.vec16 != 0, in, static_cast<i64>(mt) * BM, r, cnt, kpad, t,
                       A.part_rhs + static_cast<i64>(kb) * in * r);
@@ -476,6 +503,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
     const FusedMode& L = A.mode[A.order - 1];
     if (is_inv) {
       wait_geq(L.adone + (b % kRep) * kCS, seq * Gw, 64);
+      if constexpr (GA)  // the last mode's buffer, for the next launch
+        for (int e = tid; e < RT * RT; e += kFusedThreads) A.gsum[((A.order - 1) & 1) * RT * RT + e] = 0.0;
       form_norms(A.order - 1);
     }
     if (A.has_fit && !is_inv) wait_geq(L.nready + (b % kRep) * kCS, seq, 64);
@@ -506,15 +535,16 @@ void* mix_fn() {
   return reinterpret_cast<void*>(&fused_iteration_kernel<RT, true>);
 }
 template <int RT>
-void* rand_fn() {
-  return reinterpret_cast<void*>(&fused_rand_kernel<RT>);
+void* rand_fn(bool ga) {
+  return ga ? reinterpret_cast<void*>(&fused_rand_kernel<RT, true>)
+            : reinterpret_cast<void*>(&fused_rand_kernel<RT, false>);
 }
 
-void* pick(int rt, bool mix) {
+void* pick(int rt, bool mix, bool ga = false) {
   switch (rt) {
-    case 16: return mix ? mix_fn<16>() : rand_fn<16>();
-    case 32: return mix ? mix_fn<32>() : rand_fn<32>();
-    default: return mix ? mix_fn<64>() : rand_fn<64>();
+    case 16: return mix ? mix_fn<16>() : rand_fn<16>(ga);
+    case 32: return mix ? mix_fn<32>() : rand_fn<32>(ga);
+    default: return mix ? mix_fn<64>() : rand_fn<64>(ga);
   }
 }
 
@@ -579,14 +609,17 @@ int fused_max_grid(int rt, bool mix, size_t smem, int device) {
   if (!coop) return 0;
   void* fn = pick(rt, mix);
   CPB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (!mix)
+    CPB_CUDA(cudaFuncSetAttribute(pick(rt, false, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
   int per_sm = 0;
   CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFusedThreads, smem));
   return per_sm * sms;
 }
 
 void launch_fused_iteration(const FusedIter* dev_args, int rt, bool mix, int grid, size_t smem,
-                            cudaStream_t st) {
-  void* fn = pick(rt, mix);
+                            cudaStream_t st, bool gram_atomic) {
+  void* fn = pick(rt, mix, gram_atomic);
   void* params[] = {const_cast<FusedIter**>(&dev_args)};
   CPB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFusedThreads), params, smem, st));
 }

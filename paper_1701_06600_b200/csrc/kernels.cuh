@@ -238,6 +238,7 @@ struct FusedIter {
   unsigned* gen_rep;             // CPRAND kernel: [kRep] replicas of the mode-release generation
   unsigned seq;                  // CPRAND kernel: 1-based launch sequence (epoch of adone / nready)
   int gram_first;                // CPRAND kernel: RHS tiles wait for the summed Gram
+  int gram_atomic;               // CPRAND kernel: tiles add their Gram blocks into gsum[n & 1] (L2 fp64 adds)
   unsigned long long* cta_t;  // debug: per-CTA stamps of mode 1 [grid][16] (CPRAND_DEBUG_CTA)
 };
 size_t fused_smem_bytes(int rt, bool mix, int max_dim);
@@ -250,6 +251,6 @@ void fused_rand_tiles(i64 in, int s, int gw, int zcap, int* tm, int* tk, int* tk
 // is unavailable).
 int fused_max_grid(int rt, bool mix, size_t smem, int device);
 void launch_fused_iteration(const FusedIter* dev_args, int rt, bool mix, int grid, size_t smem,
-                            cudaStream_t st);
+                            cudaStream_t st, bool gram_atomic = false);
 
 }  // namespace cpb

@@ -529,7 +529,7 @@ void Session::setup_fused() {
     FusedIter c{};
     c.census = cen;
     CPB_CUDA(cudaMemcpyAsync(dc, &c, sizeof(c), cudaMemcpyHostToDevice, stream_));
-    launch_fused_iteration(dc, rt_, false, fgrid_, fsmem_, stream_);
+    launch_fused_iteration(dc, rt_, false, fgrid_, fsmem_, stream_, o_.atomic_gram);
     std::vector<int> sm(static_cast<size_t>(fgrid_));
     CPB_CUDA(cudaMemcpyAsync(sm.data(), cen, sm.size() * sizeof(int), cudaMemcpyDeviceToHost, stream_));
     CPB_CUDA(cudaStreamSynchronize(stream_));
@@ -564,8 +564,8 @@ void Session::setup_fused() {
       part_rhs_ = dalloc<double>(static_cast<size_t>(max_part));
     }
     gpart_ = dalloc<double>(static_cast<size_t>(nblk) * tk_max * 64);
-    gsum_ = dalloc<double>(static_cast<size_t>(rt_) * rt_);
-    CPB_CUDA(cudaMemsetAsync(gsum_, 0, sizeof(double) * rt_ * rt_, stream_));
+    gsum_ = dalloc<double>(2 * static_cast<size_t>(rt_) * rt_);
+    CPB_CUDA(cudaMemsetAsync(gsum_, 0, 2 * sizeof(double) * rt_ * rt_, stream_));
     const size_t per = (2 * static_cast<size_t>(tm_max) + static_cast<size_t>(tk_max) + 3 + 4 * kRep) * kCS;
     fcnt_ = dalloc<unsigned>(per * order_);
     CPB_CUDA(cudaMemsetAsync(fcnt_, 0, per * order_ * sizeof(unsigned), stream_));
@@ -639,6 +639,7 @@ void Session::setup_fused() {
     A.next = (ti + 1 < table_iters_) ? fargs_ + ti + 1 : nullptr;
     A.seq = static_cast<unsigned>(ti + 1);
     A.gram_first = std::getenv("CPRAND_GRAM_FIRST") ? std::atoi(std::getenv("CPRAND_GRAM_FIRST")) : 0;
+    A.gram_atomic = o_.atomic_gram ? 1 : 0;
     A.inv_cta = mix_ ? -1 : inv_cta;
     A.idle_cta = mix_ ? -1 : idle_cta;
     A.census = nullptr;
@@ -1166,7 +1167,7 @@ void Session::enqueue_iteration() {
                                  sizeof(phase_t_), cudaMemcpyHostToDevice, stream_));
     }
     if (cta_t_) CPB_CUDA(cudaMemsetAsync(cta_t_, 0, sizeof(unsigned long long) * fgrid_ * 16, stream_));
-    timed(0, 7, stream_, [&] { launch_fused_iteration(fargs_ + ti, rt_, mix_, fgrid_, fsmem_, stream_); });
+    timed(0, 7, stream_, [&] { launch_fused_iteration(fargs_ + ti, rt_, mix_, fgrid_, fsmem_, stream_, o_.atomic_gram); });
     if (timing_) {
       // collect this launch's phase stamps (timing mode only: synchronizes)
       std::vector<unsigned long long> t(static_cast<size_t>(order_ * 16));

@@ -39,6 +39,7 @@ struct Options {  // SolveOptions (solver.hpp:40-64) + device extensions
   void* nccl = nullptr;  // ncclComm_t
   int nranks = 1, rank = 0;
   i64 shard_total = 0;
+  bool atomic_gram = false;  // fused CPRAND kernel: Gram summed with L2 fp64 atomics (not reproducible)
   void validate() const;
 };
 

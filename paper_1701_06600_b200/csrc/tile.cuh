@@ -321,6 +321,34 @@ __device__ void gram_blocks(const TileSmem& t, int kpad, int nfr, int first, int
   }
 }
 
+// The same blocks added straight into the summed Gram g (both triangles,
+// ld RT) with fire-and-forget L2 fp64 adds: no split partials, no reducer.
+// The order of the adds is not fixed, so the Gram (and the run) is not
+// bitwise reproducible; the two triangles may differ in the last bit.
+template <int RT>
+__device__ void gram_blocks_add(const TileSmem& t, int kpad, int nfr, int first, int step,
+                                double* __restrict__ g) {
+  constexpr int SB = Cfg<RT>::SB;
+  const int nblk = nfr * (nfr + 1) / 2;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int q = first + warp * step; q < nblk; q += 8 * step) {
+    int bi, bj;
+    gram_block_coords(q, nfr, &bi, &bj);
+    double acc[2] = {0.0, 0.0};
+    const double* za = t.zs + (lane & 3) * SB + bi * 8 + (lane >> 2);
+    const double* zb = t.zs + (lane & 3) * SB + bj * 8 + (lane >> 2);
+#pragma unroll 4
+    for (int k = 0; k < kpad; k += 4) dmma(acc, za[k * SB], zb[k * SB]);
+    const int gi = bi * 8 + (lane >> 2), gj = bj * 8 + (lane & 3) * 2;
+    atomicAdd(g + gi * RT + gj, acc[0]);
+    atomicAdd(g + gi * RT + gj + 1, acc[1]);
+    if (bi != bj) {  // and the mirrored block (the inverse reads whole rows)
+      atomicAdd(g + gj * RT + gi, acc[0]);
+      atomicAdd(g + (gj + 1) * RT + gi, acc[1]);
+    }
+  }
+}
+
 // Split-K RHS tile: out(i, c) = sum_{s < cnt} X(roff[s] + i) Z(s, c) for the
 // 64 rows i0.. of a mode with `in` rows; out = part + kb * in * r, row-major
 // (ld r). A (fibers) streams through a 3-stage cp.async pipeline; Z stays

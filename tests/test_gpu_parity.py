@@ -365,10 +365,12 @@ def test_execution_paths_agree(pb, orc, dims, r, s):
     assert np.array_equal(chain.lam, ring.lam)
     for a, b in zip(chain.factors, ring.factors):
         assert np.array_equal(a, b)
-    for a, b in zip(fused.factors, ring.factors):
-        assert rel(a, b) < 1e-12
+    atom = pb.cprand(x, r, s, pb.SolveOptions(replicas=1, atomic_gram=True, **base))
+    for res in (fused, atom):
+        for a, b in zip(res.factors, ring.factors):
+            assert rel(a, b) < 1e-12
     ref = orc.cprand(x, r, s, orc.SolveOptions(**base))
-    for res in (fused, chain):
+    for res in (fused, chain, atom):
         assert max(abs(a[2] - b[2]) for a, b in zip(res.trace, ref.trace)) < 1e-8
 
 
@@ -427,3 +429,25 @@ def test_device_tensor_mix_matches_oracle(pb, orc):
     got = t.download()
     want = orc.mix_tensor(x, "dct", 7)
     assert rel(got, want) < 1e-12
+
+
+@pytest.mark.gpu
+def test_atomic_gram_many_tiles(pb, orc):
+    """SolveOptions(atomic_gram=True) on a problem that spreads every mode's
+    Gram over hundreds of tiles (L2 fp64 adds from many CTAs into each
+    element): same trajectory as the reproducible fused kernel to round-off."""
+    dims, r, s = (400, 300, 350), 24, 1500
+    t = pb.DeviceTensor(dims)
+    t.synth(r, 0.5, 0.01, 17)
+    base = dict(rng_seed=17, max_iters=8, stall_limit=1000, bench_mode=True)
+    runs = []
+    for atomic in (False, True):
+        sess = pb.Session("rand", t, r, s, pb.SolveOptions(atomic_gram=atomic, **base))
+        sess.run(8)
+        runs.append(sess.result())
+        sess.close()
+    t.close()
+    assert np.all(np.isfinite(runs[1].lam))
+    np.testing.assert_allclose(runs[1].lam, runs[0].lam, rtol=1e-9)
+    for a, b in zip(runs[1].factors, runs[0].factors):
+        assert rel(a, b) < 1e-9
