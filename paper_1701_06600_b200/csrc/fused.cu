@@ -344,35 +344,40 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
         wait_geq(M.mcnt, static_cast<unsigned>(ntiles));
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 8] = globaltimer();
       if (!M.dist_gram && !GA) {
+        // every block's split partials, in split order (chunks of PER
+        // elements per thread: r > 56 has more than 2048 block entries)
         constexpr int PER = 8, KC = 5;
         const int ne = M.nblk * 64;
-        double sum[PER];
+        for (int e0 = 0; e0 < ne; e0 += PER * kFusedThreads) {
+          double sum[PER];
 #pragma unroll
-        for (int u = 0; u < PER; ++u) sum[u] = 0.0;
-        for (int k0 = 0; k0 < M.tk; k0 += KC) {
-          double v[PER][KC];
+          for (int u = 0; u < PER; ++u) sum[u] = 0.0;
+          for (int k0 = 0; k0 < M.tk; k0 += KC) {
+            double v[PER][KC];
 #pragma unroll
-          for (int u = 0; u < PER; ++u) {
-            const int e = tid + u * kFusedThreads;
-            const double* src = A.gpart + static_cast<i64>(e / 64) * M.tk * 64 + (e % 64);
+            for (int u = 0; u < PER; ++u) {
+              const int e = e0 + tid + u * kFusedThreads;
+              const double* src = A.gpart + static_cast<i64>(e / 64) * M.tk * 64 + (e % 64);
 #pragma unroll
-            for (int k = 0; k < KC; ++k) v[u][k] = (e < ne && k0 + k < M.tk) ? __ldcg(src + (k0 + k) * 64) : 0.0;
+              for (int k = 0; k < KC; ++k)
+                v[u][k] = (e < ne && k0 + k < M.tk) ? __ldcg(src + (k0 + k) * 64) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < PER; ++u)
+#pragma unroll
+              for (int k = 0; k < KC; ++k)
+                if (k0 + k < M.tk) sum[u] += v[u][k];
           }
 #pragma unroll
-          for (int u = 0; u < PER; ++u)
-#pragma unroll
-            for (int k = 0; k < KC; ++k)
-              if (k0 + k < M.tk) sum[u] += v[u][k];
-        }
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-          const int e = tid + u * kFusedThreads;
-          if (e >= ne) continue;
-          int bi, bj;
-          gram_block_coords(e / 64, nfr, &bi, &bj);
-          const int el = e % 64, gi = bi * 8 + el / 8, gj = bj * 8 + el % 8;
-          A.gsum[gi * RT + gj] = sum[u];
-          A.gsum[gj * RT + gi] = sum[u];
+          for (int u = 0; u < PER; ++u) {
+            const int e = e0 + tid + u * kFusedThreads;
+            if (e >= ne) continue;
+            int bi, bj;
+            gram_block_coords(e / 64, nfr, &bi, &bj);
+            const int el = e % 64, gi = bi * 8 + el / 8, gj = bj * 8 + el % 8;
+            A.gsum[gi * RT + gj] = sum[u];
+            A.gsum[gj * RT + gi] = sum[u];
+          }
         }
       }
       __syncthreads();

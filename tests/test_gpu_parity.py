@@ -451,3 +451,28 @@ def test_atomic_gram_many_tiles(pb, orc):
     np.testing.assert_allclose(runs[1].lam, runs[0].lam, rtol=1e-9)
     for a, b in zip(runs[1].factors, runs[0].factors):
         assert rel(a, b) < 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("method", ["rand", "mix"])
+def test_fused_gram_sum_on_inverse_cta_wide_rank(pb, orc, method):
+    """More tiles than CTAs (CPRAND kernel: every Gram block's split partials
+    are summed on the inverse CTA) at a rank whose Gram has more than 2048
+    block entries (r = 60: 36 8 x 8 blocks): the persistent kernels match
+    the multi-kernel chain."""
+    dims, r, s = (700, 600, 500), 60, 6000
+    t = pb.DeviceTensor(dims)
+    t.synth(r, 0.5, 0.01, 23)
+    base = dict(rng_seed=23, max_iters=3, stall_limit=1000, bench_mode=True)
+    if method == "mix":
+        base["transform"] = "dct"
+    runs = []
+    for fused in (-1, 0):
+        sess = pb.Session(method, t, r, s, pb.SolveOptions(fused=fused, **base))
+        sess.run(3)
+        runs.append(sess.result())
+        sess.close()
+    t.close()
+    np.testing.assert_allclose(runs[0].lam, runs[1].lam, rtol=1e-9)
+    for a, b in zip(runs[0].factors, runs[1].factors):
+        assert rel(a, b) < 1e-9
