@@ -149,13 +149,17 @@ int dct_fibers_per_cta(int n, size_t smem_budget);
 // in and out may alias (in place).
 // col_div (nullable): fiber f's elements are divided by col_div[f] on load
 // (lazily normalized factor columns).
+// loads the kernel launch_mode_transform(p, x, x, st, nfib, ., forward, nullptr, .)
+// would use (lazy module loading stays out of a timed region)
+void prepare_mode_transform(const DctPlan& p, i64 st, i64 nfib, int forward);
 void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 st, i64 nfib,
                            const double* sign, int forward, const double* col_div,
                            cudaStream_t st_);
 // Whole-tensor mixing pass (mixpass.cu): persistent, pipelined, radices 2-8.
 bool mix_pass_supported(const DctPlan& p);
+// prepare_only: load and configure the kernel the call would launch, no launch
 void launch_mix_pass(const DctPlan& p, const double* in, double* out, i64 st, i64 nfib, const double* sign,
-                     int forward, cudaStream_t stream);
+                     int forward, cudaStream_t stream, bool prepare_only = false);
 // MIX path: RHS (I_n x R row-major) = D_n C^T (sum_ks part_rhs) per column
 void launch_reduce_rhs(const double* part_rhs, int ks, i64 in, int r, double* out,
                        cudaStream_t st);

@@ -106,6 +106,10 @@ int dct_fibers_per_cta(int n, size_t budget) {
   return F < 2 ? 2 : F;
 }
 
+void prepare_mode_transform(const DctPlan& p, i64 st, i64 nfib, int forward) {
+  if (nfib >= 4096 && mix_pass_supported(p)) launch_mix_pass(p, nullptr, nullptr, st, nfib, nullptr, forward, nullptr, true);
+}
+
 void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 st, i64 nfib,
                            const double* sign, int forward, const double* col_div,
                            cudaStream_t stream) {

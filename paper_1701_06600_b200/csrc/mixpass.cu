@@ -16,6 +16,8 @@
 //    division-free indexing.
 // Same algorithm and rounding structure as dct.cuh's transform_group; parity
 // with the oracle's Bluestein DCT is at tolerance (1e-12 relative).
+#include <algorithm>
+
 #include "dct.cuh"
 #include "devutil.cuh"
 
@@ -299,6 +301,265 @@ __global__ void __launch_bounds__(kPassThreads, 1) mix_pass_kernel(PlanArgs p, c
   cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// Forward pass, groups of 2 SEQ fibers (SEQ complex sequences; SEQ grows as
+// the fibers get shorter so a pass keeps ~NT butterflies per barrier), NT =
+// 256 threads per CTA for SEQ = 2 (two CTAs per SM: independent barrier
+// domains) and 512 above:
+//  * the first radix pass reads its butterfly inputs straight from global
+//    memory into registers (sign and the even/odd reorder folded into the
+//    addressing): no staging buffer, no packing pass;
+//  * those loads are issued one group ahead, so they stream in while the
+//    current group's remaining passes and epilogue run;
+//  * per-pass index constants (multiply-high magics instead of divisions)
+//    are formed once per CTA.
+
+// j / d for j * d < 2^32, with M = floor((2^32 - 1) / d) + 1
+__device__ __forceinline__ int udiv(int j, unsigned M) { return static_cast<int>(__umulhi(static_cast<unsigned>(j), M)); }
+__host__ __device__ constexpr unsigned umagic(int d) { return 0xffffffffu / static_cast<unsigned>(d) + 1u; }
+
+struct PassK {  // one Stockham pass: butterflies per sequence m, ns, twiddle step, magics
+  int m, ns, step;
+  unsigned Mm, Mns;
+};
+
+template <int SEQ>
+constexpr int fwd_threads() { return SEQ == 2 ? 256 : 512; }
+
+template <int R, int SEQ>
+__device__ void pass_seq(const PassK& c, int ss, const double2* tw, const double2* src, double2* dst) {
+  constexpr int NT = fwd_threads<SEQ>();
+  const int m = c.m, ns = c.ns, step = c.step;
+  for (int t = threadIdx.x; t < SEQ * m; t += NT) {
+    const int q = udiv(t, c.Mm), j = t - q * m;
+    const int jj = udiv(j, c.Mns), k = j - jj * ns;
+    const double2* sp = src + q * ss + j;
+    double2 v[R], w[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = sp[r * m];
+#pragma unroll
+    for (int r = 1; r < R; ++r) w[r] = tw[r * k * step];
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = dct::cmul(v[r], w[r]);
+    dft<R>(v, false);
+    double2* d = dst + q * ss + jj * ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) d[r * ns] = v[r];
+  }
+}
+
+// STG (contiguous fibers only): the group's FIB * n doubles are one
+// contiguous range; it streams into a shared staging buffer with cp.async
+// (fully coalesced) instead of the strided per-butterfly register loads.
+template <int R1, int SEQ, bool STG>
+__global__ void __launch_bounds__(fwd_threads<SEQ>(), 512 / fwd_threads<SEQ>()) mix_pass_fwd_kernel(
+    PlanArgs p, const double* in, double* out, i64 st, i64 nfib, const double* __restrict__ sign) {
+  constexpr int NT = fwd_threads<SEQ>(), FIB = 2 * SEQ;
+  extern __shared__ __align__(16) double2 psm[];
+  const int n = p.n, tid = threadIdx.x;
+  const int ss = n + 1;                                   // sequence stride (banks)
+  double2* tw = psm;                                      // [n]
+  double2* ph = tw + n;                                   // [n]
+  double2* b0 = ph + n;                                   // [SEQ * ss]
+  double2* b1 = b0 + SEQ * ss;                            // [SEQ * ss]
+  double* sg = reinterpret_cast<double*>(b1 + SEQ * ss);  // [n]
+  double* stg = sg + n + (n & 1);                         // STG: [2][FIB * n] (16-byte aligned)
+  __shared__ i64 fbase[2][FIB];
+  __shared__ PassK pk[24];
+  for (int i = tid; i < n; i += NT) {
+    tw[i] = p.tw[i];
+    ph[i] = p.phase[i];
+    sg[i] = sign ? sign[i] : 1.0;
+  }
+  if (tid == 0) {
+    int ns = R1;
+    for (int q = 1; q < p.nrad; ++q) {
+      const int R = p.radix[q];
+      PassK c;
+      c.m = n / R;
+      c.ns = ns;
+      c.step = n / (ns * R);
+      c.Mm = umagic(c.m);
+      c.Mns = umagic(ns);
+      pk[q] = c;
+      ns *= R;
+    }
+  }
+  const i64 ng = (nfib + FIB - 1) / FIB;
+  const bool contig = (st == 1);
+  // this thread's first-pass butterfly (fixed for every group): sequence bq,
+  // index bj, and the fiber element feeding each of its R1 inputs
+  // (contiguous fibers: consecutive lanes along j; strided: the SEQ
+  // sequences of one j in adjacent lanes, so a warp reads whole rows)
+  const int m1 = n / R1;
+  const bool bact = tid < SEQ * m1;
+  const int bq = !bact ? 0 : (contig ? udiv(tid, umagic(m1)) : (tid & (SEQ - 1)));
+  const int bj = !bact ? 0 : (contig ? tid - bq * m1 : (tid / SEQ));
+  int ei[R1];
+#pragma unroll
+  for (int r = 0; r < R1; ++r) {
+    const int d = bj + r * m1;
+    ei[r] = (d < (n + 1) / 2) ? 2 * d : 2 * (n - 1 - d) + 1;  // Makhoul reorder, inverted
+  }
+  auto bases = [&](i64 g, int slot) {
+    if (tid < FIB) {
+      const i64 f = g * FIB + tid;
+      const i64 hi = f / st, lo = f - hi * st;
+      fbase[slot][tid] = (g < ng && f < nfib) ? hi * st * n + lo : -1;
+    }
+  };
+  double va[R1], vb[R1];  // first-pass inputs of the group in flight
+  const bool in16 = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  auto stage = [&](i64 g, int slot) {  // STG: group g's fibers -> stg[slot]
+    double* d = stg + slot * FIB * n;
+    const i64 f0 = g * FIB;
+    const i64 cnt = g < ng ? min(static_cast<i64>(FIB), nfib - f0) * n : 0;  // doubles present
+    const double* srcp = in + f0 * n;
+    if (in16) {
+      for (int e = 2 * tid; e < FIB * n; e += 2 * NT) {
+        const i64 rem = cnt - e;
+        cp_async16(d + e, rem > 0 ? srcp + e : in, rem >= 2 ? 16 : (rem == 1 ? 8 : 0));
+      }
+    } else {
+      for (int e = tid; e < FIB * n; e += NT) cp_async8(d + e, e < cnt ? srcp + e : in, e < cnt ? 8 : 0);
+    }
+    cp_async_commit();
+  };
+  auto load_stg = [&](int slot) {  // STG: first-pass inputs from the staging buffer
+    const double* d = stg + slot * FIB * n + 2 * bq * n;
+#pragma unroll
+    for (int r = 0; r < R1; ++r) {
+      va[r] = d[ei[r]];
+      vb[r] = d[n + ei[r]];
+    }
+  };
+  auto load = [&](int slot) {
+    const i64 ba = bact ? fbase[slot][2 * bq] : -1, bb = bact ? fbase[slot][2 * bq + 1] : -1;
+    if (!contig && in16 && ba >= 0 && bb == ba + 1 && (ba & 1) == 0) {
+      // the pair of fibers is adjacent and aligned: one 16-byte load per row
+#pragma unroll
+      for (int r = 0; r < R1; ++r) {
+        const double2 t = __ldcg(reinterpret_cast<const double2*>(in + ba + static_cast<i64>(ei[r]) * st));
+        va[r] = t.x;
+        vb[r] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R1; ++r) {
+        // L1-cached: contiguous fibers read every other element per lane
+        // (the reorder), the other half hits in L1 from a neighbouring warp.
+        // Safe in place: a fiber is read once, by this CTA, before it is
+        // written, and no CTA re-reads another group's bytes.
+        const i64 off = static_cast<i64>(ei[r]) * st;
+        va[r] = ba >= 0 ? in[ba + off] : 0.0;
+        vb[r] = bb >= 0 ? in[bb + off] : 0.0;
+      }
+    }
+  };
+  bases(blockIdx.x, 0);
+  if constexpr (STG) {
+    stage(blockIdx.x, 0);
+  } else {
+    __syncthreads();
+    load(0);
+  }
+  int it = 0;
+  for (i64 g = blockIdx.x; g < ng; g += gridDim.x, ++it) {
+    const int cur = it & 1;
+    bases(g + gridDim.x, cur ^ 1);
+    if constexpr (STG) {
+      cp_async_wait<0>();
+      __syncthreads();
+      if (bact) load_stg(cur);
+    }
+    // first pass (ns = 1: no twiddles): sign, reorder, DFT_R1 -> b0
+    if (bact) {
+      double2 v[R1];
+#pragma unroll
+      for (int r = 0; r < R1; ++r) {
+        const double sgn = sg[ei[r]];
+        v[r] = make_double2(sgn * va[r], sgn * vb[r]);
+      }
+      dft<R1>(v, false);
+      double2* d = b0 + bq * ss + bj * R1;
+#pragma unroll
+      for (int r = 0; r < R1; ++r) d[r] = v[r];
+    }
+    __syncthreads();
+    // the next group streams in behind the remaining passes
+    if constexpr (STG)
+      stage(g + gridDim.x, cur ^ 1);
+    else
+      load(cur ^ 1);
+    double2* src = b0;
+    double2* dst = b1;
+    for (int stg = 1; stg < p.nrad; ++stg) {
+      const PassK c = pk[stg];
+      switch (p.radix[stg]) {
+        case 2: pass_seq<2, SEQ>(c, ss, tw, src, dst); break;
+        case 3: pass_seq<3, SEQ>(c, ss, tw, src, dst); break;
+        case 4: pass_seq<4, SEQ>(c, ss, tw, src, dst); break;
+        case 5: pass_seq<5, SEQ>(c, ss, tw, src, dst); break;
+        default: pass_seq<8, SEQ>(c, ss, tw, src, dst); break;
+      }
+      __syncthreads();
+      double2* t = src;
+      src = dst;
+      dst = t;
+    }
+    const double2* res = src;
+    // epilogue (dct::transform_group's forward formulas) + store
+    auto emit = [&](int i, int fl) {
+      const i64 b = fbase[cur][fl];
+      if (b < 0) return;
+      const int q = fl >> 1;
+      const double2 z = res[q * ss + i];
+      const double2 zc = res[q * ss + (i == 0 ? 0 : n - i)];
+      const double2 w = ph[i];
+      const double sc = (i == 0) ? p.s0 : p.sk;
+      double vx, vy;
+      if ((fl & 1) == 0) {
+        vx = 0.5 * (z.x + zc.x);
+        vy = 0.5 * (z.y - zc.y);
+      } else {
+        vx = 0.5 * (z.y + zc.y);
+        vy = -0.5 * (z.x - zc.x);
+      }
+      out[b + static_cast<i64>(i) * st] = sc * (w.x * vx - w.y * vy);
+    };
+    if (contig) {  // consecutive threads along i (fibers back to back): coalesced stores
+      const unsigned Mn = umagic(n);
+      for (int e = tid; e < FIB * n; e += NT) {
+        const int fl = udiv(e, Mn);
+        emit(e - fl * n, fl);
+      }
+    } else {  // consecutive threads along the adjacent fibers
+      for (int e0 = tid; e0 < n * FIB; e0 += NT) emit(e0 / FIB, e0 & (FIB - 1));
+    }
+    __syncthreads();
+  }
+}
+
+template <int SEQ>
+size_t mix_pass_fwd_smem(int n, bool stg) {
+  return static_cast<size_t>(n) * (16 + 16 + 8) + 8 + 2 * SEQ * static_cast<size_t>(n + 1) * 16 +
+         (stg ? 2 * 2 * SEQ * static_cast<size_t>(n) * 8 : 0);
+}
+
+// radices for the forward kernel: 8s first, then 4, 2, 5, 3, largest first
+// (0 entries: n has another prime factor)
+int fwd_radices(int n, int* rad) {
+  int k = 0, m = n;
+  while (m % 8 == 0) { rad[k++] = 8; m /= 8; }
+  while (m % 4 == 0) { rad[k++] = 4; m /= 4; }
+  while (m % 2 == 0) { rad[k++] = 2; m /= 2; }
+  while (m % 5 == 0) { rad[k++] = 5; m /= 5; }
+  while (m % 3 == 0) { rad[k++] = 3; m /= 3; }
+  if (m != 1 || k > 24) return 0;
+  std::sort(rad, rad + k, [](int a, int b) { return a > b; });
+  return k;
+}
+
 }  // namespace
 
 size_t mix_pass_smem(int n) {
@@ -311,15 +572,70 @@ bool mix_pass_supported(const DctPlan& p) {
   return mix_pass_smem(p.n) <= 220 * 1024;
 }
 
+namespace {
+template <int SEQ>
+bool launch_fwd(PlanArgs a, int nr, const int* rad, const double* in, double* out, i64 st, i64 nfib,
+                const double* sign, cudaStream_t stream, bool stg, bool prep) {
+  constexpr int NT = fwd_threads<SEQ>();
+  const int n = a.n, r1 = rad[0];
+  const int per_sm = 512 / NT;
+  if (SEQ * (n / r1) > NT || per_sm * mix_pass_fwd_smem<SEQ>(n, stg) > 220 * 1024) return false;
+  a.nrad = nr;
+  for (int i = 0; i < nr; ++i) a.radix[i] = rad[i];
+  void* fn = nullptr;
+#define CPB_FWD(R) (stg ? reinterpret_cast<void*>(&mix_pass_fwd_kernel<R, SEQ, true>) \
+                        : reinterpret_cast<void*>(&mix_pass_fwd_kernel<R, SEQ, false>))
+  switch (r1) {
+    case 2: fn = CPB_FWD(2); break;
+    case 3: fn = CPB_FWD(3); break;
+    case 4: fn = CPB_FWD(4); break;
+    case 5: fn = CPB_FWD(5); break;
+    default: fn = CPB_FWD(8); break;
+  }
+#undef CPB_FWD
+  const size_t smem = mix_pass_fwd_smem<SEQ>(n, stg);
+  CPB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int dev = 0, sms = 148, per = 1;
+  CPB_CUDA(cudaGetDevice(&dev));
+  CPB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, NT, smem));
+  if (prep) return true;  // the kernel is loaded and configured
+  const i64 ng = (nfib + 2 * SEQ - 1) / (2 * SEQ);
+  const int grid = static_cast<int>(std::min<i64>(ng, static_cast<i64>(sms) * std::max(per, 1)));
+  void* args[] = {&a, const_cast<double**>(&in), &out, &st, &nfib, const_cast<double**>(&sign)};
+  CPB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(NT), args, smem, stream));
+  return true;
+}
+
+// sequences per group: contiguous fibers of length >= 512 use 2 (two CTAs
+// per SM, direct loads); otherwise the most (<= 32) whose first pass fits 512
+// threads (contiguous fibers through the staging buffer)
+bool launch_fwd_any(PlanArgs a, int nr, const int* rad, const double* in, double* out, i64 st, i64 nfib,
+                    const double* sign, cudaStream_t stream, bool prep) {
+  const int m1 = a.n / rad[0];
+  if (st == 1 && a.n >= 512) return launch_fwd<2>(a, nr, rad, in, out, st, nfib, sign, stream, false, prep);
+  const bool stg = st == 1;
+  if (32 * m1 <= 512 && launch_fwd<32>(a, nr, rad, in, out, st, nfib, sign, stream, stg, prep)) return true;
+  if (16 * m1 <= 512 && launch_fwd<16>(a, nr, rad, in, out, st, nfib, sign, stream, stg, prep)) return true;
+  if (8 * m1 <= 512 && launch_fwd<8>(a, nr, rad, in, out, st, nfib, sign, stream, stg, prep)) return true;
+  if (4 * m1 <= 512 && launch_fwd<4>(a, nr, rad, in, out, st, nfib, sign, stream, stg, prep)) return true;
+  return launch_fwd<2>(a, nr, rad, in, out, st, nfib, sign, stream, stg, prep);
+}
+}  // namespace
+
 void launch_mix_pass(const DctPlan& pl, const double* in, double* out, i64 st, i64 nfib, const double* sign,
-                     int forward, cudaStream_t stream) {
+                     int forward, cudaStream_t stream, bool prepare_only) {
   PlanArgs a = dct_args(pl);
+  int rad[24];
+  const int nr = fwd_radices(pl.n, rad);
+  if (forward && nr > 0 && launch_fwd_any(a, nr, rad, in, out, st, nfib, sign, stream, prepare_only)) return;
   const size_t smem = mix_pass_smem(pl.n);
   static size_t configured = 0;
   if (smem > configured) {
     CPB_CUDA(cudaFuncSetAttribute(mix_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     configured = smem;
   }
+  if (prepare_only) return;
   int dev = 0, sms = 148;
   CPB_CUDA(cudaGetDevice(&dev));
   CPB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -401,6 +401,7 @@ void op_tensor_mix(Tensor* t, int transform, std::uint64_t seed, double* ms) {
     DBuf sg(signs[n].size() * sizeof(double));
     h2d(sg.p, signs[n].data(), signs[n].size());
     DctPlan plan = make_dct_plan(static_cast<int>(t->dims[n]));
+    prepare_mode_transform(plan, t->strides[n], t->p / t->dims[n], 1);
     CPB_CUDA(cudaDeviceSynchronize());
     CPB_CUDA(cudaEventRecord(e0, nullptr));
     launch_mode_transform(plan, t->d, t->d, t->strides[n], t->p / t->dims[n], sg.as<double>(), 1, nullptr, nullptr);

@@ -419,8 +419,13 @@ def test_sharded_session_rejects_bad_slab(pb):
 
 
 @pytest.mark.gpu
-def test_device_tensor_mix_matches_oracle(pb, orc):
-    dims = (24, 30, 20)
+@pytest.mark.parametrize("dims", [(24, 30, 20), (96, 100, 90), (90, 100, 96), (64, 70, 77), (640, 70, 60)])
+def test_device_tensor_mix_matches_oracle(pb, orc, dims):
+    """Whole-tensor mixing pass on the device. The larger shapes have >= 4096
+    fibers per mode, so they run the persistent pass kernels: lengths 96 /
+    100 / 90 (first radix 8 / 5 / 5; 16-32 sequences per group; fiber pairs
+    adjacent or straddling a stride boundary), 640 contiguous (2 sequences,
+    two CTAs per SM), and 77 = 7 * 11 (the generic per-CTA transform)."""
     x = orc.random_tensor(dims, 5)
     t = pb.DeviceTensor(dims)
     t.upload(x)
