@@ -17,6 +17,72 @@ __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 
+// e^{-2 pi i u r / R} multiply-accumulate DFT of R points (R in {2,3,4,5,8});
+// inverse uses the conjugate roots.
+template <int R>
+__device__ __forceinline__ void dft(double2 (&v)[R], bool inv) {
+  if constexpr (R == 2) {
+    const double2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    const double2 a = cadd(v[0], v[2]), b = csub(v[0], v[2]);
+    const double2 c = cadd(v[1], v[3]), e = csub(v[1], v[3]);
+    const double2 ej = inv ? make_double2(-e.y, e.x) : make_double2(e.y, -e.x);
+    v[0] = cadd(a, c);
+    v[2] = csub(a, c);
+    v[1] = cadd(b, ej);
+    v[3] = csub(b, ej);
+  } else if constexpr (R == 8) {
+    // two radix-4 on even/odd, twiddle the odd half by W8^k, combine
+    double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+    dft<4>(e, inv);
+    dft<4>(o, inv);
+    const double h = 0.70710678118654752440;
+    // W8^1 = (1 - i)/sqrt2 (forward), W8^2 = -i, W8^3 = (-1 - i)/sqrt2
+    const double2 o1 = inv ? make_double2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y))
+                           : make_double2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
+    const double2 o2 = inv ? make_double2(-o[2].y, o[2].x) : make_double2(o[2].y, -o[2].x);
+    const double2 o3 = inv ? make_double2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y))
+                           : make_double2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+    v[0] = cadd(e[0], o[0]);
+    v[4] = csub(e[0], o[0]);
+    v[1] = cadd(e[1], o1);
+    v[5] = csub(e[1], o1);
+    v[2] = cadd(e[2], o2);
+    v[6] = csub(e[2], o2);
+    v[3] = cadd(e[3], o3);
+    v[7] = csub(e[3], o3);
+  } else if constexpr (R == 3) {
+    const double c1 = -0.5, s1 = inv ? 0.86602540378443864676 : -0.86602540378443864676;
+    const double2 a = v[0], b = v[1], c = v[2];
+    const double2 sbc = cadd(b, c), dbc = csub(b, c);
+    v[0] = cadd(a, sbc);
+    const double2 t = make_double2(a.x + c1 * sbc.x, a.y + c1 * sbc.y);
+    // (b - c) * i s1
+    const double2 u = make_double2(-s1 * dbc.y, s1 * dbc.x);
+    v[1] = cadd(t, u);
+    v[2] = csub(t, u);
+  } else {  // R == 5
+    const double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;
+    const double s1 = inv ? 0.95105651629515357212 : -0.95105651629515357212;
+    const double s2 = inv ? 0.58778525229247312917 : -0.58778525229247312917;
+    const double2 a = v[0];
+    const double2 p1 = cadd(v[1], v[4]), m1 = csub(v[1], v[4]);
+    const double2 p2 = cadd(v[2], v[3]), m2 = csub(v[2], v[3]);
+    v[0] = make_double2(a.x + p1.x + p2.x, a.y + p1.y + p2.y);
+    const double2 t1 = make_double2(a.x + c1 * p1.x + c2 * p2.x, a.y + c1 * p1.y + c2 * p2.y);
+    const double2 t2 = make_double2(a.x + c2 * p1.x + c1 * p2.x, a.y + c2 * p1.y + c1 * p2.y);
+    // i (s1 m1 + s2 m2), i (s2 m1 - s1 m2)
+    const double2 u1 = make_double2(-(s1 * m1.y + s2 * m2.y), s1 * m1.x + s2 * m2.x);
+    const double2 u2 = make_double2(-(s2 * m1.y - s1 * m2.y), s2 * m1.x - s1 * m2.x);
+    v[1] = cadd(t1, u1);
+    v[4] = csub(t1, u1);
+    v[2] = cadd(t2, u2);
+    v[3] = csub(t2, u2);
+  }
+}
+
 // root(t) = exp(-+2 pi i t / n), t taken mod n
 __device__ __forceinline__ double2 root(const PlanArgs& p, int t, bool inv) {
   const double2 w = p.tw[t];
@@ -42,18 +108,10 @@ __device__ inline void stockham_pass(const PlanArgs& p, const double2* src, doub
       for (int r = 1; r < R; ++r) v[r] = cmul(v[r], root(p, r * k * step, inv));
     }
     double2 o[R];
-    if (R == 2) {
-      o[0] = cadd(v[0], v[1]);
-      o[1] = csub(v[0], v[1]);
-    } else if (R == 4) {
-      const double2 a = cadd(v[0], v[2]), b = csub(v[0], v[2]);
-      const double2 c = cadd(v[1], v[3]), e = csub(v[1], v[3]);
-      // forward: multiply e by -i; inverse: by +i
-      const double2 ej = inv ? make_double2(-e.y, e.x) : make_double2(e.y, -e.x);
-      o[0] = cadd(a, c);
-      o[2] = csub(a, c);
-      o[1] = cadd(b, ej);
-      o[3] = csub(b, ej);
+    if constexpr (R == 2 || R == 3 || R == 4 || R == 5 || R == 8) {
+      dft<R>(v, inv);  // closed-form butterflies
+#pragma unroll
+      for (int u = 0; u < R; ++u) o[u] = v[u];
     } else {
 #pragma unroll
       for (int u = 0; u < R; ++u) {
@@ -116,6 +174,7 @@ __device__ inline double2* fft_smem(const PlanArgs& p, double2* a, double2* b, i
 }
 
 __device__ __forceinline__ i64 fib_addr(i64 f, i64 i, i64 st, int n) {
+  if (f < st) return f + i * st;  // first slab (every fiber of a factor matrix): no division
   const i64 hi = f / st, lo = f - hi * st;
   return hi * st * n + lo + i * st;
 }

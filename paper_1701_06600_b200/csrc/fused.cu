@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
     grid_sync(A.bar);
     stamp(n, 4);
     const double* rhs = nullptr;
+    const int dF = min(M.dctF, (r + 1) & ~1);  // fibers per transform group (no empty sequences)
     if constexpr (MIX) {
       // unmix the summed RHS along I_n (linear, so equal to unmixing each fiber)
       const i64 tot = M.v.in * r;
@@ -130,8 +131,40 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
         A.rhs_full[e] = s;
       }
       grid_sync(A.bar);
+      if (M.tail1) {
+        // small mode: one CTA unmixes the RHS, applies the inverse, forms
+        // the norms and mixes the new factor, with no grid barrier between
+        if (b == 0) {
+          for (int g = 0; g * M.dctF < r; ++g) {
+            dct::transform_group(M.plan, A.rhs_full, A.rhs_full, r, r, static_cast<i64>(g) * M.dctF, dF,
+                                 M.sign, 0, nullptr, reinterpret_cast<double2*>(fsm));
+            __syncthreads();
+          }
+          constexpr int BI = kFusedThreads / RT;
+          double* gi = fsm;                  // RT x (RT+1)
+          double* rh = fsm + RT * (RT + 1);  // BI x (RT+1)
+          ph::load_ginv<RT, kFusedThreads>(A.ginv, r, gi);
+          __syncthreads();
+          const int nblk = static_cast<int>((M.v.in + BI - 1) / BI);
+          double q = 0.0;
+          for (int blk = 0; blk < nblk; ++blk)
+            q += ph::apply_block<RT, kFusedThreads>(M.v.in, r, w, A.rhs_full, static_cast<i64>(blk) * BI, gi, rh);
+          ph::ssq_store<RT, kFusedThreads>(q, r, A.ssq, rh);
+          ph::norms_final<RT, kFusedThreads>(r, M.v.in, w, 1, n == 0, A.rng, rh);
+          __syncthreads();
+          for (int g = 0; g * M.dctF < r; ++g) {
+            dct::transform_group(M.plan, M.a, M.mixed, r, r, static_cast<i64>(g) * M.dctF, dF, M.sign, 1,
+                                 M.norms, reinterpret_cast<double2*>(fsm));
+            __syncthreads();
+          }
+        }
+        stamp(n, 5);
+        grid_sync(A.bar);
+        stamp(n, 6);
+        continue;
+      }
       for (int g = b; g * M.dctF < r; g += G)
-        dct::transform_group(M.plan, A.rhs_full, A.rhs_full, r, r, static_cast<i64>(g) * M.dctF, M.dctF, M.sign, 0,
+        dct::transform_group(M.plan, A.rhs_full, A.rhs_full, r, r, static_cast<i64>(g) * M.dctF, dF, M.sign, 0,
                              nullptr, reinterpret_cast<double2*>(fsm));
       grid_sync(A.bar);
       rhs = A.rhs_full;
@@ -163,7 +196,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
     stamp(n, 6);
     if constexpr (MIX) {
       for (int g = b; g * M.dctF < r; g += G)
-        dct::transform_group(M.plan, M.a, M.mixed, r, r, static_cast<i64>(g) * M.dctF, M.dctF, M.sign, 1, M.norms,
+        dct::transform_group(M.plan, M.a, M.mixed, r, r, static_cast<i64>(g) * M.dctF, dF, M.sign, 1, M.norms,
                              reinterpret_cast<double2*>(fsm));
       grid_sync(A.bar);
     }

@@ -197,6 +197,7 @@ struct FusedMode {
   const double* sign;    // MIX: D_n
   DctArgs plan;          // MIX: DCT plan of I_n
   int dctF;              // MIX: fibers per CTA in the transform
+  int tail1;             // MIX: one CTA runs unmix -> apply -> norms -> mix (small I_n x R)
   // CPRAND kernel (fused_rand_kernel): 64-row x tklen-sample tiles
   int tm, tk, tklen;     // row blocks, sample splits, samples per split
   int nblk;              // upper 8 x 8 Gram blocks

@@ -30,71 +30,7 @@ constexpr int kGroup = 4;  // fibers per group (two complex sequences)
 
 using dct::PlanArgs;
 
-// e^{-2 pi i u r / R} multiply-accumulate DFT of R points (R in {2,3,4,5,8});
-// inverse uses the conjugate roots.
-template <int R>
-__device__ __forceinline__ void dft(double2 (&v)[R], bool inv) {
-  if constexpr (R == 2) {
-    const double2 a = v[0], b = v[1];
-    v[0] = dct::cadd(a, b);
-    v[1] = dct::csub(a, b);
-  } else if constexpr (R == 4) {
-    const double2 a = dct::cadd(v[0], v[2]), b = dct::csub(v[0], v[2]);
-    const double2 c = dct::cadd(v[1], v[3]), e = dct::csub(v[1], v[3]);
-    const double2 ej = inv ? make_double2(-e.y, e.x) : make_double2(e.y, -e.x);
-    v[0] = dct::cadd(a, c);
-    v[2] = dct::csub(a, c);
-    v[1] = dct::cadd(b, ej);
-    v[3] = dct::csub(b, ej);
-  } else if constexpr (R == 8) {
-    // two radix-4 on even/odd, twiddle the odd half by W8^k, combine
-    double2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
-    dft<4>(e, inv);
-    dft<4>(o, inv);
-    const double h = 0.70710678118654752440;
-    // W8^1 = (1 - i)/sqrt2 (forward), W8^2 = -i, W8^3 = (-1 - i)/sqrt2
-    const double2 o1 = inv ? make_double2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y))
-                           : make_double2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
-    const double2 o2 = inv ? make_double2(-o[2].y, o[2].x) : make_double2(o[2].y, -o[2].x);
-    const double2 o3 = inv ? make_double2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y))
-                           : make_double2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
-    v[0] = dct::cadd(e[0], o[0]);
-    v[4] = dct::csub(e[0], o[0]);
-    v[1] = dct::cadd(e[1], o1);
-    v[5] = dct::csub(e[1], o1);
-    v[2] = dct::cadd(e[2], o2);
-    v[6] = dct::csub(e[2], o2);
-    v[3] = dct::cadd(e[3], o3);
-    v[7] = dct::csub(e[3], o3);
-  } else if constexpr (R == 3) {
-    const double c1 = -0.5, s1 = inv ? 0.86602540378443864676 : -0.86602540378443864676;
-    const double2 a = v[0], b = v[1], c = v[2];
-    const double2 sbc = dct::cadd(b, c), dbc = dct::csub(b, c);
-    v[0] = dct::cadd(a, sbc);
-    const double2 t = make_double2(a.x + c1 * sbc.x, a.y + c1 * sbc.y);
-    // (b - c) * i s1
-    const double2 u = make_double2(-s1 * dbc.y, s1 * dbc.x);
-    v[1] = dct::cadd(t, u);
-    v[2] = dct::csub(t, u);
-  } else {  // R == 5
-    const double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;
-    const double s1 = inv ? 0.95105651629515357212 : -0.95105651629515357212;
-    const double s2 = inv ? 0.58778525229247312917 : -0.58778525229247312917;
-    const double2 a = v[0];
-    const double2 p1 = dct::cadd(v[1], v[4]), m1 = dct::csub(v[1], v[4]);
-    const double2 p2 = dct::cadd(v[2], v[3]), m2 = dct::csub(v[2], v[3]);
-    v[0] = make_double2(a.x + p1.x + p2.x, a.y + p1.y + p2.y);
-    const double2 t1 = make_double2(a.x + c1 * p1.x + c2 * p2.x, a.y + c1 * p1.y + c2 * p2.y);
-    const double2 t2 = make_double2(a.x + c2 * p1.x + c1 * p2.x, a.y + c2 * p1.y + c1 * p2.y);
-    // i (s1 m1 + s2 m2), i (s2 m1 - s1 m2)
-    const double2 u1 = make_double2(-(s1 * m1.y + s2 * m2.y), s1 * m1.x + s2 * m2.x);
-    const double2 u2 = make_double2(-(s2 * m1.y - s1 * m2.y), s2 * m1.x - s1 * m2.x);
-    v[1] = dct::cadd(t1, u1);
-    v[4] = dct::csub(t1, u1);
-    v[2] = dct::cadd(t2, u2);
-    v[3] = dct::csub(t2, u2);
-  }
-}
+using dct::dft;
 
 // One Stockham pass of radix R over two sequences of length n (src -> dst),
 // twiddles tw (shared, e^{-2 pi i t / n}).

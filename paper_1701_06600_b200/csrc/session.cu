@@ -598,6 +598,9 @@ void Session::setup_fused() {
         M.sign = signs_[static_cast<size_t>(n)];
         M.plan = dct_args(plans_[static_cast<size_t>(n)]);
         M.dctF = dct_fibers_per_cta(static_cast<int>(dims_[static_cast<size_t>(n)]), fsmem_);
+        // a few thousand factor entries: one CTA does unmix -> apply -> norms
+        // -> mix faster than three grid barriers
+        M.tail1 = (dims_[static_cast<size_t>(n)] * r_ <= 4096) ? 1 : 0;
       } else {
         const size_t k = static_cast<size_t>(n);
         M.tm = tm[k];
