@@ -80,6 +80,20 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
   auto stamp = [&](int n, int k) {
     if (A.phase_t && b == 0 && tid == 0) A.phase_t[n * 16 + k] = globaltimer();
   };
+  // grid barrier on this launch's own counter: arrive with a fire-and-forget
+  // release add, wait for the k-th multiple of the grid (no returning atomic,
+  // no reset: the counter is used by this launch only)
+  unsigned kbar = 0;
+  auto grid_bar = [&]() {
+    ++kbar;
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(A.lbar) : "memory");
+      while (tl::ld_relaxed(A.lbar) < kbar * G) __nanosleep(32);
+      asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+    }
+    __syncthreads();
+  };
   for (int n = 0; n < A.order; ++n) {
     const FusedMode& M = A.mode[n];
     const ModeWork w = work_of(A, M);
@@ -87,7 +101,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
     // ---- Z_S
     ph::z_range<RT>(M.v, A.z, static_cast<i64>(b) * kFusedThreads + tid, static_cast<i64>(G) * kFusedThreads);
     stamp(n, 1);
-    grid_sync(A.bar);
+    grid_bar();
     stamp(n, 2);
     // ---- Gram + inverse (last CTA) beside the split-K GEMM (all others)
     if (b == G - 1) {
@@ -118,7 +132,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
       }
     }
     stamp(n, 3);
-    grid_sync(A.bar);
+    grid_bar();
     stamp(n, 4);
     const double* rhs = nullptr;
     const int dF = min(M.dctF, (r + 1) & ~1);  // fibers per transform group (no empty sequences)
@@ -130,7 +144,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
         for (int k = 0; k < M.ks; ++k) s += A.part_rhs[static_cast<i64>(k) * tot + e];
         A.rhs_full[e] = s;
       }
-      grid_sync(A.bar);
+      grid_bar();
       if (M.tail1) {
         // small mode: one CTA unmixes the RHS, applies the inverse, forms
         // the norms and mixes the new factor, with no grid barrier between
@@ -159,14 +173,14 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
           }
         }
         stamp(n, 5);
-        grid_sync(A.bar);
+        grid_bar();
         stamp(n, 6);
         continue;
       }
       for (int g = b; g * M.dctF < r; g += G)
         dct::transform_group(M.plan, A.rhs_full, A.rhs_full, r, r, static_cast<i64>(g) * M.dctF, dF, M.sign, 0,
                              nullptr, reinterpret_cast<double2*>(fsm));
-      grid_sync(A.bar);
+      grid_bar();
       rhs = A.rhs_full;
     }
     // ---- apply + column norms
@@ -192,13 +206,13 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
       }
     }
     stamp(n, 5);
-    grid_sync(A.bar);
+    grid_bar();
     stamp(n, 6);
     if constexpr (MIX) {
       for (int g = b; g * M.dctF < r; g += G)
         dct::transform_group(M.plan, M.a, M.mixed, r, r, static_cast<i64>(g) * M.dctF, dF, M.sign, 1, M.norms,
                              reinterpret_cast<double2*>(fsm));
-      grid_sync(A.bar);
+      grid_bar();
     }
   }
   // ---- sampled fit + stop rule (sampling.hpp:191-210, :237-251)

@@ -229,6 +229,7 @@ struct FusedIter {
   unsigned* ticket;      // [0] norm ticket, [1] fit ticket
   unsigned* gram_done;
   unsigned* bar;         // [0] count, [1] generation
+  unsigned* lbar;        // MIX kernel: this launch's own grid-barrier arrival counter (zeroed once)
   const int* stop;
   int has_fit;
   FitArgs fit;

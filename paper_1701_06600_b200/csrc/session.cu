@@ -327,6 +327,7 @@ Session::~Session() {
   dfree(fargs_);
   dfree(phase_t_);
   dfree(fsync_);
+  dfree(lbar_);
   dfree(fcnt_);
   dfree(cta_t_);
   dfree(loc_idx_);
@@ -572,6 +573,8 @@ void Session::setup_fused() {
   }
   fsync_ = dalloc<unsigned>(kSyncWords);
   CPB_CUDA(cudaMemsetAsync(fsync_, 0, kSyncWords * sizeof(unsigned), stream_));
+  lbar_ = dalloc<unsigned>(static_cast<size_t>(table_iters_) * kCS);  // one barrier counter per launch
+  CPB_CUDA(cudaMemsetAsync(lbar_, 0, static_cast<size_t>(table_iters_) * kCS * sizeof(unsigned), stream_));
   std::vector<FusedIter> host(static_cast<size_t>(table_iters_));
   fargs_ = dalloc<FusedIter>(host.size());
   for (int ti = 0; ti < table_iters_; ++ti) {
@@ -653,6 +656,7 @@ void Session::setup_fused() {
     A.rng = rng_state_;
     A.gram_done = fsync_;
     A.bar = fsync_ + kCS;
+    A.lbar = lbar_ + static_cast<size_t>(ti) * kCS;
     A.ticket = fsync_ + 2 * kCS;
     A.stop = has_fit_ ? &state_->stopped : nullptr;
     A.has_fit = has_fit_;

@@ -165,6 +165,7 @@ class Session {
   size_t fsmem_ = 0;
   FusedIter* fargs_ = nullptr;     // [table iterations] device copies
   unsigned* fsync_ = nullptr;      // gram_done, barrier, tickets
+  unsigned* lbar_ = nullptr;       // MIX kernel: per-launch grid-barrier counters [table_iters][kCS]
   unsigned* fcnt_ = nullptr;       // CPRAND kernel counters [order][tm_max + 64 + 2 + tk_max]
   int tk_max_ = 1;
   unsigned long long* cta_t_ = nullptr;  // debug per-CTA stamps (CPRAND_DEBUG_CTA)
