@@ -134,86 +134,95 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
     stamp(n, 3);
     grid_bar();
     stamp(n, 4);
-    const double* rhs = nullptr;
-    const int dF = min(M.dctF, (r + 1) & ~1);  // fibers per transform group (no empty sequences)
-    if constexpr (MIX) {
-      // unmix the summed RHS along I_n (linear, so equal to unmixing each fiber)
+    // ---- the mode's solve in the mixed domain. The reference unmixes the
+    // summed RHS (sign after DCT-III), solves, normalizes and mixes the
+    // factor again (DCT-II after sign, mixing.hpp:284-312). The transforms
+    // are orthonormal and act on the rows while G^-1 acts on the columns, so
+    // mix(unmix(RHS) G^-1 / norms) = RHS G^-1 / norms with the same column
+    // norms: the kernel keeps the mixed factor unnormalized (M.mixed, norms
+    // applied lazily in Z_S like the CPRAND kernel) and unmixes each factor
+    // once per iteration, for the fit and the result (below).
+    {
       const i64 tot = M.v.in * r;
       for (i64 e = static_cast<i64>(b) * kFusedThreads + tid; e < tot; e += static_cast<i64>(G) * kFusedThreads) {
         double s = 0.0;
         for (int k = 0; k < M.ks; ++k) s += A.part_rhs[static_cast<i64>(k) * tot + e];
         A.rhs_full[e] = s;
       }
-      grid_bar();
-      if (M.tail1) {
-        // small mode: one CTA unmixes the RHS, applies the inverse, forms
-        // the norms and mixes the new factor, with no grid barrier between
-        if (b == 0) {
-          for (int g = 0; g * M.dctF < r; ++g) {
-            dct::transform_group(M.plan, A.rhs_full, A.rhs_full, r, r, static_cast<i64>(g) * M.dctF, dF,
-                                 M.sign, 0, nullptr, reinterpret_cast<double2*>(fsm));
+    }
+    grid_bar();
+    {
+      ModeWork wm = w;
+      wm.a = M.mixed;  // the apply writes the mixed, unnormalized factor
+      constexpr int BI = kFusedThreads / RT;
+      double* gi = fsm;                  // RT x (RT+1)
+      double* rh = fsm + RT * (RT + 1);  // BI x (RT+1)
+      const int nblk = static_cast<int>((M.v.in + BI - 1) / BI);
+      // a zero column is refilled in the unmixed domain (norms_final writes
+      // it to w.a = M.a); its mixed image replaces the mixed column
+      auto remix = [&](unsigned long long zm) {
+        for (int c = 0; c < r; ++c)
+          if ((zm >> c) & 1ull) {
             __syncthreads();
+            dct::transform_group(M.plan, M.a, M.mixed, r, c + 1, c, 2, M.sign, 1, nullptr,
+                                 reinterpret_cast<double2*>(fsm));
           }
-          constexpr int BI = kFusedThreads / RT;
-          double* gi = fsm;                  // RT x (RT+1)
-          double* rh = fsm + RT * (RT + 1);  // BI x (RT+1)
+      };
+      if (M.tail1) {  // small mode: one CTA, no ticket
+        if (b == 0) {
           ph::load_ginv<RT, kFusedThreads>(A.ginv, r, gi);
           __syncthreads();
-          const int nblk = static_cast<int>((M.v.in + BI - 1) / BI);
           double q = 0.0;
           for (int blk = 0; blk < nblk; ++blk)
-            q += ph::apply_block<RT, kFusedThreads>(M.v.in, r, w, A.rhs_full, static_cast<i64>(blk) * BI, gi, rh);
+            q += ph::apply_block<RT, kFusedThreads>(M.v.in, r, wm, A.rhs_full, static_cast<i64>(blk) * BI, gi, rh);
           ph::ssq_store<RT, kFusedThreads>(q, r, A.ssq, rh);
-          ph::norms_final<RT, kFusedThreads>(r, M.v.in, w, 1, n == 0, A.rng, rh);
-          __syncthreads();
-          for (int g = 0; g * M.dctF < r; ++g) {
-            dct::transform_group(M.plan, M.a, M.mixed, r, r, static_cast<i64>(g) * M.dctF, dF, M.sign, 1,
-                                 M.norms, reinterpret_cast<double2*>(fsm));
-            __syncthreads();
-          }
+          remix(ph::norms_final<RT, kFusedThreads>(r, M.v.in, w, 1, n == 0, A.rng, rh));
         }
-        stamp(n, 5);
-        grid_bar();
-        stamp(n, 6);
-        continue;
-      }
-      for (int g = b; g * M.dctF < r; g += G)
-        dct::transform_group(M.plan, A.rhs_full, A.rhs_full, r, r, static_cast<i64>(g) * M.dctF, dF, M.sign, 0,
-                             nullptr, reinterpret_cast<double2*>(fsm));
-      grid_bar();
-      rhs = A.rhs_full;
-    }
-    // ---- apply + column norms
-    {
-      constexpr int BI = kFusedThreads / RT;
-      double* gi = fsm;                    // RT x (RT+1)
-      double* rh = fsm + RT * (RT + 1);    // BI x (RT+1)
-      ph::load_ginv<RT, kFusedThreads>(A.ginv, r, gi);
-      __syncthreads();
-      const int nblk = static_cast<int>((M.v.in + BI - 1) / BI);
-      double q = 0.0;
-      for (int blk = b; blk < nblk; blk += G)
-        q += ph::apply_block<RT, kFusedThreads>(M.v.in, r, w, rhs, static_cast<i64>(blk) * BI, gi, rh);
-      ph::ssq_store<RT, kFusedThreads>(q, r, A.ssq + static_cast<i64>(b) * r, rh);
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) s_last = (atomicAdd(&A.ticket[0], 1u) == G - 1u);
-      __syncthreads();
-      if (s_last) {
+      } else {
+        ph::load_ginv<RT, kFusedThreads>(A.ginv, r, gi);
+        __syncthreads();
+        double q = 0.0;
+        for (int blk = b; blk < nblk; blk += G)
+          q += ph::apply_block<RT, kFusedThreads>(M.v.in, r, wm, A.rhs_full, static_cast<i64>(blk) * BI, gi, rh);
+        ph::ssq_store<RT, kFusedThreads>(q, r, A.ssq + static_cast<i64>(b) * r, rh);
         __threadfence();
-        ph::norms_final<RT, kFusedThreads>(r, M.v.in, w, G, n == 0, A.rng, rh);
-        if (tid == 0) A.ticket[0] = 0u;
+        __syncthreads();
+        if (tid == 0) s_last = (atomicAdd(&A.ticket[0], 1u) == G - 1u);
+        __syncthreads();
+        if (s_last) {
+          __threadfence();
+          remix(ph::norms_final<RT, kFusedThreads>(r, M.v.in, w, G, n == 0, A.rng, rh));
+          if (tid == 0) A.ticket[0] = 0u;
+        }
       }
     }
     stamp(n, 5);
     grid_bar();
     stamp(n, 6);
-    if constexpr (MIX) {
-      for (int g = b; g * M.dctF < r; g += G)
-        dct::transform_group(M.plan, M.a, M.mixed, r, r, static_cast<i64>(g) * M.dctF, dF, M.sign, 1, M.norms,
-                             reinterpret_cast<double2*>(fsm));
-      grid_bar();
+  }
+  // ---- the unmixed factors A_un = D DCT-III(mixed) of every mode (the fit
+  // and the result read A_un / norms), one transform group per task
+  {
+    int tasks = 0;
+    for (int m = 0; m < A.order; ++m) {
+      const int dFm = min(A.mode[m].dctF, (r + 1) & ~1);
+      tasks += (r + dFm - 1) / dFm;
     }
+    for (int t = b; t < tasks; t += G) {
+      int m = 0, g = t;
+      for (;; ++m) {
+        const int dFm = min(A.mode[m].dctF, (r + 1) & ~1);
+        const int gm = (r + dFm - 1) / dFm;
+        if (g < gm) break;
+        g -= gm;
+      }
+      const FusedMode& Q = A.mode[m];
+      const int dFm = min(Q.dctF, (r + 1) & ~1);
+      __syncthreads();
+      dct::transform_group(Q.plan, Q.mixed, Q.a, r, r, static_cast<i64>(g) * dFm, dFm, Q.sign, 0, nullptr,
+                           reinterpret_cast<double2*>(fsm));
+    }
+    grid_bar();
   }
   // ---- sampled fit + stop rule (sampling.hpp:191-210, :237-251)
   if (A.has_fit) {

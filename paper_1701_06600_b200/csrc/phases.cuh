@@ -1475,14 +1475,16 @@ __device__ void ssq_store(double q, int r, double* ssq_part, double* red) {
 // Column norms from nparts per-CTA partials (interleaved sums, combined in
 // fixed order), the lambda rule (kruskal.hpp:57-66) and the zero-column
 // refill from the device normalize RNG. One CTA of NTH threads.
-// red: (NTH / RT) x (RT + 1) doubles.
+// red: (NTH / RT) x (RT + 1) doubles. Returns (uniformly) the mask of the
+// columns that were zero and refilled.
 template <int RT, int NTH>
-__device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int first_of_pass,
+__device__ unsigned long long norms_final(int r, i64 in, const ModeWork& w, int nparts, int first_of_pass,
                             unsigned long long* rng_state, double* red, unsigned long long* dbg = nullptr,
                             const double* lam_scale = nullptr) {
   constexpr int NP = NTH / RT;
   const int tid = threadIdx.x, part = tid / RT, c = tid % RT;
   __shared__ int s_zero;
+  __shared__ unsigned long long s_zmask;
   // thread (part, c) sums a contiguous range of partials, 32 loads in flight;
   // the parts are then combined in order (deterministic)
   double q = 0.0;
@@ -1500,7 +1502,10 @@ __device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int fi
     }
   }
   red[part * (RT + 1) + c] = q;
-  if (tid == 0) s_zero = 0;
+  if (tid == 0) {
+    s_zero = 0;
+    s_zmask = 0ull;
+  }
   if (dbg && tid == 0) dbg[0] = globaltimer();
   __syncthreads();
   if (dbg && tid == 0) dbg[1] = globaltimer();
@@ -1530,9 +1535,11 @@ __device__ void norms_final(int r, i64 in, const ModeWork& w, int nparts, int fi
       if (w.norms[col] != 0.0) continue;
       for (i64 t = 0; t < in; ++t) w.a[t * r + col] = gauss(g);
       w.norms[col] = dev_stable_norm(w.a + col, in, r);
+      s_zmask |= 1ull << col;
     }
   }
   __syncthreads();
+  return s_zmask;
 }
 
 // ------------------------------------------------------------ fit

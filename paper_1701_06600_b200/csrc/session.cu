@@ -601,9 +601,15 @@ void Session::setup_fused() {
         M.sign = signs_[static_cast<size_t>(n)];
         M.plan = dct_args(plans_[static_cast<size_t>(n)]);
         M.dctF = dct_fibers_per_cta(static_cast<int>(dims_[static_cast<size_t>(n)]), fsmem_);
-        // a few thousand factor entries: one CTA does unmix -> apply -> norms
-        // -> mix faster than three grid barriers
+        // a few thousand factor entries: one CTA does apply -> norms faster
+        // than a ticket over the grid
         M.tail1 = (dims_[static_cast<size_t>(n)] * r_ <= 4096) ? 1 : 0;
+        // the kernel keeps the mixed factors unnormalized: Z_S divides by the
+        // norms (ones until a mode's first update)
+        for (int m = 0, c2 = 0; m < order_; ++m) {
+          if (m == n) continue;
+          M.v.nrm[c2++] = norms_ + static_cast<i64>(m) * r_;
+        }
       } else {
         const size_t k = static_cast<size_t>(n);
         M.tm = tm[k];
