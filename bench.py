@@ -289,7 +289,9 @@ def main() -> int:
     if fused[0]:
         # one persistent kernel per outer iteration: its algorithmic bytes are
         # every mode's sampled fibers (8 B/elem, read in place) + Z_S
-        kname = "fused_iteration_kernel (all modes + fit, persistent cooperative)"
+        kname = ("fused_rand_kernel (CPRAND: all modes of an outer iteration, persistent, flag hand-offs)"
+                 if cfg["method"] == "rand" else
+                 "fused_iteration_kernel (CPRAND-MIX: all modes of an outer iteration, persistent)")
         launches, kms = fused[0], fused[1]
         kbytes = launches * sum(e * 8 + cfg["s"] * cfg["r"] * 8 for e in elems)
         per_mode = None
@@ -375,7 +377,7 @@ def main() -> int:
         ms_modes = t.mix("dct", SEED)
         pbytes = 16.0 * float(np.prod(dims))
         gbs = [pbytes / (m * 1e-3) / 1e9 for m in ms_modes]
-        mix_pass = {"kernel": "mode_transform_kernel (sign + DCT-II per fiber, in place)",
+        mix_pass = {"kernel": "mix_pass_fwd_kernel (whole-tensor sign + DCT-II per fiber, in place)",
                     "bytes_model": "16 B per element per mode (read + write)",
                     "ms_per_mode": [round(m, 3) for m in ms_modes],
                     "gbs_per_mode": [round(g, 1) for g in gbs],
@@ -394,7 +396,11 @@ def main() -> int:
                        "gram_sum": "L2 fp64 atomics (atomic_gram)" if args.atomic_gram else
                                    "fixed-order split partials (bitwise reproducible)",
                        "parallelism": f"slab{ws} (last mode, NCCL allreduce/allgather)" if ws > 1 else "single",
-                       "l2": "inputs larger than L2 (8 GB tensor, fresh random samples per step)"},
+                       "l2": (f"inputs larger than L2 ({8 * int(np.prod(cfg['dims'])) / 1e9:.2f} GB tensor, "
+                              f"fresh random samples every step)"
+                              if 8 * int(np.prod(cfg["dims"])) > 126e6 else
+                              f"tensor ({8 * int(np.prod(cfg['dims'])) / 1e6:.0f} MB) fits in L2; no flush: "
+                              f"fresh random samples every step")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": kname,
                          "bytes_model": bytes_model, "per_mode_gbs": per_mode,
