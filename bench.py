@@ -12,9 +12,14 @@ steps ("inputs larger than L2").
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
   python bench.py --impl reference ...   # the reference's CPU path (oracle port)
 
-Multi-GPU (N > 1, torchrun): one process per GPU; the slab-sharded NCCL
-path is not enabled yet, so each rank runs an independent replica and the
-line says scaling "weak" / parallelism "replicas".
+Multi-GPU (N > 1, torchrun): one process per GPU; the tensor is slab-sharded
+along its last mode (NCCL allreduce of the R x I_n right-hand sides, allgather
+of the last factor), one global problem ("strong" scaling).
+
+Beside the bench-mode headline the line carries the two other parts of the
+BASELINE.json metric: `full_loop` (iters/s with the sampled fit estimator and
+the stop rule every iteration) and `time_to_fit` (wall time from solver entry,
+tensor resident in HBM, to the estimated fit reaching 0.99 and 1 - 1.2 eta).
 """
 from __future__ import annotations
 
@@ -149,7 +154,9 @@ def barrier(dist):
         dist.barrier()
 
 
-def launches_per_iter(cfg) -> int:
+def launches_per_iter(cfg, fused: bool) -> int:
+    if fused:
+        return 1  # one persistent kernel per outer iteration
     n = len(cfg["dims"])
     # z, gram, gram_inverse (+ fallback check), rhs_gemm, mode_apply; the gather
     # kernel only for modes without in-place reads
@@ -207,10 +214,71 @@ def run_reference(args, cfg):
     return 0
 
 
+def fit_runs(pb, t, cfg, dev, comm, steps, fresh, big):
+    """full_loop: `steps` iterations with the estimator + should_stop every
+    iteration (stall limit out of reach, so none stops early), device loop
+    time. time_to_fit: SolveOptions(fit_threshold=thr), reference defaults
+    otherwise (max_iters 200, stall limit 10), timed by wall clock from
+    solver entry (session setup: sample tables, estimator, replicas, MIX pass)
+    to the stop; counts only if the stop reason is fit_threshold."""
+    common = dict(rng_seed=SEED, fit_sample_count=cfg["phat"], transform=cfg["transform"],
+                  x_mutable=big, device=dev, comm=comm,
+                  shard_total=cfg["dims"][-1] if comm is not None else 0)
+    fresh()
+    s = pb.Session(cfg["method"], t, cfg["r"], cfg["s"],
+                   pb.SolveOptions(max_iters=steps + 3, stall_limit=1 << 30, **common))
+    s.run(3)
+    s.sync()
+    t0 = time.perf_counter()
+    ran = s.run(steps)
+    wall = time.perf_counter() - t0
+    res = s.result()
+    s.close()
+    loop_dev = res.loop_seconds_device
+    full = {"value": ran / wall, "unit": "iters/s", "iterations": ran, "wall_seconds": wall,
+            "device_loop_seconds_incl_warmup": loop_dev, "fit_sample_count": cfg["phat"],
+            "final_fit_estimate": res.trace[-1][2] if res.trace else None,
+            "note": "Session.run: estimate_fit + should_stop on device every iteration, host polls the stop flag"}
+    ttf = []
+    for thr in (0.99, round(1.0 - 1.2 * cfg["eta"], 6)):
+        fresh()
+        t0 = time.perf_counter()
+        s = pb.Session(cfg["method"], t, cfg["r"], cfg["s"], pb.SolveOptions(fit_threshold=thr, **common))
+        s.run(200)
+        s.sync()
+        wall = time.perf_counter() - t0
+        res = s.result()
+        s.close()
+        reached = res.reason == "fit_threshold"
+        ttf.append({"threshold": thr, "reached": reached, "seconds": wall if reached else None,
+                    "wall_seconds": wall, "setup_seconds": res.setup_seconds, "iterations": res.iterations,
+                    "reason": res.reason, "final_fit_estimate": res.trace[-1][2] if res.trace else None,
+                    "best_fit": res.trace[-1][4] if res.trace else None, "stall_limit": 10})
+        if not reached and res.reason == "best_fit_stall":
+            # the same run with the best-fit stall stop out of reach
+            # (stall_limit = max_iters): how long the threshold takes when
+            # the solver is allowed to continue
+            fresh()
+            t0 = time.perf_counter()
+            s = pb.Session(cfg["method"], t, cfg["r"], cfg["s"],
+                           pb.SolveOptions(fit_threshold=thr, stall_limit=200, **common))
+            s.run(200)
+            s.sync()
+            wall = time.perf_counter() - t0
+            res = s.result()
+            s.close()
+            reached = res.reason == "fit_threshold"
+            ttf.append({"threshold": thr, "reached": reached, "seconds": wall if reached else None,
+                        "wall_seconds": wall, "setup_seconds": res.setup_seconds, "iterations": res.iterations,
+                        "reason": res.reason, "final_fit_estimate": res.trace[-1][2] if res.trace else None,
+                        "best_fit": res.trace[-1][4] if res.trace else None, "stall_limit": 200})
+    return full, ttf
+
+
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -247,10 +315,22 @@ def main() -> int:
         t.synth(cfg["r"], cfg["c"], cfg["eta"], SEED)
     else:
         t.synth_slab(cfg["r"], cfg["c"], cfg["eta"], SEED, cfg["dims"][-1], comm)
+    # MIX on a tensor too large for a private mixed copy beside the replicas
+    # (C5, 84 GB): sessions mix `t` in place and `t` is regenerated before
+    # each new session, so every session starts from the same tensor
+    big = cfg["method"] in ("mix", "premix") and 8 * int(np.prod(dims)) > 40e9
+
+    def fresh():
+        if big:
+            if comm is None:
+                t.synth(cfg["r"], cfg["c"], cfg["eta"], SEED)
+            else:
+                t.synth_slab(cfg["r"], cfg["c"], cfg["eta"], SEED, cfg["dims"][-1], comm)
+
     timing_iters = max(args.steps, 10)
     total_iters = args.warmup + args.steps + timing_iters + 2
     opts = pb.SolveOptions(rng_seed=SEED, max_iters=total_iters, bench_mode=True,
-                           transform=cfg["transform"], x_mutable=False, device=dev,
+                           transform=cfg["transform"], x_mutable=big, device=dev,
                            comm=comm, shard_total=cfg["dims"][-1] if comm is not None else 0,
                            atomic_gram=args.atomic_gram)
     s = pb.Session(cfg["method"], t, cfg["r"], cfg["s"], opts)
@@ -323,7 +403,12 @@ def main() -> int:
         with open(tpath) as f:
             traffic = json.load(f).get("traffic_bytes_per_launch")
     fallbacks = s.gram_fallbacks()
+    used_fused = bool(fused[0])
     s.close()
+
+    # ---- full loop (sampled fit estimate + stop rule every iteration) and
+    # time to fit, both from the same resident tensor
+    full, ttf = fit_runs(pb, t, cfg, dev, comm, args.steps, fresh, big)
 
     # ---- the same timed loop with the Gram summed by L2 fp64 atomics
     # (SolveOptions.atomic_gram: one round trip fewer per mode, not bitwise
@@ -340,14 +425,34 @@ def main() -> int:
         atomic = {"value": args.steps / (ms2 * 1e-3), "unit": "iters/s", "ms_per_step": ms2 / args.steps,
                   "option": "SolveOptions(atomic_gram=True)"}
 
+    # ---- host copy of the tensor for e2e / cpu_baseline, taken before the
+    # mixing-pass measurement below mixes `t` in place
+    fresh()
+    want_host = (rank == 0 or comm is not None) and (args.e2e_steps > 0 or (not args.no_cpu and ws == 1))
+    buf = None
+    p = int(np.prod(dims))
+    if want_host:
+        try:
+            buf = pb.PinnedBuffer(p)
+            t.download_into(buf.array)
+        except Exception as exc:  # host RAM too small for a pinned copy
+            buf, host_skip = None, f"no pinned host copy of the {8 * p / 1e9:.1f} GB tensor: {exc}"
+    # ---- CPRAND-MIX preprocessing pass (mix_tensor, in place) on the same tensor
+    mix_pass = None
+    if rank == 0 and comm is None:
+        ms_modes = t.mix("dct", SEED)
+        pbytes = 16.0 * float(p)
+        gbs = [pbytes / (m * 1e-3) / 1e9 for m in ms_modes]
+        mix_pass = {"kernel": "mix_pass_fwd_kernel (whole-tensor sign + DCT-II per fiber, in place)",
+                    "bytes_model": "16 B per element per mode (read + write)",
+                    "ms_per_mode": [round(m, 3) for m in ms_modes],
+                    "gbs_per_mode": [round(g, 1) for g in gbs],
+                    "frac_per_mode": [round(g / hbm_peak, 3) for g in gbs]}
+    t.close()  # e2e allocates its own device copy
+
     # ---- e2e through the public one-shot call with host buffers
     e2e, cpu = None, None
-    if (rank == 0 or comm is not None) and (args.e2e_steps > 0 or not args.no_cpu):
-        p = int(np.prod(dims))
-        buf = pb.PinnedBuffer(p)
-        flat = t.download().reshape(-1, order="F")
-        buf.array[:] = flat
-        del flat
+    if buf is not None:
         xh = buf.array.reshape(dims, order="F")
         eo = pb.SolveOptions(rng_seed=SEED, max_iters=args.e2e_iters, bench_mode=True,
                              transform=cfg["transform"], device=dev, comm=comm,
@@ -366,23 +471,19 @@ def main() -> int:
                    "iters_per_step": args.e2e_iters, "seconds_per_step": dt,
                    "note": "cprand_solve(host pinned tensor): H2D + setup + bench-mode loop + D2H"}
         if not args.no_cpu and ws == 1:
-            rate, n_it, secs = cpu_oracle_rate(xh, cfg)
-            cpu = {"value": rate, "unit": "iters/s", "cores": os.cpu_count() or 1, "kind": "port",
-                   "sample": f"{n_it} bench-mode outer iterations of {args.config} on the same "
-                             f"tensor ({secs:.1f} s); gather on all host threads, LS single-threaded"}
+            if cfg["method"] == "mix" and p > (1 << 31):
+                cpu = {"value": None, "unit": "iters/s", "cores": os.cpu_count() or 1, "kind": "port",
+                       "sample": "not run: the CPU path's setup mixes the whole tensor with a single-threaded "
+                                 "Bluestein DCT per fiber (hours at this size), SURVEY.md 8(d)"}
+            else:
+                rate, n_it, secs = cpu_oracle_rate(xh, cfg)
+                cpu = {"value": rate, "unit": "iters/s", "cores": os.cpu_count() or 1, "kind": "port",
+                       "sample": f"{n_it} bench-mode outer iterations of {args.config} on the same "
+                                 f"tensor ({secs:.1f} s); gather on all host threads, LS single-threaded"}
         buf.close()
-    # ---- CPRAND-MIX preprocessing pass (mix_tensor, in place) on the same tensor
-    mix_pass = None
-    if rank == 0 and comm is None:
-        ms_modes = t.mix("dct", SEED)
-        pbytes = 16.0 * float(np.prod(dims))
-        gbs = [pbytes / (m * 1e-3) / 1e9 for m in ms_modes]
-        mix_pass = {"kernel": "mix_pass_fwd_kernel (whole-tensor sign + DCT-II per fiber, in place)",
-                    "bytes_model": "16 B per element per mode (read + write)",
-                    "ms_per_mode": [round(m, 3) for m in ms_modes],
-                    "gbs_per_mode": [round(g, 1) for g in gbs],
-                    "frac_per_mode": [round(g / hbm_peak, 3) for g in gbs]}
-    t.close()
+    elif want_host:
+        e2e = {"value": None, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "note": host_skip}
 
     if rank == 0:
         line = {
@@ -418,9 +519,9 @@ def main() -> int:
                                "gram_reduce"]),
                              [round(x, 2) for x in phases])) if phases else None,
                          "gram_fallbacks": fallbacks, "mix_pass": mix_pass},
-            "atomic_gram": atomic,
+            "atomic_gram": atomic, "full_loop": full, "time_to_fit": ttf,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-            "gpu_launches": launches_per_iter(cfg) * args.steps,
+            "gpu_launches": launches_per_iter(cfg, used_fused) * args.steps,
         }
         print(json.dumps(line), flush=True)
     if comm is not None:

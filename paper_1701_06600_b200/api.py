@@ -194,6 +194,12 @@ class DeviceTensor:
         check(lib().cprand_tensor_download(self.h, _p(out)))
         return out.reshape(self.dims, order="F")
 
+    def download_into(self, flat: np.ndarray) -> None:
+        """Copy the tensor (column-major) into a caller-owned float64 buffer."""
+        if flat.dtype != np.float64 or flat.size != self.size or not flat.flags["C_CONTIGUOUS"]:
+            raise ValueError("download_into needs a contiguous float64 buffer of the tensor's size")
+        check(lib().cprand_tensor_download(self.h, _p(flat)))
+
     def synth(self, r: int, collinearity: float, eta: float, seed: int, want_factors=False):
         fs = [np.empty((d, r), dtype=np.float64, order="F") for d in self.dims] if want_factors else None
         check(lib().cprand_tensor_synth(self.h, C.c_int64(r), C.c_double(collinearity),

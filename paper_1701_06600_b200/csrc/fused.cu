@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
                                   t / M.mtiles, fsm);
         else
           ph::gemm_tile<RT, false>(M.v.x, 0, M.v.base, A.z, M.v.in, M.v.s, r, M.ks_len, A.part_rhs, t % M.mtiles,
-                                   t / M.mtiles, fsm);
+                                   t / M.mtiles, fsm, M.est);
       }
     }
     stamp(n, 3);

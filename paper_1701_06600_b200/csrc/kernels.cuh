@@ -188,6 +188,7 @@ void launch_synth(double* x, int order, const i64* dims, int r, const double* co
 struct FusedMode {
   ModeView v;            // x / base: in-place fiber source and row offsets
   int vec16;
+  i64 est;               // MIX kernel: element stride of the fibers (1: mode 1 / replica)
   int mtiles, ks, ks_len;
   int gparts, gklen;
   double tol;

@@ -1309,14 +1309,16 @@ __device__ bool inverse_b8r(const double* __restrict__ g, int r, double tol, dou
 // part[kb](i, c) = sum_{s in split kb} X_S(s, i) Z(s, c) for the 128-row
 // tile mt: 256 threads, 8 x RT/16 register tile (columns strided by 16 for
 // conflict-free loads), 3-stage cp.async pipeline. A rows at
-// xs + row_off[s] (fibers read in place) or xs + s * ld (gathered X_S).
+// xs + row_off[s] (fibers read in place) or xs + s * ld (gathered X_S);
+// element i of a row at + i * est (est > 1: a strided mode read in place
+// from the tensor itself, one 8-byte cp.async per element, !VEC16 only).
 // sh: GSTAGES * GBK * (GBM + RT) doubles.
 constexpr int GBM = 128, GBK = 16, GSTAGES = 3;
 
 template <int RT, bool VEC16>
 __device__ void gemm_tile(const double* __restrict__ xs, i64 ld, const i64* __restrict__ row_off,
                           const double* __restrict__ z, i64 in, int s_total, int r, int ks_len,
-                          double* __restrict__ part, int mt, int kb, double* sh) {
+                          double* __restrict__ part, int mt, int kb, double* sh, i64 est = 1) {
   constexpr int NT = 256;
   constexpr int TN = RT / 16, TM = GBM / 16;
   double* as = sh;                        // [GSTAGES][GBK][GBM]
@@ -1353,7 +1355,7 @@ __device__ void gemm_tile(const double* __restrict__ xs, i64 ld, const i64* __re
         const i64 i = i0 + ic;
         const bool ok = (s < s_end) && (i < in);
         const i64 ro = (s < s_end) ? (row_off ? row_off[s] : static_cast<i64>(s) * ld) : 0;
-        cp_async8(ab + sl * GBM + ic, ok ? xs + ro + i : xs, ok ? 8 : 0);
+        cp_async8(ab + sl * GBM + ic, ok ? xs + ro + i * est : xs, ok ? 8 : 0);
       }
     }
     for (int c = tid; c < GBK * RT / 2; c += NT) {

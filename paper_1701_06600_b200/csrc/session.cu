@@ -500,7 +500,10 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
 void Session::setup_fused() {
   bool all_direct = true;
   for (int n = 0; n < order_; ++n) all_direct = all_direct && direct_[static_cast<size_t>(n)];
-  if (o_.fused == 0 || !all_direct || o_.exhaustive_samples || shard_) return;
+  // the MIX kernel also reads strided modes without a replica in place
+  // (one 8-byte load per element); the CPRAND kernel's tiles need every
+  // mode contiguous
+  if (o_.fused == 0 || (!all_direct && !mix_) || o_.exhaustive_samples || shard_) return;
   i64 max_dim = 1;
   for (i64 d : dims_) max_dim = std::max(max_dim, d);
   int zcap = 0;
@@ -586,9 +589,15 @@ void Session::setup_fused() {
     for (int n = 0; n < order_; ++n) {
       FusedMode& M = A.mode[n];
       M.v = view(it, n);
-      M.v.x = (n == 0) ? xsolve_ : rep_[static_cast<size_t>(n)];
-      M.v.base = dbase_ptr(it, n);
-      M.vec16 = vec16_[static_cast<size_t>(n)];
+      if (direct_[static_cast<size_t>(n)]) {
+        M.v.x = (n == 0) ? xsolve_ : rep_[static_cast<size_t>(n)];
+        M.v.base = dbase_ptr(it, n);
+        M.vec16 = vec16_[static_cast<size_t>(n)];
+        M.est = 1;
+      } else {  // tensor base offsets, fibers at the mode's stride
+        M.vec16 = 0;
+        M.est = tstrides_[static_cast<size_t>(n)];
+      }
       M.mtiles = ceil_div(dims_[static_cast<size_t>(n)], 128);
       M.ks = ks_[static_cast<size_t>(n)];
       M.ks_len = ks_len_[static_cast<size_t>(n)];

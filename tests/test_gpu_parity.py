@@ -266,6 +266,27 @@ def test_dct_mix_end_to_end_matches_oracle(pb, orc, method):
         assert rel(a, b) < 1e-6
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims", [(16, 12, 10, 8), (21, 10, 15), (12, 9, 7, 11)])
+def test_mix_kernel_strided_in_place_reads(pb, orc, dims):
+    """The persistent MIX kernel reads a strided mode that has no mode-major
+    replica straight from the tensor (one 8-byte load per element, C5's
+    modes 2-3). Same GEMM inputs as through the replicas, so the two runs
+    agree bitwise; both follow the oracle trajectory."""
+    x, _ = orc.gen_baseline(dims, 3, 0.9, 0.01, 7)
+    opts = dict(rng_seed=7, max_iters=12, transform="dct", stall_limit=1000)
+    rep = pb.cprand_mix(x, 3, 60, pb.SolveOptions(replicas=1, **opts))
+    strided = pb.cprand_mix(x, 3, 60, pb.SolveOptions(replicas=0, **opts))
+    assert np.array_equal(rep.lam, strided.lam)
+    for a, b in zip(rep.factors, strided.factors):
+        assert np.array_equal(a, b)
+    ref = orc.solve("mix", x, 3, 60, orc.SolveOptions(**opts))
+    assert strided.iterations == ref.iterations
+    assert max(abs(a[2] - b[2]) for a, b in zip(strided.trace, ref.trace)) < 1e-7
+    for a, b in zip(strided.factors, ref.factors):
+        assert rel(a, b) < 1e-6
+
+
 def test_mixed_solver_recovers(pb, orc):
     g = orc.Engine(931, raw=True)
     fs = [g.matrix(d, 2, 0.1, 1.0) for d in (10, 9, 8)]
