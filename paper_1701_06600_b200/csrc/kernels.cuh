@@ -157,6 +157,9 @@ void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 
                            cudaStream_t st_);
 // Whole-tensor mixing pass (mixpass.cu): persistent, pipelined, radices 2-8.
 bool mix_pass_supported(const DctPlan& p);
+// TMA-fed forward pass (mixtma.cu); false when the shape does not suit it
+bool launch_mix_tma(const DctPlan& p, double* x, i64 st, i64 nfib, const double* sign, cudaStream_t stream,
+                    bool prepare_only);
 // prepare_only: load and configure the kernel the call would launch, no launch
 void launch_mix_pass(const DctPlan& p, const double* in, double* out, i64 st, i64 nfib, const double* sign,
                      int forward, cudaStream_t stream, bool prepare_only = false);

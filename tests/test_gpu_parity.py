@@ -457,6 +457,55 @@ def test_device_tensor_mix_matches_oracle(pb, orc, dims):
     assert rel(got, want) < 1e-12
 
 
+@pytest.mark.parametrize("dims", [(200, 120, 64), (80, 80, 80, 80), (320, 32, 48), (100, 24, 40, 16)])
+def test_tma_mix_pass_matches_v2(pb, orc, dims):
+    """The TMA-fed mixing pass (mixtma.cu: bulk / tensor-map tile loads and
+    stores, in-place Stockham passes) against the v2 pass kernel
+    (CPRAND_MIX_V2=1, oracle-checked above): the same butterflies, twiddles
+    and epilogue formulas; only the compiler's FMA contraction differs, so
+    the mixed tensors agree to a few ulp (1e-14 relative). Strided modes with
+    64-512 B rows, one or several TMA boxes per tile (n > 256), mode 1 with
+    whole-fiber bulk copies."""
+    import os
+    t = pb.DeviceTensor(dims)
+    t.synth(4, 0.3, 0.01, 11)
+    x = t.download()
+    os.environ["CPRAND_MIX_TMA"] = "1"  # also for n < 512, where it is not the default
+    try:
+        new = t.mix("dct", 3)
+    finally:
+        del os.environ["CPRAND_MIX_TMA"]
+    got = t.download()
+    t.upload(x)
+    os.environ["CPRAND_MIX_V2"] = "1"
+    try:
+        old = t.mix("dct", 3)
+    finally:
+        del os.environ["CPRAND_MIX_V2"]
+    want = t.download()
+    t.close()
+    assert len(new) == len(old) == len(dims)
+    assert rel(got, want) < 1e-14
+
+
+def test_tma_mix_pass_matches_oracle(pb, orc):
+    """TMA pass against the oracle's mix_tensor (Bluestein DCT) on a shape
+    whose every mode has >= 4096 fibers."""
+    import os
+    dims = (64, 40, 48, 32)
+    x = orc.random_tensor(dims, 9)
+    t = pb.DeviceTensor(dims)
+    t.upload(x)
+    os.environ["CPRAND_MIX_TMA"] = "1"
+    try:
+        t.mix("dct", 5)
+    finally:
+        del os.environ["CPRAND_MIX_TMA"]
+    got = t.download()
+    t.close()
+    assert rel(got, orc.mix_tensor(x, "dct", 5)) < 1e-12
+
+
 @pytest.mark.gpu
 def test_atomic_gram_many_tiles(pb, orc):
     """SolveOptions(atomic_gram=True) on a problem that spreads every mode's
