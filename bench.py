@@ -460,15 +460,19 @@ def main() -> int:
         if args.e2e_steps > 0:
             pb.solve(cfg["method"], xh, cfg["r"], cfg["s"], eo)  # warm
             t0 = time.perf_counter()
+            calls = []
             for _ in range(args.e2e_steps):
+                tc = time.perf_counter()
                 res = pb.solve(cfg["method"], xh, cfg["r"], cfg["s"], eo)
                 _ = float(res.lam[0])  # result on the host
+                calls.append({"wall": round(time.perf_counter() - tc, 4), "setup": round(res.setup_seconds, 4),
+                              "loop_device": round(res.loop_seconds_device, 4)})
             dt = (time.perf_counter() - t0) / args.e2e_steps
             table_bytes = args.e2e_iters * n_modes * cfg["s"] * ((n_modes - 1) * 4 + 8)
             e2e = {"value": args.e2e_iters / dt, "unit": "iters/s",
                    "h2d_bytes_per_step": p * 8 + table_bytes,
                    "d2h_bytes_per_step": 8 * cfg["r"] * (sum(cfg["dims"]) + 1),
-                   "iters_per_step": args.e2e_iters, "seconds_per_step": dt,
+                   "iters_per_step": args.e2e_iters, "seconds_per_step": dt, "calls": calls,
                    "note": "cprand_solve(host pinned tensor): H2D + setup + bench-mode loop + D2H"}
         if not args.no_cpu and ws == 1:
             if cfg["method"] == "mix" and p > (1 << 31):

@@ -197,6 +197,11 @@ void cprand_session_destroy(cprand_session_t s);
 void* cprand_host_alloc_pinned(uint64_t bytes);
 void cprand_host_free_pinned(void* p);
 
+/* Tensor-sized device blocks (a solve's uploaded tensor, its mixed copy,
+ * the mode-major replicas) are cached after release and reused by the next
+ * solve of the same shape; this frees the cache (all devices). */
+void cprand_device_cache_release(void);
+
 /* ---- operator-level entry points (host buffers in/out) ---- */
 int cprand_gather_fibers(const double* x, const int64_t* dims, int32_t order, int32_t mode,
                          const int64_t* idxs, int64_t s, double* out /* I_n x S */);

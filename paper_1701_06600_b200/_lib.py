@@ -71,7 +71,7 @@ EXPORTS = [
     "cprand_tensor_synth", "cprand_tensor_device_ptr", "cprand_tensor_destroy",
     "cprand_session_create", "cprand_session_run", "cprand_session_enqueue",
     "cprand_session_sync", "cprand_session_timed_enqueue", "cprand_host_alloc_pinned",
-    "cprand_host_free_pinned", "cprand_session_stream", "cprand_session_set_kernel_timing",
+    "cprand_host_free_pinned", "cprand_device_cache_release", "cprand_session_stream", "cprand_session_set_kernel_timing",
     "cprand_session_kernel_stats", "cprand_session_phase_us", "cprand_session_gram_fallbacks",
     "cprand_session_result", "cprand_session_destroy",
     "cprand_gather_fibers", "cprand_skr", "cprand_mode_update", "cprand_fit_values",
@@ -110,6 +110,8 @@ def lib() -> C.CDLL:
     L.cprand_host_alloc_pinned.argtypes = [C.c_uint64]
     L.cprand_host_free_pinned.argtypes = [C.c_void_p]
     L.cprand_host_free_pinned.restype = None
+    L.cprand_device_cache_release.argtypes = []
+    L.cprand_device_cache_release.restype = None
     _lib = L
     return L
 

@@ -1,0 +1,102 @@
+// Device blocks of tensor size (the tensor a one-shot cprand_solve uploads,
+// the private mixed copy, the mode-major replicas) are kept after release
+// and handed out again for a request of the same size on the same device:
+// repeated solves on same-shaped tensors (the e2e path, a serving loop) do
+// not pay cudaMalloc / cudaFree of tens of GB each call. A failed cudaMalloc
+// flushes the cache and retries; replica planning counts cached bytes as
+// free (big_cached_bytes).
+#include <mutex>
+#include <vector>
+
+#include "devutil.cuh"
+
+namespace cpb {
+
+namespace {
+struct Block {
+  int device;
+  size_t bytes;
+  void* p;
+};
+constexpr size_t kBigMin = size_t{256} << 20;  // cache blocks of >= 256 MB
+constexpr int kMaxCached = 6;
+std::mutex g_mu;
+std::vector<Block> g_cache;  // oldest first
+
+void flush_device(int dev) {
+  for (auto it = g_cache.begin(); it != g_cache.end();) {
+    if (it->device == dev) {
+      cudaFree(it->p);
+      it = g_cache.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+}  // namespace
+
+void* big_alloc(size_t bytes) {
+  if (bytes == 0) bytes = 1;
+  int dev = 0;
+  CPB_CUDA(cudaGetDevice(&dev));
+  if (bytes >= kBigMin) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
+      if (it->device == dev && it->bytes == bytes) {
+        void* p = it->p;
+        g_cache.erase(it);
+        return p;
+      }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      flush_device(dev);
+    }
+    e = cudaMalloc(&p, bytes);
+  }
+  CPB_CUDA(e);
+  return p;
+}
+
+void big_free(void* p, size_t bytes) {
+  if (!p) return;
+  int dev = 0;
+  if (bytes >= kBigMin && cudaGetDevice(&dev) == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_cache.push_back({dev, bytes, p});
+    while (static_cast<int>(g_cache.size()) > kMaxCached) {
+      cudaFree(g_cache.front().p);
+      g_cache.erase(g_cache.begin());
+    }
+    return;
+  }
+  cudaFree(p);
+}
+
+size_t big_cached_bytes() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  std::lock_guard<std::mutex> lk(g_mu);
+  size_t s = 0;
+  for (const auto& b : g_cache)
+    if (b.device == dev) s += b.bytes;
+  return s;
+}
+
+void big_release_all() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (const auto& b : g_cache) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(b.device);
+    cudaFree(b.p);
+    cudaSetDevice(cur);
+  }
+  g_cache.clear();
+}
+
+}  // namespace cpb

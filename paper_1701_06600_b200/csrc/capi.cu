@@ -306,6 +306,8 @@ void cprand_host_free_pinned(void* p) {
   if (p) cudaFreeHost(p);
 }
 
+void cprand_device_cache_release(void) { cpb::big_release_all(); }
+
 void* cprand_session_stream(cprand_session_t s) { return s ? static_cast<void*>(s->s->stream()) : nullptr; }
 
 int cprand_session_set_kernel_timing(cprand_session_t s, int32_t on) {

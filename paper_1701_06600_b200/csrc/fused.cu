@@ -142,15 +142,18 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
     // norms: the kernel keeps the mixed factor unnormalized (M.mixed, norms
     // applied lazily in Z_S like the CPRAND kernel) and unmixes each factor
     // once per iteration, for the fit and the result (below).
-    {
+    // small modes (one CTA applies): sum the split-K partials over the grid
+    // first; otherwise each apply block sums its rows' partials as it loads
+    // them (same order, k = 0, 1, ...: the same bits), no extra barrier
+    if (M.tail1) {
       const i64 tot = M.v.in * r;
       for (i64 e = static_cast<i64>(b) * kFusedThreads + tid; e < tot; e += static_cast<i64>(G) * kFusedThreads) {
         double s = 0.0;
         for (int k = 0; k < M.ks; ++k) s += A.part_rhs[static_cast<i64>(k) * tot + e];
         A.rhs_full[e] = s;
       }
+      grid_bar();
     }
-    grid_bar();
     {
       ModeWork wm = w;
       wm.a = M.mixed;  // the apply writes the mixed, unnormalized factor
@@ -178,20 +181,23 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
           ph::ssq_store<RT, kFusedThreads>(q, r, A.ssq, rh);
           remix(ph::norms_final<RT, kFusedThreads>(r, M.v.in, w, 1, n == 0, A.rng, rh));
         }
-      } else {
+      } else if (static_cast<int>(b) < min(static_cast<int>(G), nblk)) {
+        // the CTAs that own row blocks: apply, column sums of squares, ticket;
+        // the last of them forms the norms from their napp partials
+        const unsigned napp = static_cast<unsigned>(min(static_cast<int>(G), nblk));
         ph::load_ginv<RT, kFusedThreads>(A.ginv, r, gi);
         __syncthreads();
         double q = 0.0;
         for (int blk = b; blk < nblk; blk += G)
-          q += ph::apply_block<RT, kFusedThreads>(M.v.in, r, wm, A.rhs_full, static_cast<i64>(blk) * BI, gi, rh);
+          q += ph::apply_block<RT, kFusedThreads>(M.v.in, r, wm, nullptr, static_cast<i64>(blk) * BI, gi, rh);
         ph::ssq_store<RT, kFusedThreads>(q, r, A.ssq + static_cast<i64>(b) * r, rh);
         __threadfence();
         __syncthreads();
-        if (tid == 0) s_last = (atomicAdd(&A.ticket[0], 1u) == G - 1u);
+        if (tid == 0) s_last = (atomicAdd(&A.ticket[0], 1u) == napp - 1u);
         __syncthreads();
         if (s_last) {
           __threadfence();
-          remix(ph::norms_final<RT, kFusedThreads>(r, M.v.in, w, G, n == 0, A.rng, rh));
+          remix(ph::norms_final<RT, kFusedThreads>(r, M.v.in, w, static_cast<int>(napp), n == 0, A.rng, rh));
           if (tid == 0) A.ticket[0] = 0u;
         }
       }

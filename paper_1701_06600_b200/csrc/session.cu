@@ -117,11 +117,11 @@ Tensor::Tensor(const std::vector<i64>& d, int dev) : dims(d), device(dev) {
     p *= v;
   }
   CPB_CUDA(cudaSetDevice(device));
-  CPB_CUDA(cudaMalloc(&this->d, static_cast<size_t>(p) * sizeof(double)));
+  this->d = static_cast<double*>(big_alloc(static_cast<size_t>(p) * sizeof(double)));
 }
 
 Tensor::~Tensor() {
-  if (owned && d) cudaFree(d);
+  if (owned && d) big_free(d, static_cast<size_t>(p) * sizeof(double));
 }
 
 HostModel init_random(const std::vector<i64>& dims, int r, std::uint64_t seed) {
@@ -322,7 +322,10 @@ Session::~Session() {
   if (stream2_) cudaStreamSynchronize(stream2_);
   if (gstream_) cudaStreamSynchronize(gstream_);
   for (auto& b : ring_) dfree(b);
-  for (auto& b : rep_) dfree(b);
+  for (auto& b : rep_) {
+    if (b) big_free(b, static_cast<size_t>(tp_) * sizeof(double));
+    b = nullptr;
+  }
   dfree(dbase_);
   dfree(fargs_);
   dfree(phase_t_);
@@ -363,7 +366,8 @@ Session::~Session() {
   dfree(fit_part_);
   dfree(state_);
   dfree(trace_dev_);
-  dfree(xcopy_);
+  if (xcopy_) big_free(xcopy_, static_cast<size_t>(p_) * sizeof(double));
+  xcopy_ = nullptr;
   if (stop_host_) cudaFreeHost(stop_host_);
   for (auto& e : it_events_) cudaEventDestroy(e);
   for (auto& e : ev_pool_) cudaEventDestroy(e);
@@ -983,7 +987,7 @@ void Session::mix_setup() {
   if (o_.x_mutable) {
     xsolve_ = x_->d;
   } else {
-    xcopy_ = dalloc<double>(static_cast<size_t>(p_));
+    xcopy_ = static_cast<double*>(big_alloc(static_cast<size_t>(p_) * sizeof(double)));
     CPB_CUDA(cudaMemcpyAsync(xcopy_, x_->d, sizeof(double) * p_, cudaMemcpyDeviceToDevice, stream_));
     xsolve_ = xcopy_;
   }
@@ -1021,6 +1025,7 @@ void Session::plan_replicas() {
   if (o_.replicas == 0) return;
   size_t free_b = 0, total_b = 0;
   CPB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  free_b += big_cached_bytes();  // cached tensor-sized blocks are reused or flushed on demand
   const i64 bytes = tp_ * 8;
   i64 budget = static_cast<i64>(free_b) - (i64{6} << 30);  // keep 6 GB for work buffers
   if ((mix_ || premix_) && !o_.x_mutable) budget -= bytes;  // the private mixed copy comes first
@@ -1040,7 +1045,7 @@ void Session::plan_replicas() {
 void Session::build_replicas() {
   for (int n = 1; n < order_; ++n) {
     if (!direct_[static_cast<size_t>(n)]) continue;
-    rep_[static_cast<size_t>(n)] = dalloc<double>(static_cast<size_t>(tp_));
+    rep_[static_cast<size_t>(n)] = static_cast<double*>(big_alloc(static_cast<size_t>(tp_) * sizeof(double)));
     launch_replica(xsolve_, tdims_[static_cast<size_t>(n)], tstrides_[static_cast<size_t>(n)], tp_,
                    rep_[static_cast<size_t>(n)], stream_);
   }

@@ -51,6 +51,12 @@ struct Trace {
   double best;
 };
 
+// Cache of tensor-sized device blocks (bigalloc.cu).
+void* big_alloc(size_t bytes);
+void big_free(void* p, size_t bytes);
+size_t big_cached_bytes();
+void big_release_all();
+
 struct Tensor {
   std::vector<i64> dims, strides;
   i64 p = 0;
