@@ -255,7 +255,7 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
         if ((d & (d - 1)) != 0) throw InvalidArgument("wht requires power-of-two mode lengths");
     if (method == 3 && transform_ == 0)
       throw InvalidArgument("premix requires a real orthogonal transform");
-    if (transform_ == 0) throw Unsupported("FFT (complex) mixing is not on the B200 path yet; use dct");
+    if (transform_ == 0) cmix_ = true;  // complex mixing (cfft.cu)
     if (transform_ == 2) throw Unsupported("WHT mixing is not on the B200 path yet; use dct");
   }
   if (order_ > kMaxOrder) throw Unsupported("tensor order > 8");
@@ -346,6 +346,11 @@ Session::~Session() {
   dfree(z_);
   for (auto& f : fac_) dfree(f);
   for (auto& f : mixed_) dfree(f);
+  for (auto& f : mixedc_) dfree(f);
+  dfree(zc_);
+  dfree(cbuf_);
+  if (xc_) big_free(xc_, static_cast<size_t>(p_) * 2 * sizeof(double));
+  xc_ = nullptr;
   for (auto& f : fit_idx_) dfree(f);
   for (auto& s : signs_) dfree(s);
   for (auto& p : plans_) free_dct_plan(p);
@@ -437,6 +442,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   xsolve_ = x_->d;
   if (!o_.bench_mode && !premix_) build_fit_estimator(x_->d);
   if (mix_ || premix_) mix_setup();
+  if (cmix_) cmix_setup();
   if (!o_.bench_mode && premix_) {
     // cprand(x_hat) builds its estimator and norm on the mixed tensor
     launch_sumsq(xsolve_, tp_, fit_part_, nparts, fit_part_ + nparts, stream_);
@@ -485,7 +491,11 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   tickets_ = dalloc<unsigned>(8);
   CPB_CUDA(cudaMemsetAsync(tickets_, 0, 8 * sizeof(unsigned), stream_));
   ssq_ = dalloc<double>(static_cast<size_t>(std::max<i64>(max_apply, 4 * sms_) * r_));
-  if (mix_ || shard_) rhs_full_ = dalloc<double>(static_cast<size_t>(max_in * r_));
+  if (mix_ || shard_ || cmix_) rhs_full_ = dalloc<double>(static_cast<size_t>(max_in * r_));
+  if (cmix_) {
+    zc_ = dalloc<double>(static_cast<size_t>(2 * max_s * r_));
+    cbuf_ = dalloc<double>(static_cast<size_t>(2 * max_in * r_));
+  }
 
   // ---- fit / stop state
   state_ = dalloc<FitState>(1);
@@ -507,7 +517,7 @@ void Session::setup_fused() {
   // the MIX kernel also reads strided modes without a replica in place
   // (one 8-byte load per element); the CPRAND kernel's tiles need every
   // mode contiguous
-  if (o_.fused == 0 || (!all_direct && !mix_) || o_.exhaustive_samples || shard_) return;
+  if (o_.fused == 0 || (!all_direct && !mix_) || o_.exhaustive_samples || shard_ || cmix_) return;
   i64 max_dim = 1;
   for (i64 d : dims_) max_dim = std::max(max_dim, d);
   int zcap = 0;
@@ -1007,6 +1017,52 @@ void Session::mix_setup() {
   mix_seconds_ = seconds_since(tm);
 }
 
+// FFT-kind CPRAND-MIX setup (cprand_mix_impl<Complex>, mixing.hpp:258-282):
+// X_hat = X x_1 F_1 D_1 ... (complex, unitary FFT per mode, mix_tensor
+// :130-156) and the mixed images F_n D_n A_n of the initial factors.
+void Session::cmix_setup() {
+  const auto tm = Clock::now();
+  signs_host_ = mixing_signs(dims_, transform_, o_.rng_seed);
+  for (int n = 0; n < order_; ++n) {
+    const size_t k = static_cast<size_t>(n);
+    signs_.push_back(dalloc<double>(static_cast<size_t>(dims_[k])));
+    CPB_CUDA(cudaMemcpyAsync(signs_.back(), signs_host_[k].data(), sizeof(double) * dims_[k], cudaMemcpyHostToDevice,
+                             stream_));
+    plans_.push_back(make_dct_plan(static_cast<int>(dims_[k])));
+  }
+  xc_ = static_cast<double*>(big_alloc(static_cast<size_t>(p_) * 2 * sizeof(double)));
+  for (int n = 0; n < order_; ++n) {
+    const size_t k = static_cast<size_t>(n);
+    launch_cfft_mode(plans_[k], n == 0 ? x_->d : nullptr, n == 0 ? nullptr : xc_, xc_, nullptr, strides_[k],
+                     p_ / dims_[k], signs_[k], 1, nullptr, stream_);
+  }
+  for (int n = 0; n < order_; ++n) {
+    const size_t k = static_cast<size_t>(n);
+    mixedc_.push_back(dalloc<double>(static_cast<size_t>(2 * dims_[k] * r_)));
+    launch_cfft_mode(plans_[k], fac_[k], nullptr, mixedc_.back(), nullptr, r_, r_, signs_[k], 1, nullptr, stream_);
+  }
+  CPB_CUDA(cudaStreamSynchronize(stream_));
+  mix_seconds_ = seconds_since(tm);
+}
+
+// One FFT-kind mode update (mixing.hpp:284-298): complex Z_S, Gram
+// Re(Z^H Z) and its inverse, C = Z^H X_hat_S, unmix the R rows of C
+// (F^H, then D_n, real part), apply + norms + lambda, mix the new factor.
+void Session::enqueue_mode_cmix(int it, int n, const int* stop) {
+  const size_t k = static_cast<size_t>(n);
+  const ModeView v = view(it, n);
+  ModeWork w = work(n);
+  // real_least_squares stacks [Re Z; Im Z]: 2S rows in the rank threshold
+  w.tol = static_cast<double>(std::max(2 * v.s, r_)) * 2.220446049250313e-16;
+  launch_zc(v, zc_, stream_);
+  launch_gramc(zc_, v.s, r_, rt_, part_gram_, stream_);
+  launch_gram_inverse(part_gram_, 1, r_, w.tol, w.ginv, w.gfull, w.info, stop, stream_);
+  launch_rhsc(xc_, base_ptr(it, n), strides_[k], v.in, v.s, zc_, r_, cbuf_, stream_);
+  launch_cfft_mode(plans_[k], nullptr, cbuf_, nullptr, rhs_full_, r_, r_, signs_[k], 0, nullptr, stream_);
+  launch_mode_apply(v.in, r_, w, rhs_full_, n == 0, rng_state_, stream_);
+  launch_cfft_mode(plans_[k], fac_[k], nullptr, mixedc_[k], nullptr, r_, r_, signs_[k], 1, w.norms, stream_);
+}
+
 const i64* Session::dbase_ptr(int it, int n) const {
   const int ti = o_.exhaustive_samples ? 0 : it - 1;
   return dbase_ + base_off_[static_cast<size_t>(ti * order_ + n)];
@@ -1022,6 +1078,10 @@ void Session::plan_replicas() {
   rep_.assign(static_cast<size_t>(order_), nullptr);
   direct_[0] = 1;
   vec16_[0] = (order_ == 1) || (tdims_[0] % 2 == 0);
+  if (cmix_) {  // the FFT path reads the complex X_hat in place (no ring, no replicas)
+    direct_.assign(static_cast<size_t>(order_), 1);
+    return;
+  }
   if (o_.replicas == 0) return;
   size_t free_b = 0, total_b = 0;
   CPB_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -1043,6 +1103,7 @@ void Session::plan_replicas() {
 }
 
 void Session::build_replicas() {
+  if (cmix_) return;
   for (int n = 1; n < order_; ++n) {
     if (!direct_[static_cast<size_t>(n)]) continue;
     rep_[static_cast<size_t>(n)] = static_cast<double*>(big_alloc(static_cast<size_t>(tp_) * sizeof(double)));
@@ -1073,8 +1134,9 @@ ModeView Session::view(int it, int n) const {
   for (int m = 0; m < N; ++m) {
     if (m == n) continue;
     v.rows[c] = rb + static_cast<i64>(c) * sn;
-    v.fac[c] = mix_ ? mixed_[static_cast<size_t>(m)] : fac_[static_cast<size_t>(m)];
-    v.nrm[c] = mix_ ? nullptr : norms_ + static_cast<i64>(m) * r_;
+    v.fac[c] = cmix_ ? mixedc_[static_cast<size_t>(m)]
+                     : (mix_ ? mixed_[static_cast<size_t>(m)] : fac_[static_cast<size_t>(m)]);
+    v.nrm[c] = (mix_ || cmix_) ? nullptr : norms_ + static_cast<i64>(m) * r_;
     ++c;
   }
   v.base = base_ptr(it, n);
@@ -1284,6 +1346,10 @@ void Session::enqueue_iteration() {
   for (int n = 0; n < order_; ++n) {
     if (shard_) {
       enqueue_mode_sharded(it, n, stop);
+      continue;
+    }
+    if (cmix_) {
+      enqueue_mode_cmix(it, n, stop);
       continue;
     }
     const ModeView v = view(it, n);

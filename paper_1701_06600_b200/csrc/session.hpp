@@ -107,6 +107,8 @@ class Session {
   void build_tables();
   void build_fit_estimator(const double* xsrc);
   void mix_setup();
+  void cmix_setup();                          // FFT-kind MIX: complex X_hat, mixed factors
+  void enqueue_mode_cmix(int it, int n, const int* stop);
   void alloc_ring();
   void enqueue_gather(int git);
   void enqueue_iteration();
@@ -129,6 +131,11 @@ class Session {
   Options o_;
   int transform_ = -1;
   bool mix_ = false, premix_ = false;
+  bool cmix_ = false;  // cprand_mix with the FFT kind (complex mixing, cfft.cu)
+  double* xc_ = nullptr;            // complex X_hat (interleaved), P pairs
+  std::vector<double*> mixedc_;     // complex mixed factors, I_n x R row-major pairs
+  double* zc_ = nullptr;            // complex Z_S, S x R pairs
+  double* cbuf_ = nullptr;          // C = Z^H X_hat_S, I_n x R pairs
   std::vector<i64> dims_, strides_;  // global (model) shape
   i64 p_ = 0;
   std::vector<i64> tdims_, tstrides_;  // the tensor this session reads (a slab when sharded)

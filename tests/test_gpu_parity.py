@@ -287,6 +287,38 @@ def test_mix_kernel_strided_in_place_reads(pb, orc, dims):
         assert rel(a, b) < 1e-6
 
 
+@pytest.mark.parametrize("dims,r,s,transform", [((16, 12, 10, 8), 3, 60, None), ((21, 10, 15), 3, 40, "fft"),
+                                                 ((14, 9, 25), 4, 50, "fft"), ((40, 36, 30), 5, 100, None)])
+def test_fft_mix_end_to_end_matches_oracle(pb, orc, dims, r, s, transform):
+    """cprand_mix with the reference's default transform, the unitary FFT
+    (complex X_hat and mixed factors, real-constrained stacked solve,
+    cfft.cu): same iterations and fit trace as the oracle's
+    cprand_mix_impl<Complex>, factors to round-off. Lengths with factors
+    2, 3, 5, 7 (Stockham radices) and 4-way."""
+    x, _ = orc.gen_baseline(dims, r, 0.7, 0.01, 13)
+    opts = dict(rng_seed=13, max_iters=15, transform=transform, stall_limit=1000)
+    ref = orc.solve("mix", x, r, s, orc.SolveOptions(**opts))
+    got = pb.cprand_mix(x, r, s, pb.SolveOptions(**opts))
+    assert got.iterations == ref.iterations
+    fg = np.array([t[2] for t in got.trace])
+    fr = np.array([t[2] for t in ref.trace])
+    assert np.max(np.abs(fg - fr)) < 1e-7
+    for a, b in zip(got.factors, ref.factors):
+        assert rel(a, b) < 1e-6
+    assert rel(got.lam, ref.lam) < 1e-6
+
+
+def test_fft_mix_free_running_stop_rule(pb, orc):
+    """FFT-kind CPRAND-MIX with the reference's stop rule (default options):
+    the device stops at the same iteration for the same reason."""
+    x, _ = orc.gen_baseline((30, 24, 20), 4, 0.5, 0.01, 21)
+    opts = dict(rng_seed=21)
+    ref = orc.solve("mix", x, 4, 80, orc.SolveOptions(**opts))
+    got = pb.cprand_mix(x, 4, 80, pb.SolveOptions(**opts))
+    assert got.iterations == ref.iterations and got.reason == ref.reason
+    assert abs(got.trace[-1][2] - ref.trace[-1][2]) < 1e-6
+
+
 def test_mixed_solver_recovers(pb, orc):
     g = orc.Engine(931, raw=True)
     fs = [g.matrix(d, 2, 0.1, 1.0) for d in (10, 9, 8)]
