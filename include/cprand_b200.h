@@ -35,7 +35,7 @@
  *   2 std::invalid_argument / std::out_of_range   (CLI exit 2)
  *   3 numerical_consistency_error                 (CLI exit 3)
  *   4 CUDA / NCCL runtime failure
- *   5 valid for the reference but outside this path (e.g. R > 64, WHT mixing)
+ *   5 valid for the reference but outside this path (e.g. R > 64, HOSVD init)
  *   1 anything else
  */
 #ifndef CPRAND_B200_H

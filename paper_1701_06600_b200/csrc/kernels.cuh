@@ -132,6 +132,7 @@ struct DctArgs {
   double s0, sk;
 };
 struct DctPlan {
+  int kind = 1;  // 1: DCT-II (tables below), 2: Walsh-Hadamard (n a power of two, no tables)
   int n = 0;
   int nrad = 0;
   int radix[24];
@@ -140,6 +141,8 @@ struct DctPlan {
   double s0 = 0, sk = 0;     // orthonormal scales sqrt(1/n), sqrt(2/n)
 };
 DctPlan make_dct_plan(int n);  // allocates device tables
+// the real orthogonal mixing transform of a kind (1 DCT-II, 2 WHT) along length n
+DctPlan make_mix_plan(int kind, int n);
 void free_dct_plan(DctPlan& p);
 DctArgs dct_args(const DctPlan& p);
 // fibers per CTA for a length-n transform within smem_budget bytes (even, >= 2)

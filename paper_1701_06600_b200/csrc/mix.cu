@@ -33,6 +33,65 @@ __global__ void __launch_bounds__(kMixThreads) mode_transform_kernel(PlanArgs p,
   dct::transform_group(p, in, out, st, nfib, static_cast<i64>(blockIdx.x) * F, F, sign, forward, col_div, sbuf);
 }
 
+// Walsh-Hadamard mixing (transforms.hpp:170-197): natural (Hadamard) order,
+// butterflies x[i+k] = u + v, x[i+k+len] = u - v for len = 1, 2, 4, ..., then
+// the 1/sqrt(n) scale: the reference's operations in its order, so the
+// result is bit-identical. forward: sign first; adjoint (= forward): sign
+// after. F fibers per CTA in shared memory.
+__global__ void __launch_bounds__(kMixThreads) wht_mode_kernel(int n, const double* in, double* out, i64 st,
+                                                              i64 nfib, int F, const double* __restrict__ sign,
+                                                              int forward, const double* __restrict__ col_div,
+                                                              double scale) {
+  extern __shared__ __align__(16) double wbuf[];
+  const i64 f0 = static_cast<i64>(blockIdx.x) * F;
+  const int cnt = static_cast<int>(min(static_cast<i64>(F), nfib - f0));
+  const bool contig = (st == 1);
+  for (int t = threadIdx.x; t < F * n; t += blockDim.x) {
+    int fl, i;
+    if (contig) {
+      fl = t / n;
+      i = t - fl * n;
+    } else {
+      i = t / F;
+      fl = t - i * F;
+    }
+    double v = 0.0;
+    if (fl < cnt) {
+      v = in[dct::fib_addr(f0 + fl, i, st, n)];
+      if (col_div) v = v / col_div[f0 + fl];
+      if (forward && sign) v = v * sign[i];
+    }
+    wbuf[fl * n + i] = v;
+  }
+  __syncthreads();
+  const int half = n / 2;
+  for (int len = 1; len < n; len <<= 1) {
+    for (int t = threadIdx.x; t < F * half; t += blockDim.x) {
+      const int fl = t / half, k2 = t - fl * half;
+      const int i = (k2 / len) * 2 * len + (k2 % len);
+      double* x = wbuf + fl * n;
+      const double u = x[i], v = x[i + len];
+      x[i] = u + v;
+      x[i + len] = u - v;
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < F * n; t += blockDim.x) {
+    int fl, i;
+    if (contig) {
+      fl = t / n;
+      i = t - fl * n;
+    } else {
+      i = t / F;
+      fl = t - i * F;
+    }
+    if (fl >= cnt) continue;
+    double v = wbuf[fl * n + i] * scale;
+    if (!forward && sign) v = v * sign[i];
+    out[dct::fib_addr(f0 + fl, i, st, n)] = v;
+  }
+}
+
 __global__ void reduce_rhs_kernel(const double* __restrict__ part, int ks, i64 in, int r,
                                   double* __restrict__ out) {
   const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -81,6 +140,17 @@ DctPlan make_dct_plan(int n) {
   return p;
 }
 
+DctPlan make_mix_plan(int kind, int n) {
+  if (kind == 2) {
+    if (n < 1 || (n & (n - 1)) != 0) throw InvalidArgument("wht requires power-of-two mode lengths");
+    DctPlan p;
+    p.kind = 2;
+    p.n = n;
+    return p;
+  }
+  return make_dct_plan(n);
+}
+
 void free_dct_plan(DctPlan& p) {
   if (p.tw) cudaFree(p.tw);
   if (p.phase) cudaFree(p.phase);
@@ -107,6 +177,7 @@ int dct_fibers_per_cta(int n, size_t budget) {
 }
 
 void prepare_mode_transform(const DctPlan& p, i64 st, i64 nfib, int forward) {
+  if (p.kind == 2) return;
   if (nfib >= 4096 && mix_pass_supported(p)) launch_mix_pass(p, nullptr, nullptr, st, nfib, nullptr, forward, nullptr, true);
 }
 
@@ -114,6 +185,21 @@ void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 
                            const double* sign, int forward, const double* col_div,
                            cudaStream_t stream) {
   if (nfib <= 0) return;
+  if (p.kind == 2) {
+    int F = static_cast<int>((96 * 1024) / (8 * static_cast<size_t>(p.n)));
+    F = F > 32 ? 32 : (F < 1 ? 1 : F);
+    const size_t smem = static_cast<size_t>(F) * p.n * sizeof(double);
+    static size_t configured = 0;
+    if (smem > configured) {
+      CPB_CUDA(cudaFuncSetAttribute(wht_mode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      configured = smem;
+    }
+    const double scale = 1.0 / std::sqrt(static_cast<double>(p.n));
+    wht_mode_kernel<<<static_cast<unsigned>((nfib + F - 1) / F), kMixThreads, smem, stream>>>(
+        p.n, in, out, st, nfib, F, sign, forward, col_div, scale);
+    CPB_LAUNCH_CHECK();
+    return;
+  }
   if (nfib >= 4096 && col_div == nullptr && in == out && mix_pass_supported(p)) {
     launch_mix_pass(p, in, out, st, nfib, sign, forward, stream);  // whole-tensor pass
     return;

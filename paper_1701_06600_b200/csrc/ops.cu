@@ -85,9 +85,8 @@ std::vector<double> row_major(const double* cm, i64 rows, int r) {
 }
 
 void require_transform(int transform) {
-  if (transform == 1 || transform == 3) return;
-  if (transform == 0) throw Unsupported("FFT (complex) mixing is not on the B200 path yet; use dct");
-  if (transform == 2) throw Unsupported("WHT mixing is not on the B200 path yet; use dct");
+  if (transform == 1 || transform == 2 || transform == 3) return;
+  if (transform == 0) throw Unsupported("the operator-level FFT mixing entry points are complex; use cprand_solve");
   throw InvalidArgument("unknown transform kind");
 }
 
@@ -167,7 +166,7 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
   if (mix) {
     signs = mixing_signs(dims, transform, mix_seed);
     for (int k = 0; k < n; ++k) {
-      plans.push_back(make_dct_plan(static_cast<int>(dims[static_cast<size_t>(k)])));
+      plans.push_back(make_mix_plan(transform, static_cast<int>(dims[static_cast<size_t>(k)])));
       dsigns.push_back(std::make_unique<DBuf>(signs[static_cast<size_t>(k)].size() * sizeof(double)));
       h2d(dsigns.back()->p, signs[static_cast<size_t>(k)].data(), signs[static_cast<size_t>(k)].size());
     }
@@ -333,7 +332,7 @@ void op_transform_tensor(const double* x, const std::vector<i64>& dims, int tran
   DBuf dx(p * sizeof(double));
   h2d(dx.p, x, static_cast<size_t>(p));
   for (size_t m = 0; m < dims.size(); ++m) {
-    DctPlan pl = make_dct_plan(static_cast<int>(dims[m]));
+    DctPlan pl = make_mix_plan(transform, static_cast<int>(dims[m]));
     DBuf ds(signs[m].size() * sizeof(double));
     h2d(ds.p, signs[m].data(), signs[m].size());
     launch_mode_transform(pl, dx.as<double>(), dx.as<double>(), st[m], p / dims[m], ds.as<double>(), 1, nullptr,
@@ -355,7 +354,7 @@ void op_transform_factor(const double* a, i64 rows, int r, const std::vector<i64
     return;
   }
   auto signs = mixing_signs(dims, transform, seed);
-  DctPlan pl = make_dct_plan(static_cast<int>(rows));
+  DctPlan pl = make_mix_plan(transform, static_cast<int>(rows));
   DBuf da(static_cast<size_t>(rows * r) * sizeof(double)), ds(rows * sizeof(double));
   h2d(da.p, a, static_cast<size_t>(rows * r));
   h2d(ds.p, signs[static_cast<size_t>(mode)].data(), static_cast<size_t>(rows));
@@ -377,7 +376,7 @@ void op_unmix_rows(const double* g, i64 s, i64 in, const std::vector<i64>& dims,
     return;
   }
   auto signs = mixing_signs(dims, transform, seed);
-  DctPlan pl = make_dct_plan(static_cast<int>(in));
+  DctPlan pl = make_mix_plan(transform, static_cast<int>(in));
   DBuf dg(static_cast<size_t>(s * in) * sizeof(double)), ds(in * sizeof(double));
   h2d(dg.p, g, static_cast<size_t>(s * in));
   h2d(ds.p, signs[static_cast<size_t>(mode)].data(), static_cast<size_t>(in));
@@ -391,7 +390,7 @@ void op_unmix_rows(const double* g, i64 s, i64 in, const std::vector<i64>& dims,
 // mix_tensor (mixing.hpp:130-156) in place on a device tensor: per mode,
 // sign then orthonormal DCT-II; ms[mode] = CUDA-event time of that pass.
 void op_tensor_mix(Tensor* t, int transform, std::uint64_t seed, double* ms) {
-  if (transform != 1) throw Unsupported("in-place device mixing supports the dct transform");
+  if (transform != 1 && transform != 2) throw Unsupported("in-place device mixing supports the dct and wht transforms");
   CPB_CUDA(cudaSetDevice(t->device));
   const auto signs = mixing_signs(t->dims, transform, seed);
   cudaEvent_t e0, e1;
@@ -400,7 +399,7 @@ void op_tensor_mix(Tensor* t, int transform, std::uint64_t seed, double* ms) {
   for (size_t n = 0; n < t->dims.size(); ++n) {
     DBuf sg(signs[n].size() * sizeof(double));
     h2d(sg.p, signs[n].data(), signs[n].size());
-    DctPlan plan = make_dct_plan(static_cast<int>(t->dims[n]));
+    DctPlan plan = make_mix_plan(transform, static_cast<int>(t->dims[n]));
     prepare_mode_transform(plan, t->strides[n], t->p / t->dims[n], 1);
     CPB_CUDA(cudaDeviceSynchronize());
     CPB_CUDA(cudaEventRecord(e0, nullptr));

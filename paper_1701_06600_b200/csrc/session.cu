@@ -256,13 +256,13 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
     if (method == 3 && transform_ == 0)
       throw InvalidArgument("premix requires a real orthogonal transform");
     if (transform_ == 0) cmix_ = true;  // complex mixing (cfft.cu)
-    if (transform_ == 2) throw Unsupported("WHT mixing is not on the B200 path yet; use dct");
   }
   if (order_ > kMaxOrder) throw Unsupported("tensor order > 8");
   if (r > kMaxRank) throw Unsupported("rank > 64 is not supported by the fused sm_100a kernels");
   if (o_.init == 1) throw Unsupported("hosvd init is outside the randomized B200 path");
-  mix_ = (method == 2 && transform_ == 1);
-  premix_ = (method == 3 && transform_ == 1);
+  // real orthogonal kinds (DCT-II, WHT) share the real MIX / PREMIX path
+  mix_ = (method == 2 && (transform_ == 1 || transform_ == 2));
+  premix_ = (method == 3 && (transform_ == 1 || transform_ == 2));
   dims_ = x->dims;
   strides_ = x->strides;
   p_ = x->p;
@@ -517,7 +517,10 @@ void Session::setup_fused() {
   // the MIX kernel also reads strided modes without a replica in place
   // (one 8-byte load per element); the CPRAND kernel's tiles need every
   // mode contiguous
-  if (o_.fused == 0 || (!all_direct && !mix_) || o_.exhaustive_samples || shard_ || cmix_) return;
+  // the MIX kernel's in-kernel transforms are DCT-II: WHT runs the chain
+  if (o_.fused == 0 || (!all_direct && !mix_) || o_.exhaustive_samples || shard_ || cmix_ ||
+      (mix_ && transform_ == 2))
+    return;
   i64 max_dim = 1;
   for (i64 d : dims_) max_dim = std::max(max_dim, d);
   int zcap = 0;
@@ -992,7 +995,7 @@ void Session::mix_setup() {
     signs_.push_back(dalloc<double>(static_cast<size_t>(dims_[static_cast<size_t>(n)])));
     CPB_CUDA(cudaMemcpyAsync(signs_.back(), signs_host_[static_cast<size_t>(n)].data(),
                              sizeof(double) * dims_[static_cast<size_t>(n)], cudaMemcpyHostToDevice, stream_));
-    plans_.push_back(make_dct_plan(static_cast<int>(dims_[static_cast<size_t>(n)])));
+    plans_.push_back(make_mix_plan(transform_, static_cast<int>(dims_[static_cast<size_t>(n)])));
   }
   if (o_.x_mutable) {
     xsolve_ = x_->d;

@@ -319,6 +319,33 @@ def test_fft_mix_free_running_stop_rule(pb, orc):
     assert abs(got.trace[-1][2] - ref.trace[-1][2]) < 1e-6
 
 
+@pytest.mark.parametrize("method", ["mix", "premix"])
+def test_wht_mix_end_to_end_matches_oracle(pb, orc, method):
+    """Walsh-Hadamard mixing (power-of-two modes): the real MIX / PREMIX path
+    with the WHT kind follows the oracle's trajectory."""
+    x, _ = orc.gen_baseline((16, 8, 32, 4), 3, 0.8, 0.01, 17)
+    opts = dict(rng_seed=17, max_iters=15, transform="wht", stall_limit=1000)
+    ref = orc.solve(method, x, 3, 60, orc.SolveOptions(**opts))
+    got = pb.solve(method, x, 3, 60, pb.SolveOptions(**opts))
+    assert got.iterations == ref.iterations
+    assert max(abs(a[2] - b[2]) for a, b in zip(got.trace, ref.trace)) < 1e-7
+    for a, b in zip(got.factors, ref.factors):
+        assert rel(a, b) < 1e-6
+
+
+def test_wht_operators_bit_exact(pb, orc):
+    """WHT mix_tensor / mix_factor / unmix: the reference's butterfly order and
+    scale, so the device results equal the oracle's bit for bit."""
+    dims = (32, 16, 64)
+    x = orc.random_tensor(dims, 4)
+    assert np.array_equal(pb.mix_tensor(x, "wht", 9), orc.mix_tensor(x, "wht", 9))
+    a = np.asfortranarray(np.random.default_rng(1).standard_normal((16, 5)))
+    assert np.array_equal(pb.mix_factor(a, dims, "wht", 9, 1), orc.mix_factor(a, dims, "wht", 9, 1))
+    assert np.array_equal(pb.unmix_factor(a, dims, "wht", 9, 1), orc.unmix_factor(a, dims, "wht", 9, 1))
+    with pytest.raises(pb.InvalidArgument):
+        pb.cprand_mix(orc.random_tensor((6, 8, 8), 2), 2, 10, pb.SolveOptions(transform="wht"))
+
+
 def test_mixed_solver_recovers(pb, orc):
     g = orc.Engine(931, raw=True)
     fs = [g.matrix(d, 2, 0.1, 1.0) for d in (10, 9, 8)]
