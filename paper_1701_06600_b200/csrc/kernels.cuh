@@ -181,6 +181,8 @@ void launch_reduce_rhs(const double* part_rhs, int ks, i64 in, int r, double* ou
 
 // ---- slab sharding (shard.cu) ---------------------------------------------
 void launch_gather_z_rows(const double* z, const int* idx, int cnt, int rt, double* out, cudaStream_t st);
+// slab [M][L] <-> P row blocks packed back to back (distributed last-mode mixing)
+void launch_slab_blocks(double* x, double* buf, i64 m, i64 l, i64 mb, int pack, cudaStream_t st);
 int apply_rows_grid(i64 rows, int r);
 void launch_apply_rows(i64 rows, int r, const double* rhs, const double* ginv, double* a_out, double* ssq_part,
                        cudaStream_t st);

@@ -274,7 +274,8 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
     nccl_ = o_.nccl;
     nranks_ = o_.nranks;
     rank_ = o_.rank;
-    if (method != 1) throw Unsupported("slab sharding covers the cprand method (rand)");
+    if (method != 1 && !(method == 2 && (transform_ == 1 || transform_ == 2)))
+      throw Unsupported("slab sharding covers cprand and cprand_mix with a real transform (dct, wht)");
     if (o_.exhaustive_samples || o_.exact_fit_trace) throw Unsupported("exhaustive / exact-fit runs are not sharded");
     if (order_ < 2) throw InvalidArgument("slab sharding needs a tensor of order >= 2");
     const i64 total = o_.shard_total > 0 ? o_.shard_total : tdims_.back();
@@ -371,7 +372,8 @@ Session::~Session() {
   dfree(fit_part_);
   dfree(state_);
   dfree(trace_dev_);
-  if (xcopy_) big_free(xcopy_, static_cast<size_t>(p_) * sizeof(double));
+  if (xcopy_) big_free(xcopy_, static_cast<size_t>(tp_) * sizeof(double));
+  dfree(rhs_gather_);
   xcopy_ = nullptr;
   if (stop_host_) cudaFreeHost(stop_host_);
   for (auto& e : it_events_) cudaEventDestroy(e);
@@ -492,6 +494,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   CPB_CUDA(cudaMemsetAsync(tickets_, 0, 8 * sizeof(unsigned), stream_));
   ssq_ = dalloc<double>(static_cast<size_t>(std::max<i64>(max_apply, 4 * sms_) * r_));
   if (mix_ || shard_ || cmix_) rhs_full_ = dalloc<double>(static_cast<size_t>(max_in * r_));
+  if (shard_ && mix_) rhs_gather_ = dalloc<double>(static_cast<size_t>(lmax_ * nranks_ * r_));
   if (cmix_) {
     zc_ = dalloc<double>(static_cast<size_t>(2 * max_s * r_));
     cbuf_ = dalloc<double>(static_cast<size_t>(2 * max_in * r_));
@@ -737,6 +740,60 @@ void Session::allgather(double* buf, i64 per_rank) {
   if (r != ncclSuccess) throw CudaError(std::string("ncclAllGather: ") + ncclGetErrorString(r));
 }
 
+// mix_tensor's last mode on a slab-sharded tensor: the
+// slab [M][L] (M = the leading modes' product) is cut into P row blocks;
+// one all-to-all gives every rank its row block with the whole last mode
+// ([Mb][I_N], fibers at stride Mb), the transform runs locally, and the
+// reverse all-to-all puts the mixed slab back.
+void Session::mix_last_mode_sharded() {
+  const int N = order_;
+  const i64 L = tdims_[static_cast<size_t>(N - 1)], total = dims_[static_cast<size_t>(N - 1)];
+  i64 M = 1;
+  for (int k = 0; k < N - 1; ++k) M *= tdims_[static_cast<size_t>(k)];
+  const int P = nranks_;
+  const i64 mb = (M + P - 1) / P;
+  auto mq = [&](int q) { return std::max<i64>(0, std::min(M, static_cast<i64>(q + 1) * mb) - static_cast<i64>(q) * mb); };
+  auto lp = [&](int q) {
+    return std::max<i64>(0, std::min(total, static_cast<i64>(q + 1) * lmax_) - static_cast<i64>(q) * lmax_);
+  };
+  const i64 mine = mq(rank_);
+  double* buf = static_cast<double*>(big_alloc(static_cast<size_t>(std::max<i64>(1, M * L)) * sizeof(double)));
+  double* wk = static_cast<double*>(big_alloc(static_cast<size_t>(std::max<i64>(1, mine * total)) * sizeof(double)));
+  const auto comm = static_cast<ncclComm_t>(nccl_);
+  auto nccl_ok = [](ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw CudaError(std::string(what) + ": " + ncclGetErrorString(r));
+  };
+  launch_slab_blocks(xsolve_, buf, M, L, mb, 1, stream_);
+  nccl_ok(ncclGroupStart(), "ncclGroupStart");
+  for (int q = 0; q < P; ++q)
+    if (mq(q) * L > 0)
+      nccl_ok(ncclSend(buf + static_cast<i64>(q) * mb * L, static_cast<size_t>(mq(q) * L), ncclDouble, q, comm, stream_),
+              "ncclSend");
+  for (int q = 0; q < P; ++q)
+    if (mine * lp(q) > 0)
+      nccl_ok(ncclRecv(wk + mine * static_cast<i64>(q) * lmax_, static_cast<size_t>(mine * lp(q)), ncclDouble, q, comm,
+                       stream_),
+              "ncclRecv");
+  nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+  const size_t k = static_cast<size_t>(N - 1);
+  if (mine > 0) launch_mode_transform(plans_[k], wk, wk, mine, mine, signs_[k], 1, nullptr, stream_);
+  nccl_ok(ncclGroupStart(), "ncclGroupStart");
+  for (int q = 0; q < P; ++q)
+    if (mine * lp(q) > 0)
+      nccl_ok(ncclSend(wk + mine * static_cast<i64>(q) * lmax_, static_cast<size_t>(mine * lp(q)), ncclDouble, q, comm,
+                       stream_),
+              "ncclSend");
+  for (int q = 0; q < P; ++q)
+    if (mq(q) * L > 0)
+      nccl_ok(ncclRecv(buf + static_cast<i64>(q) * mb * L, static_cast<size_t>(mq(q) * L), ncclDouble, q, comm, stream_),
+              "ncclRecv");
+  nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+  launch_slab_blocks(xsolve_, buf, M, L, mb, 0, stream_);
+  CPB_CUDA(cudaStreamSynchronize(stream_));
+  big_free(buf, static_cast<size_t>(std::max<i64>(1, M * L)) * sizeof(double));
+  big_free(wk, static_cast<size_t>(std::max<i64>(1, mine * total)) * sizeof(double));
+}
+
 // One mode of the slab-sharded loop: Z_S, the Gram and its
 // inverse are replicated; the RHS contracts only this rank's fibers.
 //  n < N-1: fibers of the samples whose last-mode index is in the slab;
@@ -779,9 +836,24 @@ void Session::enqueue_mode_sharded(int it, int n, const int* stop) {
     CPB_CUDA(cudaMemsetAsync(rhs_full_, 0, sizeof(double) * in_loc * r_, stream_));
   }
   CPB_CUDA(cudaStreamWaitEvent(stream_, ev_inv_, 0));
+  const size_t k = static_cast<size_t>(n);
   if (!last) {
-    allreduce_sum(rhs_full_, dims_[static_cast<size_t>(n)] * r_);
+    allreduce_sum(rhs_full_, dims_[k] * r_);
+    // MIX (mixing.hpp:291-298): unmix the summed RHS rows, solve, mix the new factor
+    if (mix_) launch_mode_transform(plans_[k], rhs_full_, rhs_full_, r_, r_, signs_[k], 0, nullptr, stream_);
     timed(n, 5, stream_, [&] { launch_mode_apply(v.in, r_, w, rhs_full_, n == 0, rng_state_, stream_); });
+    if (mix_) launch_mode_transform(plans_[k], fac_[k], mixed_[k], r_, r_, signs_[k], 1, w.norms, stream_);
+  } else if (mix_) {
+    // the RHS rows of every slab on every rank, unmixed along the whole mode,
+    // then the same replicated solve as the other modes
+    const i64 total = dims_[k];
+    if (slab_len_ > 0)
+      CPB_CUDA(cudaMemcpyAsync(rhs_gather_ + slab_off_ * r_, rhs_full_, sizeof(double) * slab_len_ * r_,
+                               cudaMemcpyDeviceToDevice, stream_));
+    allgather(rhs_gather_, lmax_ * r_);
+    launch_mode_transform(plans_[k], rhs_gather_, rhs_gather_, r_, r_, signs_[k], 0, nullptr, stream_);
+    timed(n, 5, stream_, [&] { launch_mode_apply(total, r_, w, rhs_gather_, n == 0, rng_state_, stream_); });
+    launch_mode_transform(plans_[k], fac_[k], mixed_[k], r_, r_, signs_[k], 1, w.norms, stream_);
   } else {
     const int g = apply_rows_grid(std::max<i64>(slab_len_, 1), r_);
     double* ssq = sh_part_ + static_cast<i64>(g) * r_;
@@ -1000,14 +1072,22 @@ void Session::mix_setup() {
   if (o_.x_mutable) {
     xsolve_ = x_->d;
   } else {
-    xcopy_ = static_cast<double*>(big_alloc(static_cast<size_t>(p_) * sizeof(double)));
-    CPB_CUDA(cudaMemcpyAsync(xcopy_, x_->d, sizeof(double) * p_, cudaMemcpyDeviceToDevice, stream_));
+    xcopy_ = static_cast<double*>(big_alloc(static_cast<size_t>(tp_) * sizeof(double)));
+    CPB_CUDA(cudaMemcpyAsync(xcopy_, x_->d, sizeof(double) * tp_, cudaMemcpyDeviceToDevice, stream_));
     xsolve_ = xcopy_;
   }
-  // mix_tensor (mixing.hpp:130-156): per mode, sign then DCT-II, in place
-  for (int n = 0; n < order_; ++n)
-    launch_mode_transform(plans_[static_cast<size_t>(n)], xsolve_, xsolve_, strides_[static_cast<size_t>(n)],
-                          p_ / dims_[static_cast<size_t>(n)], signs_[static_cast<size_t>(n)], 1, nullptr, stream_);
+  // mix_tensor (mixing.hpp:130-156): per mode, sign then the transform, in
+  // place; sharded: the slab holds whole fibers of modes < N-1, mode N-1
+  // crosses the slabs (mix_last_mode_sharded)
+  for (int n = 0; n < order_; ++n) {
+    const size_t k = static_cast<size_t>(n);
+    if (shard_ && n == order_ - 1) {
+      mix_last_mode_sharded();
+      continue;
+    }
+    if (tp_ > 0)
+      launch_mode_transform(plans_[k], xsolve_, xsolve_, tstrides_[k], tp_ / tdims_[k], signs_[k], 1, nullptr, stream_);
+  }
   if (mix_) {
     for (int n = 0; n < order_; ++n) {
       const i64 rows = dims_[static_cast<size_t>(n)];

@@ -121,6 +121,7 @@ class Session {
   void allreduce_sum(double* buf, i64 n);
   void allgather(double* buf, i64 per_rank);
   void enqueue_mode_sharded(int it, int n, const int* stop);
+  void mix_last_mode_sharded();  // mode N-1 of mix_tensor across the slabs (two all-to-alls)
   void collect_kernel_times();
   cudaEvent_t timing_event();
 
@@ -131,7 +132,8 @@ class Session {
   Options o_;
   int transform_ = -1;
   bool mix_ = false, premix_ = false;
-  bool cmix_ = false;  // cprand_mix with the FFT kind (complex mixing, cfft.cu)
+  bool cmix_ = false;
+  double* rhs_gather_ = nullptr;    // sharded MIX: P * lmax rows of the last mode's RHS  // cprand_mix with the FFT kind (complex mixing, cfft.cu)
   double* xc_ = nullptr;            // complex X_hat (interleaved), P pairs
   std::vector<double*> mixedc_;     // complex mixed factors, I_n x R row-major pairs
   double* zc_ = nullptr;            // complex Z_S, S x R pairs

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Kernels of the slab-sharded CPRAND loop (one process per GPU, tensor split
 // along its last mode). The collectives between them are NCCL
 // calls on the session stream (session.cu).
@@ -113,6 +114,33 @@ __global__ void gather_values_masked_kernel(const double* __restrict__ x, const 
 }
 
 }  // namespace
+
+// Block transpose for the distributed last-mode transform: the slab X
+// (column-major [M][L], M = product of the leading modes) cut into P row
+// blocks q = [q Mb, min(M, (q+1) Mb)); block q is packed contiguously
+// ([Mq][L], column-major) at offset q Mb L of buf. unpack is the inverse.
+__global__ void slab_blocks_kernel(double* __restrict__ x, double* __restrict__ buf, i64 m, i64 l, i64 mb,
+                                   int pack) {
+  const i64 tot = m * l;
+  for (i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; e < tot;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 col = e / m, row = e - col * m;
+    const i64 q = row / mb, mq = min(mb, m - q * mb);
+    const i64 b = q * mb * l + col * mq + (row - q * mb);
+    if (pack)
+      buf[b] = x[e];
+    else
+      x[e] = buf[b];
+  }
+}
+
+void launch_slab_blocks(double* x, double* buf, i64 m, i64 l, i64 mb, int pack, cudaStream_t st) {
+  const i64 tot = m * l;
+  if (tot == 0) return;
+  const int grid = static_cast<int>(std::min<i64>((tot + 255) / 256, 148 * 16));
+  slab_blocks_kernel<<<grid, 256, 0, st>>>(x, buf, m, l, mb, pack);
+  CPB_LAUNCH_CHECK();
+}
 
 void launch_gather_z_rows(const double* z, const int* idx, int cnt, int rt, double* out, cudaStream_t st) {
   const i64 n = static_cast<i64>(cnt) * rt;

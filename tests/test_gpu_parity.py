@@ -493,8 +493,40 @@ def test_sharded_session_rejects_bad_slab(pb):
     t.synth(3, 0.0, 0.0, 1)
     with pytest.raises(pb.InvalidArgument):
         pb.Session("rand", t, 3, 20, pb.SolveOptions(comm=comm, shard_total=20))
-    with pytest.raises(pb.UnsupportedOnDevice):
-        pb.Session("mix", t, 3, 20, pb.SolveOptions(comm=comm, shard_total=8, transform="dct"))
+    with pytest.raises(pb.UnsupportedOnDevice):  # complex mixing is not sharded
+        pb.Session("mix", t, 3, 20, pb.SolveOptions(comm=comm, shard_total=8, transform="fft"))
+    comm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transform", ["dct", "wht"])
+def test_sharded_mix_session_single_rank(pb, orc, transform):
+    """Slab-sharded CPRAND-MIX through NCCL with one rank: the distributed
+    mixing pass (block pack, send/recv group, last-mode transform, reverse
+    exchange, unpack), local-sample RHS + allreduce, the last mode's RHS
+    slab rows allgathered and unmixed, replicated solve and mixed factors.
+    Reproduces the unsharded chain and tracks the oracle's cprand_mix."""
+    dims, r, s = (16, 8, 32), 3, 60
+    comm = pb.Comm(pb.Comm.unique_id(), 0, 1, 0)
+    t1 = pb.DeviceTensor(dims)
+    t1.synth(r, 0.5, 0.01, 9)
+    t2 = pb.DeviceTensor(dims)
+    t2.synth_slab(r, 0.5, 0.01, 9, dims[-1], comm)
+    base = dict(rng_seed=9, max_iters=12, stall_limit=1000, transform=transform)
+    full = pb.Session("mix", t1, r, s, pb.SolveOptions(fused=0, **base))
+    full.run(12)
+    ref = full.result()
+    sh = pb.Session("mix", t2, r, s, pb.SolveOptions(comm=comm, shard_total=dims[-1], **base))
+    sh.run(12)
+    got = sh.result()
+    assert got.iterations == ref.iterations
+    for a, b in zip(got.factors, ref.factors):
+        assert rel(a, b) < 1e-10
+    assert max(abs(a[2] - b[2]) for a, b in zip(got.trace, ref.trace)) < 1e-10
+    o = orc.solve("mix", t1.download(), r, s, orc.SolveOptions(**base))
+    assert max(abs(a[2] - b[2]) for a, b in zip(got.trace, o.trace)) < 1e-8
+    for h in (sh, full):
+        h.close()
     comm.close()
 
 
