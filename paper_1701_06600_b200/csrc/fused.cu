@@ -243,10 +243,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
     __syncthreads();
     if (tid == 0) s_last = (atomicAdd(&A.ticket[1], 1u) == G - 1u);
     __syncthreads();
-    if (s_last && tid == 0) {
+    if (s_last) {  // the last CTA: every partial is written
       __threadfence();
-      A.ticket[1] = 0u;
-      ph::fit_final(f, nvb);
+      if (tid == 0) A.ticket[1] = 0u;
+      ph::fit_final(f, nvb, red);
     }
   }
 }
@@ -576,6 +576,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
     }
     if (A.has_fit && !is_inv) wait_geq(L.nready + (b % kRep) * kCS, seq, 64);
   }
+  // debug stamps of the tail (slot 14 of modes 0..2: norms seen, fit block, fit final)
+  if (A.phase_t && b == 0 && tid == 0) A.phase_t[14] = globaltimer();
   // ---- sampled fit + stop rule (sampling.hpp:191-210, :237-251)
   if (A.has_fit) {
     const FitArgs& f = A.fit;
@@ -585,14 +587,16 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       const double part = ph::fit_block(f, vb, red);
       if (tid == 0) f.partials[vb] = part;
     }
+    if (A.phase_t && b == 0 && tid == 0 && A.order > 1) A.phase_t[16 + 14] = globaltimer();
     __threadfence();
     __syncthreads();
     if (tid == 0) s_last = (atomicAdd(&A.ticket[1], 1u) == G - 1u);
     __syncthreads();
-    if (s_last && tid == 0) {
+    if (s_last) {  // the last CTA: every partial is written
       __threadfence();
-      A.ticket[1] = 0u;
-      ph::fit_final(f, nvb);
+      if (tid == 0) A.ticket[1] = 0u;
+      ph::fit_final(f, nvb, red);
+      if (A.phase_t && A.order > 2 && tid == 0) A.phase_t[32 + 14] = globaltimer();
     }
   }
 }
@@ -621,7 +625,7 @@ size_t rand_smem_for(int zcap) {
   need = std::max<i64>(need, static_cast<i64>(RT) * (RT + 1) + 2 * static_cast<i64>(tl::BM) * (RT + 1));
   need = std::max<i64>(need, 48 * RT + 256);
   need = std::max<i64>(need, static_cast<i64>(kFusedThreads / RT) * (RT + 1));
-  need = std::max<i64>(need, 256);
+  need = std::max<i64>(need, ph::kFitSmemDoubles);
   return static_cast<size_t>(need) * sizeof(double);
 }
 
@@ -664,7 +668,7 @@ size_t fused_smem_bytes(int rt, bool mix, int max_dim) {
   need = std::max(need, static_cast<size_t>(ph::GS * rt) * sizeof(double));
   need = std::max(need, static_cast<size_t>(rt * (rt + 1) + (kFusedThreads / rt) * (rt + 1)) * sizeof(double));
   need = std::max(need, static_cast<size_t>(16 * rt + 40) * sizeof(double));
-  need = std::max(need, static_cast<size_t>(256) * sizeof(double));
+  need = std::max(need, static_cast<size_t>(ph::kFitSmemDoubles) * sizeof(double));
   if (mix) need = std::max(need, static_cast<size_t>(2) * 16 * static_cast<size_t>(max_dim));
   return need;
 }

@@ -142,7 +142,7 @@ __global__ void stamp_start_kernel(FitState* s) {
 
 __global__ void __launch_bounds__(kThreads) estimate_fit_kernel(FitArgs a) {
   if (a.state->stopped) return;
-  __shared__ double red[kThreads];
+  __shared__ double red[ph::kFitSmemDoubles];
   __shared__ bool s_last;
   const double part = ph::fit_block(a, blockIdx.x, red);
   if (threadIdx.x == 0) {
@@ -151,10 +151,10 @@ __global__ void __launch_bounds__(kThreads) estimate_fit_kernel(FitArgs a) {
     s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1u);
   }
   __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
+  if (!s_last) return;
   __threadfence();
-  *a.ticket = 0u;
-  ph::fit_final(a, gridDim.x);
+  if (threadIdx.x == 0) *a.ticket = 0u;
+  ph::fit_final(a, gridDim.x, red);
 }
 
 }  // namespace

@@ -1548,27 +1548,85 @@ __device__ unsigned long long norms_final(int r, i64 in, const ModeWork& w, int 
 // Squared error over the 256 sampled entries of virtual block vb (one
 // thread per entry, fixed tree reduction); model_entry kruskal.hpp:37-44.
 // red: 256 doubles. Result valid in thread 0.
-__device__ inline double fit_block(const FitArgs& a, i64 vb, double* red) {
-  const i64 j = vb * 256 + threadIdx.x;
-  double e2 = 0.0;
-  if (j < a.phat) {
-    double sum = 0.0;
-    for (int q = 0; q < a.r; ++q) {
-      double p = __ldcg(a.lambda + q);
-      for (int n = 0; n < a.order; ++n) {
-        double f = __ldcg(a.fac[n] + static_cast<i64>(a.idx[n][j]) * a.r + q);
-        if (a.nrm[n]) f = f / __ldcg(a.nrm[n] + q);
-        p = __dmul_rn(p, f);
-      }
-      sum = __dadd_rn(sum, p);
-    }
-    const double e = a.values[j] - sum;
-    e2 = e * e;
+// 256 sampled entries per block: 32 groups of 8 lanes, each group takes 8
+// entries, U at a time. A group reads an entry's factor rows with its 8
+// lanes on consecutive columns (q = lane, lane + 8, ...: 64-byte runs, so a
+// warp load touches 4-8 sectors, not 32 lines), each lane multiplies its
+// columns, the group sums them with three shuffles. The model value is
+// sum_q lambda_q prod_n A_un(i_n, q) / norm_n(q) (kruskal.hpp:37-44,
+// sampling.hpp:191-210); the column scale lambda_q / prod_n norm_n(q) is
+// formed once per block in shared memory (red[256..]), so a term costs N
+// multiplies instead of N divisions (a reassociation: the estimate agrees
+// with the reference's to a few ulp). red: 256 + 64 doubles.
+template <int KM, int QC, int U>
+__device__ inline double fit_block_t(const FitArgs& a, i64 vb, double* red) {
+  const int r = a.r, N = a.order;
+  double* s_sc = red + 256;  // [64]
+  for (int q = threadIdx.x; q < r; q += blockDim.x) {
+    double den = 1.0;
+    for (int n = 0; n < N; ++n)
+      if (a.nrm[n]) den *= __ldcg(a.nrm[n] + q);
+    s_sc[q] = __ldcg(a.lambda + q) / den;
   }
-  red[threadIdx.x] = e2;
+  const double* fac[KM];
+#pragma unroll
+  for (int n = 0; n < KM; ++n) fac[n] = n < N ? a.fac[n] : nullptr;
   __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+  const int grp = threadIdx.x / 8, l = threadIdx.x % 8;
+  double part = 0.0;  // lane 0: the group's squared residuals, entries in order
+  for (int k = 0; k < 8; k += U) {
+    i64 row[U][KM];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const i64 j = vb * 256 + grp * 8 + k + u;
+      ok[u] = j < a.phat;
+#pragma unroll
+      for (int n = 0; n < KM; ++n) row[u][n] = (ok[u] && n < N) ? static_cast<i64>(__ldg(a.idx[n] + j)) * r : 0;
+    }
+    double s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) s[u] = 0.0;
+    for (int q0 = l; q0 < r; q0 += 8 * QC) {
+      double f[U][QC][KM];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int c = 0; c < QC; ++c)
+#pragma unroll
+          for (int n = 0; n < KM; ++n)
+            f[u][c][n] = (ok[u] && n < N && q0 + 8 * c < r) ? __ldcg(fac[n] + row[u][n] + q0 + 8 * c) : 1.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int c = 0; c < QC; ++c) {
+          const int q = q0 + 8 * c;
+          if (q >= r) break;
+          double p = s_sc[q];
+#pragma unroll
+          for (int n = 0; n < KM; ++n) {
+            if (n >= N) break;
+            p = __dmul_rn(p, f[u][c][n]);
+          }
+          s[u] = __dadd_rn(s[u], p);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double v = s[u];
+      v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 4));
+      v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 2));
+      v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 1));
+      if (ok[u]) {
+        const double e = a.values[vb * 256 + grp * 8 + k + u] - v;
+        part += e * e;
+      }
+    }
+  }
+  red[threadIdx.x] = (l == 0) ? part : 0.0;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
     __syncthreads();
   }
   const double out = red[0];
@@ -1576,11 +1634,28 @@ __device__ inline double fit_block(const FitArgs& a, i64 vb, double* red) {
   return out;
 }
 
+constexpr int kFitSmemDoubles = 256 + 64;
+
+__device__ inline double fit_block(const FitArgs& a, i64 vb, double* red) {
+  return a.order <= 4 ? fit_block_t<4, 4, 2>(a, vb, red) : fit_block_t<kMaxOrder, 1, 2>(a, vb, red);
+}
+
 // Fit from the block partials (in order), sampling.hpp:192,207-209, and the
 // stop rule should_stop (sampling.hpp:237-251); one thread.
-__device__ inline void fit_final(const FitArgs& a, i64 nblocks) {
-  double sq = 0.0;
-  for (i64 b = 0; b < nblocks; ++b) sq += a.partials[b];
+// Whole CTA (blockDim 256): the block partials summed by a fixed tree (each
+// thread adds partials t, t + 256, ... in order first); thread 0 then
+// finishes. red: >= 256 doubles of shared memory.
+__device__ inline void fit_final(const FitArgs& a, i64 nblocks, double* red) {
+  double t = 0.0;
+  for (i64 b = threadIdx.x; b < nblocks; b += blockDim.x) t += __ldcg(a.partials + b);
+  red[threadIdx.x] = t;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (static_cast<int>(threadIdx.x) < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  const double sq = red[0];
   double fit;
   if (a.x_norm == 0.0) {
     fit = 1.0;

@@ -1362,6 +1362,12 @@ void Session::enqueue_iteration() {
         }
       }
       ++phase_acc_n_;
+      if (std::getenv("CPRAND_DEBUG_TAIL") && !mix_ && order_ >= 3) {
+        const unsigned long long* q = t.data();
+        const auto us = [&](unsigned long long v) { return v ? 1e-3 * static_cast<double>(v - q[0]) : -1.0; };
+        std::fprintf(stderr, "tail: last mode end %.1f, norms seen %.1f, fit block %.1f, fit final %.1f us\n",
+                     us(q[(order_ - 1) * 16 + 6]), us(q[14]), us(q[16 + 14]), us(q[32 + 14]));
+      }
       if (cta_t_) {  // debug: per-CTA timeline of mode 1 (us after the earliest mode start)
         std::vector<unsigned long long> c(static_cast<size_t>(fgrid_) * 16);
         CPB_CUDA(cudaMemcpy(c.data(), cta_t_, c.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
