@@ -36,3 +36,10 @@ $(DROPIN): tests/cpp/dropin_smoke.cpp include/cprand_b200/cprand.hpp $(LIB)
 	@mkdir -p build
 	g++ -std=c++20 -O2 -Iinclude -o $@ $< -Lpaper_1701_06600_b200 -lcprand_b200 -Wl,-rpath,'$$ORIGIN/../paper_1701_06600_b200'
 .PHONY: dropin
+
+CLI := build/cprand_b200
+cli: $(CLI)
+$(CLI): tools/cprand_b200_cli.cpp include/cprand_b200/cprand.hpp include/cprand_b200/io.hpp $(LIB)
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Iinclude -o $@ $< -Lpaper_1701_06600_b200 -lcprand_b200 -Wl,-rpath,'$$ORIGIN/../paper_1701_06600_b200'
+.PHONY: cli
