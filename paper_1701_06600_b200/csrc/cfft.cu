@@ -17,6 +17,7 @@
 //
 // The FFT is dct.cuh's mixed-radix Stockham (fft_smem) on complex fibers
 // staged in shared memory, unitary scaling 1/sqrt(n) as ModeTransform.
+#include <algorithm>
 #include <cmath>
 
 #include "dct.cuh"
@@ -93,68 +94,63 @@ __global__ void __launch_bounds__(kCThreads) cfft_mode_kernel(PlanArgs p, const 
 
 // Z_S(s, c) = prod over kept modes (ascending) of mixed_m(i_m(s), c), complex
 // (skr, sampling.hpp:74-92, on Mat<Complex>); v.fac[k] = the kept modes'
-// mixed factors, complex row-major [i][c].
-__global__ void zc_kernel(ModeView v, double2* __restrict__ z) {
+// mixed factors, complex row-major [i][c]. Written as the stacked real
+// matrix [Re Z; Im Z] (2S x RT, zero-padded columns): its Gram is
+// Re(Z^H Z), the Gram of real_least_squares' stacked system, so the real
+// path's Gram kernel and inverse run on it unchanged.
+__global__ void zc_kernel(ModeView v, int rt, double* __restrict__ zs) {
   const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= static_cast<i64>(v.s) * v.r) return;
-  const int s = static_cast<int>(e / v.r), c = static_cast<int>(e - static_cast<i64>(s) * v.r);
-  double2 zv = make_double2(1.0, 0.0);
-  for (int k = 0; k < v.kept; ++k) {
-    const double2 a = reinterpret_cast<const double2*>(v.fac[k])[static_cast<i64>(v.rows[k][s]) * v.r + c];
-    zv = dct::cmul(zv, a);
-  }
-  z[e] = zv;
-}
-
-// G = Re(Z^H Z) = Re Z^T Re Z + Im Z^T Im Z, written RT x RT (zero padded) as
-// the single partial the Gram inverse reads
-__global__ void gramc_kernel(const double2* __restrict__ z, int s, int r, int rt, double* __restrict__ g) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= rt * rt) return;
-  const int a = e / rt, c = e - a * rt;
-  double acc = 0.0;
-  if (a < r && c < r)
-    for (int j = 0; j < s; ++j) {
-      const double2 za = z[static_cast<i64>(j) * r + a], zc = z[static_cast<i64>(j) * r + c];
-      acc = fma(za.x, zc.x, acc);
-      acc = fma(za.y, zc.y, acc);
+  if (e >= static_cast<i64>(v.s) * rt) return;
+  const int s = static_cast<int>(e / rt), c = static_cast<int>(e - static_cast<i64>(s) * rt);
+  double2 zv = make_double2(0.0, 0.0);
+  if (c < v.r) {
+    zv = make_double2(1.0, 0.0);
+    for (int k = 0; k < v.kept; ++k) {
+      const double2 a = reinterpret_cast<const double2*>(v.fac[k])[static_cast<i64>(v.rows[k][s]) * v.r + c];
+      zv = dct::cmul(zv, a);
     }
-  g[e] = acc;
+  }
+  zs[static_cast<i64>(s) * rt + c] = zv.x;
+  zs[(static_cast<i64>(v.s) + s) * rt + c] = zv.y;
 }
 
-// C(i, c) = sum_s conj(Z(s, c)) X_hat(base_s + i st): the complex RHS before
-// unmixing, I_n x R row-major. A CTA holds 32 rows i and every column; the
-// Z rows stream through shared memory in chunks.
+// Split-K partials of C(i, c) = sum_s conj(Z(s, c)) X_hat(base_s + i st),
+// the complex RHS before unmixing: CTA (row block of 32, split kb) sums the
+// samples [kb klen, ...) into part[kb] (I_n x R complex row-major). Z is read
+// from the stacked real layout (Re rows 0..S-1, Im rows S..2S-1, ld rt).
 constexpr int kRows = 32;
 constexpr int kZChunk = 32;
 __global__ void __launch_bounds__(kCThreads) rhsc_kernel(const double2* __restrict__ xh, const i64* __restrict__ base,
-                                                          i64 st, i64 in, int s, const double2* __restrict__ z, int r,
-                                                          double2* __restrict__ out) {
-  __shared__ double2 zs[kZChunk * 64];
-  __shared__ double2 xs[kZChunk * kRows];
+                                                          i64 st, i64 in, int s, int klen, const double* __restrict__ zs,
+                                                          int rt, int r, double2* __restrict__ part) {
+  __shared__ double2 zsm[kZChunk * 64];
+  __shared__ double2 xsm[kZChunk * kRows];
   const i64 i0 = static_cast<i64>(blockIdx.x) * kRows;
+  const int sb = blockIdx.y * klen, se = min(s, sb + klen);
   const int tid = threadIdx.x;
-  // thread -> (row il, columns c = cg, cg + 8, ...)
   const int il = tid % kRows, cg = tid / kRows;  // 8 column groups
   double2 acc[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) acc[q] = make_double2(0.0, 0.0);
-  for (int s0 = 0; s0 < s; s0 += kZChunk) {
-    const int cnt = min(kZChunk, s - s0);
-    for (int e = tid; e < cnt * r; e += kCThreads) zs[e] = z[static_cast<i64>(s0) * r + e];
+  for (int s0 = sb; s0 < se; s0 += kZChunk) {
+    const int cnt = min(kZChunk, se - s0);
+    for (int e = tid; e < cnt * r; e += kCThreads) {
+      const int sl = e / r, c = e - sl * r;
+      zsm[e] = make_double2(zs[static_cast<i64>(s0 + sl) * rt + c], zs[static_cast<i64>(s + s0 + sl) * rt + c]);
+    }
     for (int e = tid; e < cnt * kRows; e += kCThreads) {
       const int sl = e / kRows, ii = e - sl * kRows;
       const i64 i = i0 + ii;
-      xs[e] = (i < in) ? xh[base[s0 + sl] + i * st] : make_double2(0.0, 0.0);
+      xsm[e] = (i < in) ? xh[base[s0 + sl] + i * st] : make_double2(0.0, 0.0);
     }
     __syncthreads();
     for (int sl = 0; sl < cnt; ++sl) {
-      const double2 x = xs[sl * kRows + il];
+      const double2 x = xsm[sl * kRows + il];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int c = cg + 8 * q;
         if (c < r) {
-          const double2 zc = zs[sl * r + c];
+          const double2 zc = zsm[sl * r + c];
           // conj(z) * x
           acc[q].x = fma(zc.x, x.x, fma(zc.y, x.y, acc[q].x));
           acc[q].y = fma(zc.x, x.y, fma(-zc.y, x.x, acc[q].y));
@@ -168,8 +164,20 @@ __global__ void __launch_bounds__(kCThreads) rhsc_kernel(const double2* __restri
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int c = cg + 8 * q;
-      if (c < r) out[i * r + c] = acc[q];
+      if (c < r) part[(static_cast<i64>(blockIdx.y) * in + i) * r + c] = acc[q];
     }
+}
+
+// C = sum of the split partials in split order
+__global__ void rhsc_reduce_kernel(const double2* __restrict__ part, int ks, i64 n, double2* __restrict__ out) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double2 a = part[e];
+  for (int k = 1; k < ks; ++k) {
+    const double2 b = part[static_cast<i64>(k) * n + e];
+    a = make_double2(a.x + b.x, a.y + b.y);
+  }
+  out[e] = a;
 }
 
 int fibers_per_cta(int n) {
@@ -198,23 +206,32 @@ void launch_cfft_mode(const DctPlan& pl, const double* in_real, const double* in
   CPB_LAUNCH_CHECK();
 }
 
-void launch_zc(const ModeView& v, double* z, cudaStream_t stream) {
-  const i64 tot = static_cast<i64>(v.s) * v.r;
-  zc_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(v, reinterpret_cast<double2*>(z));
+void launch_zc(const ModeView& v, int rt, double* zs, cudaStream_t stream) {
+  const i64 tot = static_cast<i64>(v.s) * rt;
+  zc_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(v, rt, zs);
   CPB_LAUNCH_CHECK();
 }
 
-void launch_gramc(const double* z, int s, int r, int rt, double* g, cudaStream_t stream) {
-  gramc_kernel<<<(rt * rt + 255) / 256, 256, 0, stream>>>(reinterpret_cast<const double2*>(z), s, r, rt, g);
-  CPB_LAUNCH_CHECK();
+int rhsc_splits(i64 in, int s, int sms) {
+  const i64 rb = (in + kRows - 1) / kRows;
+  i64 ks = std::max<i64>(1, (2 * static_cast<i64>(sms)) / rb);
+  ks = std::min<i64>(ks, (s + kZChunk - 1) / kZChunk);
+  return static_cast<int>(std::max<i64>(1, ks));
 }
 
-void launch_rhsc(const double* xh, const i64* base, i64 st, i64 in, int s, const double* z, int r, double* out,
-                 cudaStream_t stream) {
+void launch_rhsc(const double* xh, const i64* base, i64 st, i64 in, int s, const double* zs, int rt, int r,
+                 double* part, double* out, int sms, cudaStream_t stream) {
   if (r > 64) throw Unsupported("FFT mixing: rank > 64");
-  rhsc_kernel<<<static_cast<unsigned>((in + kRows - 1) / kRows), kCThreads, 0, stream>>>(
-      reinterpret_cast<const double2*>(xh), base, st, in, s, reinterpret_cast<const double2*>(z), r,
-      reinterpret_cast<double2*>(out));
+  const int ks = rhsc_splits(in, s, sms);
+  const int klen = ((s + ks - 1) / ks + kZChunk - 1) / kZChunk * kZChunk;
+  const int ksu = (s + klen - 1) / klen;
+  dim3 grid(static_cast<unsigned>((in + kRows - 1) / kRows), static_cast<unsigned>(ksu));
+  rhsc_kernel<<<grid, kCThreads, 0, stream>>>(reinterpret_cast<const double2*>(xh), base, st, in, s, klen, zs, rt, r,
+                                              reinterpret_cast<double2*>(part));
+  CPB_LAUNCH_CHECK();
+  const i64 n = in * r;
+  rhsc_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
+      reinterpret_cast<const double2*>(part), ksu, n, reinterpret_cast<double2*>(out));
   CPB_LAUNCH_CHECK();
 }
 

@@ -162,13 +162,16 @@ void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 
 bool mix_pass_supported(const DctPlan& p);
 // FFT-kind CPRAND-MIX (cfft.cu): unitary complex FFT along a mode (complex
 // data as interleaved double pairs), complex Z_S from the mixed factors in
-// v.fac, Re(Z^H Z) (RT x RT), C = Z^H X_hat_S (I_n x R complex row-major)
+// v.fac, C = Z^H X_hat_S (I_n x R complex row-major)
 void launch_cfft_mode(const DctPlan& pl, const double* in_real, const double* in_c, double* out_c, double* out_real,
                       i64 st, i64 nfib, const double* sign, int forward, const double* col_div, cudaStream_t stream);
-void launch_zc(const ModeView& v, double* z, cudaStream_t stream);
-void launch_gramc(const double* z, int s, int r, int rt, double* g, cudaStream_t stream);
-void launch_rhsc(const double* xh, const i64* base, i64 st, i64 in, int s, const double* z, int r, double* out,
-                 cudaStream_t stream);
+// complex Z_S as the stacked real matrix [Re Z; Im Z] (2S x rt)
+void launch_zc(const ModeView& v, int rt, double* zs, cudaStream_t stream);
+// C = Z^H X_hat_S: split-K partials (<= rhsc_splits(in, s, sms) x I_n x R
+// complex, in part) reduced in split order into out
+int rhsc_splits(i64 in, int s, int sms);
+void launch_rhsc(const double* xh, const i64* base, i64 st, i64 in, int s, const double* zs, int rt, int r,
+                 double* part, double* out, int sms, cudaStream_t stream);
 // TMA-fed forward pass (mixtma.cu); false when the shape does not suit it
 bool launch_mix_tma(const DctPlan& p, double* x, i64 st, i64 nfib, const double* sign, cudaStream_t stream,
                     bool prepare_only);

@@ -350,6 +350,7 @@ Session::~Session() {
   for (auto& f : mixedc_) dfree(f);
   dfree(zc_);
   dfree(cbuf_);
+  dfree(cpart_);
   if (xc_) big_free(xc_, static_cast<size_t>(p_) * 2 * sizeof(double));
   xc_ = nullptr;
   for (auto& f : fit_idx_) dfree(f);
@@ -496,8 +497,18 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   if (mix_ || shard_ || cmix_) rhs_full_ = dalloc<double>(static_cast<size_t>(max_in * r_));
   if (shard_ && mix_) rhs_gather_ = dalloc<double>(static_cast<size_t>(lmax_ * nranks_ * r_));
   if (cmix_) {
-    zc_ = dalloc<double>(static_cast<size_t>(2 * max_s * r_));
+    zc_ = dalloc<double>(static_cast<size_t>(2 * max_s * rt_));
     cbuf_ = dalloc<double>(static_cast<size_t>(2 * max_in * r_));
+    int ksmax = 1;
+    for (int n = 0; n < order_; ++n)
+      ksmax = std::max(ksmax, rhsc_splits(dims_[static_cast<size_t>(n)], s_mode_[static_cast<size_t>(n)], sms_));
+    cpart_ = dalloc<double>(static_cast<size_t>(2 * ksmax) * max_in * r_);
+    int gp, glen;
+    gram_splits(2 * static_cast<int>(max_s), &gp, &glen);
+    if (gp > max_gp) {
+      dfree(part_gram_);
+      part_gram_ = dalloc<double>(static_cast<size_t>(gp) * rt_ * rt_);
+    }
   }
 
   // ---- fit / stop state
@@ -1137,10 +1148,12 @@ void Session::enqueue_mode_cmix(int it, int n, const int* stop) {
   ModeWork w = work(n);
   // real_least_squares stacks [Re Z; Im Z]: 2S rows in the rank threshold
   w.tol = static_cast<double>(std::max(2 * v.s, r_)) * 2.220446049250313e-16;
-  launch_zc(v, zc_, stream_);
-  launch_gramc(zc_, v.s, r_, rt_, part_gram_, stream_);
-  launch_gram_inverse(part_gram_, 1, r_, w.tol, w.ginv, w.gfull, w.info, stop, stream_);
-  launch_rhsc(xc_, base_ptr(it, n), strides_[k], v.in, v.s, zc_, r_, cbuf_, stream_);
+  launch_zc(v, rt_, zc_, stream_);
+  int gp, glen;
+  gram_splits(2 * v.s, &gp, &glen);
+  launch_gram(zc_, 2 * v.s, r_, part_gram_, stop, stream_);  // Re(Z^H Z): the stacked real system's Gram
+  launch_gram_inverse(part_gram_, gp, r_, w.tol, w.ginv, w.gfull, w.info, stop, stream_);
+  launch_rhsc(xc_, base_ptr(it, n), strides_[k], v.in, v.s, zc_, rt_, r_, cpart_, cbuf_, sms_, stream_);
   launch_cfft_mode(plans_[k], nullptr, cbuf_, nullptr, rhs_full_, r_, r_, signs_[k], 0, nullptr, stream_);
   launch_mode_apply(v.in, r_, w, rhs_full_, n == 0, rng_state_, stream_);
   launch_cfft_mode(plans_[k], fac_[k], nullptr, mixedc_[k], nullptr, r_, r_, signs_[k], 1, w.norms, stream_);

@@ -136,8 +136,9 @@ class Session {
   double* rhs_gather_ = nullptr;    // sharded MIX: P * lmax rows of the last mode's RHS  // cprand_mix with the FFT kind (complex mixing, cfft.cu)
   double* xc_ = nullptr;            // complex X_hat (interleaved), P pairs
   std::vector<double*> mixedc_;     // complex mixed factors, I_n x R row-major pairs
-  double* zc_ = nullptr;            // complex Z_S, S x R pairs
+  double* zc_ = nullptr;            // complex Z_S as stacked real [Re Z; Im Z], 2S x RT
   double* cbuf_ = nullptr;          // C = Z^H X_hat_S, I_n x R pairs
+  double* cpart_ = nullptr;         // split-K partials of C
   std::vector<i64> dims_, strides_;  // global (model) shape
   i64 p_ = 0;
   std::vector<i64> tdims_, tstrides_;  // the tensor this session reads (a slab when sharded)
