@@ -1439,13 +1439,23 @@ __device__ double apply_block(i64 in, int r, const ModeWork& w, const double* __
     } else {
       const double* p = w.part_rhs + i * r + c;
       const i64 step = in * r;
+      // 16 partials in flight per round trip, summed in split order
       int k = 0;
-      for (; k + 6 <= w.ks; k += 6) {
-        const double v0 = __ldcg(p + k * step), v1 = __ldcg(p + (k + 1) * step), v2 = __ldcg(p + (k + 2) * step);
-        const double v3 = __ldcg(p + (k + 3) * step), v4 = __ldcg(p + (k + 4) * step), v5 = __ldcg(p + (k + 5) * step);
-        s = (((((s + v0) + v1) + v2) + v3) + v4) + v5;
+      for (; k + 16 <= w.ks; k += 16) {
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = __ldcg(p + (k + u) * step);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s += v[u];
       }
-      for (; k < w.ks; ++k) s += __ldcg(p + k * step);
+      if (k < w.ks) {
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = (k + u < w.ks) ? __ldcg(p + (k + u) * step) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (k + u < w.ks) s += v[u];
+      }
     }
   }
   rh[il * LD + c] = s;

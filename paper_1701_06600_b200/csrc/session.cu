@@ -641,9 +641,12 @@ void Session::setup_fused() {
         M.sign = signs_[static_cast<size_t>(n)];
         M.plan = dct_args(plans_[static_cast<size_t>(n)]);
         M.dctF = dct_fibers_per_cta(static_cast<int>(dims_[static_cast<size_t>(n)]), fsmem_);
-        // a few thousand factor entries: one CTA does apply -> norms faster
-        // than a ticket over the grid
-        M.tail1 = (dims_[static_cast<size_t>(n)] * r_ <= 4096) ? 1 : 0;
+        // a few thousand factor entries: one CTA may do apply -> norms
+        // (measured: since the apply blocks sum the split partials themselves,
+        // the multi-CTA apply beats the one-CTA tail also for C3's 80 x 10
+        // factors: 10.7 k vs 9.8 k it/s; CPRAND_TAIL1_MAX re-enables the tail)
+        static const i64 tail1_max = std::getenv("CPRAND_TAIL1_MAX") ? std::atoll(std::getenv("CPRAND_TAIL1_MAX")) : 0;
+        M.tail1 = (dims_[static_cast<size_t>(n)] * r_ <= tail1_max) ? 1 : 0;
         // the kernel keeps the mixed factors unnormalized: Z_S divides by the
         // norms (ones until a mode's first update)
         for (int m = 0, c2 = 0; m < order_; ++m) {
