@@ -311,32 +311,28 @@ __device__ bool inverse_cta(const double* __restrict__ part, int nparts, int r, 
   for (int t = 0; t < TR; ++t)
 #pragma unroll
     for (int u = 0; u < TC; ++u) a[t][u] = 0.0;
-  {  // G = sum of the split partials in split order, 4 partials per batch
-    int k = 0;
-    for (; k + 4 <= nparts; k += 4) {
-      double v[4][TR][TC];
+  {  // G = sum of the split partials in split order, PB partials per batch
+     // (about 32 loads in flight per thread; the last batch predicated)
+    constexpr int PB = (32 / (TR * TC)) > 4 ? (32 / (TR * TC)) : 4;
+    for (int k = 0; k < nparts; k += PB) {
+      double v[PB][TR][TC];
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+      for (int x = 0; x < PB; ++x)
 #pragma unroll
         for (int t = 0; t < TR; ++t)
 #pragma unroll
           for (int u = 0; u < TC; ++u)
-            v[x][t][u] = (row[t] < r && col[u] < r)
+            v[x][t][u] = (k + x < nparts && row[t] < r && col[u] < r)
                              ? __ldcg(part + static_cast<i64>(k + x) * RT * RT + row[t] * RT + col[u])
                              : 0.0;
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+      for (int x = 0; x < PB; ++x)
+        if (k + x < nparts)
 #pragma unroll
-        for (int t = 0; t < TR; ++t)
+          for (int t = 0; t < TR; ++t)
 #pragma unroll
-          for (int u = 0; u < TC; ++u) a[t][u] += v[x][t][u];
+            for (int u = 0; u < TC; ++u) a[t][u] += v[x][t][u];
     }
-    for (; k < nparts; ++k)
-#pragma unroll
-      for (int t = 0; t < TR; ++t)
-#pragma unroll
-        for (int u = 0; u < TC; ++u)
-          if (row[t] < r && col[u] < r) a[t][u] += __ldcg(part + static_cast<i64>(k) * RT * RT + row[t] * RT + col[u]);
   }
   // d_max for the threshold and the padding diagonal
   if (tid == 0) misc[0] = 0.0;
