@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
             const int nq = (M.nblk - mt + M.tm - 1) / M.tm;
             for (int e = tid; e < nq * 64; e += kFusedThreads) {
               const int q = mt + (e / 64) * M.tm, el = e % 64;
-              const double sum = sum_strided(A.gpart + static_cast<i64>(q) * M.tk * 64 + el, 64, M.tk);
+              const double sum = sum_strided32(A.gpart + static_cast<i64>(q) * M.tk * 64 + el, 64, M.tk);
               int bi, bj;
               gram_block_coords(q, nfr, &bi, &bj);
               const int gi = bi * 8 + el / 8, gj = bj * 8 + el % 8;
