@@ -315,10 +315,17 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
     k_ms_[k].assign(static_cast<size_t>(order_), 0.0);
     k_work_[k].assign(static_cast<size_t>(order_), 0.0);
   }
-  setup(init_lambda, init_factors);
+  try {
+    setup(init_lambda, init_factors);
+  } catch (...) {
+    stop_table_thread();  // a joinable std::thread must not outlive the failed constructor
+    throw;
+  }
 }
 
 Session::~Session() {
+  stop_table_thread();
+  if (tstream_) cudaStreamSynchronize(tstream_);
   if (stream_) cudaStreamSynchronize(stream_);
   if (stream2_) cudaStreamSynchronize(stream2_);
   if (gstream_) cudaStreamSynchronize(gstream_);
@@ -385,6 +392,8 @@ Session::~Session() {
   }
   if (ev_loop0_) cudaEventDestroy(ev_loop0_);
   if (ev_loop1_) cudaEventDestroy(ev_loop1_);
+  for (auto& e : table_ev_) cudaEventDestroy(e);
+  if (tstream_) cudaStreamDestroy(tstream_);
   if (stream_) cudaStreamDestroy(stream_);
   if (stream2_) cudaStreamDestroy(stream2_);
   if (gstream_) cudaStreamDestroy(gstream_);
@@ -407,6 +416,13 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
     }
   }
   t0_ = Clock::now();
+  const bool dbg_setup = std::getenv("CPRAND_DEBUG_SETUP") != nullptr;
+  auto mark = [&](const char* what) {
+    if (dbg_setup) {
+      CPB_CUDA(cudaStreamSynchronize(stream_));
+      std::fprintf(stderr, "setup %-12s %.2f ms\n", what, 1e3 * seconds_since(t0_));
+    }
+  };
   // ---- init (solver.hpp:185-201)
   HostModel m;
   if (o_.init == 2) {
@@ -436,16 +452,20 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   rng_state_ = dalloc<unsigned long long>(313);
   launch_rng_seed(rng_state_, seeded_engine_seed_value(o_.rng_seed, kInitStream + 7), stream_);
 
+  mark("init");
   // ---- which modes read their fibers in place (mode 1, or a mode-major replica)
   plan_replicas();
   // ---- sample tables (data independent: all drawn up front)
   build_tables();
+  mark("tables");
 
   // ---- estimator on the ORIGINAL tensor for rand / mix (mixing.hpp:268-273)
   xsolve_ = x_->d;
   if (!o_.bench_mode && !premix_) build_fit_estimator(x_->d);
+  mark("estimator");
   if (mix_ || premix_) mix_setup();
   if (cmix_) cmix_setup();
+  mark("mixing");
   if (!o_.bench_mode && premix_) {
     // cprand(x_hat) builds its estimator and norm on the mixed tensor
     launch_sumsq(xsolve_, tp_, fit_part_, nparts, fit_part_ + nparts, stream_);
@@ -457,6 +477,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   }
 
   build_replicas();
+  mark("replicas");
 
   // ---- per-mode work buffers
   i64 max_part = 1, max_in = 1, max_apply = 1, max_s = 1;
@@ -520,8 +541,10 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   CPB_CUDA(cudaHostAlloc(&stop_host_, sizeof(int), cudaHostAllocMapped));
   *stop_host_ = 0;
   CPB_CUDA(cudaHostGetDevicePointer(&stop_dev_, stop_host_, 0));
+  mark("buffers");
   setup_fused();
   CPB_CUDA(cudaStreamSynchronize(stream_));
+  mark("fused");
   setup_seconds_ = seconds_since(t0_);
 }
 
@@ -922,18 +945,44 @@ void Session::build_tables() {
       rows_total += static_cast<i64>(N - 1) * s_mode_[static_cast<size_t>(n)];
       base_total += s_mode_[static_cast<size_t>(n)];
     }
-  std::vector<int> rows(static_cast<size_t>(std::max<i64>(rows_total, 1)));
-  std::vector<i64> base(static_cast<size_t>(std::max<i64>(base_total, 1)), 0);
-  std::vector<i64> dbase(static_cast<size_t>(std::max<i64>(base_total, 1)), 0);
+  row_off_.push_back(rows_total);  // end sentinels: block ranges of iterations [a, b)
+  base_off_.push_back(base_total);
+  // the sharded path compacts local sample lists from every table here;
+  // otherwise only the first chunk is drawn now and a host thread draws the
+  // rest behind the solver (sampling.hpp:283-286: one stream, same order)
+  const bool async = !shard_ && !o_.exhaustive_samples && table_iters_ > table_chunk_;
+  const size_t nrows = static_cast<size_t>(std::max<i64>(rows_total, 1));
+  const size_t nbase = static_cast<size_t>(std::max<i64>(base_total, 1));
+  std::vector<int> rows_v;
+  std::vector<i64> base_v, dbase_v;
+  int* rows;
+  i64 *base, *dbase;
+  if (async) {  // kept for the drawing thread; pageable and uninitialized (every
+                // entry is written before its chunk is uploaded; pinning or
+                // zero-filling 30 MB up front costs more than the first chunk)
+    rows_hv_.reset(new int[nrows]);
+    base_hv_.reset(new i64[nbase]);
+    dbase_hv_.reset(new i64[nbase]);
+    rows = rows_hv_.get();
+    base = base_hv_.get();
+    dbase = dbase_hv_.get();
+  } else {
+    rows_v.assign(nrows, 0);
+    base_v.assign(nbase, 0);
+    dbase_v.assign(nbase, 0);
+    rows = rows_v.data();
+    base = base_v.data();
+    dbase = dbase_v.data();
+  }
   std::vector<int> lidx;
   std::vector<i64> ldb;
-  auto rng = seeded_engine(o_.rng_seed, kSamplingStream);
-  for (int it = 0; it < table_iters_; ++it)
+  auto draw = [this, N, rows, base, dbase, &lidx, &ldb](int it0, int it1, std::mt19937_64& rng) {
+  for (int it = it0; it < it1; ++it)
     for (int n = 0; n < N; ++n) {
       const int sn = s_mode_[static_cast<size_t>(n)];
-      int* rb = rows.data() + row_off_[static_cast<size_t>(it * N + n)];
-      i64* bb = base.data() + base_off_[static_cast<size_t>(it * N + n)];
-      i64* db = dbase.data() + base_off_[static_cast<size_t>(it * N + n)];
+      int* rb = rows + row_off_[static_cast<size_t>(it * N + n)];
+      i64* bb = base + base_off_[static_cast<size_t>(it * N + n)];
+      i64* db = dbase + base_off_[static_cast<size_t>(it * N + n)];
       std::vector<int> km;
       std::vector<i64> jk;  // unfolding column weights J_k of the tensor read (tensor.hpp:92-106)
       {
@@ -1004,6 +1053,10 @@ void Session::build_tables() {
         loc_cnt_.push_back(cnt);
       }
     }
+  };
+  auto rng = seeded_engine(o_.rng_seed, kSamplingStream);
+  const int first = async ? table_chunk_ : table_iters_;
+  draw(0, first, rng);
   if (shard_) {
     loc_idx_ = dalloc<int>(std::max<size_t>(lidx.size(), 1));
     loc_dbase_ = dalloc<i64>(std::max<size_t>(ldb.size(), 1));
@@ -1013,14 +1066,61 @@ void Session::build_tables() {
     }
     CPB_CUDA(cudaStreamSynchronize(stream_));
   }
-  rows_ = dalloc<int>(rows.size());
-  base_ = dalloc<i64>(base.size());
-  dbase_ = dalloc<i64>(dbase.size());
-  CPB_CUDA(cudaMemcpyAsync(dbase_, dbase.data(), dbase.size() * sizeof(i64), cudaMemcpyHostToDevice, stream_));
-  CPB_CUDA(cudaMemcpyAsync(rows_, rows.data(), rows.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
-  CPB_CUDA(cudaMemcpyAsync(base_, base.data(), base.size() * sizeof(i64), cudaMemcpyHostToDevice, stream_));
-  CPB_CUDA(cudaStreamSynchronize(stream_));  // host vectors die here
+  rows_ = dalloc<int>(nrows);
+  base_ = dalloc<i64>(nbase);
+  dbase_ = dalloc<i64>(nbase);
+  // iterations [a, b) of the tables: contiguous ranges of the three arrays
+  auto upload = [this, N, rows, base, dbase](int a, int b, cudaStream_t st) {
+    const i64 r0 = row_off_[static_cast<size_t>(a * N)], r1 = row_off_[static_cast<size_t>(b * N)];
+    const i64 b0 = base_off_[static_cast<size_t>(a * N)], b1 = base_off_[static_cast<size_t>(b * N)];
+    if (r1 > r0)
+      CPB_CUDA(cudaMemcpyAsync(rows_ + r0, rows + r0, sizeof(int) * (r1 - r0), cudaMemcpyHostToDevice, st));
+    if (b1 > b0) {
+      CPB_CUDA(cudaMemcpyAsync(base_ + b0, base + b0, sizeof(i64) * (b1 - b0), cudaMemcpyHostToDevice, st));
+      CPB_CUDA(cudaMemcpyAsync(dbase_ + b0, dbase + b0, sizeof(i64) * (b1 - b0), cudaMemcpyHostToDevice, st));
+    }
+  };
+  upload(0, first, stream_);
+  CPB_CUDA(cudaStreamSynchronize(stream_));  // the synchronous part's host vectors may die here
+  tables_ready_.store(first);
+  synced_main_ = synced_g_ = first;
+  if (!async) return;
+  const int nchunks = (table_iters_ - first + table_chunk_ - 1) / table_chunk_;
+  table_ev_.resize(static_cast<size_t>(nchunks));
+  for (auto& e : table_ev_) CPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CPB_CUDA(cudaStreamCreateWithFlags(&tstream_, cudaStreamNonBlocking));
+  const int dev = x_->device;
+  table_thread_ = std::thread([this, draw, upload, dev, first, rng]() mutable {
+    cudaSetDevice(dev);
+    for (int it0 = first, c = 0; it0 < table_iters_ && !tables_stop_.load(); it0 += table_chunk_, ++c) {
+      const int it1 = std::min(table_iters_, it0 + table_chunk_);
+      draw(it0, it1, rng);
+      upload(it0, it1, tstream_);
+      cudaEventRecord(table_ev_[static_cast<size_t>(c)], tstream_);
+      tables_ready_.store(it1, std::memory_order_release);
+    }
+  });
 }
+
+// Iteration `it` (1-based) may be enqueued on stream st once its tables are
+// uploaded: wait for the drawing thread, then make st wait for the chunk
+// events not yet covered (synced: iterations st already waits for).
+void Session::wait_tables(int it, cudaStream_t st, int& synced) {
+  if (it <= synced || it > table_iters_) return;
+  while (tables_ready_.load(std::memory_order_acquire) < it) std::this_thread::yield();
+  const int ready = tables_ready_.load(std::memory_order_acquire);
+  const int first = table_chunk_;
+  for (int c = (synced - first) / table_chunk_; first + c * table_chunk_ < ready; ++c)
+    CPB_CUDA(cudaStreamWaitEvent(st, table_ev_[static_cast<size_t>(c)], 0));
+  synced = ready;
+}
+
+void Session::stop_table_thread() {
+  tables_stop_.store(true);
+  if (table_thread_.joinable()) table_thread_.join();
+}
+
+
 
 void Session::build_fit_estimator(const double* xsrc) {
   // sampling.hpp:155-179 (exhaustive: sampling.hpp:182-186)
@@ -1034,6 +1134,9 @@ void Session::build_fit_estimator(const double* xsrc) {
     auto rng = seeded_engine(o_.rng_seed, kFitStream);
     offs = sample_offsets_without_replacement(p_, o_.fit_sample_count, rng);
   }
+  const bool dbg = std::getenv("CPRAND_DEBUG_SETUP") != nullptr;
+  const auto te = Clock::now();
+  if (dbg) std::fprintf(stderr, "  estimator offsets drawn %.2f ms after setup start\n", 1e3 * seconds_since(t0_));
   phat_ = static_cast<i64>(offs.size());
   i64* d_off = dalloc<i64>(offs.size());
   CPB_CUDA(cudaMemcpyAsync(d_off, offs.data(), offs.size() * sizeof(i64), cudaMemcpyHostToDevice, stream_));
@@ -1060,6 +1163,10 @@ void Session::build_fit_estimator(const double* xsrc) {
     CPB_CUDA(cudaStreamSynchronize(stream_));  // loc dies here
   } else {
     launch_gather_values(xsrc, d_off, phat_, fit_vals_, stream_);
+  }
+  if (dbg) {
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+    std::fprintf(stderr, "  estimator values gathered +%.2f ms\n", 1e3 * seconds_since(te));
   }
   std::vector<int> idx(offs.size());
   for (int n = 0; n < order_; ++n) {
@@ -1317,6 +1424,7 @@ void Session::timed(int mode, int kind, cudaStream_t st, F&& launch) {
 }
 
 void Session::enqueue_gather(int git) {
+  wait_tables(git, gstream_, synced_g_);
   for (int n = 0; n < order_; ++n) {
     if (direct_[static_cast<size_t>(n)]) continue;
     const size_t slot = static_cast<size_t>(((git - 1) % depth_) * order_ + n);
@@ -1333,6 +1441,7 @@ void Session::enqueue_gather(int git) {
 
 void Session::enqueue_iteration() {
   const int it = it_ + 1;
+  wait_tables(it, stream_, synced_main_);
   if (!loop_started_) {
     CPB_CUDA(cudaEventRecord(ev_loop0_, stream_));
     launch_stamp_start(state_, stream_);

@@ -1,8 +1,11 @@
 // Host runtime of the B200 CPRAND path: device tensors, solver sessions.
 #pragma once
 
+#include <atomic>
 #include <chrono>
 #include <functional>
+#include <memory>
+#include <thread>
 #include <cstdint>
 #include <optional>
 #include <random>
@@ -105,6 +108,10 @@ class Session {
  private:
   void setup(const double* init_lambda, const double* const* init_factors);
   void build_tables();
+  // sample tables beyond the first chunk are drawn by a host thread while
+  // the device iterates (sampling is data independent; one RNG stream)
+  void wait_tables(int it, cudaStream_t st, int& synced);
+  void stop_table_thread();
   void build_fit_estimator(const double* xsrc);
   void mix_setup();
   void cmix_setup();                          // FFT-kind MIX: complex X_hat, mixed factors
@@ -167,6 +174,15 @@ class Session {
   // tables
   std::vector<int> s_mode_;         // samples per mode (S, or P/I_n when exhaustive)
   int table_iters_ = 0;
+  std::thread table_thread_;
+  std::atomic<int> tables_ready_{0};  // iterations whose tables are uploaded (chunk events recorded)
+  std::atomic<bool> tables_stop_{false};
+  int table_chunk_ = 16;
+  int synced_main_ = 0, synced_g_ = 0;  // iterations each stream already waits for
+  std::vector<cudaEvent_t> table_ev_;   // one per chunk
+  cudaStream_t tstream_ = nullptr;
+  std::unique_ptr<int[]> rows_hv_;      // host tables (async drawing)
+  std::unique_ptr<i64[]> base_hv_, dbase_hv_;
   int* rows_ = nullptr;             // [iter][mode] blocks of (N-1) x S_n
   i64* base_ = nullptr;             // [iter][mode] blocks of S_n
   i64* dbase_ = nullptr;            // same layout: row offsets the GEMM reads in place
