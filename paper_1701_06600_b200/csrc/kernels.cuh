@@ -105,7 +105,7 @@ struct FitArgs {
   unsigned* ticket;
   FitState* state;
   TraceRec* trace;
-  int* stop_host_mapped;         // zero-copy mirror of state->stopped (may be null)
+  int* stop_host_mapped;         // zero-copy stop marks, [iteration] = 1 where the run stopped (may be null)
   int iteration;
   int max_iters;
   int has_threshold;

@@ -1697,7 +1697,7 @@ __device__ inline void fit_final(const FitArgs& a, i64 nblocks, double* red) {
     st->reason = reason;
     __threadfence_system();
     st->stopped = 1;
-    if (a.stop_host_mapped) *reinterpret_cast<volatile int*>(a.stop_host_mapped) = 1;
+    if (a.stop_host_mapped) reinterpret_cast<volatile int*>(a.stop_host_mapped)[a.iteration] = 1;
   }
 }
 

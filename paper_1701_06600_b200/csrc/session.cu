@@ -538,8 +538,13 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   fs.best_fit = -INFINITY;
   CPB_CUDA(cudaMemcpyAsync(state_, &fs, sizeof(fs), cudaMemcpyHostToDevice, stream_));
   trace_dev_ = dalloc<TraceRec>(static_cast<size_t>(o_.max_iters));
-  CPB_CUDA(cudaHostAlloc(&stop_host_, sizeof(int), cudaHostAllocMapped));
-  *stop_host_ = 0;
+  // per-iteration stop marks (zero-copy): the host decides whether to
+  // enqueue iteration k from the mark of iteration k - kInFlight, which is
+  // the same on every rank of a sharded run (the fit is replicated), so all
+  // ranks enqueue the same collectives
+  const size_t nmarks = static_cast<size_t>(o_.max_iters) + 2;
+  CPB_CUDA(cudaHostAlloc(&stop_host_, nmarks * sizeof(int), cudaHostAllocMapped));
+  std::fill(stop_host_, stop_host_ + nmarks, 0);
   CPB_CUDA(cudaHostGetDevicePointer(&stop_dev_, stop_host_, 0));
   mark("buffers");
   setup_fused();
@@ -1653,7 +1658,12 @@ int Session::run(int n) {
       // keep kInFlight iterations queued; stop enqueueing once the device
       // stop rule has fired
       CPB_CUDA(cudaEventSynchronize(it_events_[static_cast<size_t>(k % kInFlight)]));
-      if (*reinterpret_cast<volatile int*>(stop_host_)) break;
+      // iterations up to k - kInFlight have completed (event above); a stop
+      // there is final (later launches return at once)
+      bool stopped = false;
+      for (int j = 1; j <= start + k - kInFlight + 1 && !stopped; ++j)
+        stopped = reinterpret_cast<volatile int*>(stop_host_)[j] != 0;
+      if (stopped) break;
     }
     enqueue_iteration();
     CPB_CUDA(cudaEventRecord(it_events_[static_cast<size_t>(k % kInFlight)], stream_));

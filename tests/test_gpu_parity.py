@@ -487,6 +487,32 @@ def test_sharded_session_single_rank(pb, orc):
 
 
 @pytest.mark.gpu
+def test_sharded_session_stops_with_the_unsharded_run(pb, orc):
+    """A sharded run that stops early (fit threshold / stall stop): the host
+    decides each enqueue from the per-iteration stop mark of iteration
+    k - kInFlight, the same on every rank, so the ranks issue the same
+    collectives; one rank: same stop iteration and reason as unsharded."""
+    dims, r, s = (24, 20, 22), 4, 60
+    comm = pb.Comm(pb.Comm.unique_id(), 0, 1, 0)
+    t1 = pb.DeviceTensor(dims)
+    t1.synth(r, 0.5, 0.01, 9)
+    t2 = pb.DeviceTensor(dims)
+    t2.synth_slab(r, 0.5, 0.01, 9, dims[-1], comm)
+    for extra in (dict(fit_threshold=0.97), dict(stall_limit=3)):
+        base = dict(rng_seed=9, max_iters=120, **extra)
+        full = pb.Session("rand", t1, r, s, pb.SolveOptions(fused=0, **base))
+        full.run(120)
+        ref = full.result()
+        sh = pb.Session("rand", t2, r, s, pb.SolveOptions(comm=comm, shard_total=dims[-1], **base))
+        sh.run(120)
+        got = sh.result()
+        assert got.reason == ref.reason and got.iterations == ref.iterations < 120
+        for h in (sh, full):
+            h.close()
+    comm.close()
+
+
+@pytest.mark.gpu
 def test_sharded_session_rejects_bad_slab(pb):
     comm = pb.Comm(pb.Comm.unique_id(), 0, 1, 0)
     t = pb.DeviceTensor((10, 9, 8))
