@@ -111,25 +111,38 @@ __global__ void __launch_bounds__(kApplyThreads) mode_apply_kernel(i64 in, int r
 // through 32 x 32 shared-memory tiles (coalesced reads and writes). Column j
 // of the unfolding (unfold_column_index, tensor.hpp:92-106) = lo + st_n hi,
 // so a sampled fiber becomes the contiguous row y + I_n * j.
+// Tiles of TI = 64 tensor rows (mode-n index i) x 32 fastest-index columns:
+// 8 loads of 256-byte row runs per thread in flight, 512-byte runs written.
 __global__ void __launch_bounds__(256) replica_kernel(const double* __restrict__ x, i64 in, i64 st,
                                                       i64 nhi, double* __restrict__ y) {
-  __shared__ double tile[32][33];
-  const i64 tiles_lo = (st + 31) / 32, tiles_i = (in + 31) / 32;
+  constexpr int TI = 64;
+  __shared__ double tile[TI][33];
+  const i64 tiles_lo = (st + 31) / 32, tiles_i = (in + TI - 1) / TI;
   const i64 per_hi = tiles_lo * tiles_i;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
   for (i64 blk = blockIdx.x; blk < nhi * per_hi; blk += gridDim.x) {
     const i64 hi = blk / per_hi, rem = blk % per_hi;
     const i64 ti = rem / tiles_lo, tl = rem % tiles_lo;
     const double* src = x + hi * st * in;
     double* dst = y + hi * st * in;
-    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
-    for (int k = ty; k < 32; k += 8) {
-      const i64 i = ti * 32 + k, lo = tl * 32 + tx;
-      tile[k][tx] = (i < in && lo < st) ? __ldcs(src + i * st + lo) : 0.0;
+    double v[TI / 8];
+#pragma unroll
+    for (int q = 0; q < TI / 8; ++q) {
+      const i64 i = ti * TI + ty + 8 * q, lo = tl * 32 + tx;
+      v[q] = (i < in && lo < st) ? __ldcs(src + i * st + lo) : 0.0;
     }
+#pragma unroll
+    for (int q = 0; q < TI / 8; ++q) tile[ty + 8 * q][tx] = v[q];
     __syncthreads();
-    for (int k = ty; k < 32; k += 8) {
-      const i64 lo = tl * 32 + k, i = ti * 32 + tx;
-      if (i < in && lo < st) dst[lo * in + i] = tile[tx][k];
+    // column lo of the tile: TI consecutive i, written as two 32-lane runs
+#pragma unroll
+    for (int q = 0; q < 32 / 8; ++q) {
+      const i64 lo = tl * 32 + ty + 8 * q;
+#pragma unroll
+      for (int h = 0; h < TI / 32; ++h) {
+        const i64 i = ti * TI + 32 * h + tx;
+        if (i < in && lo < st) __stcs(dst + lo * in + i, tile[32 * h + tx][ty + 8 * q]);
+      }
     }
     __syncthreads();
   }
