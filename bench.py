@@ -404,6 +404,27 @@ def main() -> int:
             traffic = json.load(f).get("traffic_bytes_per_launch")
     fallbacks = s.gram_fallbacks()
     used_fused = bool(fused[0])
+    # ---- the metric's "sampled-gather HBM GB/s vs peak": gather_fibers of
+    # 10 iterations' sample tables (every mode) into scratch, batched (the
+    # samples are data independent), from the mode-major replicas and from
+    # the tensor's own layout (B_min = 8 B / element for
+    # contiguous rows, 32 B for strided modes)
+    gather = None
+    if comm is None:
+        gi = min(10, total_iters)
+        ms_r, bu_r, bm_r = s.gather_bench(gi, True)
+        ms_x, bu_x, bm_x = s.gather_bench(gi, False)
+        gather = {"iterations": gi, "kernel": "gather_rows_kernel",
+                  "replicas": {"ms": round(ms_r, 4), "useful_gbs": round(bu_r / (ms_r * 1e-3) / 1e9, 1),
+                               "frac_useful": round(bu_r / (ms_r * 1e-3) / 1e9 / hbm_peak, 3),
+                               "read_write_gbs": round(2 * bu_r / (ms_r * 1e-3) / 1e9, 1),
+                               "frac_read_write": round(2 * bu_r / (ms_r * 1e-3) / 1e9 / hbm_peak, 3)},
+                  "tensor_layout": {"ms": round(ms_x, 4), "useful_gbs": round(bu_x / (ms_x * 1e-3) / 1e9, 1),
+                                    "b_min_gbs": round(bm_x / (ms_x * 1e-3) / 1e9, 1),
+                                    "frac_b_min": round(bm_x / (ms_x * 1e-3) / 1e9 / hbm_peak, 3)},
+                  "note": "one launch per mode over all iterations' fibers; useful / B_min count the reads, "
+                          "read_write adds the X_S write (8 B / element); the solver itself reads the fibers "
+                          "in place inside the persistent kernel"}
     s.close()
 
     # ---- full loop (sampled fit estimate + stop rule every iteration) and
@@ -523,7 +544,7 @@ def main() -> int:
                                "gram_reduce"]),
                              [round(x, 2) for x in phases])) if phases else None,
                          "gram_fallbacks": fallbacks, "mix_pass": mix_pass},
-            "atomic_gram": atomic, "full_loop": full, "time_to_fit": ttf,
+            "atomic_gram": atomic, "full_loop": full, "time_to_fit": ttf, "sampled_gather": gather,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches_per_iter(cfg, used_fused) * args.steps,
         }

@@ -189,6 +189,12 @@ int cprand_session_kernel_stats(cprand_session_t s, int32_t mode, int32_t kind, 
 int cprand_session_phase_us(cprand_session_t s, double* out, int32_t cap, int32_t* n);
 /* Diagnostics: Gram solves that took the pivoted-Cholesky (min-norm) path. */
 int cprand_session_gram_fallbacks(cprand_session_t s, int64_t* out);
+/* Measurement: batched gather_fibers (tensor.hpp:188-212) of the session's
+ * sample tables, iterations 1..iters x every mode, from the mode-major
+ * replicas (replicas != 0) or the tensor itself; CUDA-event ms and the
+ * useful / minimum-traffic bytes moved. */
+int cprand_session_gather_bench(cprand_session_t s, int32_t iters, int32_t replicas, double* ms,
+                                double* bytes_useful, double* bytes_min);
 int cprand_session_result(cprand_session_t s, double* out_lambda, double* const* out_factors,
                           cprand_trace_record_t* trace, int32_t trace_cap, cprand_result_t* res);
 void cprand_session_destroy(cprand_session_t s);

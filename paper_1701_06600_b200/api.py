@@ -291,6 +291,14 @@ class Session:
         check(lib().cprand_session_gram_fallbacks(self.h, C.byref(n)))
         return n.value
 
+    def gather_bench(self, iters: int, replicas: bool) -> tuple:
+        """Batched sampled-fiber gather of iterations 1..iters (every mode):
+        (ms, useful bytes, minimum-traffic bytes)."""
+        ms, bu, bm = C.c_double(), C.c_double(), C.c_double()
+        check(lib().cprand_session_gather_bench(self.h, iters, int(replicas), C.byref(ms), C.byref(bu),
+                                                C.byref(bm)))
+        return ms.value, bu.value, bm.value
+
     def result(self) -> SolveResult:
         lam = np.empty(self.r, dtype=np.float64)
         fs = [np.empty((d, self.r), dtype=np.float64, order="F") for d in self.dims]

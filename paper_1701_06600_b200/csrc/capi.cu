@@ -337,6 +337,14 @@ int cprand_session_gram_fallbacks(cprand_session_t s, int64_t* out) {
   return guarded([&] { need(s); *out = s->s->gram_fallbacks(); });
 }
 
+int cprand_session_gather_bench(cprand_session_t s, int32_t iters, int32_t replicas, double* ms,
+                                double* bytes_useful, double* bytes_min) {
+  return guarded([&] {
+    need(s);
+    *ms = s->s->gather_bench(iters, replicas != 0, bytes_useful, bytes_min);
+  });
+}
+
 int cprand_session_result(cprand_session_t s, double* out_lambda, double* const* out_factors,
                           cprand_trace_record_t* trace, int32_t trace_cap, cprand_result_t* res) {
   return guarded([&] { need(s); fill_result(*s->s, out_lambda, out_factors, trace, trace_cap, res); });

@@ -910,6 +910,61 @@ void Session::enqueue_mode_sharded(int it, int n, const int* stop) {
   }
 }
 
+double Session::gather_bench(int iters, bool replicas, double* bytes_useful, double* bytes_min) {
+  iters = std::max(1, std::min(iters, table_iters_));
+  i64 maxld = 1, maxs = 1;
+  for (int n = 0; n < order_; ++n) {
+    maxld = std::max<i64>(maxld, static_cast<i64>(iters) * s_mode_[static_cast<size_t>(n)] * tdims_[static_cast<size_t>(n)]);
+    maxs = std::max<i64>(maxs, static_cast<i64>(iters) * s_mode_[static_cast<size_t>(n)]);
+  }
+  double* scratch = dalloc<double>(static_cast<size_t>(maxld));
+  for (int it = 1; it <= iters; ++it) wait_tables(it, stream_, synced_main_);
+  // per mode, the iterations' fiber offsets back to back: one launch per mode
+  std::vector<i64*> offs(static_cast<size_t>(order_), nullptr);
+  std::vector<i64> strides(static_cast<size_t>(order_), 1);
+  std::vector<const double*> src(static_cast<size_t>(order_), nullptr);
+  for (int n = 0; n < order_; ++n) {
+    const size_t k = static_cast<size_t>(n);
+    const bool rep = replicas && n >= 1 && rep_[k] != nullptr;
+    src[k] = rep ? rep_[k] : xsolve_;
+    strides[k] = rep ? 1 : tstrides_[k];
+    offs[k] = dalloc<i64>(static_cast<size_t>(maxs));
+    const int sn = s_mode_[k];
+    for (int it = 1; it <= iters; ++it)
+      CPB_CUDA(cudaMemcpyAsync(offs[k] + static_cast<i64>(it - 1) * sn, rep ? dbase_ptr(it, n) : base_ptr(it, n),
+                               sizeof(i64) * sn, cudaMemcpyDeviceToDevice, stream_));
+  }
+  cudaEvent_t a, b;
+  CPB_CUDA(cudaEventCreate(&a));
+  CPB_CUDA(cudaEventCreate(&b));
+  double useful = 0.0, bmin = 0.0;
+  auto pass = [&](bool count) {
+    for (int n = 0; n < order_; ++n) {
+      const size_t k = static_cast<size_t>(n);
+      const int cnt = iters * s_mode_[k];
+      launch_gather_rows(src[k], tdims_[k], strides[k], offs[k], cnt, scratch, tdims_[k], stream_);
+      if (count) {
+        useful += 8.0 * cnt * tdims_[k];
+        bmin += (strides[k] == 1 ? 8.0 : 32.0) * cnt * tdims_[k];
+      }
+    }
+  };
+  pass(false);  // warm (instruction cache, TLB)
+  CPB_CUDA(cudaEventRecord(a, stream_));
+  pass(true);
+  CPB_CUDA(cudaEventRecord(b, stream_));
+  CPB_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  CPB_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  for (auto& p : offs) dfree(p);
+  dfree(scratch);
+  *bytes_useful = useful;
+  *bytes_min = bmin;
+  return ms;
+}
+
 long long Session::gram_fallbacks() {
   if (!info_) return 0;
   CPB_CUDA(cudaStreamSynchronize(stream_));

@@ -214,6 +214,13 @@ class Session {
   }
   // Gram inverses that took the pivoted-Cholesky fallback so far (waits)
   long long gram_fallbacks();
+  // Batched sampled-fiber gather (gather_fibers, tensor.hpp:188-212) of the
+  // tables of iterations 1..iters, every mode, into scratch: from the
+  // mode-major replicas (replicas = true, contiguous rows) or from the tensor
+  // itself (strided modes: one 32-byte sector per element). Returns the
+  // CUDA-event time (ms); bytes: useful (8 B / element) and B_min (8 B mode 1
+  // or replica rows, 32 B strided).
+  double gather_bench(int iters, bool replicas, double* bytes_useful, double* bytes_min);
  private:
   std::vector<double> phase_acc_;
   int phase_acc_n_ = 0;
