@@ -668,3 +668,20 @@ def test_fused_gram_sum_on_inverse_cta_wide_rank(pb, orc, method):
     np.testing.assert_allclose(runs[0].lam, runs[1].lam, rtol=1e-9)
     for a, b in zip(runs[0].factors, runs[1].factors):
         assert rel(a, b) < 1e-9
+
+
+def test_session_gather_bench_bytes(pb, orc):
+    """The batched sampled-gather measurement moves exactly the fibers of
+    the requested iterations: useful bytes 8 * iters * sum_n S I_n; B_min
+    counts 32 B per element for strided modes read from the tensor."""
+    dims, r, s = (40, 30, 20), 3, 50
+    t = pb.DeviceTensor(dims)
+    t.synth(r, 0.0, 0.0, 3)
+    sess = pb.Session("rand", t, r, s, pb.SolveOptions(rng_seed=3, max_iters=40, bench_mode=True, replicas=1))
+    ms, useful, bmin = sess.gather_bench(10, True)
+    assert ms > 0 and useful == 8.0 * 10 * s * sum(dims) and bmin == useful
+    ms, useful, bmin = sess.gather_bench(10, False)
+    assert useful == 8.0 * 10 * s * sum(dims)
+    assert bmin == 8.0 * 10 * s * dims[0] + 32.0 * 10 * s * (dims[1] + dims[2])
+    sess.close()
+    t.close()
