@@ -144,6 +144,13 @@ typedef struct cprand_session_s* cprand_session_t;
 
 int cprand_tensor_create(const int64_t* dims, int32_t order, int32_t device, cprand_tensor_t* out);
 int cprand_tensor_upload(cprand_tensor_t t, const double* host);
+/* exact_fit (solver.hpp:161-181): 1 - ||X - M|| / ||X|| of the Kruskal model
+ * (lambda[r], column-major factors I_n x r) via the mode-1 MTTKRP on the
+ * device and the Gram expansion; 1 for a zero tensor. */
+int cprand_tensor_exact_fit(cprand_tensor_t t, const double* lambda, const double* const* factors, int64_t r,
+                            double* fit);
+int cprand_exact_fit(const double* x, const int64_t* dims, int32_t order, const double* lambda,
+                     const double* const* factors, int64_t r, int32_t device, double* fit);
 int cprand_tensor_download(cprand_tensor_t t, double* host);
 /* BASELINE.json generator in HBM: factors G_n L^T (host RNG, seeded_engine
  * (seed, 5)), lambda = 1, eta-scaled Philox Gaussian noise. out_factors

@@ -179,6 +179,22 @@ inline Index default_sample_count(Index r) {
   return v;
 }
 
+// exact_fit (solver.hpp:161-181) on the device: 1 - ||X - M|| / ||X||
+inline double exact_fit(const TensorD& x, const KruskalModel& m, int device = -1) {
+  if (m.order() != x.order()) throw std::invalid_argument("exact_fit: model dims do not match tensor");
+  std::vector<const double*> f;
+  for (Index n = 0; n < m.order(); ++n) {
+    if (m.factors[static_cast<size_t>(n)].rows != x.dims[static_cast<size_t>(n)] ||
+        m.factors[static_cast<size_t>(n)].cols != m.rank())
+      throw std::invalid_argument("exact_fit: model dims do not match tensor");
+    f.push_back(m.factors[static_cast<size_t>(n)].data());
+  }
+  double fit = 0.0;
+  detail::throw_status(cprand_exact_fit(x.values.data(), x.dims.data(), static_cast<int32_t>(x.order()),
+                                        m.lambda.data(), f.data(), m.rank(), device, &fit));
+  return fit;
+}
+
 inline SolveResult cprand(const TensorD& x, Index r, Index s, const SolveOptions& opts) {
   return detail::run(CPRAND_METHOD_RAND, x, r, s, opts);
 }

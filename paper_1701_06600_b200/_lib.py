@@ -73,6 +73,7 @@ EXPORTS = [
     "cprand_session_sync", "cprand_session_timed_enqueue", "cprand_host_alloc_pinned",
     "cprand_host_free_pinned", "cprand_device_cache_release", "cprand_session_stream", "cprand_session_set_kernel_timing",
     "cprand_session_kernel_stats", "cprand_session_phase_us", "cprand_session_gram_fallbacks", "cprand_session_gather_bench",
+    "cprand_tensor_exact_fit", "cprand_exact_fit",
     "cprand_session_result", "cprand_session_destroy",
     "cprand_gather_fibers", "cprand_skr", "cprand_mode_update", "cprand_fit_values",
     "cprand_estimate_fit", "cprand_mix_tensor", "cprand_mix_factor", "cprand_unmix_factor",

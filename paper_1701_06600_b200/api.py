@@ -200,6 +200,14 @@ class DeviceTensor:
             raise ValueError("download_into needs a contiguous float64 buffer of the tensor's size")
         check(lib().cprand_tensor_download(self.h, _p(flat)))
 
+    def exact_fit(self, lam, factors) -> float:
+        """exact_fit (solver.hpp:161-181) of the model (lam, factors) to this tensor."""
+        lam = np.ascontiguousarray(np.asarray(lam, dtype=np.float64))
+        fs = [_f64(f) for f in factors]
+        out = C.c_double()
+        check(lib().cprand_tensor_exact_fit(self.h, _p(lam), _ptrs(fs), C.c_int64(lam.size), C.byref(out)))
+        return out.value
+
     def synth(self, r: int, collinearity: float, eta: float, seed: int, want_factors=False):
         fs = [np.empty((d, r), dtype=np.float64, order="F") for d in self.dims] if want_factors else None
         check(lib().cprand_tensor_synth(self.h, C.c_int64(r), C.c_double(collinearity),
@@ -407,6 +415,16 @@ def estimate_fit(lam, factors, idxs, values, x_norm: float, total: int) -> float
                                     len(fs), C.c_int64(lam.size), _p(idxs), _p(vals),
                                     C.c_int64(vals.size), C.c_double(x_norm), C.c_int64(total),
                                     C.byref(out)))
+    return out.value
+
+
+def exact_fit(x: np.ndarray, lam, factors, device: int = -1) -> float:
+    """exact_fit (solver.hpp:161-181) on the device from a host tensor."""
+    lam = np.ascontiguousarray(np.asarray(lam, dtype=np.float64))
+    fs = [_f64(f) for f in factors]
+    out = C.c_double()
+    check(lib().cprand_exact_fit(_p(_flat(x)), _p(_dims(x.shape)), x.ndim, _p(lam), _ptrs(fs),
+                                 C.c_int64(lam.size), device, C.byref(out)))
     return out.value
 
 

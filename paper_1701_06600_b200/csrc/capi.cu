@@ -192,6 +192,28 @@ int cprand_solve(int32_t method, const double* x, const int64_t* dims, int32_t o
   });
 }
 
+int cprand_tensor_exact_fit(cprand_tensor_t t, const double* lambda, const double* const* factors, int64_t r,
+                            double* fit) {
+  return guarded([&] {
+    need(t);
+    if (!lambda || !factors || !fit) throw InvalidArgument("exact_fit: null model or output");
+    *fit = device_exact_fit(*t->t, lambda, factors, static_cast<int>(r));
+  });
+}
+
+int cprand_exact_fit(const double* x, const int64_t* dims, int32_t order, const double* lambda,
+                     const double* const* factors, int64_t r, int32_t device, double* fit) {
+  return guarded([&] {
+    const auto d = dims_of(dims, order);
+    if (!x || !lambda || !factors || !fit) throw InvalidArgument("exact_fit: null input");
+    const int dev = pick_device(device);
+    CPB_CUDA(cudaSetDevice(dev));
+    Tensor t(d, dev);
+    CPB_CUDA(cudaMemcpy(t.d, x, sizeof(double) * t.p, cudaMemcpyHostToDevice));
+    *fit = device_exact_fit(t, lambda, factors, static_cast<int>(r));
+  });
+}
+
 int cprand_tensor_create(const int64_t* dims, int32_t order, int32_t device, cprand_tensor_t* out) {
   return guarded([&] {
     const auto d = dims_of(dims, order);

@@ -60,6 +60,11 @@ void big_free(void* p, size_t bytes);
 size_t big_cached_bytes();
 void big_release_all();
 
+struct Tensor;
+// exact_fit (solver.hpp:161-181) of the model (lambda, column-major factors)
+// to a device tensor: mode-1 MTTKRP on the device + the Gram expansion
+double device_exact_fit(const Tensor& t, const double* lambda, const double* const* factors, int r);
+
 struct Tensor {
   std::vector<i64> dims, strides;
   i64 p = 0;

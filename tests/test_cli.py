@@ -46,8 +46,10 @@ def test_usage_and_argument_errors(cli, tmp_path):
     assert rc == 2 and "--in is required" in err
     rc, _, err = run(cli, "decompose", "--in", "x", "--rank", "3", "--out", "m", "--bogus", "1")
     assert rc == 2 and "unknown option" in err
-    rc, _, err = run(cli, "eval", "--in", "x")
+    rc, _, err = run(cli, "gen", "--out", "x")
     assert rc == 2 and "not on the B200 path" in err
+    rc, _, err = run(cli, "eval", "--in", "x")
+    assert rc == 2 and "--model is required" in err
 
 
 def test_dnt1_reader_rejects_bad_files(cli, tmp_path):
@@ -111,3 +113,37 @@ def test_bench_iter_csv(cli, tmp_path):
     assert all(float(r[3]) > 0 for r in rows)
     rc, _, err = run(cli, "bench-iter", "--in", str(f), "--rank", "4", "--method", "als")
     assert rc == 2 and "outside the B200 path" in err
+
+
+@pytest.mark.gpu
+def test_eval_fit_and_score(cli, tmp_path):
+    """eval: the exact fit on the GPU and the score against a truth model
+    (the decompose output read back through the model JSON reader)."""
+    import oracle as orc
+    x, truth = orc.gen_baseline((20, 18, 16), 3, 0.3, 0.01, 8)
+    f = tmp_path / "x.dnt"
+    write_dnt1(f, x)
+    rc, _, err = run(cli, "decompose", "--in", str(f), "--method", "rand", "--rank", "3", "--samples", "60",
+                     "--seed", "8", "--max-iters", "30", "--out", str(tmp_path / "m.json"))
+    assert rc == 0, err
+    model = json.loads((tmp_path / "m.json").read_text())
+    lam = np.array(model["lambda"])
+    fs = [np.array(a) for a in model["factors"]]
+    (tmp_path / "t.json").write_text(json.dumps({"lambda": [1.0] * 3, "factors": [a.tolist() for a in truth]}))
+    rc, out, err = run(cli, "eval", "--model", str(tmp_path / "m.json"), "--in", str(f),
+                       "--truth", str(tmp_path / "t.json"))
+    assert rc == 0, err
+    kv = dict(l.split(",") for l in out.strip().split("\n"))
+    assert abs(float(kv["fit"]) - orc.exact_fit(x, lam, fs)) < 1e-10
+    assert abs(float(kv["score"]) - orc.score(fs, truth)) < 1e-12
+    # R > 8: the Hungarian matching (synth.hpp:181-185)
+    g = np.random.default_rng(5)
+    a = [g.standard_normal((d, 10)) for d in (20, 18, 16)]
+    b = [g.standard_normal((d, 10)) for d in (20, 18, 16)]
+    for name, fs_ in (("a.json", a), ("b.json", b)):
+        (tmp_path / name).write_text(json.dumps({"lambda": [1.0] * 10, "factors": [m.tolist() for m in fs_]}))
+    rc, out, err = run(cli, "eval", "--model", str(tmp_path / "a.json"), "--in", str(f),
+                       "--truth", str(tmp_path / "b.json"))
+    assert rc == 0, err
+    kv = dict(l.split(",") for l in out.strip().split("\n"))
+    assert abs(float(kv["score"]) - orc.score(a, b)) < 1e-12

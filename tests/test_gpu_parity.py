@@ -685,3 +685,23 @@ def test_session_gather_bench_bytes(pb, orc):
     assert bmin == 8.0 * 10 * s * dims[0] + 32.0 * 10 * s * (dims[1] + dims[2])
     sess.close()
     t.close()
+
+
+@pytest.mark.parametrize("dims,r", [((30, 24, 20), 4), ((12, 10, 8, 6), 3), ((64, 40, 50), 20)])
+def test_exact_fit_matches_oracle(pb, orc, dims, r):
+    """exact_fit (solver.hpp:161-181) on the device (mode-1 MTTKRP through the
+    split-K GEMM, Gram expansion) against the oracle's, for a solved model
+    and for a random one; zero tensor -> 1."""
+    x, _ = orc.gen_baseline(dims, r, 0.5, 0.01, 6)
+    res = orc.cprand(x, r, 60, orc.SolveOptions(rng_seed=6, max_iters=10, stall_limit=1000))
+    want = orc.exact_fit(x, res.lam, res.factors)
+    assert abs(pb.exact_fit(x, res.lam, res.factors) - want) < 1e-10
+    t = pb.DeviceTensor(dims)
+    t.upload(x)
+    assert abs(t.exact_fit(res.lam, res.factors) - want) < 1e-10
+    g = np.random.default_rng(2)
+    lam = g.standard_normal(r)
+    fs = [g.standard_normal((d, r)) for d in dims]
+    assert abs(t.exact_fit(lam, fs) - orc.exact_fit(x, lam, fs)) < 1e-10
+    t.close()
+    assert pb.exact_fit(np.zeros(dims), lam, fs) == 1.0

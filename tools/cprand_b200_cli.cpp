@@ -10,16 +10,21 @@
 //                [--trace trace.csv] [--device D]
 //   cprand_b200 bench-iter --in X.dnt --rank R [--method M]... [--samples S]
 //                [--iters N] [--transform fft|dct|wht] [--seed N] [--out f.csv]
+//   cprand_b200 eval --model M.json --in X.dnt [--truth T.json]
+//                (exact fit on the GPU: mode-1 MTTKRP + Gram expansion;
+//                 score: synth.hpp:146-185 on the host)
 //
 // Exit codes as the reference (cprand_main.cpp:365-386): 0 ok, 2 usage /
 // invalid input / any other error, 3 numerical consistency error.
-// `gen`, `bench-fitcheck` and `eval` are not on the B200 path:
-// use the reference's tool for them; the DNT1 files are the same.
+// `gen` and `bench-fitcheck` are not on the B200 path: use the
+// reference's tool for them; the DNT1 files are the same.
 #include <cprand_b200/cprand.hpp>
 #include <cprand_b200/io.hpp>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
+#include <limits>
 #include <iostream>
 #include <map>
 #include <optional>
@@ -150,10 +155,8 @@ int run_decompose(const Args& a) {
   }
   std::cout << std::setprecision(17);
   std::cout << "method=" << method_name(m) << " iters=" << res.iterations << " fit=";
-  if (res.trace.empty())
-    std::cout << (res.reason == cprand::StopReason::zero_tensor ? "1" : "nan");
-  else
-    std::cout << res.trace.back().fit;
+  // the reference reports the exact fit when there is no trace (cprand_main.cpp:157-160)
+  std::cout << (res.trace.empty() ? cprand::exact_fit(x, res.model) : res.trace.back().fit);
   std::cout << " time_s=" << res.total_seconds << " stop=" << stop_name(res.reason) << '\n';
   return 0;
 }
@@ -194,9 +197,109 @@ int run_bench_iter(const Args& a) {
   return 0;
 }
 
+// score (synth.hpp:146-185): best matching of the per-component products of
+// column cosines over the modes; exhaustive for R <= 8, Hungarian beyond
+std::vector<int> hungarian_min(const std::vector<double>& cost, int n) {
+  const double inf = std::numeric_limits<double>::infinity();
+  std::vector<double> u(n + 1, 0.0), v(n + 1, 0.0), minv(n + 1);
+  std::vector<int> p(n + 1, 0), way(n + 1, 0);
+  std::vector<char> used(n + 1);
+  for (int i = 1; i <= n; ++i) {
+    p[0] = i;
+    int j0 = 0;
+    std::fill(minv.begin(), minv.end(), inf);
+    std::fill(used.begin(), used.end(), 0);
+    do {
+      used[j0] = 1;
+      const int i0 = p[j0];
+      double delta = inf;
+      int j1 = 0;
+      for (int j = 1; j <= n; ++j)
+        if (!used[j]) {
+          const double cur = cost[static_cast<size_t>((i0 - 1) * n + (j - 1))] - u[i0] - v[j];
+          if (cur < minv[j]) {
+            minv[j] = cur;
+            way[j] = j0;
+          }
+          if (minv[j] < delta) {
+            delta = minv[j];
+            j1 = j;
+          }
+        }
+      for (int j = 0; j <= n; ++j)
+        if (used[j]) {
+          u[p[j]] += delta;
+          v[j] -= delta;
+        } else {
+          minv[j] -= delta;
+        }
+      j0 = j1;
+    } while (p[j0] != 0);
+    do {
+      const int j1 = way[j0];
+      p[j0] = p[j1];
+      j0 = j1;
+    } while (j0);
+  }
+  std::vector<int> match(n);
+  for (int j = 1; j <= n; ++j) match[p[j] - 1] = j - 1;
+  return match;
+}
+
+double score(const cprand::KruskalModel& a, const cprand::KruskalModel& b) {
+  if (a.order() != b.order() || a.rank() != b.rank()) throw std::invalid_argument("score: models must share dims and rank");
+  const int r = static_cast<int>(a.rank());
+  std::vector<double> ps(static_cast<size_t>(r * r), 1.0);
+  for (Index n = 0; n < a.order(); ++n) {
+    const cprand::Matd& fa = a.factors[static_cast<size_t>(n)];
+    const cprand::Matd& fb = b.factors[static_cast<size_t>(n)];
+    if (fa.rows != fb.rows) throw std::invalid_argument("score: models must share dims and rank");
+    auto norm = [](const cprand::Matd& f, int c) {
+      double s2 = 0.0;
+      for (Index i = 0; i < f.rows; ++i) s2 += f(i, c) * f(i, c);
+      return std::sqrt(s2);
+    };
+    for (int i = 0; i < r; ++i)
+      for (int j = 0; j < r; ++j) {
+        const double na = norm(fa, i), nb = norm(fb, j);
+        double dot = 0.0;
+        for (Index k = 0; k < fa.rows; ++k) dot += fa(k, i) * fb(k, j);
+        ps[static_cast<size_t>(i * r + j)] *= (na > 0 && nb > 0) ? dot / (na * nb) : 0.0;
+      }
+  }
+  double total = 0.0;
+  if (r <= 8) {
+    std::vector<int> perm(static_cast<size_t>(r));
+    for (int i = 0; i < r; ++i) perm[static_cast<size_t>(i)] = i;
+    double best = -std::numeric_limits<double>::infinity();
+    do {
+      double t = 0.0;
+      for (int i = 0; i < r; ++i) t += ps[static_cast<size_t>(i * r + perm[static_cast<size_t>(i)])];
+      best = std::max(best, t);
+    } while (std::next_permutation(perm.begin(), perm.end()));
+    total = best;
+  } else {
+    std::vector<double> neg(ps.size());
+    for (size_t e = 0; e < ps.size(); ++e) neg[e] = -ps[e];
+    const auto m = hungarian_min(neg, r);
+    for (int i = 0; i < r; ++i) total += ps[static_cast<size_t>(i * r + m[static_cast<size_t>(i)])];
+  }
+  return total / r;
+}
+
+int run_eval(const Args& a) {
+  const cprand::KruskalModel m = cprand::read_model_file(a.one("model"));
+  const cprand::TensorD x = cprand::read_tensor_file(a.one("in"));
+  std::cout << std::setprecision(17);
+  std::cout << "fit," << cprand::exact_fit(x, m) << '\n';
+  if (a.has("truth")) std::cout << "score," << score(m, cprand::read_model_file(a.one("truth"))) << '\n';
+  return 0;
+}
+
 void usage(std::ostream& os) {
   os << "usage: cprand_b200 decompose --in X.dnt --rank R --method rand|mix|premix --out model.json [options]\n"
-        "       cprand_b200 bench-iter --in X.dnt --rank R [--method M]... [--iters N] [options]\n";
+        "       cprand_b200 bench-iter --in X.dnt --rank R [--method M]... [--iters N] [options]\n"
+        "       cprand_b200 eval --model M.json --in X.dnt [--truth T.json]\n";
 }
 
 }  // namespace
@@ -222,7 +325,13 @@ int main(int argc, char** argv) {
         if (!a.has(req)) throw std::invalid_argument(std::string("--") + req + " is required");
       return run_bench_iter(a);
     }
-    if (cmd == "gen" || cmd == "bench-fitcheck" || cmd == "eval") {
+    if (cmd == "eval") {
+      const Args a = parse(argc, argv, 2, {"model", "truth", "in"});
+      for (const char* req : {"model", "in"})
+        if (!a.has(req)) throw std::invalid_argument(std::string("--") + req + " is required");
+      return run_eval(a);
+    }
+    if (cmd == "gen" || cmd == "bench-fitcheck") {
       std::cerr << "error: '" << cmd << "' is not on the B200 path; use the reference's tool (same DNT1 files)\n";
       return 2;
     }
