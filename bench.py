@@ -239,6 +239,14 @@ def fit_runs(pb, t, cfg, dev, comm, steps, fresh, big):
             "device_loop_seconds_incl_warmup": loop_dev, "fit_sample_count": cfg["phat"],
             "final_fit_estimate": res.trace[-1][2] if res.trace else None,
             "note": "Session.run: estimate_fit + should_stop on device every iteration, host polls the stop flag"}
+    # the exact fit of the same final model (solver.hpp:161-181, device MTTKRP),
+    # the check the sampled estimate replaces (bench-fitcheck)
+    if comm is None and not big:
+        t.exact_fit(res.lam, res.factors)  # warm
+        t0 = time.perf_counter()
+        ef = t.exact_fit(res.lam, res.factors)
+        full["exact_fit"] = {"value": ef, "seconds": time.perf_counter() - t0,
+                             "estimate_minus_exact": (res.trace[-1][2] - ef) if res.trace else None}
     ttf = []
     for thr in (0.99, round(1.0 - 1.2 * cfg["eta"], 6)):
         fresh()
