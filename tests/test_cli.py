@@ -147,3 +147,15 @@ def test_eval_fit_and_score(cli, tmp_path):
     assert rc == 0, err
     kv = dict(l.split(",") for l in out.strip().split("\n"))
     assert abs(float(kv["score"]) - orc.score(a, b)) < 1e-12
+
+
+def test_io_header_round_trips(tmp_path):
+    """include/cprand_b200/io.hpp on the CPU: DNT1 and model-JSON round trips
+    bit for bit (17 significant digits), malformed inputs rejected."""
+    exe = tmp_path / "io_roundtrip"
+    subprocess.check_call(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-o", str(exe),
+                           os.path.join(ROOT, "tests", "cpp", "io_roundtrip.cpp"),
+                           "-L", os.path.join(ROOT, "paper_1701_06600_b200"), "-lcprand_b200",
+                           "-Wl,-rpath," + os.path.join(ROOT, "paper_1701_06600_b200")])
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stdout + out.stderr
