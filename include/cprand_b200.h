@@ -162,6 +162,14 @@ double* cprand_tensor_device_ptr(cprand_tensor_t t);
  * mode, sign then orthonormal DCT-II; ms_per_mode[order] (nullable) receives
  * the CUDA-event time of each mode's pass. */
 int cprand_tensor_mix(cprand_tensor_t t, int32_t transform, uint64_t seed, double* ms_per_mode);
+/* The passes of modes [mode_begin, mode_end) of mix_tensor only (signs drawn
+ * for every mode, as the whole pass does), ms_per_mode indexed by mode. */
+int cprand_tensor_mix_modes(cprand_tensor_t t, int32_t transform, uint64_t seed, int32_t mode_begin,
+                            int32_t mode_end, double* ms_per_mode);
+/* gather_fibers (tensor.hpp:188-212) read from a device tensor by plain
+ * strided copies (no kernel): idxs S x (order-1) column-major, out I_n x S
+ * column-major. For checking tensors too large to download. */
+int cprand_tensor_read_fibers(cprand_tensor_t t, int32_t mode, const int64_t* idxs, int64_t s, double* out);
 /* Slab of the BASELINE.json tensor with last dim shard_total (rank/nranks
  * from comm); noise scaled by the global norms (allreduced). Declared after
  * cprand_comm_t below. */
@@ -196,6 +204,9 @@ int cprand_session_kernel_stats(cprand_session_t s, int32_t mode, int32_t kind, 
 int cprand_session_phase_us(cprand_session_t s, double* out, int32_t cap, int32_t* n);
 /* Diagnostics: Gram solves that took the pivoted-Cholesky (min-norm) path. */
 int cprand_session_gram_fallbacks(cprand_session_t s, int64_t* out);
+/* 1 when the session runs one persistent kernel per outer iteration, 0 for
+ * the multi-kernel chain. */
+int cprand_session_fused(cprand_session_t s, int32_t* out);
 /* Measurement: batched gather_fibers (tensor.hpp:188-212) of the session's
  * sample tables, iterations 1..iters x every mode, from the mode-major
  * replicas (replicas != 0) or the tensor itself; CUDA-event ms and the

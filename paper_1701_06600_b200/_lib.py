@@ -79,6 +79,7 @@ EXPORTS = [
     "cprand_estimate_fit", "cprand_mix_tensor", "cprand_mix_factor", "cprand_unmix_factor",
     "cprand_unmix_rows", "cprand_debug_normal_stream", "cprand_comm_unique_id",
     "cprand_comm_create", "cprand_comm_destroy", "cprand_tensor_synth_slab", "cprand_tensor_mix",
+    "cprand_tensor_mix_modes", "cprand_tensor_read_fibers", "cprand_session_fused",
 ]
 
 _lib = None

@@ -221,6 +221,20 @@ class DeviceTensor:
         check(lib().cprand_tensor_mix(self.h, TRANSFORMS[transform], C.c_uint64(seed), _p(ms)))
         return [float(v) for v in ms]
 
+    def mix_modes(self, transform: str, seed: int, mode_begin: int, mode_end: int) -> list:
+        """The passes of modes [mode_begin, mode_end) of mix_tensor, in place."""
+        ms = np.zeros(len(self.dims), dtype=np.float64)
+        check(lib().cprand_tensor_mix_modes(self.h, TRANSFORMS[transform], C.c_uint64(seed), mode_begin,
+                                            mode_end, _p(ms)))
+        return [float(v) for v in ms[mode_begin:mode_end]]
+
+    def read_fibers(self, mode: int, idxs: np.ndarray) -> np.ndarray:
+        """gather_fibers of the device tensor by plain strided copies (I_n x S)."""
+        idxs = np.asfortranarray(idxs, dtype=np.int64)
+        out = np.empty((self.dims[mode], idxs.shape[0]), dtype=np.float64, order="F")
+        check(lib().cprand_tensor_read_fibers(self.h, mode, _p(idxs), C.c_int64(idxs.shape[0]), _p(out)))
+        return out
+
     def synth_slab(self, r: int, collinearity: float, eta: float, seed: int, shard_total: int, comm,
                    want_factors=False):
         """This rank's slab of the BASELINE.json tensor (last dim shard_total)."""
@@ -292,6 +306,13 @@ class Session:
         n = C.c_int32()
         check(lib().cprand_session_phase_us(self.h, out, 16, C.byref(n)))
         return [out[i] for i in range(min(n.value, 16))]
+
+    @property
+    def fused(self) -> bool:
+        """True when one persistent kernel runs each outer iteration."""
+        v = C.c_int32()
+        check(lib().cprand_session_fused(self.h, C.byref(v)))
+        return bool(v.value)
 
     def gram_fallbacks(self) -> int:
         """Gram solves so far that took the pivoted-Cholesky min-norm path."""

@@ -273,6 +273,22 @@ int cprand_tensor_mix(cprand_tensor_t t, int32_t transform, uint64_t seed, doubl
   });
 }
 
+int cprand_tensor_mix_modes(cprand_tensor_t t, int32_t transform, uint64_t seed, int32_t mode_begin,
+                            int32_t mode_end, double* ms_per_mode) {
+  return guarded([&] {
+    need(t);
+    op_tensor_mix(t->t.get(), transform, seed, ms_per_mode, mode_begin, mode_end);
+  });
+}
+
+int cprand_tensor_read_fibers(cprand_tensor_t t, int32_t mode, const int64_t* idxs, int64_t s, double* out) {
+  return guarded([&] {
+    need(t);
+    if (s < 0) throw InvalidArgument("sample count must be >= 0");
+    op_read_fibers(t->t.get(), mode, idxs, s, out);
+  });
+}
+
 double* cprand_tensor_device_ptr(cprand_tensor_t t) { return t ? t->t->d : nullptr; }
 
 void cprand_tensor_destroy(cprand_tensor_t t) { delete t; }
@@ -352,6 +368,13 @@ int cprand_session_phase_us(cprand_session_t s, double* out, int32_t cap, int32_
     const auto v = s->s->phase_us();
     *n = static_cast<int32_t>(v.size());
     for (size_t i = 0; i < v.size() && static_cast<int32_t>(i) < cap; ++i) out[i] = v[i];
+  });
+}
+
+int cprand_session_fused(cprand_session_t s, int32_t* out) {
+  return guarded([&] {
+    need(s);
+    *out = s->s->fused() ? 1 : 0;
   });
 }
 

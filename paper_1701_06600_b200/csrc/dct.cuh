@@ -189,6 +189,15 @@ __device__ inline void transform_group(const PlanArgs& p, const double* in, doub
   double2* b1 = sbuf + np * n;
   const int total = F * n;
   const bool contig = (st == 1);
+  // Two real fibers share one complex FFT, which leaks rounding between
+  // them; a fiber that is exactly zero must stay exactly zero, as in the
+  // reference's per-fiber transform (a zero factor column is refilled only
+  // when its norm is exactly 0, kruskal.hpp:57-63). Bit fl of s_nz: fiber
+  // f0 + fl has a nonzero entry (groups of more than 64 fibers: not tracked).
+  __shared__ unsigned long long s_nz;
+  if (threadIdx.x == 0) s_nz = F > 64 ? ~0ull : 0ull;
+  __syncthreads();
+  unsigned long long nz = 0ull;
   // ---- load (coalesced along i for contiguous fibers, along f otherwise)
   for (int t = threadIdx.x; t < total; t += blockDim.x) {
     int fl, i;
@@ -204,6 +213,7 @@ __device__ inline void transform_group(const PlanArgs& p, const double* in, doub
     if (f < nfib) {
       v = in[fib_addr(f, i, st, n)];
       if (col_div) v = v / col_div[f];  // lazily normalized factor column
+      if (v != 0.0 && fl < 64) nz |= 1ull << fl;
     }
     const int q = fl >> 1;
     if (forward) {
@@ -216,6 +226,7 @@ __device__ inline void transform_group(const PlanArgs& p, const double* in, doub
       slot[fl & 1] = v;
     }
   }
+  if (nz) atomicOr(&s_nz, nz);
   __syncthreads();
   double2* res;
   if (forward) {
@@ -271,6 +282,7 @@ __device__ inline void transform_group(const PlanArgs& p, const double* in, doub
       v = ((fl & 1) ? z.y : z.x) * invn;
       v *= sign[i];  // D_n after the adjoint (mixing.hpp:231)
     }
+    if (fl < 64 && !((s_nz >> fl) & 1ull)) v = 0.0;
     out[fib_addr(f, i, st, n)] = v;
   }
   __syncthreads();  // sbuf may be reused by the caller

@@ -18,6 +18,7 @@
 // kernels use (phases.cuh, dct.cuh), with the same reduction orders.
 #include "dct.cuh"
 #include "phases.cuh"
+#include "qr.cuh"
 #include "tile.cuh"
 
 namespace cpb {
@@ -133,7 +134,12 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
       } else {
         fail = ph::inverse_cta<RT, kFusedThreads>(A.part_gram, M.gparts, r, M.tol, A.ginv, A.gfull, A.info, fsm);
       }
-      if (fail) ph::pinv_fallback<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
+      if (fail) {
+        if (A.qrws)  // QR path (kr_linalg.hpp:105-118): the apply takes its rows from qr_rows
+          ph::qr_factor<RT>(A.z, M.v.s, r, M.qtol, A.qrws, A.ginv, A.info, fsm);
+        else
+          ph::pinv_fallback<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
+      }
       if (tid == 0) *A.gram_done = 0u;
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 7] = globaltimer();  // inverse done
     } else {
@@ -168,18 +174,29 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
     // small modes (one CTA applies): sum the split-K partials over the grid
     // first; otherwise each apply block sums its rows' partials as it loads
     // them (same order, k = 0, 1, ...: the same bits), no extra barrier
+    // QR mode (the inverse's pivot test failed): the rows come from qr_rows
+    const bool qr = A.qrws && __ldcg(A.info + 2) != 0;
+    const QrSrc qs{M.v.x, M.v.base, 0, M.est, M.v.s};
     if (M.tail1) {
       const i64 tot = M.v.in * r;
-      for (i64 e = static_cast<i64>(b) * kFusedThreads + tid; e < tot; e += static_cast<i64>(G) * kFusedThreads) {
-        double s = 0.0;
-        for (int k = 0; k < M.ks; ++k) s += A.part_rhs[static_cast<i64>(k) * tot + e];
-        A.rhs_full[e] = s;
+      if (qr) {
+        constexpr int BQ = kFusedThreads / RT;
+        for (i64 blk = b; blk * BQ < M.v.in; blk += G)
+          ph::qr_rows<RT, kFusedThreads>(qs, A.qrws, r, M.v.in, blk * BQ, BQ, A.rhs_full + blk * BQ * r, r, fsm);
+      } else {
+        for (i64 e = static_cast<i64>(b) * kFusedThreads + tid; e < tot; e += static_cast<i64>(G) * kFusedThreads) {
+          double s = 0.0;
+          for (int k = 0; k < M.ks; ++k) s += A.part_rhs[static_cast<i64>(k) * tot + e];
+          A.rhs_full[e] = s;
+        }
       }
       grid_bar();
     }
     {
       ModeWork wm = w;
       wm.a = M.mixed;  // the apply writes the mixed, unnormalized factor
+      wm.q = qs;
+      wm.qrws = A.qrws;
       constexpr int BI = kFusedThreads / RT;
       double* gi = fsm;                  // RT x (RT+1)
       double* rh = fsm + RT * (RT + 1);  // BI x (RT+1)
@@ -212,7 +229,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
         __syncthreads();
         double q = 0.0;
         for (int blk = b; blk < nblk; blk += G)
-          q += ph::apply_block<RT, kFusedThreads>(M.v.in, r, wm, nullptr, static_cast<i64>(blk) * BI, gi, rh);
+          q += qr ? ph::apply_block_qr<RT, kFusedThreads>(M.v.in, r, wm, static_cast<i64>(blk) * BI, rh,
+                                                           rh + BI * (RT + 1))
+                  : ph::apply_block<RT, kFusedThreads>(M.v.in, r, wm, nullptr, static_cast<i64>(blk) * BI, gi, rh);
         ph::ssq_store<RT, kFusedThreads>(q, r, A.ssq + static_cast<i64>(b) * r, rh);
         __threadfence();
         __syncthreads();
@@ -391,9 +410,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
     const FusedMode& Q = A.mode[m];
     ModeWork wq = work_of(A, Q);
     wq.ssq = A.ssq + static_cast<i64>(m & 1) * G * r;
-    ph::norms_final<RT, kFusedThreads>(r, Q.v.in, wq, static_cast<int>(Gw), m == 0, A.rng, fsm, nullptr,
-                                       m >= 1 ? A.mode[m - 1].norms : nullptr);
+    const unsigned long long zm = ph::norms_final<RT, kFusedThreads>(
+        r, Q.v.in, wq, static_cast<int>(Gw), m == 0, A.rng, fsm, nullptr, m >= 1 ? A.mode[m - 1].norms : nullptr);
     signal_add_rep(Q.nready, 1u, kRep);
+    return zm;
   };
   for (int n = 0; n < A.order; ++n) {
     const FusedMode& M = A.mode[n];
@@ -413,7 +433,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       for (int e = tid; e < P.tm; e += kFusedThreads) P.gm_cnt[e * kCS] = 0u;
     }
     if (is_inv) {
-      if (n >= 1) form_norms(n - 1);  // off the critical path: overlaps this mode's Z / Gram
+      // off the critical path: overlaps this mode's Z / Gram. A zero column
+      // refilled here (kruskal.hpp:57-63) may race with the tile CTAs reading
+      // the previous factor's rows for this mode's Z_S: the mode then takes
+      // the QR path on a Z_S rebuilt below from the refilled factor.
+      const unsigned long long zmask = n >= 1 ? form_norms(n - 1) : 0ull;
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 13] = globaltimer();
       // ---- Gram: the row-block reducers summed it (dist_gram), or sum the
       // split partials of every 8 x 8 block here (split order)
@@ -468,9 +492,23 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       __syncthreads();
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 15] = globaltimer();
       // ---- inverse (pivoted-Cholesky min-norm fallback when rank deficient)
-      const bool fail = ph::inverse_la<RT>(A.gsum + (GA ? (n & 1) * RT * RT : 0), r, M.tol, A.ginv, A.gfull, A.info, fsm,
-                                           A.phase_t ? A.phase_t + n * 16 + 11 : nullptr);
-      if (fail) ph::pinv_fallback<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
+      const bool rebuild = zmask != 0ull && A.qrws;
+      const bool fail = rebuild || ph::inverse_la<RT>(A.gsum + (GA ? (n & 1) * RT * RT : 0), r, M.tol, A.ginv,
+                                                      A.gfull, A.info, fsm, A.phase_t ? A.phase_t + n * 16 + 11 : nullptr);
+      if (fail) {
+        if (A.qrws) {  // QR path (kr_linalg.hpp:105-118)
+          const double* zq = A.z;
+          if (rebuild) {  // Z_S from the refilled factor, into the workspace's V block
+            ph::z_range<RT>(M.v, A.qrws, tid, kFusedThreads);
+            __threadfence_block();
+            __syncthreads();
+            zq = A.qrws;
+          }
+          ph::qr_factor<RT>(zq, M.v.s, r, M.qtol, A.qrws, A.ginv, A.info, fsm);
+        } else {
+          ph::pinv_fallback<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
+        }
+      }
       signal_add_rep(M.grdy, 1u, kRep);
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 7] = globaltimer();
     } else if (!is_idle) {
@@ -546,7 +584,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
       double* rh = gi + RT * LD;    // rows_per x LD
       const int rows_per = (BM + M.tk - 1) / M.tk;
       double* ob = rh + rows_per * LD;
-      bool have_ginv = false;
+      bool have_ginv = false, qr = false;
+      const QrSrc qs{M.v.x, M.v.base, 0, 1, M.v.s};
+      // QR staging: after ob, or ob itself when it is large enough
+      double* qstage = rows_per * LD >= ph::qr_rows_smem_doubles<RT, kFusedThreads>() ? ob : ob + rows_per * LD;
       for (int tt = rank; tt < ntiles; tt += Gw) {
         const int mt = tt % M.tm, kb = tt / M.tm;
         const i64 r0 = static_cast<i64>(mt) * BM + static_cast<i64>(kb) * rows_per;
@@ -567,8 +608,14 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
             gi[x * LD + y] = __ldcg(A.ginv + e);
           }
           have_ginv = true;
+          qr = A.qrws && __ldcg(A.info + 2) != 0;
         }
         __syncthreads();
+        if (qr) {  // QR mode: the rows from the sampled fibers (qr.cuh), times ginv = I
+          constexpr int BQ = kFusedThreads / RT;
+          for (int ch = 0; ch < nrow; ch += BQ)
+            ph::qr_rows<RT, kFusedThreads>(qs, A.qrws, r, in, r0 + ch, min(BQ, nrow - ch), rh + ch * LD, LD, qstage);
+        }
         for (int e = tid; e < nrow * r; e += kFusedThreads) {
           const int il = e / r, c = e - il * r;
           double o = 0.0;
@@ -649,6 +696,7 @@ size_t rand_smem_for(int zcap) {
   need = std::max<i64>(need, 48 * RT + 256);
   need = std::max<i64>(need, static_cast<i64>(kFusedThreads / RT) * (RT + 1));
   need = std::max<i64>(need, ph::kFitSmemDoubles);
+  need = std::max<i64>(need, ph::qr_factor_smem_doubles<RT>());
   return static_cast<size_t>(need) * sizeof(double);
 }
 
@@ -693,6 +741,14 @@ size_t fused_smem_bytes(int rt, bool mix, int max_dim) {
   need = std::max(need, static_cast<size_t>(16 * rt + 40) * sizeof(double));
   need = std::max(need, static_cast<size_t>(ph::kFitSmemDoubles) * sizeof(double));
   if (mix) need = std::max(need, static_cast<size_t>(2) * 16 * static_cast<size_t>(max_dim));
+  // QR path: the factorization (inverse CTA) and the apply's QR staging
+  const size_t qf = rt == 16 ? ph::qr_factor_smem_doubles<16>() : rt == 32 ? ph::qr_factor_smem_doubles<32>()
+                                                                          : ph::qr_factor_smem_doubles<64>();
+  const size_t qa = static_cast<size_t>(rt * (rt + 1) + (kFusedThreads / rt) * (rt + 1)) +
+                    (rt == 16 ? ph::qr_rows_smem_doubles<16, kFusedThreads>()
+                              : rt == 32 ? ph::qr_rows_smem_doubles<32, kFusedThreads>()
+                                         : ph::qr_rows_smem_doubles<64, kFusedThreads>());
+  need = std::max(need, std::max(qf, qa) * sizeof(double));
   return need;
 }
 

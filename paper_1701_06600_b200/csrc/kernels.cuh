@@ -24,6 +24,15 @@ void launch_base_offsets(const int* rows, int kept, int s, const i64* kstride_ho
 //   gram, gram_inverse (stream s2)    pinv(Z_S^T Z_S)                kr_linalg.hpp:105
 //   rhs_gemm                          split-K Z_S^T X_S^T partials
 //   mode_apply                        A_un = RHS * Ginv, norms, lambda kruskal.hpp:51
+// Fiber source of the QR path's rows (qr.cuh): X_S(i, s) = x[(row_off ?
+// row_off[s] : s * ld) + i * est].
+struct QrSrc {
+  const double* x;
+  const i64* row_off;
+  i64 ld, est;
+  int s;
+};
+
 struct ModeWork {
   double* z;           // [S][RT] sampled Khatri-Rao rows (zero padded)
   double* part_gram;   // [gram_parts][RT][RT]
@@ -41,7 +50,17 @@ struct ModeWork {
   int ks;              // sample splits of the RHS GEMM
   int ks_len;          // samples per split (multiple of the K tile)
   double tol;          // Gram pivot threshold (relative to the largest diagonal)
+  // QR path (qr.cuh, kr_linalg.hpp:105-118): used when a Gram pivot is <= tol
+  // * d_max and qrws is set; otherwise the pivoted-Cholesky min-norm fallback
+  double* qrws;         // workspace (qr_ws_doubles), or null
+  double qtol;          // the reference's rank threshold max(S, R) * eps
+  QrSrc q;              // the sampled fibers (set per iteration)
 };
+// doubles of QR workspace for S samples at rank bucket rt
+inline i64 qr_ws_doubles(int s, int rt) { return 2 * static_cast<i64>(s) * rt + 4 * static_cast<i64>(rt) * rt + 64; }
+// Gauss-Jordan pivot ratio below which the normal equations give way to the
+// QR path (normal-equation error grows like cond(Z_S)^2 eps)
+constexpr double kNeTol = 1e-6;
 
 int rank_bucket(int r);  // 16 / 32 / 64
 void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms);
@@ -54,8 +73,11 @@ void launch_gather_rows(const double* x, i64 in, i64 stride, const i64* base, in
 void launch_z(const ModeView& v, double* z, const int* stop, cudaStream_t st);
 void launch_gram(const double* z, int s, int r, double* part, const int* stop, cudaStream_t st);
 // gfull: gram_scratch_doubles(r) of global scratch (the reduced Gram + fallback work)
+// w.qrws set: a failed pivot test runs the QR factorization of w.z (qr.cuh),
+// else the pivoted-Cholesky pseudo-inverse of the Gram.
 void launch_gram_inverse(const double* part_gram, int nparts, int r, double tol, double* ginv,
-                         double* gfull, int* info, const int* stop, cudaStream_t st);
+                         double* gfull, int* info, const int* stop, cudaStream_t st,
+                         const double* z = nullptr, int s = 0, double qtol = 0.0, double* qrws = nullptr);
 // A rows at xs + row_off[s] (fibers read in place) or xs + s * ld (gathered
 // X_S, zero padded to ld); vec16 requires 16 B aligned row starts.
 void launch_rhs_gemm(const double* xs, i64 ld, const i64* row_off, bool vec16, const double* z, i64 in,
@@ -181,6 +203,8 @@ void launch_mix_pass(const DctPlan& p, const double* in, double* out, i64 st, i6
 // MIX path: RHS (I_n x R row-major) = D_n C^T (sum_ks part_rhs) per column
 void launch_reduce_rhs(const double* part_rhs, int ks, i64 in, int r, double* out,
                        cudaStream_t st);
+// the same, or (QR mode, w.info[2] set by the fallback) the QR solution rows
+void launch_reduce_rhs_qr(const ModeWork& w, i64 in, int r, double* out, cudaStream_t st);
 
 // ---- slab sharding (shard.cu) ---------------------------------------------
 void launch_gather_z_rows(const double* z, const int* idx, int cnt, int rt, double* out, cudaStream_t st);
@@ -212,6 +236,7 @@ struct FusedMode {
   int mtiles, ks, ks_len;
   int gparts, gklen;
   double tol;
+  double qtol;           // QR path rank threshold max(S, R) * eps
   double* a;             // A_un of this mode
   double* norms;         // its column norms
   double* mixed;         // MIX: mixed image of the factor
@@ -244,7 +269,8 @@ struct FusedIter {
   int order, r, first_mode_first_of_pass;
   FusedMode mode[kMaxOrder];
   double *z, *part_gram, *ginv, *gfull, *part_rhs, *ssq, *rhs_full, *lambda;
-  double *gpart, *gsum;  // CPRAND kernel: Gram block partials [nblk][tk][64], reduced Gram [RT][RT]
+  double *gpart, *gsum;
+  double* qrws;          // QR path workspace (qr.cuh), or null  // CPRAND kernel: Gram block partials [nblk][tk][64], reduced Gram [RT][RT]
   int* info;
   unsigned long long* rng;
   unsigned* ticket;      // [0] norm ticket, [1] fit ticket

@@ -16,6 +16,8 @@
 #include <vector>
 
 #include "dct.cuh"
+#include "qr.cuh"
+#include <algorithm>
 
 namespace cpb {
 
@@ -98,6 +100,30 @@ __global__ void reduce_rhs_kernel(const double* __restrict__ part, int ks, i64 i
   if (e >= in * r) return;
   double s = 0.0;
   for (int k = 0; k < ks; ++k) s += part[static_cast<i64>(k) * in * r + e];
+  out[e] = s;
+}
+
+// MIX chain: the RHS reduction, or in QR mode (qr.cuh) the QR solution rows
+// of block b (BI = 256 / RT rows; the unmix transform and the apply with
+// ginv = I follow as for the RHS)
+template <int RT>
+__global__ void __launch_bounds__(256) reduce_rhs_qr_kernel(ModeWork w, i64 in, int r, double* __restrict__ out) {
+  if (w.stop && *w.stop) return;
+  constexpr int BI = 256 / RT;
+  if (w.qrws && __ldcg(w.info + 2) != 0) {
+    __shared__ double st[ph::qr_rows_smem_doubles<RT, 256>()];
+    __shared__ double rows[BI * (RT + 1)];
+    const i64 i0 = static_cast<i64>(blockIdx.x) * BI;
+    if (i0 >= in) return;  // uniform per block
+    ph::qr_rows<RT, 256>(w.q, w.qrws, r, in, i0, BI, rows, RT + 1, st);
+    const int il = threadIdx.x / RT, c = threadIdx.x % RT;
+    if (i0 + il < in && c < r) out[(i0 + il) * r + c] = rows[il * (RT + 1) + c];
+    return;
+  }
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= in * r) return;
+  double s = 0.0;
+  for (int k = 0; k < w.ks; ++k) s += w.part_rhs[static_cast<i64>(k) * in * r + e];
   out[e] = s;
 }
 
@@ -230,6 +256,17 @@ void launch_mode_transform(const DctPlan& p, const double* in, double* out, i64 
   if (blocks > 0x7fffffffLL) throw Unsupported("too many fibers for one launch");
   mode_transform_kernel<<<static_cast<unsigned>(blocks), kMixThreads, smem, stream>>>(
       a, in, out, st, nfib, F, sign, forward, col_div);
+  CPB_LAUNCH_CHECK();
+}
+
+void launch_reduce_rhs_qr(const ModeWork& w, i64 in, int r, double* out, cudaStream_t st) {
+  const int rt = rank_bucket(r);
+  const int grid = std::max(ceil_div(in * r, 256), ceil_div(in, 256 / rt));
+  switch (rt) {
+    case 16: reduce_rhs_qr_kernel<16><<<grid, 256, 0, st>>>(w, in, r, out); break;
+    case 32: reduce_rhs_qr_kernel<32><<<grid, 256, 0, st>>>(w, in, r, out); break;
+    default: reduce_rhs_qr_kernel<64><<<grid, 256, 0, st>>>(w, in, r, out); break;
+  }
   CPB_LAUNCH_CHECK();
 }
 

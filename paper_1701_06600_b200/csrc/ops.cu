@@ -225,16 +225,23 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
   w.stop = nullptr;
   w.ks = ks;
   w.ks_len = len;
-  w.tol = static_cast<double>(std::max<i64>(s, r)) * 2.220446049250313e-16;
+  // normal equations while every Gauss-Jordan pivot > kNeTol * d_max, else
+  // the QR path with the reference's rank threshold (qr.cuh)
+  DBuf qrws(static_cast<size_t>(qr_ws_doubles(static_cast<int>(s), rt)) * sizeof(double));
+  w.qtol = static_cast<double>(std::max<i64>(s, r)) * 2.220446049250313e-16;
+  w.tol = kNeTol;
+  w.qrws = qrws.as<double>();
+  w.q = QrSrc{xs.as<double>(), nullptr, ld, 1, static_cast<int>(s)};
   launch_gather_rows(v.x, in, v.stride, v.base, static_cast<int>(s), xs.as<double>(), ld, stream);
   launch_z(v, w.z, nullptr, stream);
   launch_gram(w.z, static_cast<int>(s), r, w.part_gram, nullptr, stream);
-  launch_gram_inverse(w.part_gram, gp, r, w.tol, w.ginv, w.gfull, w.info, nullptr, stream);
+  launch_gram_inverse(w.part_gram, gp, r, w.tol, w.ginv, w.gfull, w.info, nullptr, stream, w.z,
+                      static_cast<int>(s), w.qtol, w.qrws);
   launch_rhs_gemm(xs.as<double>(), ld, nullptr, true, w.z, in, static_cast<int>(s), r, ks, len, w.part_rhs, nullptr,
                   stream);
   const double* rhsp = nullptr;
   if (mix) {
-    launch_reduce_rhs(prhs.as<double>(), ks, in, r, rhs.as<double>(), stream);
+    launch_reduce_rhs_qr(w, in, r, rhs.as<double>(), stream);
     launch_mode_transform(plans[static_cast<size_t>(mode)], rhs.as<double>(), rhs.as<double>(), r, r,
                           dsigns[static_cast<size_t>(mode)]->as<double>(), 0, nullptr, stream);
     rhsp = rhs.as<double>();
@@ -389,14 +396,19 @@ void op_unmix_rows(const double* g, i64 s, i64 in, const std::vector<i64>& dims,
 
 // mix_tensor (mixing.hpp:130-156) in place on a device tensor: per mode,
 // sign then orthonormal DCT-II; ms[mode] = CUDA-event time of that pass.
-void op_tensor_mix(Tensor* t, int transform, std::uint64_t seed, double* ms) {
+void op_tensor_mix(Tensor* t, int transform, std::uint64_t seed, double* ms, int mode_begin, int mode_end) {
   if (transform != 1 && transform != 2) throw Unsupported("in-place device mixing supports the dct and wht transforms");
+  const int order = static_cast<int>(t->dims.size());
+  if (mode_end < 0) mode_end = order;
+  if (mode_begin < 0 || mode_begin > mode_end || mode_end > order) throw InvalidArgument("mode range out of bounds");
   CPB_CUDA(cudaSetDevice(t->device));
+  // every mode's signs are drawn in order from one stream (mixing.hpp:34-40),
+  // so a sub-range of the passes uses the same signs as the whole pass
   const auto signs = mixing_signs(t->dims, transform, seed);
   cudaEvent_t e0, e1;
   CPB_CUDA(cudaEventCreate(&e0));
   CPB_CUDA(cudaEventCreate(&e1));
-  for (size_t n = 0; n < t->dims.size(); ++n) {
+  for (size_t n = static_cast<size_t>(mode_begin); n < static_cast<size_t>(mode_end); ++n) {
     DBuf sg(signs[n].size() * sizeof(double));
     h2d(sg.p, signs[n].data(), signs[n].size());
     DctPlan plan = make_mix_plan(transform, static_cast<int>(t->dims[n]));
@@ -413,6 +425,27 @@ void op_tensor_mix(Tensor* t, int transform, std::uint64_t seed, double* ms) {
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+}
+
+void op_read_fibers(const Tensor* t, int mode, const i64* idxs, i64 s, double* out) {
+  // plain strided copies (no kernel): an independent read path for checking
+  // the device tensor against the oracle at sizes too large to download
+  const int order = static_cast<int>(t->dims.size());
+  if (mode < 0 || mode >= order) throw InvalidArgument("mode out of range");
+  CPB_CUDA(cudaSetDevice(t->device));
+  const i64 in = t->dims[static_cast<size_t>(mode)], st = t->strides[static_cast<size_t>(mode)];
+  for (i64 j = 0; j < s; ++j) {
+    i64 base = 0;
+    for (int c = 0, k = 0; k < order; ++k) {
+      if (k == mode) continue;
+      const i64 v = idxs[j + static_cast<i64>(c) * s];
+      if (v < 0 || v >= t->dims[static_cast<size_t>(k)]) throw InvalidArgument("sample index out of range");
+      base += v * t->strides[static_cast<size_t>(k)];
+      ++c;
+    }
+    CPB_CUDA(cudaMemcpy2D(out + j * in, sizeof(double), t->d + base, static_cast<size_t>(st) * sizeof(double),
+                          sizeof(double), static_cast<size_t>(in), cudaMemcpyDeviceToHost));
+  }
 }
 
 void op_debug_normals(std::uint64_t seed, int n, double* out) {

@@ -450,7 +450,10 @@ __device__ bool inverse_cta(const double* __restrict__ part, int nparts, int r, 
       for (int u = 0; u < TC; ++u)
         if (row[t] < r && col[u] < r) ginv[row[t] * r + col[u]] = a[t][u];
   }
-  if (tid == 0) info[0] = fail ? -1 : r;
+  if (tid == 0) {
+    info[0] = fail ? -1 : r;
+    info[2] = 0;  // normal-equations mode (qr_factor sets 1)
+  }
   __syncthreads();
   CPB_INV_STAMP(31);
   return fail;
@@ -780,7 +783,10 @@ __device__ bool inverse_la(const double* __restrict__ g, int r, double tol, doub
       }
     }
   }
-  if (tid == 0) info[0] = fail ? -1 : r;
+  if (tid == 0) {
+    info[0] = fail ? -1 : r;
+    info[2] = 0;  // normal-equations mode (qr_factor sets 1)
+  }
   __syncthreads();
   CPB_INV_STAMP(31);
   return fail;
@@ -1027,7 +1033,10 @@ __device__ bool inverse_b8(const double* __restrict__ g, int r, double tol, doub
       }
     }
   }
-  if (tid == 0) info[0] = fail ? -1 : r;
+  if (tid == 0) {
+    info[0] = fail ? -1 : r;
+    info[2] = 0;  // normal-equations mode (qr_factor sets 1)
+  }
   __syncthreads();
   CPB_INV_STAMP(31);
   return fail;
@@ -1296,7 +1305,10 @@ __device__ bool inverse_b8r(const double* __restrict__ g, int r, double tol, dou
       }
     }
   }
-  if (tid == 0) info[0] = fail ? -1 : r;
+  if (tid == 0) {
+    info[0] = fail ? -1 : r;
+    info[2] = 0;  // normal-equations mode (qr_factor sets 1)
+  }
   __syncthreads();
   return fail;
 }

@@ -371,6 +371,7 @@ Session::~Session() {
   dfree(part_gram_);
   dfree(ginv_);
   dfree(gfull_);
+  dfree(qrws_);
   dfree(info_);
   dfree(tickets_);
   dfree(ssq_);
@@ -510,6 +511,9 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   alloc_ring();
   ginv_ = dalloc<double>(static_cast<size_t>(r_ * r_));
   gfull_ = dalloc<double>(static_cast<size_t>(gram_scratch_doubles(r_)));
+  // QR path of the LS step (qr.cuh) wherever every sampled fiber is on this
+  // device; the sharded and FFT-kind paths keep the pivoted-Cholesky fallback
+  if (!shard_ && !cmix_) qrws_ = dalloc<double>(static_cast<size_t>(qr_ws_doubles(static_cast<int>(max_s), rt_)));
   info_ = dalloc<int>(4);
   CPB_CUDA(cudaMemsetAsync(info_, 0, 4 * sizeof(int), stream_));
   tickets_ = dalloc<unsigned>(8);
@@ -645,6 +649,7 @@ void Session::setup_fused() {
     A = FusedIter{};
     A.order = order_;
     A.r = r_;
+    A.qrws = qrws_;
     for (int n = 0; n < order_; ++n) {
       FusedMode& M = A.mode[n];
       M.v = view(it, n);
@@ -662,6 +667,7 @@ void Session::setup_fused() {
       M.ks_len = ks_len_[static_cast<size_t>(n)];
       gram_splits(s_mode_[static_cast<size_t>(n)], &M.gparts, &M.gklen);
       M.tol = work(n).tol;
+      M.qtol = work(n).qtol;
       M.a = fac_[static_cast<size_t>(n)];
       M.norms = norms_ + static_cast<i64>(n) * r_;
       if (mix_) {
@@ -1427,10 +1433,18 @@ ModeWork Session::work(int n) const {
   w.stop = has_fit_ ? &state_->stopped : nullptr;
   w.ks = ks_[static_cast<size_t>(n)];
   w.ks_len = ks_len_[static_cast<size_t>(n)];
-  // Gram-domain image of the reference's rank threshold max(S,R)*eps on
-  // |R_kk|/|R_11| (kr_linalg.hpp:88-92): Gram pivots are squared singular
-  // values, so the pivot test is d_k <= max(S,R)*eps * max_j G_jj.
-  w.tol = static_cast<double>(std::max(s_mode_[static_cast<size_t>(n)], r_)) * 2.220446049250313e-16;
+  // The reference's rank threshold max(S,R)*eps on |R_kk| / max pivot of
+  // the column-pivoted QR (kr_linalg.hpp:88-92, 105-118) is applied by the
+  // QR path itself (qtol). The normal equations are used while every
+  // Gauss-Jordan pivot exceeds kNeTol * max_j G_jj (their error grows like
+  // cond(Z_S)^2 eps); below, the mode takes the QR path. Without a QR
+  // workspace (sharded / FFT-kind paths) the pivot test is the Gram-domain
+  // d_k <= max(S,R)*eps * max_j G_jj, which flags |R_kk|/|R_11| <= about
+  // sqrt(max(S,R)*eps) (a pivoted-Cholesky min-norm solve follows): stricter
+  // than the reference there (Numerics).
+  w.qtol = static_cast<double>(std::max(s_mode_[static_cast<size_t>(n)], r_)) * 2.220446049250313e-16;
+  w.qrws = qrws_;
+  w.tol = qrws_ ? kNeTol : w.qtol;
   return w;
 }
 
@@ -1627,19 +1641,23 @@ void Session::enqueue_iteration() {
       continue;
     }
     const ModeView v = view(it, n);
-    const ModeWork w = work(n);
+    ModeWork w = work(n);
     const size_t slot = static_cast<size_t>(((it - 1) % depth_) * order_ + n);
+    const bool direct = direct_[static_cast<size_t>(n)];
+    // the fibers the QR path reads (the RHS GEMM's source)
+    w.q = direct ? QrSrc{n == 0 ? xsolve_ : rep_[static_cast<size_t>(n)], dbase_ptr(it, n), 0, 1, v.s}
+                 : QrSrc{ring_[slot], nullptr, ld_[static_cast<size_t>(n)], 1, v.s};
     // Z_S; the Gram and its pseudo-inverse run on s2 beside the RHS GEMM
     timed(n, 2, stream_, [&] { launch_z(v, w.z, stop, stream_); });
     CPB_CUDA(cudaEventRecord(ev_z_, stream_));
     CPB_CUDA(cudaStreamWaitEvent(stream2_, ev_z_, 0));
     timed(n, 3, stream2_, [&] { launch_gram(w.z, v.s, r_, w.part_gram, stop, stream2_); });
     timed(n, 4, stream2_, [&] {
-      launch_gram_inverse(w.part_gram, w.gram_parts, r_, w.tol, w.ginv, w.gfull, w.info, stop, stream2_);
+      launch_gram_inverse(w.part_gram, w.gram_parts, r_, w.tol, w.ginv, w.gfull, w.info, stop, stream2_, w.z, v.s,
+                          w.qtol, w.qrws);
     });
     CPB_CUDA(cudaEventRecord(ev_inv_, stream2_));
     // RHS GEMM: fibers read in place (mode 1 / replica) or from the gather ring
-    const bool direct = direct_[static_cast<size_t>(n)];
     if (!direct) CPB_CUDA(cudaStreamWaitEvent(stream_, ev_gathered_[slot], 0));
     timed(n, 1, stream_, [&] {
       if (direct)
@@ -1649,18 +1667,19 @@ void Session::enqueue_iteration() {
         launch_rhs_gemm(ring_[slot], ld_[static_cast<size_t>(n)], nullptr, true, w.z, v.in, v.s, r_, w.ks, w.ks_len,
                         w.part_rhs, stop, stream_);
     });
-    if (!direct) CPB_CUDA(cudaEventRecord(ev_consumed_[slot], stream_));
     CPB_CUDA(cudaStreamWaitEvent(stream_, ev_inv_, 0));
     timed(n, 5, stream_, [&] {
       const double* rhs = nullptr;
       if (mix_) {
-        launch_reduce_rhs(part_rhs_, w.ks, v.in, r_, rhs_full_, stream_);
+        launch_reduce_rhs_qr(w, v.in, r_, rhs_full_, stream_);
         launch_mode_transform(plans_[static_cast<size_t>(n)], rhs_full_, rhs_full_, r_, r_,
                               signs_[static_cast<size_t>(n)], 0, nullptr, stream_);
         rhs = rhs_full_;
       }
       launch_mode_apply(v.in, r_, w, rhs, n == 0, rng_state_, stream_);
     });
+    // the ring slot is free once the apply ran (the QR path reads it there)
+    if (!direct) CPB_CUDA(cudaEventRecord(ev_consumed_[slot], stream_));
     if (mix_)  // mixed image of the new (normalized) factor (mixing.hpp:297-298)
       timed(n, 6, stream_, [&] {
         launch_mode_transform(plans_[static_cast<size_t>(n)], fac_[static_cast<size_t>(n)],

@@ -246,6 +246,7 @@ class Session {
   double* part_gram_ = nullptr;
   double* ginv_ = nullptr;
   double* gfull_ = nullptr;
+  double* qrws_ = nullptr;   // QR path workspace (qr.cuh)
   int* info_ = nullptr;
   unsigned* tickets_ = nullptr;
   double* ssq_ = nullptr;
@@ -310,7 +311,9 @@ void op_transform_factor(const double* a, i64 rows, int r, const std::vector<i64
 void op_unmix_rows(const double* g, i64 s, i64 in, const std::vector<i64>& dims, int transform,
                    std::uint64_t seed, int mode, double* out);
 void op_debug_normals(std::uint64_t seed, int n, double* out);
-void op_tensor_mix(Tensor* t, int transform, std::uint64_t seed, double* ms);
+void op_tensor_mix(Tensor* t, int transform, std::uint64_t seed, double* ms, int mode_begin = 0,
+                   int mode_end = -1);
+void op_read_fibers(const Tensor* t, int mode, const i64* idxs, i64 s, double* out);
 void op_synth(Tensor* t, int r, double c, double eta, std::uint64_t seed, double* const* out_factors,
               i64 last_off = 0, i64 global_last = 0, const std::function<void(double*)>& reduce_sums = nullptr);
 

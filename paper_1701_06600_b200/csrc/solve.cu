@@ -5,17 +5,20 @@
 //
 //   z_kernel        Z_S rows (sampling.hpp:82-90), factors read A_un / norm
 //   gram_kernel     split-K Z_S^T Z_S partials                 (stream s2)
-//   gram_inverse    pinv of the Gram: Gauss-Jordan with a pivot test, then
-//                   a pivoted-Cholesky fallback kernel          (stream s2)
+//   gram_inverse    inverse of the Gram: Gauss-Jordan with a pivot test,
+//                   then the QR-path factorization kernel (qr.cuh) or, where
+//                   no workspace is given, a pivoted-Cholesky fallback  (s2)
 //   rhs_gemm        split-K Z_S^T X_S^T partials, FP64 FMA
 //   mode_apply      A_un = RHS * pinv(G), column norms, lambda rule
 //                   (kruskal.hpp:51-67), zero-column refill
 //
 // The reference solves min ||Z_S A^T - X_S^T|| by pivoted QR
 // (kr_linalg.hpp:105-118); the normal equations used here agree with it to
-// ~kappa(Z_S)^2 eps, inside the 1e-10 parity bar for the configs' Z_S.
+// ~kappa(Z_S)^2 eps, inside the 1e-10 parity bar while every Gauss-Jordan
+// pivot is above kNeTol * d_max; below, the mode takes the QR path.
 // Reductions run in a fixed order, so results are bitwise reproducible.
 #include "phases.cuh"
+#include "qr.cuh"
 
 namespace cpb {
 
@@ -68,6 +71,17 @@ __global__ void __launch_bounds__(kThreads) gram_pinv_fallback_kernel(double* gf
   ph::pinv_fallback<RT>(gfull, r, tol, ginv, info, perm);
 }
 
+// QR path (qr.cuh): exits at once unless the inverse's pivot test failed
+template <int RT>
+__global__ void __launch_bounds__(kThreads) qr_fallback_kernel(const double* __restrict__ z, int s, int r,
+                                                               double qtol, double* ws, double* __restrict__ ginv,
+                                                               int* info, const int* stop) {
+  if (stop && *stop) return;
+  if (info[0] >= 0) return;
+  extern __shared__ __align__(16) double qsm[];
+  ph::qr_factor<RT>(z, s, r, qtol, ws, ginv, info, qsm);
+}
+
 template <int RT, bool VEC16>
 __global__ void __launch_bounds__(kThreads) rhs_gemm_kernel(const double* __restrict__ xs, i64 ld,
                                                             const i64* __restrict__ row_off,
@@ -88,12 +102,18 @@ __global__ void __launch_bounds__(kApplyThreads) mode_apply_kernel(i64 in, int r
                                                                    unsigned long long* rng_state) {
   if (w.stop && *w.stop) return;
   constexpr int BI = kApplyThreads / RT;
-  __shared__ double gi[RT * (RT + 1)];
+  constexpr int GI = RT * (RT + 1) > ph::qr_rows_smem_doubles<RT, kApplyThreads>()
+                         ? RT * (RT + 1) : ph::qr_rows_smem_doubles<RT, kApplyThreads>();
+  __shared__ double gi[GI];  // the inverse, or the QR rows' staging
   __shared__ double rh[BI * (RT + 1)];
   __shared__ bool s_last;
-  ph::load_ginv<RT, kApplyThreads>(w.ginv, r, gi);
+  // QR mode (the MIX path brings its QR rows in rhs_full, times ginv = I)
+  const bool qr = w.qrws && !rhs_full && __ldcg(w.info + 2) != 0;
+  if (!qr) ph::load_ginv<RT, kApplyThreads>(w.ginv, r, gi);
   __syncthreads();
-  const double q = ph::apply_block<RT, kApplyThreads>(in, r, w, rhs_full, static_cast<i64>(blockIdx.x) * BI, gi, rh);
+  const i64 i0 = static_cast<i64>(blockIdx.x) * BI;
+  const double q = qr ? ph::apply_block_qr<RT, kApplyThreads>(in, r, w, i0, rh, gi)
+                      : ph::apply_block<RT, kApplyThreads>(in, r, w, rhs_full, i0, gi, rh);
   ph::ssq_store<RT, kApplyThreads>(q, r, w.ssq + static_cast<i64>(blockIdx.x) * r, rh);
   __threadfence();
   __syncthreads();
@@ -221,19 +241,32 @@ void launch_gram(const double* z, int s, int r, double* part, const int* stop, c
 
 template <int RT>
 static void inverse_t(const double* pg, int nparts, int r, double tol, double* ginv, double* gfull,
-                      int* info, const int* stop, cudaStream_t st) {
+                      int* info, const int* stop, cudaStream_t st, const double* z, int s, double qtol,
+                      double* qrws) {
   gram_inverse_kernel<RT><<<1, kInvThreads, 0, st>>>(pg, nparts, r, tol, ginv, gfull, info, stop);
   CPB_LAUNCH_CHECK();
-  gram_pinv_fallback_kernel<RT><<<1, kThreads, 0, st>>>(gfull, r, tol, ginv, info, stop);
+  if (qrws) {
+    const size_t sm = static_cast<size_t>(ph::qr_factor_smem_doubles<RT>()) * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+      CPB_CUDA(cudaFuncSetAttribute(qr_fallback_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sm)));
+      configured = true;
+    }
+    qr_fallback_kernel<RT><<<1, kThreads, sm, st>>>(z, s, r, qtol, qrws, ginv, info, stop);
+  } else {
+    gram_pinv_fallback_kernel<RT><<<1, kThreads, 0, st>>>(gfull, r, tol, ginv, info, stop);
+  }
   CPB_LAUNCH_CHECK();
 }
 
 void launch_gram_inverse(const double* part_gram, int nparts, int r, double tol, double* ginv,
-                         double* gfull, int* info, const int* stop, cudaStream_t st) {
+                         double* gfull, int* info, const int* stop, cudaStream_t st, const double* z, int s,
+                         double qtol, double* qrws) {
   switch (rank_bucket(r)) {
-    case 16: inverse_t<16>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st); break;
-    case 32: inverse_t<32>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st); break;
-    default: inverse_t<64>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st); break;
+    case 16: inverse_t<16>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st, z, s, qtol, qrws); break;
+    case 32: inverse_t<32>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st, z, s, qtol, qrws); break;
+    default: inverse_t<64>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st, z, s, qtol, qrws); break;
   }
 }
 
