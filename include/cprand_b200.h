@@ -264,12 +264,22 @@ int cprand_debug_normal_stream(uint64_t seed, int32_t n, double* out);
  * estimator are replicated; modes n < N-1 contract each rank's fibers and
  * allreduce the R x I_n right-hand sides, mode N-1 forms each rank's factor
  * rows, allreduces the column sums of squares and allgathers the slabs
- * (SURVEY.md §8e). Method rand only. */
+ * (SURVEY.md §8e). Methods rand and mix with a real transform (dct, wht);
+ * the DCT/WHT mixing pass exchanges slab blocks across the ranks. */
 typedef struct cprand_comm_s* cprand_comm_t;
 int cprand_comm_unique_id(uint8_t out[128]);
 int cprand_comm_create(const uint8_t id[128], int32_t rank, int32_t nranks, int32_t device,
                        cprand_comm_t* out);
 void cprand_comm_destroy(cprand_comm_t c);
+/* Loopback communicators: P ranks of ONE process on one device, one host
+ * thread per rank (each creates its slab tensor and session and drives it).
+ * Collectives meet at host barriers and read each other's device buffers in
+ * rank order. For running the sharded path where only one GPU exists (tests);
+ * not a performance path. */
+typedef struct cprand_loopback_s* cprand_loopback_t;
+int cprand_loopback_group_create(int32_t nranks, cprand_loopback_t* out);
+void cprand_loopback_group_destroy(cprand_loopback_t g);  /* after its communicators */
+int cprand_comm_create_loopback(cprand_loopback_t g, int32_t rank, int32_t device, cprand_comm_t* out);
 int cprand_tensor_synth_slab(cprand_tensor_t t, int64_t r, double collinearity, double eta, uint64_t seed,
                              int64_t shard_total, cprand_comm_t comm, double* const* out_factors);
 

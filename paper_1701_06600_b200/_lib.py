@@ -80,6 +80,7 @@ EXPORTS = [
     "cprand_unmix_rows", "cprand_debug_normal_stream", "cprand_comm_unique_id",
     "cprand_comm_create", "cprand_comm_destroy", "cprand_tensor_synth_slab", "cprand_tensor_mix",
     "cprand_tensor_mix_modes", "cprand_tensor_read_fibers", "cprand_session_fused",
+    "cprand_loopback_group_create", "cprand_loopback_group_destroy", "cprand_comm_create_loopback",
 ]
 
 _lib = None
@@ -107,6 +108,8 @@ def lib() -> C.CDLL:
     L.cprand_session_stream.argtypes = [C.c_void_p]
     L.cprand_comm_destroy.argtypes = [C.c_void_p]
     L.cprand_comm_destroy.restype = None
+    L.cprand_loopback_group_destroy.argtypes = [C.c_void_p]
+    L.cprand_loopback_group_destroy.restype = None
     L.cprand_options_init.restype = None
     L.cprand_host_alloc_pinned.restype = C.c_void_p
     L.cprand_host_alloc_pinned.argtypes = [C.c_uint64]

@@ -261,9 +261,13 @@ class Session:
     """Solver session over a DeviceTensor (setup once, iterate, read result)."""
 
     def __init__(self, method: str, t: DeviceTensor, r: int, s: int, opts: SolveOptions):
-        self.t, self.r, self.dims, self.opts = t, r, t.dims, opts
+        # the model's shape: a sharded session's tensor is a slab of the last mode
+        dims = t.dims
+        if opts.comm is not None and opts.shard_total > 0:
+            dims = tuple(dims[:-1]) + (int(opts.shard_total),)
+        self.t, self.r, self.dims, self.opts = t, r, dims, opts
         self.h = C.c_void_p()
-        il, ifs, iptr = _init_arrays(opts, t.dims, r)
+        il, ifs, iptr = _init_arrays(opts, dims, r)
         self._keep = (il, ifs)
         check(lib().cprand_session_create(METHODS[method], t.h, C.c_int64(r), C.c_int64(s),
                                           C.byref(opts.to_c()), _p(il) if il is not None else None,
@@ -495,13 +499,22 @@ def debug_normal_stream(seed: int, n: int) -> np.ndarray:
 
 class Comm:
     """NCCL communicator for slab-sharded runs (one process per GPU). Rank 0
-    creates the id (unique_id()), every rank passes it to Comm(...)."""
+    creates the id (unique_id()), every rank passes it to Comm(...).
+    Comm.loopback(group, rank) makes a rank of a LoopbackGroup instead."""
 
-    def __init__(self, uid: bytes, rank: int, nranks: int, device: int):
+    def __init__(self, uid: bytes | None, rank: int, nranks: int, device: int, _group=None):
         self.rank, self.nranks, self.device = rank, nranks, device
         self.h = C.c_void_p()
+        self._group = _group  # keeps a loopback group alive
+        if _group is not None:
+            check(lib().cprand_comm_create_loopback(_group.h, rank, device, C.byref(self.h)))
+            return
         buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
         check(lib().cprand_comm_create(buf, rank, nranks, device, C.byref(self.h)))
+
+    @staticmethod
+    def loopback(group: "LoopbackGroup", rank: int, device: int = 0) -> "Comm":
+        return Comm(None, rank, group.nranks, device, _group=group)
 
     @staticmethod
     def unique_id() -> bytes:
@@ -519,3 +532,27 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+class LoopbackGroup:
+    """P ranks of one process on one device (cprand_loopback_*): each rank's
+    host thread creates Comm.loopback(group, rank), its slab tensor and its
+    session; collectives meet at host barriers and sum in rank order. For
+    running the sharded path with one GPU (tests), not for performance."""
+
+    def __init__(self, nranks: int):
+        self.nranks = nranks
+        self.h = C.c_void_p()
+        check(lib().cprand_loopback_group_create(nranks, C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().cprand_loopback_group_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+

@@ -1,6 +1,5 @@
 // extern "C" boundary (include/cprand_b200.h). Exceptions never cross it:
 // each entry point maps the internal error taxonomy onto status codes.
-#include <nccl.h>
 
 #include <cmath>
 #include <cstring>
@@ -49,8 +48,12 @@ std::vector<i64> dims_of(const int64_t* dims, int32_t order) {
 }  // namespace
 
 struct cprand_comm_s {
-  ncclComm_t comm = nullptr;
+  std::unique_ptr<cpb::Comm> comm;  // NCCL, or a rank of a loopback group
   int rank = 0, nranks = 1, device = 0;
+};
+
+struct cprand_loopback_s {
+  std::shared_ptr<cpb::LoopbackGroup> g;
 };
 
 namespace {
@@ -76,7 +79,7 @@ Options opts_of(const cprand_options_t* o) {
   r.atomic_gram = o->atomic_gram != 0;
   if (o->comm != nullptr) {
     const auto* c = static_cast<const cprand_comm_s*>(o->comm);
-    r.nccl = c->comm;
+    r.comm = c->comm.get();
     r.nranks = c->nranks;
     r.rank = c->rank;
     r.shard_total = o->shard_total;
@@ -216,7 +219,8 @@ int cprand_exact_fit(const double* x, const int64_t* dims, int32_t order, const 
 
 int cprand_tensor_create(const int64_t* dims, int32_t order, int32_t device, cprand_tensor_t* out) {
   return guarded([&] {
-    const auto d = dims_of(dims, order);
+    if (dims == nullptr || order < 1) throw InvalidArgument("tensor order must be >= 1");
+    const std::vector<i64> d(dims, dims + order);  // Tensor checks them (an empty slab may have last dim 0)
     auto* h = new cprand_tensor_s;
     h->t = std::make_unique<Tensor>(d, pick_device(device));
     *out = h;
@@ -258,10 +262,7 @@ int cprand_tensor_synth_slab(cprand_tensor_t t, int64_t r, double c, double eta,
     const i64 off = lmax * comm->rank;
     const i64 len = std::max<i64>(0, std::min<i64>(shard_total, off + lmax) - off);
     if (t->t->dims.back() != len) throw InvalidArgument("slab tensor must hold rows [rank*ceil(I/P), ...)");
-    auto reduce = [&](double* sums) {
-      const ncclResult_t e = ncclAllReduce(sums, sums, 2, ncclDouble, ncclSum, comm->comm, nullptr);
-      if (e != ncclSuccess) throw CudaError(std::string("ncclAllReduce: ") + ncclGetErrorString(e));
-    };
+    auto reduce = [&](double* sums) { comm->comm->allreduce_sum(sums, 2, nullptr); };
     op_synth(t->t.get(), static_cast<int>(r), c, eta, seed, out_factors, off, shard_total, reduce);
   });
 }
@@ -466,38 +467,44 @@ int cprand_debug_normal_stream(uint64_t seed, int32_t n, double* out) {
 }
 
 int cprand_comm_unique_id(uint8_t out[128]) {
-  return guarded([&] {
-    ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess) throw CudaError("ncclGetUniqueId failed");
-    static_assert(sizeof(id) == 128, "ncclUniqueId size");
-    std::memcpy(out, &id, 128);
-  });
+  return guarded([&] { nccl_unique_id(out); });
 }
 
 int cprand_comm_create(const uint8_t id[128], int32_t rank, int32_t nranks, int32_t device,
                        cprand_comm_t* out) {
   return guarded([&] {
     if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("bad rank / nranks");
-    auto* c = new cprand_comm_s;
+    auto c = std::make_unique<cprand_comm_s>();
     c->rank = rank;
     c->nranks = nranks;
     c->device = pick_device(device);
-    CPB_CUDA(cudaSetDevice(c->device));
-    ncclUniqueId uid;
-    std::memcpy(&uid, id, 128);
-    const ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
-    if (r != ncclSuccess) {
-      delete c;
-      throw CudaError(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
-    }
-    *out = c;
+    c->comm = make_nccl_comm(id, rank, nranks, c->device);
+    *out = c.release();
   });
 }
 
-void cprand_comm_destroy(cprand_comm_t c) {
-  if (!c) return;
-  if (c->comm) ncclCommDestroy(c->comm);
-  delete c;
+int cprand_loopback_group_create(int32_t nranks, cprand_loopback_t* out) {
+  return guarded([&] {
+    auto g = std::make_unique<cprand_loopback_s>();
+    g->g = std::make_shared<LoopbackGroup>(nranks);
+    *out = g.release();
+  });
 }
+
+void cprand_loopback_group_destroy(cprand_loopback_t g) { delete g; }
+
+int cprand_comm_create_loopback(cprand_loopback_t g, int32_t rank, int32_t device, cprand_comm_t* out) {
+  return guarded([&] {
+    if (!g) throw InvalidArgument("null loopback group");
+    auto c = std::make_unique<cprand_comm_s>();
+    c->rank = rank;
+    c->nranks = g->g->nranks;
+    c->device = pick_device(device);
+    c->comm = make_loopback_comm(g->g, rank, c->device);
+    *out = c.release();
+  });
+}
+
+void cprand_comm_destroy(cprand_comm_t c) { delete c; }
 
 }  // extern "C"

@@ -16,7 +16,6 @@
 //    host keeps a bounded number of iterations in flight.
 #include "session.hpp"
 
-#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -111,8 +110,11 @@ void Options::validate() const {  // solver.hpp:54-63
 Tensor::Tensor(const std::vector<i64>& d, int dev) : dims(d), device(dev) {
   if (dims.empty()) throw InvalidArgument("tensor order must be >= 1");
   p = 1;
-  for (i64 v : dims) {
-    if (v < 1) throw InvalidArgument("tensor dims must be >= 1");
+  for (size_t k = 0; k < dims.size(); ++k) {
+    const i64 v = dims[k];
+    // a zero-length last mode is an empty slab of a sharded tensor
+    if (v < 1 && !(v == 0 && k + 1 == dims.size() && dims.size() > 1))
+      throw InvalidArgument("tensor dims must be >= 1");
     strides.push_back(p);
     p *= v;
   }
@@ -250,9 +252,11 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
   if (method == 2) transform_ = o_.transform >= 0 ? o_.transform : 0;
   if (method == 3) transform_ = o_.transform >= 0 ? o_.transform : 1;
   if (method >= 2) {
-    if (transform_ == 2)
-      for (i64 d : x->dims)
+    if (transform_ == 2)  // the model's shape (a sharded session's tensor is a slab of the last mode)
+      for (size_t k = 0; k < x->dims.size(); ++k) {
+        const i64 d = (o_.comm && k + 1 == x->dims.size() && o_.shard_total > 0) ? o_.shard_total : x->dims[k];
         if ((d & (d - 1)) != 0) throw InvalidArgument("wht requires power-of-two mode lengths");
+      }
     if (method == 3 && transform_ == 0)
       throw InvalidArgument("premix requires a real orthogonal transform");
     if (transform_ == 0) cmix_ = true;  // complex mixing (cfft.cu)
@@ -269,9 +273,9 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
   tdims_ = x->dims;
   tstrides_ = x->strides;
   tp_ = x->p;
-  if (o_.nccl) {
+  if (o_.comm) {
     shard_ = true;
-    nccl_ = o_.nccl;
+    comm_ = o_.comm;
     nranks_ = o_.nranks;
     rank_ = o_.rank;
     if (method != 1 && !(method == 2 && (transform_ == 1 || transform_ == 2)))
@@ -292,6 +296,7 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
     }
     p_ = st;
   }
+  if (p_ == 0) throw InvalidArgument("tensor has no entries");
   CPB_CUDA(cudaSetDevice(x->device));
   CPB_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, x->device));
   rt_ = rank_bucket(r);
@@ -776,16 +781,12 @@ void Session::setup_fused() {
 
 void Session::allreduce_sum(double* buf, i64 n) {
   if (!shard_ || n == 0) return;
-  const ncclResult_t r = ncclAllReduce(buf, buf, static_cast<size_t>(n), ncclDouble, ncclSum,
-                                       static_cast<ncclComm_t>(nccl_), stream_);
-  if (r != ncclSuccess) throw CudaError(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+  comm_->allreduce_sum(buf, n, stream_);
 }
 
 void Session::allgather(double* buf, i64 per_rank) {
   if (!shard_ || per_rank == 0) return;
-  const ncclResult_t r = ncclAllGather(buf + static_cast<i64>(rank_) * per_rank, buf, static_cast<size_t>(per_rank),
-                                       ncclDouble, static_cast<ncclComm_t>(nccl_), stream_);
-  if (r != ncclSuccess) throw CudaError(std::string("ncclAllGather: ") + ncclGetErrorString(r));
+  comm_->allgather(buf, per_rank, stream_);
 }
 
 // mix_tensor's last mode on a slab-sharded tensor: the
@@ -807,35 +808,28 @@ void Session::mix_last_mode_sharded() {
   const i64 mine = mq(rank_);
   double* buf = static_cast<double*>(big_alloc(static_cast<size_t>(std::max<i64>(1, M * L)) * sizeof(double)));
   double* wk = static_cast<double*>(big_alloc(static_cast<size_t>(std::max<i64>(1, mine * total)) * sizeof(double)));
-  const auto comm = static_cast<ncclComm_t>(nccl_);
-  auto nccl_ok = [](ncclResult_t r, const char* what) {
-    if (r != ncclSuccess) throw CudaError(std::string(what) + ": " + ncclGetErrorString(r));
-  };
+  std::vector<const double*> snd(static_cast<size_t>(P));
+  std::vector<double*> rcv(static_cast<size_t>(P));
+  std::vector<i64> sc(static_cast<size_t>(P)), rc(static_cast<size_t>(P));
   launch_slab_blocks(xsolve_, buf, M, L, mb, 1, stream_);
-  nccl_ok(ncclGroupStart(), "ncclGroupStart");
-  for (int q = 0; q < P; ++q)
-    if (mq(q) * L > 0)
-      nccl_ok(ncclSend(buf + static_cast<i64>(q) * mb * L, static_cast<size_t>(mq(q) * L), ncclDouble, q, comm, stream_),
-              "ncclSend");
-  for (int q = 0; q < P; ++q)
-    if (mine * lp(q) > 0)
-      nccl_ok(ncclRecv(wk + mine * static_cast<i64>(q) * lmax_, static_cast<size_t>(mine * lp(q)), ncclDouble, q, comm,
-                       stream_),
-              "ncclRecv");
-  nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+  for (int q = 0; q < P; ++q) {  // row block q of this slab -> rank q; rank q's slab of my row block <- q
+    const size_t u = static_cast<size_t>(q);
+    snd[u] = buf + static_cast<i64>(q) * mb * L;
+    sc[u] = mq(q) * L;
+    rcv[u] = wk + mine * static_cast<i64>(q) * lmax_;
+    rc[u] = mine * lp(q);
+  }
+  comm_->exchange(snd, sc, rcv, rc, stream_);
   const size_t k = static_cast<size_t>(N - 1);
   if (mine > 0) launch_mode_transform(plans_[k], wk, wk, mine, mine, signs_[k], 1, nullptr, stream_);
-  nccl_ok(ncclGroupStart(), "ncclGroupStart");
-  for (int q = 0; q < P; ++q)
-    if (mine * lp(q) > 0)
-      nccl_ok(ncclSend(wk + mine * static_cast<i64>(q) * lmax_, static_cast<size_t>(mine * lp(q)), ncclDouble, q, comm,
-                       stream_),
-              "ncclSend");
-  for (int q = 0; q < P; ++q)
-    if (mq(q) * L > 0)
-      nccl_ok(ncclRecv(buf + static_cast<i64>(q) * mb * L, static_cast<size_t>(mq(q) * L), ncclDouble, q, comm, stream_),
-              "ncclRecv");
-  nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+  for (int q = 0; q < P; ++q) {  // and back
+    const size_t u = static_cast<size_t>(q);
+    snd[u] = wk + mine * static_cast<i64>(q) * lmax_;
+    sc[u] = mine * lp(q);
+    rcv[u] = buf + static_cast<i64>(q) * mb * L;
+    rc[u] = mq(q) * L;
+  }
+  comm_->exchange(snd, sc, rcv, rc, stream_);
   launch_slab_blocks(xsolve_, buf, M, L, mb, 0, stream_);
   CPB_CUDA(cudaStreamSynchronize(stream_));
   big_free(buf, static_cast<size_t>(std::max<i64>(1, M * L)) * sizeof(double));

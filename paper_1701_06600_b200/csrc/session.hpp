@@ -11,6 +11,7 @@
 #include <random>
 #include <vector>
 
+#include "comm.hpp"
 #include "kernels.cuh"
 
 namespace cpb {
@@ -37,9 +38,9 @@ struct Options {  // SolveOptions (solver.hpp:40-64) + device extensions
   bool x_mutable = false;
   int replicas = -1;  // mode-major replicas for strided modes: -1 auto, 0 off, 1 on
   int fused = -1;     // persistent per-iteration kernel: -1 auto, 0 off (multi-kernel chain)
-  // slab sharding over NCCL: the session's tensor is this rank's slab of the
-  // last mode, rows [rank * ceil(I/P), ...) of a tensor with last dim shard_total
-  void* nccl = nullptr;  // ncclComm_t
+  // slab sharding: the session's tensor is this rank's slab of the last
+  // mode, rows [rank * ceil(I/P), ...) of a tensor with last dim shard_total
+  Comm* comm = nullptr;  // NCCL (one process per GPU) or loopback (tests)
   int nranks = 1, rank = 0;
   i64 shard_total = 0;
   bool atomic_gram = false;  // fused CPRAND kernel: Gram summed with L2 fp64 atomics (not reproducible)
@@ -157,7 +158,7 @@ class Session {
   i64 tp_ = 0;
   // slab sharding
   bool shard_ = false;
-  void* nccl_ = nullptr;
+  Comm* comm_ = nullptr;
   int nranks_ = 1, rank_ = 0;
   i64 slab_off_ = 0, slab_len_ = 0, lmax_ = 0;
   std::vector<i64> loc_off_;   // [iter][mode] offset into loc_idx_ / loc_dbase_

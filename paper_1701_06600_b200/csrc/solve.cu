@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(256) replica_kernel(const double* __restrict__
 }  // namespace
 
 void launch_replica(const double* x, i64 in, i64 st, i64 p, double* y, cudaStream_t stream) {
+  if (p == 0) return;  // an empty slab
   const i64 nhi = p / (st * in);
   replica_kernel<<<148 * 8, 256, 0, stream>>>(x, in, st, nhi, y);
   CPB_LAUNCH_CHECK();
