@@ -154,6 +154,17 @@ def barrier(dist):
         dist.barrier()
 
 
+def config_of(name: str, cfg, ws: int) -> dict:
+    """The workload description, identical in both arms (the driver compares them)."""
+    nbytes = 8 * int(np.prod(cfg["dims"]))
+    return {"workload": name, "dims": list(cfg["dims"]), "R": cfg["r"], "S": cfg["s"], "P_hat": cfg["phat"],
+            "method": cfg["method"], "transform": cfg["transform"], "bench_mode": True,
+            "parallelism": f"slab{ws} (last mode)" if ws > 1 else "single",
+            "l2": (f"inputs larger than L2 ({nbytes / 1e9:.2f} GB tensor, fresh random samples every step)"
+                   if nbytes > 126e6 else
+                   f"tensor ({nbytes / 1e6:.0f} MB) fits in L2; no flush: fresh random samples every step")}
+
+
 def launches_per_iter(cfg, fused: bool) -> int:
     if fused:
         return 1  # one persistent kernel per outer iteration
@@ -200,10 +211,8 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (BASELINE.json generator, seed 1)",
-        "config": {"workload": args.config, "dims": list(cfg["dims"]), "R": cfg["r"], "S": cfg["s"],
-                   "method": cfg["method"], "transform": cfg["transform"], "bench_mode": True,
-                   "l2": "tensor >> L2 (host run)"},
+        "data": "synthetic (BASELINE.json generator in HBM, seed 1)",
+        "config": config_of(args.config, cfg, ws),
         "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "port",
                          "sample": f"{args.steps} bench-mode outer iterations of {args.config} "
                                    f"(oracle restatement of the C++ reference; gather on "
@@ -283,6 +292,54 @@ def fit_runs(pb, t, cfg, dev, comm, steps, fresh, big):
     return full, ttf
 
 
+def c5_record(pb, dev, hbm_peak, steps, warmup, cpu: bool):
+    """The largest single-GPU configuration (C5: 320^4 = 84 GB, R = 20,
+    S = 1200, DCT CPRAND-MIX) measured beside the C4 headline: the mixing
+    pass per mode, the bench-mode rate of the persistent CPRAND-MIX kernel
+    on the session-mixed tensor, and the CPU reference path's bench-iter rate
+    on the same (device-mixed) tensor."""
+    cfg = CONFIGS["c5"]
+    p = int(np.prod(cfg["dims"]))
+    t = pb.DeviceTensor(cfg["dims"], device=dev)
+    t.synth(cfg["r"], cfg["c"], cfg["eta"], SEED)
+    ms_modes = t.mix("dct", SEED)
+    gbs = [16.0 * p / (m * 1e-3) / 1e9 for m in ms_modes]
+    out = {"config": config_of("c5", cfg, 1),
+           "mix_pass": {"ms_per_mode": [round(m, 3) for m in ms_modes], "gbs_per_mode": [round(g, 1) for g in gbs],
+                        "frac_per_mode": [round(g / hbm_peak, 3) for g in gbs],
+                        "bytes_model": "16 B per element per mode (read + write)"}}
+    t.synth(cfg["r"], cfg["c"], cfg["eta"], SEED)
+    s = pb.Session("mix", t, cfg["r"], cfg["s"],
+                   pb.SolveOptions(rng_seed=SEED, max_iters=warmup + steps + 2, bench_mode=True, transform="dct",
+                                   x_mutable=True, device=dev))
+    s.run(warmup)
+    ms = s.timed_enqueue(steps)
+    out.update({"value": steps / (ms * 1e-3), "unit": "iters/s", "ms_per_step": ms / steps, "steps": steps,
+                "kernel": "fused_iteration_kernel<32, MIX> (persistent)" if s.fused else "multi-kernel chain"})
+    s.close()
+    if cpu:
+        try:
+            buf = pb.PinnedBuffer(p)
+        except Exception as exc:  # host RAM too small for the 84 GB copy
+            out["cpu_baseline"] = {"value": None, "note": f"no host copy of the 84 GB mixed tensor: {exc}"}
+        else:
+            t.download_into(buf.array)  # the session mixed t in place: X_hat
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle as orc
+            os.environ.setdefault("CPRAND_THREADS", str(os.cpu_count() or 1))
+            per = orc.bench_mix_premixed(buf.array, cfg["dims"], cfg["r"], cfg["s"], "dct", SEED, 1)
+            n = int(max(1, min(40, 15.0 / max(per, 1e-6))))
+            secs = orc.bench_mix_premixed(buf.array, cfg["dims"], cfg["r"], cfg["s"], "dct", SEED, n)
+            out["cpu_baseline"] = {
+                "value": n / secs, "unit": "iters/s", "cores": os.cpu_count() or 1, "kind": "port",
+                "sample": f"{n} bench-mode CPRAND-MIX iterations (the reference's loop body, mixing.hpp:283-298) "
+                          f"on the device-mixed C5 tensor ({secs:.1f} s); bench-iter excludes setup "
+                          f"(tools/cprand_main.cpp:195-198), so the host mixing pass (hours) is not run"}
+            buf.close()
+    t.close()
+    return out
+
+
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -293,6 +350,7 @@ def main() -> int:
     ap.add_argument("--e2e-iters", type=int, default=100, help="iterations per e2e solve call")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 record of the default (c4) run")
     ap.add_argument("--atomic-gram", action="store_true",
                     help="time the loop with SolveOptions(atomic_gram=True) (not bitwise reproducible)")
     args = ap.parse_args()
@@ -313,6 +371,10 @@ def main() -> int:
     comm = None
     dims = list(cfg["dims"])
     if ws > 1:
+        # the communicator's topology / NVLS choice in the log (to stderr-bound
+        # NCCL INFO lines; the JSON line stays the last stdout line)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
         from paper_1701_06600_b200 import shard
         uid = [pb.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -518,23 +580,22 @@ def main() -> int:
         e2e = {"value": None, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                "note": host_skip}
 
+    c5 = None
+    if args.config == "c4" and ws == 1 and not args.no_c5:
+        pb.lib().cprand_device_cache_release()
+        c5 = c5_record(pb, dev, hbm_peak, args.steps, args.warmup, not args.no_cpu)
+        pb.lib().cprand_device_cache_release()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE.json generator in HBM, seed 1)",
-            "config": {"workload": args.config, "dims": list(cfg["dims"]), "R": cfg["r"],
-                       "S": cfg["s"], "P_hat": cfg["phat"], "method": cfg["method"],
-                       "transform": cfg["transform"], "bench_mode": True,
-                       "gram_sum": "L2 fp64 atomics (atomic_gram)" if args.atomic_gram else
-                                   "fixed-order split partials (bitwise reproducible)",
-                       "parallelism": f"slab{ws} (last mode, NCCL allreduce/allgather)" if ws > 1 else "single",
-                       "l2": (f"inputs larger than L2 ({8 * int(np.prod(cfg['dims'])) / 1e9:.2f} GB tensor, "
-                              f"fresh random samples every step)"
-                              if 8 * int(np.prod(cfg["dims"])) > 126e6 else
-                              f"tensor ({8 * int(np.prod(cfg['dims'])) / 1e6:.0f} MB) fits in L2; no flush: "
-                              f"fresh random samples every step")},
+            "config": config_of(args.config, cfg, ws),
+            "gram_sum": "L2 fp64 atomics (atomic_gram)" if args.atomic_gram else
+                        "fixed-order split partials (bitwise reproducible)",
+            "comm": "NCCL allreduce / allgather / send-recv" if ws > 1 else None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": kname,
                          "bytes_model": bytes_model, "per_mode_gbs": per_mode,
@@ -553,7 +614,7 @@ def main() -> int:
                              [round(x, 2) for x in phases])) if phases else None,
                          "gram_fallbacks": fallbacks, "mix_pass": mix_pass},
             "atomic_gram": atomic, "full_loop": full, "time_to_fit": ttf, "sampled_gather": gather,
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "c5": c5,
             "gpu_launches": launches_per_iter(cfg, used_fused) * args.steps,
         }
         print(json.dumps(line), flush=True)

@@ -1657,4 +1657,55 @@ double score(const KruskalModel& a, const KruskalModel& b) {
   return tot / static_cast<double>(r);
 }
 
+// bench-iter (tools/cprand_main.cpp:179-206, setup excluded from the rate)
+// of cprand_mix_impl (mixing.hpp:258-318) on a tensor that is ALREADY mixed
+// (the device-mixed C5 tensor, 84 GB: the reference's own setup would mix it
+// again on the host for hours, and bench-iter does not time setup). The loop
+// body is cprand_mix_impl's, bench mode (no estimator); the fibers are read
+// in place from x_hat (no copy of the tensor). Real kinds (dct, wht) only.
+// Returns the wall seconds of `iters` iterations. Test infrastructure (the
+// cpu_baseline leg of bench.py), not part of the reference.
+double bench_mix_premixed(const double* x_hat, const Shape& shape, Index r, Index s, TransformKind kind,
+                          std::uint64_t seed, int iters) {
+  {
+    if (kind == TransformKind::fft) throw std::invalid_argument("real transforms only");
+    const MixingOperator op = make_mixing_operator(shape, kind, seed);
+    KruskalModel model = init_random(shape, r, seed);
+    auto sample_rng = seeded_engine(seed, 2);
+    auto norm_rng = seeded_engine(seed, 1 + 7);
+    std::vector<Index> strides(shape.size());
+    Index st = 1;
+    for (std::size_t k = 0; k < shape.size(); ++k) {
+      strides[k] = st;
+      st *= shape[k];
+    }
+    std::vector<Matd> mixed(shape.size());
+    for (std::size_t n = 0; n < shape.size(); ++n) mixed[n] = mix_factor<double>(model.factors[n], op, static_cast<Index>(n));
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int it = 0; it < iters; ++it)
+      for (Index n = 0; n < static_cast<Index>(shape.size()); ++n) {
+        const SampleSet samples = draw_samples(shape, n, s, sample_rng);
+        const Matd zs = skr(samples, mixed, n);
+        // gather_fibers (tensor.hpp:188-212) from the caller's buffer
+        const Index in = shape[static_cast<std::size_t>(n)], stn = strides[static_cast<std::size_t>(n)];
+        Matd gathered(in, s);
+        parallel_for(Index{0}, s, Index{1 << 14} / std::max<Index>(in, 1), [&](Index col) {
+          Index base = 0, c = 0;
+          for (Index k = 0; k < static_cast<Index>(shape.size()); ++k) {
+            if (k == n) continue;
+            base += samples.idxs(col, c++) * strides[static_cast<std::size_t>(k)];
+          }
+          double* dst = gathered.col(col);
+          for (Index i = 0; i < in; ++i) dst[i] = x_hat[base + i * stn];
+        });
+        const Matd rhs = unmix_sampled_rhs<double>(transpose(gathered), op, n);
+        model.factors[static_cast<std::size_t>(n)] = transpose(real_least_squares(zs, rhs));
+        normalize_columns(model, n, n == 0, norm_rng);
+        mixed[static_cast<std::size_t>(n)] = mix_factor<double>(model.factors[static_cast<std::size_t>(n)], op, n);
+      }
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+}
+
+
 }  // namespace orc

@@ -223,6 +223,9 @@ SolveResult cprand_mix(const TensorD& x, Index r, Index s, const SolveOptions& o
 SolveResult cprand_premix(const TensorD& x, Index r, Index s, const SolveOptions& opts,
                           const MixingOperator& op);
 SolveResult cprand_premix(const TensorD& x, Index r, Index s, const SolveOptions& opts);
+// bench-iter of cprand_mix on an already-mixed tensor read in place (bench.py cpu_baseline for C5)
+double bench_mix_premixed(const double* x_hat, const Shape& shape, Index r, Index s, TransformKind kind,
+                          std::uint64_t seed, int iters);
 
 // Dense transforms (test helpers).
 void dct_forward(double* x, Index n);

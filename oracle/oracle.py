@@ -546,3 +546,13 @@ def score(fa, fb) -> float:
     _check(lib().orc_score(_ptrs(fa), _ptrs(fb), _p(_dims([f.shape[0] for f in fa])), len(fa),
                            C.c_int64(fa[0].shape[1]), C.byref(out)))
     return out.value
+
+
+def bench_mix_premixed(x_hat_flat: np.ndarray, dims, r: int, s: int, kind: str, seed: int, iters: int) -> float:
+    """Seconds of `iters` bench-mode cprand_mix iterations on an already-mixed
+    tensor (column-major flat buffer, read in place)."""
+    out = C.c_double()
+    _check(lib().orc_bench_mix_premixed(_p(x_hat_flat), _p(_dims(dims)), len(dims), C.c_int64(r), C.c_int64(s),
+                                        TRANSFORMS[kind], C.c_uint64(seed), int(iters), C.byref(out)))
+    return out.value
+

@@ -483,4 +483,12 @@ int orc_score(const double* const* fa, const double* const* fb, const std::int64
   });
 }
 
+int orc_bench_mix_premixed(const double* x_hat, const std::int64_t* dims, int order, std::int64_t r,
+                           std::int64_t s, int transform, std::uint64_t seed, int iters, double* out_seconds) {
+  return guarded([&] {
+    *out_seconds = bench_mix_premixed(x_hat, shape_of(dims, order), r, s, static_cast<TransformKind>(transform),
+                                      seed, iters);
+  });
+}
+
 }  // extern "C"

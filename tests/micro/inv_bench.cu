@@ -10,6 +10,7 @@ __device__ unsigned long long g_st[32];
 #define CPB_INV_STAMP_AT(k, s, who) \
   if ((s) == 5 && (who)) g_st[(k) - 24] = clock64();
 #include "phases.cuh"
+#include "inv8_variants.cuh"
 
 using namespace cpb;
 
