@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
     const i64 in = M.v.in;
     const int ntiles = M.tm * M.tk;
     if (n >= 1 && !is_idle)  // the previous mode's factor rows are all written
-      wait_geq(A.mode[n - 1].adone + (b % kRep) * kCS, seq * Gw, 64);
+      wait_geq(A.mode[n - 1].adone + (b % kRep) * kCS, seq * Gw);
     stamp(n, 0);
     if (b == 0) {  // reset the previous mode's counters: every wait on them is over
       const FusedMode& P = A.mode[(n + A.order - 1) % A.order];
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
     } else if (!is_idle) {
       const TileSmem t = tile_smem<RT>(fsm, M.zcap);
       if (n >= 2)  // Z_S divides by the norms of the modes before n-1
-        wait_geq(A.mode[n - 2].nready + (b % kRep) * kCS, seq, 64);
+        wait_geq(A.mode[n - 2].nready + (b % kRep) * kCS, seq);
       // this CTA's share of every one of its splits' Z rows, then signal
       // (no waiting here, so CTAs with several tiles cannot deadlock)
       for (int tt = rank; tt < ntiles; tt += Gw) {
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
         // the RHS streams the fibers only after the Gram is summed, so the
         // Gram's round trips do not queue behind the fiber traffic (the RHS
         // has slack: it is consumed after the inverse)
-        if (M.dist_gram && A.gram_first && !GA) wait_geq(M.gdone + (b % kRep) * kCS, static_cast<unsigned>(M.nblk), 64);
+        if (M.dist_gram && A.gram_first && !GA) wait_geq(M.gdone + (b % kRep) * kCS, static_cast<unsigned>(M.nblk));
         if (tt == static_cast<int>(rank)) stamp(n, 2);
         gemm_tile<RT>(M.v.x, M.vec16 != 0, in, static_cast<i64>(mt) * BM, r, cnt, kpad, t,
                       A.part_rhs + static_cast<i64>(kb) * in * r);
@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
           rh[il * LD + c] = sum_strided(p, step, M.tk);
         }
         if (!have_ginv) {
-          wait_geq(M.grdy + (rank % kRep) * kCS, 1u, 64);
+          wait_geq(M.grdy + (rank % kRep) * kCS, 1u);
           for (int e = tid; e < r * r; e += kFusedThreads) {
             const int x = e / r, y = e - x * r;
             gi[x * LD + y] = __ldcg(A.ginv + e);
@@ -639,12 +639,12 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
   {  // norms of the last mode (the next launch's Z_S and the fit need them)
     const FusedMode& L = A.mode[A.order - 1];
     if (is_inv) {
-      wait_geq(L.adone + (b % kRep) * kCS, seq * Gw, 64);
+      wait_geq(L.adone + (b % kRep) * kCS, seq * Gw);
       if constexpr (GA)  // the last mode's buffer, for the next launch
         for (int e = tid; e < RT * RT; e += kFusedThreads) A.gsum[((A.order - 1) & 1) * RT * RT + e] = 0.0;
       form_norms(A.order - 1);
     }
-    if (A.has_fit && !is_inv) wait_geq(L.nready + (b % kRep) * kCS, seq, 64);
+    if (A.has_fit && !is_inv) wait_geq(L.nready + (b % kRep) * kCS, seq);
   }
   // debug stamps of the tail (slot 14 of modes 0..2: norms seen, fit block, fit final)
   if (A.phase_t && b == 0 && tid == 0) A.phase_t[14] = globaltimer();
