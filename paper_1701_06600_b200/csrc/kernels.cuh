@@ -197,6 +197,9 @@ void launch_rhsc(const double* xh, const i64* base, i64 st, i64 in, int s, const
 // TMA-fed forward pass (mixtma.cu); false when the shape does not suit it
 bool launch_mix_tma(const DctPlan& p, double* x, i64 st, i64 nfib, const double* sign, cudaStream_t stream,
                     bool prepare_only);
+// register four-step pass (mixreg.cu) for strided modes; false when the shape does not suit it
+bool launch_mix_reg(const DctPlan& p, double* x, i64 st, i64 nfib, const double* sign, cudaStream_t stream,
+                    bool prepare_only);
 // prepare_only: load and configure the kernel the call would launch, no launch
 void launch_mix_pass(const DctPlan& p, const double* in, double* out, i64 st, i64 nfib, const double* sign,
                      int forward, cudaStream_t stream, bool prepare_only = false);

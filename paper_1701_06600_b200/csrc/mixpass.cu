@@ -561,6 +561,8 @@ bool launch_fwd_any(PlanArgs a, int nr, const int* rad, const double* in, double
 
 void launch_mix_pass(const DctPlan& pl, const double* in, double* out, i64 st, i64 nfib, const double* sign,
                      int forward, cudaStream_t stream, bool prepare_only) {
+  // v4: register four-step FFT for strided modes of supported lengths (mixreg.cu)
+  if (forward && in == out && launch_mix_reg(pl, out, st, nfib, sign, stream, prepare_only)) return;
   // v3: TMA-fed in-place pipeline (mixtma.cu) when the shape suits it
   if (forward && in == out && launch_mix_tma(pl, out, st, nfib, sign, stream, prepare_only)) return;
   PlanArgs a = dct_args(pl);

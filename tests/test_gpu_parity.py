@@ -557,18 +557,23 @@ def test_sharded_mix_session_single_rank(pb, orc, transform):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("dims", [(24, 30, 20), (96, 100, 90), (90, 100, 96), (64, 70, 77), (640, 70, 60)])
+@pytest.mark.parametrize("dims", [(24, 30, 20), (96, 100, 90), (90, 100, 96), (64, 70, 77), (640, 70, 60),
+                                  (320, 37, 120), (33, 320, 130), (50, 256, 90), (40, 1000, 110),
+                                  (256, 17, 16, 2)])
 def test_device_tensor_mix_matches_oracle(pb, orc, dims):
     """Whole-tensor mixing pass on the device. The larger shapes have >= 4096
     fibers per mode, so they run the persistent pass kernels: lengths 96 /
     100 / 90 (first radix 8 / 5 / 5; 16-32 sequences per group; fiber pairs
     adjacent or straddling a stride boundary), 640 contiguous (2 sequences,
-    two CTAs per SM), and 77 = 7 * 11 (the generic per-CTA transform)."""
+    two CTAs per SM), and 77 = 7 * 11 (the generic per-CTA transform). The
+    v4 register kernels (mixreg.cu): n = 320 / 256 contiguous with a partial
+    last tile of odd width, n = 320 / 256 / 1000 strided at strides 33 / 50 /
+    40 (partial tiles, a tile holding one unpaired fiber)."""
     x = orc.random_tensor(dims, 5)
     t = pb.DeviceTensor(dims)
     t.upload(x)
     ms = t.mix("dct", 7)
-    assert len(ms) == 3 and all(m > 0 for m in ms)
+    assert len(ms) == len(dims) and all(m > 0 for m in ms)
     got = t.download()
     want = orc.mix_tensor(x, "dct", 7)
     assert rel(got, want) < 1e-12
