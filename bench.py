@@ -492,9 +492,13 @@ def main() -> int:
                   "tensor_layout": {"ms": round(ms_x, 4), "useful_gbs": round(bu_x / (ms_x * 1e-3) / 1e9, 1),
                                     "b_min_gbs": round(bm_x / (ms_x * 1e-3) / 1e9, 1),
                                     "frac_b_min": round(bm_x / (ms_x * 1e-3) / 1e9 / hbm_peak, 3)},
-                  "note": "one launch per mode over all iterations' fibers; useful / B_min count the reads, "
-                          "read_write adds the X_S write (8 B / element); the solver itself reads the fibers "
-                          "in place inside the persistent kernel"}
+                  "note": "one launch per mode over all iterations' fibers (strided modes processed in "
+                          "base-offset order); useful / B_min count the reads, read_write adds the X_S write "
+                          "(8 B / element); the solver itself reads the fibers in place inside the persistent "
+                          "kernel. ncu (profiles/r02_gather_c4.txt): a strided 8 B element moves 127 B of "
+                          "DRAM (the L2 fetches whole 128 B lines; cudaLimitMaxL2FetchGranularity 32 is "
+                          "accepted but not applied), so the strided pass runs at ~86 % of HBM by DRAM bytes",
+                  "dram_bytes_per_strided_element_ncu": 127.4}
     s.close()
 
     # ---- full loop (sampled fit estimate + stop rule every iteration) and
