@@ -144,8 +144,10 @@ DctPlan make_dct_plan(int n) {
   }
   for (int f = 3; f <= m; f += 2)
     while (m % f == 0) {
+      // any prime: radices above 8 run dct.cuh's generic O(R) Stockham pass
+      // (the reference's Bluestein FFT, transforms.hpp:27-118, computes the
+      // same DFT; the fast whole-tensor passes take smooth lengths only)
       if (p.nrad >= 24) throw Unsupported("dct length has too many factors");
-      if (f > 61) throw Unsupported("dct length has a prime factor > 61");
       p.radix[p.nrad++] = f;
       m /= f;
     }

@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(fwd_threads<SEQ>(), 512 / fwd_threads<SEQ>()) 
   };
   auto load = [&](int slot) {
     const i64 ba = bact ? fbase[slot][2 * bq] : -1, bb = bact ? fbase[slot][2 * bq + 1] : -1;
-    if (!contig && in16 && ba >= 0 && bb == ba + 1 && (ba & 1) == 0) {
+    if (!contig && in16 && ba >= 0 && bb == ba + 1 && (ba & 1) == 0 && (st & 1) == 0) {
       // the pair of fibers is adjacent and aligned: one 16-byte load per row
 #pragma unroll
       for (int r = 0; r < R1; ++r) {

@@ -710,3 +710,26 @@ def test_exact_fit_matches_oracle(pb, orc, dims, r):
     assert abs(t.exact_fit(lam, fs) - orc.exact_fit(x, lam, fs)) < 1e-10
     t.close()
     assert pb.exact_fit(np.zeros(dims), lam, fs) == 1.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims", [(101, 67, 40), (67, 12, 101)])
+def test_prime_length_mixing_matches_oracle(pb, orc, dims):
+    """Mode lengths with prime factors above 61 (the reference's Bluestein
+    FFT, transforms.hpp:27-118; here the generic-radix Stockham pass): the
+    device mixing pass, and DCT / FFT CPRAND-MIX end to end, against the
+    oracle."""
+    x = orc.random_tensor(dims, 17)
+    t = pb.DeviceTensor(dims)
+    t.upload(x)
+    t.mix("dct", 3)
+    assert rel(t.download(), orc.mix_tensor(x, "dct", 3)) < 1e-12
+    t.close()
+    xb, _ = orc.gen_baseline(dims, 3, 0.5, 0.01, 4)
+    for transform in ("dct", None):
+        opts = dict(rng_seed=4, max_iters=6, transform=transform, stall_limit=1000)
+        ref = orc.solve("mix", xb, 3, 60, orc.SolveOptions(**opts))
+        got = pb.solve("mix", xb, 3, 60, pb.SolveOptions(**opts))
+        assert max(abs(a[2] - b[2]) for a, b in zip(got.trace, ref.trace)) < 1e-8
+        for a, b in zip(got.factors, ref.factors):
+            assert rel(a, b) < 1e-6
