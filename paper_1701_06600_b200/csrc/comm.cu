@@ -57,6 +57,56 @@ class NcclComm final : public Comm {
   }
   const char* kind() const override { return "nccl"; }
 
+  // CUDA IPC: peers' allocations mapped into this process (NVLink P2P).
+  // share_pointers returns an empty vector (on every rank) when some rank
+  // could not map a peer's memory; the session then runs the chain.
+  int peer_mode() const override { return 1; }
+  std::vector<void*> share_pointers(void* mine) override {
+    cudaIpcMemHandle_t h;
+    CPB_CUDA(cudaIpcGetMemHandle(&h, mine));
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    char* d = nullptr;
+    CPB_CUDA(cudaMalloc(&d, hb * static_cast<size_t>(nranks)));
+    CPB_CUDA(cudaMemcpy(d + hb * static_cast<size_t>(rank), &h, hb, cudaMemcpyHostToDevice));
+    nccl_ok(ncclAllGather(d + hb * static_cast<size_t>(rank), d, hb, ncclChar, comm_, nullptr), "ncclAllGather");
+    CPB_CUDA(cudaStreamSynchronize(nullptr));
+    std::vector<char> all(hb * static_cast<size_t>(nranks));
+    CPB_CUDA(cudaMemcpy(all.data(), d, all.size(), cudaMemcpyDeviceToHost));
+    CPB_CUDA(cudaFree(d));
+    std::vector<void*> out(static_cast<size_t>(nranks), nullptr);
+    double ok = 1.0;
+    for (int q = 0; q < nranks; ++q) {
+      if (q == rank) {
+        out[static_cast<size_t>(q)] = mine;
+        continue;
+      }
+      cudaIpcMemHandle_t hq;
+      std::memcpy(&hq, all.data() + hb * static_cast<size_t>(q), hb);
+      if (cudaIpcOpenMemHandle(&out[static_cast<size_t>(q)], hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        out[static_cast<size_t>(q)] = nullptr;
+        ok = 0.0;
+      }
+    }
+    double* dk = nullptr;  // every rank must have mapped every peer
+    CPB_CUDA(cudaMalloc(&dk, sizeof(double)));
+    CPB_CUDA(cudaMemcpy(dk, &ok, sizeof(double), cudaMemcpyHostToDevice));
+    nccl_ok(ncclAllReduce(dk, dk, 1, ncclDouble, ncclMin, comm_, nullptr), "ncclAllReduce");
+    CPB_CUDA(cudaStreamSynchronize(nullptr));
+    CPB_CUDA(cudaMemcpy(&ok, dk, sizeof(double), cudaMemcpyDeviceToHost));
+    CPB_CUDA(cudaFree(dk));
+    if (ok < 0.5) {
+      release_pointers(out);
+      return {};
+    }
+    return out;
+  }
+  void release_pointers(std::vector<void*>& ptrs) override {
+    for (int q = 0; q < static_cast<int>(ptrs.size()); ++q)
+      if (q != rank && ptrs[static_cast<size_t>(q)]) cudaIpcCloseMemHandle(ptrs[static_cast<size_t>(q)]);
+    ptrs.clear();
+  }
+
  private:
   ncclComm_t comm_ = nullptr;
 };
@@ -139,6 +189,31 @@ class LoopbackComm final : public Comm {
   }
   const char* kind() const override { return "loopback"; }
 
+  int peer_mode() const override { return 2; }
+  std::vector<void*> share_pointers(void* mine) override {
+    g_->ptrs[static_cast<size_t>(rank)] = mine;
+    g_->bar.arrive_and_wait();
+    std::vector<void*> out = g_->ptrs;
+    g_->bar.arrive_and_wait();
+    return out;
+  }
+  void launch_group(const void* my_args, cudaStream_t st,
+                    const std::function<void(const std::vector<const void*>&, cudaStream_t)>& launch) override {
+    // every rank's stream position, then one launch on rank 0's stream that
+    // all ranks' streams wait for (no rank's kernel waits on another launch)
+    CPB_CUDA(cudaEventRecord(g_->ev[static_cast<size_t>(rank)], st));
+    g_->ptrs[static_cast<size_t>(rank)] = const_cast<void*>(my_args);
+    g_->bar.arrive_and_wait();
+    if (rank == 0) {
+      for (int q = 1; q < nranks; ++q) CPB_CUDA(cudaStreamWaitEvent(st, g_->ev[static_cast<size_t>(q)], 0));
+      std::vector<const void*> args(g_->ptrs.begin(), g_->ptrs.end());
+      launch(args, st);
+      CPB_CUDA(cudaEventRecord(g_->ev_launch, st));
+    }
+    g_->bar.arrive_and_wait();
+    if (rank != 0) CPB_CUDA(cudaStreamWaitEvent(st, g_->ev_launch, 0));
+  }
+
  private:
   std::shared_ptr<LoopbackGroup> g_;
   double* tmp_ = nullptr;
@@ -149,8 +224,17 @@ class LoopbackComm final : public Comm {
 
 LoopbackGroup::LoopbackGroup(int p)
     : nranks(p), bar(p), slot(static_cast<size_t>(p), nullptr),
-      sends(static_cast<size_t>(p)), counts(static_cast<size_t>(p)) {
+      sends(static_cast<size_t>(p)), counts(static_cast<size_t>(p)), ptrs(static_cast<size_t>(p), nullptr),
+      ev(static_cast<size_t>(p), nullptr) {
   if (p < 1 || p > kMaxLoopRanks) throw InvalidArgument("loopback group: 1..16 ranks");
+  for (auto& e : ev) CPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CPB_CUDA(cudaEventCreateWithFlags(&ev_launch, cudaEventDisableTiming));
+}
+
+LoopbackGroup::~LoopbackGroup() {
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  if (ev_launch) cudaEventDestroy(ev_launch);
 }
 
 std::unique_ptr<Comm> make_nccl_comm(const unsigned char id[128], int rank, int nranks, int device) {

@@ -364,17 +364,50 @@ __device__ __forceinline__ void prefetch_tables(const FusedIter& A, unsigned b) 
   }
 }
 
-// GA: the Gram is summed with L2 fp64 atomics (FusedIter::gram_atomic)
-template <int RT, bool GA>
-__global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const FusedIter* __restrict__ args) {
+// Peer path: sys-scope polling with a time-out (a rank that never arrives
+// must not hang the GPU: after 20 s the wait gives up and flags *err, which
+// the host turns into an error).
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void peer_wait(const unsigned* p, unsigned target, int* err) {
+  if (threadIdx.x == 0) {
+    unsigned long long t0 = 0;
+    while (ld_relaxed_sys(p) < target) {
+      const unsigned long long now = globaltimer();
+      if (!t0) t0 = now;
+      if (now - t0 > 20000000000ull) {
+        atomicExch(err, 1);
+        break;
+      }
+    }
+    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void red_release_sys(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// GA: the Gram is summed with L2 fp64 atomics (FusedIter::gram_atomic).
+// PEER: the slab-sharded path (FusedIter::np ranks exchanging through peer
+// memory): modes n < N-1 contract this rank's fibers and exchange the RHS
+// rows of every apply share with the counterpart CTAs of the other ranks
+// (summed in rank order, so every rank applies the same rows); the last mode
+// applies the slab's rows and stores them, with their column sums of
+// squares, into every rank's factor.
+template <int RT, bool GA, bool PEER>
+__device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, const unsigned G, const unsigned b) {
   using namespace tl;
   const FusedIter& A = *args;
   if (A.stop && *A.stop) return;  // uniform: the flag only changes in a previous launch
   extern __shared__ __align__(16) double fsm[];
   __shared__ int perm[RT];
   __shared__ bool s_last;
-  const unsigned G = gridDim.x, b = blockIdx.x;
   const int tid = threadIdx.x;
+  const int np = PEER ? A.np : 1;
   if (A.census) {
     if (tid == 0) {
       unsigned sm;
@@ -410,8 +443,13 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
     const FusedMode& Q = A.mode[m];
     ModeWork wq = work_of(A, Q);
     wq.ssq = A.ssq + static_cast<i64>(m & 1) * G * r;
+    int nparts = static_cast<int>(Gw);
+    if (PEER && np > 1 && m == A.order - 1) {  // every rank's slab partials, in (rank, CTA) order
+      wq.ssq = A.pssq[A.prank];
+      nparts = np * static_cast<int>(Gw);
+    }
     const unsigned long long zm = ph::norms_final<RT, kFusedThreads>(
-        r, Q.v.in, wq, static_cast<int>(Gw), m == 0, A.rng, fsm, nullptr, m >= 1 ? A.mode[m - 1].norms : nullptr);
+        r, Q.in_full, wq, nparts, m == 0, A.rng, fsm, nullptr, m >= 1 ? A.mode[m - 1].norms : nullptr);
     signal_add_rep(Q.nready, 1u, kRep);
     return zm;
   };
@@ -422,6 +460,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
     const int ntiles = M.tm * M.tk;
     if (n >= 1 && !is_idle)  // the previous mode's factor rows are all written
       wait_geq(A.mode[n - 1].adone + (b % kRep) * kCS, seq * Gw);
+    if (PEER && np > 1 && n == 0 && seq > 1 && !is_idle)  // every rank's last-mode rows of the previous launch
+      peer_wait(A.mode[A.order - 1].adone + (b % kRep) * kCS, A.lastw * (seq - 1), A.perr);
     stamp(n, 0);
     if (b == 0) {  // reset the previous mode's counters: every wait on them is over
       const FusedMode& P = A.mode[(n + A.order - 1) % A.order];
@@ -572,8 +612,22 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
         // has slack: it is consumed after the inverse)
         if (M.dist_gram && A.gram_first && !GA) wait_geq(M.gdone + (b % kRep) * kCS, static_cast<unsigned>(M.nblk));
         if (tt == static_cast<int>(rank)) stamp(n, 2);
-        gemm_tile<RT>(M.v.x, M.vec16 != 0, in, static_cast<i64>(mt) * BM, r, cnt, kpad, t,
-                      A.part_rhs + static_cast<i64>(kb) * in * r);
+        if (PEER && np > 1 && n < A.order - 1) {
+          // this rank's fibers: local split kb of the owner-ordered range
+          const int l0 = M.loff + kb * M.tkllen;
+          const int cl = max(0, min(M.loff + M.lcnt, l0 + M.tkllen) - l0);
+          const int kpl = (cl + BK - 1) / BK * BK;
+          if (cl > 0) {
+            for (int g = l0 / M.tklen; g <= (l0 + cl - 1) / M.tklen; ++g)
+              wait_geq(M.kb_cnt + g * kCS, static_cast<unsigned>(M.tm));
+            z_load<RT>(M.v, A.z, l0, cl, kpl, t);
+          }
+          gemm_tile<RT>(M.v.x, M.vec16 != 0, in, static_cast<i64>(mt) * BM, r, cl, kpl, t,
+                        A.part_rhs + static_cast<i64>(kb) * in * r);
+        } else {
+          gemm_tile<RT>(M.v.x, M.vec16 != 0, in, static_cast<i64>(mt) * BM, r, cnt, kpad, t,
+                        A.part_rhs + static_cast<i64>(kb) * in * r);
+        }
         signal_add(M.mt_cnt + mt * kCS, 1u);
       }
       stamp(n, 3);
@@ -601,6 +655,28 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
           const double* p = A.part_rhs + (r0 + il) * r + c;
           rh[il * LD + c] = sum_strided(p, step, M.tk);
         }
+        if (PEER && np > 1 && n < A.order - 1) {
+          // every rank gets these rows' local sums (block prank of its
+          // receive buffer); the counterpart CTAs of the other ranks own the
+          // same rows (same tiling), and all sum the np blocks in rank order
+          __syncthreads();
+          for (int q = 0; q < np; ++q) {
+            double* dst = A.precv[q] + static_cast<i64>(A.prank) * A.rcv_ld + r0 * r;
+            for (int e = tid; e < nrow * r; e += kFusedThreads) dst[e] = rh[(e / r) * LD + e % r];
+          }
+          __threadfence_system();
+          __syncthreads();
+          const i64 slot = (static_cast<i64>(n) * A.ptiles + tt) * kCS;
+          if (tid < np) red_release_sys(A.prcnt[tid] + slot, 1u);
+          peer_wait(A.prcnt[A.prank] + slot, static_cast<unsigned>(np) * seq, A.perr);
+          const double* src = A.precv[A.prank] + r0 * r;
+          for (int e = tid; e < nrow * r; e += kFusedThreads) {
+            const int il = e / r, c = e - il * r;
+            double sum = 0.0;
+            for (int q = 0; q < np; ++q) sum += __ldcv(src + q * A.rcv_ld + e);
+            rh[il * LD + c] = sum;
+          }
+        }
         if (!have_ginv) {
           wait_geq(M.grdy + (rank % kRep) * kCS, 1u);
           for (int e = tid; e < r * r; e += kFusedThreads) {
@@ -620,7 +696,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
           const int il = e / r, c = e - il * r;
           double o = 0.0;
           for (int cc = 0; cc < r; ++cc) o = fma(rh[il * LD + cc], gi[cc * LD + c], o);
-          M.a[(r0 + il) * r + c] = o;
+          if (PEER && np > 1 && n == A.order - 1) {  // slab rows into every rank's factor
+            for (int q = 0; q < np; ++q) A.pfac[q][(A.slab_off + r0 + il) * r + c] = o;
+          } else {
+            M.a[(r0 + il) * r + c] = o;
+          }
           ob[il * LD + c] = o;
         }
         __syncthreads();
@@ -629,22 +709,33 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
         __syncthreads();
       }
       stamp(n, 4);
-      if (tid < r) A.ssq[static_cast<i64>(n & 1) * G * r + static_cast<i64>(rank) * r + tid] = q2;
-      signal_add_rep(M.adone, 1u, kRep);
+      if (PEER && np > 1 && n == A.order - 1) {
+        if (tid < r)
+          for (int q = 0; q < np; ++q) A.pssq[q][(static_cast<i64>(A.prank) * Gw + rank) * r + tid] = q2;
+        __threadfence_system();
+        __syncthreads();
+        if (tid < np * kRep) red_release_sys(A.pdone[tid / kRep] + (tid % kRep) * kCS, 1u);
+      } else {
+        if (tid < r) A.ssq[static_cast<i64>(n & 1) * G * r + static_cast<i64>(rank) * r + tid] = q2;
+        signal_add_rep(M.adone, 1u, kRep);
+      }
       stamp(n, 5);
     }
     stamp(n, 6);
   }
   if (A.next) prefetch_tables(*A.next, b);
   {  // norms of the last mode (the next launch's Z_S and the fit need them)
-    const FusedMode& L = A.mode[A.order - 1];
+    const FusedMode& Lm = A.mode[A.order - 1];
     if (is_inv) {
-      wait_geq(L.adone + (b % kRep) * kCS, seq * Gw);
+      if (PEER && np > 1)
+        peer_wait(Lm.adone + (b % kRep) * kCS, A.lastw * seq, A.perr);
+      else
+        wait_geq(Lm.adone + (b % kRep) * kCS, seq * Gw);
       if constexpr (GA)  // the last mode's buffer, for the next launch
         for (int e = tid; e < RT * RT; e += kFusedThreads) A.gsum[((A.order - 1) & 1) * RT * RT + e] = 0.0;
       form_norms(A.order - 1);
     }
-    if (A.has_fit && !is_inv) wait_geq(L.nready + (b % kRep) * kCS, seq);
+    if (A.has_fit && !is_inv) wait_geq(Lm.nready + (b % kRep) * kCS, seq);
   }
   // debug stamps of the tail (slot 14 of modes 0..2: norms seen, fit block, fit final)
   if (A.phase_t && b == 0 && tid == 0) A.phase_t[14] = globaltimer();
@@ -671,21 +762,38 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const Fuse
   }
 }
 
+template <int RT, bool GA>
+__global__ void __launch_bounds__(kFusedThreads, 2) fused_rand_kernel(const FusedIter* __restrict__ args) {
+  rand_body<RT, GA, false>(args, gridDim.x, blockIdx.x);
+}
+// the peer path: L.groups rank groups of gridDim.x / L.groups CTAs
+template <int RT>
+__global__ void __launch_bounds__(kFusedThreads, 2) peer_rand_kernel(const FusedLaunch L) {
+  const unsigned G = gridDim.x / static_cast<unsigned>(L.groups);
+  const unsigned grp = blockIdx.x / G;
+  const FusedIter* ap = L.a[0];
+#pragma unroll
+  for (int q = 1; q < kMaxPeer; ++q)  // unrolled selects (a dynamic index would go through local memory)
+    if (static_cast<int>(grp) == q) ap = L.a[q];
+  rand_body<RT, false, true>(ap, G, blockIdx.x - grp * G);
+}
+
 template <int RT>
 void* mix_fn() {
   return reinterpret_cast<void*>(&fused_iteration_kernel<RT, true>);
 }
 template <int RT>
-void* rand_fn(bool ga) {
+void* rand_fn(bool ga, bool peer = false) {
+  if (peer) return reinterpret_cast<void*>(&peer_rand_kernel<RT>);
   return ga ? reinterpret_cast<void*>(&fused_rand_kernel<RT, true>)
             : reinterpret_cast<void*>(&fused_rand_kernel<RT, false>);
 }
 
-void* pick(int rt, bool mix, bool ga = false) {
+void* pick(int rt, bool mix, bool ga = false, bool peer = false) {
   switch (rt) {
-    case 16: return mix ? mix_fn<16>() : rand_fn<16>(ga);
-    case 32: return mix ? mix_fn<32>() : rand_fn<32>(ga);
-    default: return mix ? mix_fn<64>() : rand_fn<64>(ga);
+    case 16: return mix ? mix_fn<16>() : rand_fn<16>(ga, peer);
+    case 32: return mix ? mix_fn<32>() : rand_fn<32>(ga, peer);
+    default: return mix ? mix_fn<64>() : rand_fn<64>(ga, peer);
   }
 }
 
@@ -722,7 +830,7 @@ size_t fused_rand_smem(int rt, int zcap) {
 }
 
 void fused_rand_tiles(i64 in, int s, int gw, int zcap, int* tm, int* tk, int* tklen) {
-  const int m = ceil_div(in, tl::BM);
+  const int m = std::max(1, ceil_div(in, tl::BM));  // an empty slab still gets one (empty) row block
   int k = std::max(1, gw / m);
   k = std::max(k, ceil_div(s, zcap));
   int len = ceil_div(s, k);
@@ -759,9 +867,12 @@ int fused_max_grid(int rt, bool mix, size_t smem, int device) {
   if (!coop) return 0;
   void* fn = pick(rt, mix);
   CPB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  if (!mix)
+  if (!mix) {
     CPB_CUDA(cudaFuncSetAttribute(pick(rt, false, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
+    CPB_CUDA(cudaFuncSetAttribute(pick(rt, false, false, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  }
   int per_sm = 0;
   CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFusedThreads, smem));
   return per_sm * sms;
@@ -771,6 +882,13 @@ void launch_fused_iteration(const FusedIter* dev_args, int rt, bool mix, int gri
                             cudaStream_t st, bool gram_atomic) {
   void* fn = pick(rt, mix, gram_atomic);
   void* params[] = {const_cast<FusedIter**>(&dev_args)};
+  CPB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFusedThreads), params, smem, st));
+}
+
+void launch_fused_peer(const FusedLaunch& l, int rt, int grid, size_t smem, cudaStream_t st) {
+  void* fn = pick(rt, false, false, true);
+  FusedLaunch lc = l;
+  void* params[] = {&lc};
   CPB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFusedThreads), params, smem, st));
 }
 

@@ -259,6 +259,12 @@ struct FusedMode {
   unsigned* adone;       // [kRep] replicas: tile CTAs whose factor rows are written (epoch count)
   unsigned* gdone;       // [kRep] replicas: Gram blocks summed (dist_gram)
   unsigned* nready;      // [kRep] replicas: this mode's norms / lambda are formed (epoch count)
+  i64 in_full;           // rows of the whole factor (a sharded last mode: I_N, not the slab)
+  // peer path (slab-sharded CPRAND kernel, np > 1), modes n < N-1: the
+  // sample list is ordered by owner rank (the same order on every rank), so
+  // this rank's fibers are the contiguous range [loff, loff + lcnt); the RHS
+  // tiles cut it into tk local splits of tkllen samples
+  int loff, lcnt, tkllen;
   unsigned* mcnt;        // [0] Gram blocks summed (or tiles written), [1] inverse ready,
                          // [2] tile CTAs whose sums of squares are written        (stride kCS)
 };
@@ -266,6 +272,7 @@ struct FusedMode {
 // shared line serialize): kCS words apart.
 constexpr int kCS = 32;
 constexpr int kRep = 16;  // replicas of widely polled flags
+constexpr int kMaxPeer = 8;  // ranks of the peer path
 constexpr int kSyncWords = 3 * kCS + 128 * kCS + kRep * kCS;  // gram_done, barrier, tickets, group tickets, gen replicas
 struct FusedIter;
 struct FusedIter {
@@ -296,6 +303,28 @@ struct FusedIter {
   int gram_first;                // CPRAND kernel: RHS tiles wait for the summed Gram
   int gram_atomic;               // CPRAND kernel: tiles add their Gram blocks into gsum[n & 1] (L2 fp64 adds)
   unsigned long long* cta_t;  // debug: per-CTA stamps of mode 1 [grid][16] (CPRAND_DEBUG_CTA)
+  // ---- peer path: the slab-sharded CPRAND kernel exchanging through peer
+  // memory (NVLink P2P stores of CUDA-IPC-mapped buffers, one process per
+  // GPU; or P rank groups of one launch on one device in the tests).
+  // Pointers [q] are rank q's buffers as this rank addresses them.
+  int np, prank;                 // ranks, this rank (np = 1: no exchange)
+  double* precv[kMaxPeer];       // rank q's RHS receive buffer [np][rcv_ld] (block p from rank p)
+  unsigned* prcnt[kMaxPeer];     // rank q's per-(mode, tile) arrival counters [order][ptiles] (stride kCS)
+  double* pfac[kMaxPeer];        // rank q's last-mode factor A_un [I_N][r]
+  double* pssq[kMaxPeer];        // rank q's last-mode column sums of squares [np][Gw][r]
+  unsigned* pdone[kMaxPeer];     // rank q's last-mode apply counter replicas [kRep] (stride kCS)
+  i64 rcv_ld;                    // doubles per sender block of precv
+  int ptiles;                    // tile slots per mode in prcnt
+  unsigned lastw;                // last-mode apply signals per launch, all ranks (sum of Gw)
+  i64 slab_off;                  // first row of this rank's slab in the last mode
+  int* perr;                     // set when a peer wait timed out (the host raises)
+};
+// One launch of the CPRAND kernel: `groups` rank groups of gridDim.x / groups
+// CTAs, group g running a[g] (groups > 1: the peer path's one-device test
+// harness; production launches one group per GPU).
+struct FusedLaunch {
+  const FusedIter* a[kMaxPeer];
+  int groups;
 };
 size_t fused_smem_bytes(int rt, bool mix, int max_dim);
 // CPRAND kernel: Z rows per tile, its dynamic shared memory, and the tiling
@@ -308,5 +337,7 @@ void fused_rand_tiles(i64 in, int s, int gw, int zcap, int* tm, int* tk, int* tk
 int fused_max_grid(int rt, bool mix, size_t smem, int device);
 void launch_fused_iteration(const FusedIter* dev_args, int rt, bool mix, int grid, size_t smem,
                             cudaStream_t st, bool gram_atomic = false);
+// The peer path's CPRAND kernel (grid = groups x group size).
+void launch_fused_peer(const FusedLaunch& l, int rt, int grid, size_t smem, cudaStream_t st);
 
 }  // namespace cpb

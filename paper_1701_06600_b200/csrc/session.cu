@@ -351,6 +351,13 @@ Session::~Session() {
   dfree(zloc_);
   dfree(sh_part_);
   dfree(gpart_);
+  if (comm_) {
+    comm_->release_pointers(parena_all_);
+    comm_->release_pointers(pfac_all_);
+  }
+  dfree(parena_);
+  if (perr_host_) cudaFreeHost(perr_host_);
+  perr_host_ = nullptr;
   dfree(gsum_);
   for (auto& e : ev_gathered_) cudaEventDestroy(e);
   for (auto& e : ev_consumed_) cudaEventDestroy(e);
@@ -569,7 +576,24 @@ void Session::setup_fused() {
   // (one 8-byte load per element); the CPRAND kernel's tiles need every
   // mode contiguous
   // the MIX kernel's in-kernel transforms are DCT-II: WHT runs the chain
-  if (o_.fused == 0 || (!all_direct && !mix_) || o_.exhaustive_samples || shard_ || cmix_ ||
+  // the sharded CPRAND path runs the peer kernel when every rank can
+  // (collective decision: every rank takes the same path)
+  if (shard_) {
+    static const bool peer_env = !(std::getenv("CPRAND_PEER") && std::atoi(std::getenv("CPRAND_PEER")) == 0);
+    const bool can = !mix_ && all_direct && o_.fused != 0 && peer_env && nranks_ <= kMaxPeer &&
+                     comm_->peer_mode() != 0;
+    double* f = dalloc<double>(1);
+    const double v = can ? 1.0 : 0.0;
+    CPB_CUDA(cudaMemcpyAsync(f, &v, sizeof(double), cudaMemcpyHostToDevice, stream_));
+    allreduce_sum(f, 1);
+    double tot = 0.0;
+    CPB_CUDA(cudaMemcpyAsync(&tot, f, sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+    dfree(f);
+    if (tot < nranks_ - 0.5) return;
+    peer_ = true;
+  }
+  if (o_.fused == 0 || (!all_direct && !mix_) || o_.exhaustive_samples || (shard_ && !peer_) || cmix_ ||
       (mix_ && transform_ == 2))
     return;
   i64 max_dim = 1;
@@ -581,21 +605,31 @@ void Session::setup_fused() {
     zcap = fused_rand_zcap(rt_);
     fsmem_ = fused_rand_smem(rt_, zcap);
   }
-  if (fsmem_ > 200 * 1024) return;
+  if (fsmem_ > 200 * 1024) {
+    peer_ = false;  // (the same on every rank: it depends on R only)
+    return;
+  }
   fgrid_ = fused_max_grid(rt_, mix_, fsmem_, x_->device);
+  // one device for every rank (the tests' loopback group): the ranks are
+  // groups of one launch, each with an equal share of the co-resident grid
+  const bool emulated = peer_ && comm_->peer_mode() == 2;
+  if (emulated) fgrid_ /= nranks_;
   int max_gp = 1;
   for (int n = 0; n < order_; ++n) {
     int gp, gl;
     gram_splits(s_mode_[static_cast<size_t>(n)], &gp, &gl);
     max_gp = std::max(max_gp, gp);
   }
-  if (fgrid_ < max_gp + 2) return;
+  if (fgrid_ < max_gp + 2) {
+    if (peer_) throw Unsupported("peer path: too few co-resident CTAs per rank");
+    return;
+  }
   // CPRAND kernel roles: a census launch maps CTAs to SMs; the Gram-inverse
   // CTA gets its SM to itself (its partner CTA idles) so the serial inverse
   // does not share the FP64 pipe with a GEMM tile. Only performance depends
   // on the mapping staying the same across launches.
   int inv_cta = fgrid_ - 1, idle_cta = -1;
-  if (!mix_) {
+  if (!mix_ && !emulated) {
     int* cen = dalloc<int>(static_cast<size_t>(fgrid_));
     FusedIter* dc = dalloc<FusedIter>(1);
     FusedIter c{};
@@ -623,7 +657,7 @@ void Session::setup_fused() {
     int& tk_max = tk_max_;
     for (int n = 0; n < order_; ++n) {
       const size_t k = static_cast<size_t>(n);
-      fused_rand_tiles(dims_[k], s_mode_[k], gw, zcap, &tm[k], &tk[k], &tkl[k]);
+      fused_rand_tiles(tdims_[k], s_mode_[k], gw, zcap, &tm[k], &tk[k], &tkl[k]);
       tm_max = std::max(tm_max, tm[k]);
       tk_max = std::max(tk_max, tk[k]);
       max_part = std::max(max_part, static_cast<i64>(tk[k]) * dims_[k] * r_);
@@ -641,6 +675,49 @@ void Session::setup_fused() {
     const size_t per = (2 * static_cast<size_t>(tm_max) + static_cast<size_t>(tk_max) + 3 + 4 * kRep) * kCS;
     fcnt_ = dalloc<unsigned>(per * order_);
     CPB_CUDA(cudaMemsetAsync(fcnt_, 0, per * order_ * sizeof(unsigned), stream_));
+  }
+  // peer path buffers: one arena per rank (receive buffer, per-tile arrival
+  // counters, last-mode sums of squares, last-mode apply counter), mapped by
+  // every rank together with the last mode's factor
+  i64 rcv_ld = 1, off_cnt = 0, off_ssq = 0, off_done = 0;
+  int ptiles = 1;
+  unsigned lastw = 0;
+  if (peer_) {
+    for (int n = 0; n + 1 < order_; ++n) {
+      rcv_ld = std::max<i64>(rcv_ld, dims_[static_cast<size_t>(n)] * r_);
+      ptiles = std::max(ptiles, tm[static_cast<size_t>(n)] * tk[static_cast<size_t>(n)]);
+    }
+    auto al = [](i64 b) { return (b + 255) / 256 * 256; };
+    off_cnt = al(static_cast<i64>(nranks_) * rcv_ld * 8);
+    off_ssq = off_cnt + al(static_cast<i64>(order_) * ptiles * kCS * 4);
+    off_done = off_ssq + al(static_cast<i64>(nranks_) * gw * r_ * 8);
+    const i64 bytes = off_done + al(static_cast<i64>(kRep) * kCS * 4);
+    parena_ = dalloc<char>(static_cast<size_t>(bytes));
+    CPB_CUDA(cudaMemsetAsync(parena_, 0, static_cast<size_t>(bytes), stream_));
+    CPB_CUDA(cudaHostAlloc(&perr_host_, sizeof(int), cudaHostAllocMapped));
+    *perr_host_ = 0;
+    CPB_CUDA(cudaHostGetDevicePointer(&perr_dev_, perr_host_, 0));
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+    // every rank's Gw (equal on identical devices; summed, not assumed)
+    double* f = dalloc<double>(1);
+    const double v = gw;
+    CPB_CUDA(cudaMemcpyAsync(f, &v, sizeof(double), cudaMemcpyHostToDevice, stream_));
+    allreduce_sum(f, 1);
+    double tot = 0.0;
+    CPB_CUDA(cudaMemcpyAsync(&tot, f, sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+    dfree(f);
+    lastw = static_cast<unsigned>(tot + 0.5);
+    if (lastw != static_cast<unsigned>(gw) * static_cast<unsigned>(nranks_))
+      throw Unsupported("peer path: ranks with different grids");
+    parena_all_ = comm_->share_pointers(parena_);
+    pfac_all_ = comm_->share_pointers(fac_[static_cast<size_t>(order_ - 1)]);
+    if (parena_all_.empty() || pfac_all_.empty()) {  // no peer mapping on some rank: the chain
+      comm_->release_pointers(parena_all_);
+      comm_->release_pointers(pfac_all_);
+      peer_ = false;
+      return;
+    }
   }
   fsync_ = dalloc<unsigned>(kSyncWords);
   CPB_CUDA(cudaMemsetAsync(fsync_, 0, kSyncWords * sizeof(unsigned), stream_));
@@ -705,10 +782,20 @@ void Session::setup_fused() {
         M.mcnt = c + static_cast<size_t>(tm_max + tk_max_) * kCS;
         M.gm_cnt = c + static_cast<size_t>(tm_max + tk_max_ + 3) * kCS;
         M.dist_gram = (tm[k] * tk[k] <= gw) ? 1 : 0;
+        M.in_full = dims_[k];
+        M.v.in = tdims_[k];  // a sharded last mode: the slab's rows
+        if (peer_) {
+          const size_t pi = static_cast<size_t>(ti * order_ + n);
+          M.loff = ploff_[pi];
+          M.lcnt = plcnt_[pi];
+          M.tkllen = M.lcnt > 0 ? std::max(4, (ceil_div(M.lcnt, tk[k]) + 3) / 4 * 4) : 0;
+        }
         M.grdy = c + static_cast<size_t>(2 * tm_max + tk_max_ + 3) * kCS;
         M.adone = M.grdy + static_cast<size_t>(kRep) * kCS;
         M.nready = M.adone + static_cast<size_t>(kRep) * kCS;
         M.gdone = M.nready + static_cast<size_t>(kRep) * kCS;
+        if (peer_ && nranks_ > 1 && n == order_ - 1)  // counted by every rank's apply CTAs
+          M.adone = reinterpret_cast<unsigned*>(parena_ + off_done);
         // Z_S of mode n >= 1 uses mode n-1's rows unnormalized (its norms are
         // formed concurrently; they only rescale columns of the solution)
         if (n >= 1) {
@@ -735,6 +822,24 @@ void Session::setup_fused() {
     A.gram_first = std::getenv("CPRAND_GRAM_FIRST") ? std::atoi(std::getenv("CPRAND_GRAM_FIRST")) : 0;
     A.gram_atomic = o_.atomic_gram ? 1 : 0;
     A.inv_cta = mix_ ? -1 : inv_cta;
+    A.np = 1;
+    if (peer_) {
+      A.np = nranks_;
+      A.prank = rank_;
+      for (int q = 0; q < nranks_; ++q) {
+        char* base = static_cast<char*>(parena_all_[static_cast<size_t>(q)]);
+        A.precv[q] = reinterpret_cast<double*>(base);
+        A.prcnt[q] = reinterpret_cast<unsigned*>(base + off_cnt);
+        A.pssq[q] = reinterpret_cast<double*>(base + off_ssq);
+        A.pdone[q] = reinterpret_cast<unsigned*>(base + off_done);
+        A.pfac[q] = static_cast<double*>(pfac_all_[static_cast<size_t>(q)]);
+      }
+      A.rcv_ld = rcv_ld;
+      A.ptiles = ptiles;
+      A.lastw = lastw;
+      A.slab_off = slab_off_;
+      A.perr = perr_dev_;
+    }
     A.idle_cta = mix_ ? -1 : idle_cta;
     A.census = nullptr;
     A.ssq = ssq_;
@@ -1111,6 +1216,40 @@ void Session::build_tables() {
             place(j);
           }
         }
+      }
+      if (shard_ && !mix_ && n < N - 1 && !o_.exhaustive_samples) {
+        // peer path: the samples ordered by the rank that owns their fiber
+        // (stable, the same order on every rank), so this rank's fibers are
+        // one contiguous range; only the summation order of the Gram and the
+        // RHS changes
+        std::vector<int> ord(static_cast<size_t>(sn));
+        std::iota(ord.begin(), ord.end(), 0);
+        const int* last = rb + static_cast<i64>(N - 2) * sn;
+        std::stable_sort(ord.begin(), ord.end(),
+                         [&](int a, int b2) { return last[a] / lmax_ < last[b2] / lmax_; });
+        std::vector<int> rtmp(static_cast<size_t>(sn));
+        for (int c = 0; c < N - 1; ++c) {
+          int* col = rb + static_cast<i64>(c) * sn;
+          for (int j = 0; j < sn; ++j) rtmp[static_cast<size_t>(j)] = col[ord[static_cast<size_t>(j)]];
+          std::copy(rtmp.begin(), rtmp.end(), col);
+        }
+        std::vector<i64> btmp(static_cast<size_t>(sn)), dtmp(static_cast<size_t>(sn));
+        int lo = 0, cnt = 0;
+        for (int j = 0; j < sn; ++j) {
+          const int o = ord[static_cast<size_t>(j)];
+          btmp[static_cast<size_t>(j)] = bb[o];
+          dtmp[static_cast<size_t>(j)] = db[o];
+          const i64 ow = last[j] / lmax_;  // last[] is already permuted
+          if (ow < rank_) ++lo;
+          if (ow == rank_) ++cnt;
+        }
+        std::copy(btmp.begin(), btmp.end(), bb);
+        std::copy(dtmp.begin(), dtmp.end(), db);
+        ploff_.push_back(lo);
+        plcnt_.push_back(cnt);
+      } else if (shard_) {
+        ploff_.push_back(0);
+        plcnt_.push_back(sn);
       }
       if (shard_) {  // local sample lists (mode N-1: every sample)
         loc_off_.push_back(static_cast<i64>(lidx.size()));
@@ -1545,7 +1684,19 @@ void Session::enqueue_iteration() {
                                  sizeof(phase_t_), cudaMemcpyHostToDevice, stream_));
     }
     if (cta_t_) CPB_CUDA(cudaMemsetAsync(cta_t_, 0, sizeof(unsigned long long) * fgrid_ * 16, stream_));
-    timed(0, 7, stream_, [&] { launch_fused_iteration(fargs_ + ti, rt_, mix_, fgrid_, fsmem_, stream_, o_.atomic_gram); });
+    if (peer_) {
+      // every rank's kernel (one launch per rank over NVLink, or one launch
+      // of every rank's group on a shared device)
+      const auto go = [&](const std::vector<const void*>& args, cudaStream_t st) {
+        FusedLaunch l{};
+        l.groups = static_cast<int>(args.size());
+        for (size_t q = 0; q < args.size(); ++q) l.a[q] = static_cast<const FusedIter*>(args[q]);
+        launch_fused_peer(l, rt_, fgrid_ * l.groups, fsmem_, st);
+      };
+      timed(0, 7, stream_, [&] { comm_->launch_group(fargs_ + ti, stream_, go); });
+    } else {
+      timed(0, 7, stream_, [&] { launch_fused_iteration(fargs_ + ti, rt_, mix_, fgrid_, fsmem_, stream_, o_.atomic_gram); });
+    }
     if (timing_) {
       // collect this launch's phase stamps (timing mode only: synchronizes)
       std::vector<unsigned long long> t(static_cast<size_t>(order_ * 16));
@@ -1803,6 +1954,12 @@ void Session::sync() {
   CPB_CUDA(cudaStreamSynchronize(stream2_));
   CPB_CUDA(cudaStreamSynchronize(stream_));
   collect_kernel_times();
+  check_peer_error();
+}
+
+void Session::check_peer_error() {
+  if (perr_host_ && *reinterpret_cast<volatile int*>(perr_host_))
+    throw CudaError("peer path: a rank's data did not arrive within 20 s (a rank stopped or diverged)");
 }
 
 void Session::collect_kernel_times() {

@@ -209,6 +209,14 @@ class Session {
   unsigned long long* cta_t_ = nullptr;  // debug per-CTA stamps (CPRAND_DEBUG_CTA)
   double* gpart_ = nullptr;        // CPRAND kernel Gram block partials
   double* gsum_ = nullptr;         // CPRAND kernel reduced Gram [RT][RT]
+  // peer path (sharded CPRAND kernel exchanging through peer memory)
+  bool peer_ = false;              // this session launches the peer kernel
+  char* parena_ = nullptr;         // receive buffer, counters, last-mode ssq partials
+  std::vector<void*> parena_all_, pfac_all_;  // every rank's arena / last-mode factor
+  int* perr_host_ = nullptr;       // pinned mapped: a peer wait timed out
+  int* perr_dev_ = nullptr;
+  std::vector<int> ploff_, plcnt_; // [iter][mode] this rank's range of the owner-ordered samples
+  void check_peer_error();
   unsigned long long* phase_t_ = nullptr;  // fused phase timestamps [order][8] (timing mode)
  public:
   // fused path: mean per-mode phase durations (us) over the timed launches:

@@ -55,7 +55,10 @@ def run_ranks(pb, nranks, body, timeout=600):
     return out
 
 
-def sharded_solve(pb, x, method, r, s, nranks, **kw):
+def sharded_solve(pb, x, method, r, s, nranks, expect_fused=None, **kw):
+    """expect_fused: assert that every rank's session runs (True) or does not
+    run (False) the peer kernel (the persistent CPRAND kernel exchanging the
+    RHS rows / last-mode slabs through peer memory)."""
     from paper_1701_06600_b200 import shard
     total = x.shape[-1]
 
@@ -65,6 +68,8 @@ def sharded_solve(pb, x, method, r, s, nranks, **kw):
         if ln:
             t.upload(np.asfortranarray(x[..., off:off + ln]))
         sess = pb.Session(method, t, r, s, pb.SolveOptions(comm=comm, shard_total=total, device=0, **kw))
+        if expect_fused is not None:
+            assert sess.fused == expect_fused
         sess.run(kw["max_iters"])
         res = sess.result()
         sess.close()
@@ -77,6 +82,7 @@ def sharded_solve(pb, x, method, r, s, nranks, **kw):
 def check_against_unsharded(pb, x, method, r, s, results, **kw):
     t = pb.DeviceTensor(x.shape, device=0)
     t.upload(x)
+    kw = {k: v for k, v in kw.items() if k != "fused"}
     full = pb.Session(method, t, r, s, pb.SolveOptions(fused=0, device=0, **kw))
     full.run(kw["max_iters"])
     ref = full.result()
@@ -98,19 +104,36 @@ def check_against_unsharded(pb, x, method, r, s, results, **kw):
     return ref
 
 
+@pytest.mark.parametrize("fused", [-1, 0])
 @pytest.mark.parametrize("nranks,dims", [(2, (24, 20, 22)), (3, (24, 20, 23)), (4, (24, 20, 23)),
                                          (4, (24, 20, 5))])
-def test_loopback_sharded_cprand(pb, orc, nranks, dims):
-    """Modes < N-1: local-sample RHS + allreduce; mode N-1: slab rows, column
-    sums of squares allreduced, slabs allgathered (23 % 3, 23 % 4 != 0; last
-    dim 5 over 4 ranks leaves rank 3 with an empty slab)."""
+def test_loopback_sharded_cprand(pb, orc, nranks, dims, fused):
+    """Modes < N-1: local-sample RHS summed over the ranks; mode N-1: slab
+    rows, column sums of squares over the ranks, slabs gathered (23 % 3,
+    23 % 4 != 0; last dim 5 over 4 ranks leaves rank 3 with an empty slab).
+    fused=-1: the peer kernel (every rank a group of one cooperative launch,
+    exchanging through each other's buffers); fused=0: the multi-kernel
+    chain with the loopback collectives."""
     r, s = 4, 60
     x, _ = orc.gen_baseline(dims, r, 0.5, 0.01, 11)
-    kw = dict(rng_seed=11, max_iters=10, stall_limit=1000)
-    res = sharded_solve(pb, x, "rand", r, s, nranks, **kw)
+    kw = dict(rng_seed=11, max_iters=10, stall_limit=1000, fused=fused)
+    res = sharded_solve(pb, x, "rand", r, s, nranks, expect_fused=(fused != 0), **kw)
     check_against_unsharded(pb, x, "rand", r, s, res, **kw)
+    kw.pop("fused")
     o = orc.cprand(x, r, s, orc.SolveOptions(**kw))
     assert max(abs(a[2] - b[2]) for a, b in zip(res[0].trace, o.trace)) < 1e-8
+
+
+@pytest.mark.parametrize("nranks,dims,r,s", [(2, (200, 90, 61), 20, 500), (3, (130, 70, 90), 12, 400),
+                                             (4, (90, 300, 70), 36, 700), (2, (64, 64, 64), 50, 900)])
+def test_loopback_peer_kernel_tiled(pb, orc, nranks, dims, r, s):
+    """The peer kernel at sizes where a mode has several 64-row blocks and
+    sample splits, every rank bucket (RT = 32 / 64), apply shares exchanged
+    per counterpart CTA, 61 % 2 and 70 % 4 != 0."""
+    x, _ = orc.gen_baseline(dims, r, 0.5, 0.01, 21)
+    kw = dict(rng_seed=21, max_iters=6, stall_limit=1000)
+    res = sharded_solve(pb, x, "rand", r, s, nranks, expect_fused=True, **kw)
+    check_against_unsharded(pb, x, "rand", r, s, res, **kw)
 
 
 @pytest.mark.parametrize("nranks,dims,transform", [(2, (16, 8, 32), "dct"), (3, (16, 8, 32), "dct"),
