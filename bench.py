@@ -599,7 +599,9 @@ def main() -> int:
             "config": config_of(args.config, cfg, ws),
             "gram_sum": "L2 fp64 atomics (atomic_gram)" if args.atomic_gram else
                         "fixed-order split partials (bitwise reproducible)",
-            "comm": "NCCL allreduce / allgather / send-recv" if ws > 1 else None,
+            "comm": (("peer kernel: RHS rows / last-mode slabs stored into every rank's buffers "
+                      "(CUDA IPC mappings over NVLink, sys-scope flags); NCCL for setup")
+                     if used_fused else "NCCL allreduce / allgather / send-recv") if ws > 1 else None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": kname,
                          "bytes_model": bytes_model, "per_mode_gbs": per_mode,

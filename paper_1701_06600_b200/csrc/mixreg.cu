@@ -19,6 +19,10 @@
 // Measured on B200 (tests/micro/mix_rate.py, 16 B / element): C5 (n = 320)
 // 3.7 TB/s on mode 1 and 4.4-4.6 TB/s on the strided modes (v2: 2.2 / 3.2);
 // n = 256: 4.2 / 5.0-5.2; C4 (n = 1000) strided 3.0 TB/s (v3: 2.2-2.3).
+// Round 2: the strided two-stage kernel prefetches its next tile into L2
+// (C5 strided modes 4.5 -> 5.1-5.2 TB/s; the three-stage kernel lost with it
+// and does not), and mode 1 of n = 1000 runs the three-stage FFT from a
+// cp.async-staged tile (mix_reg3c_kernel: C4 mode 1 2.16 -> 2.9 TB/s).
 // Rounding differs from v2 / v3 in the FFT order only (parity tests: 1e-12).
 #include <algorithm>
 
@@ -76,6 +80,17 @@ __device__ __forceinline__ void dft_reg(double2 (&v)[N], const double2* roots, i
 // Makhoul's reorder: permuted point m holds input element src(m)
 __device__ __forceinline__ int makhoul_src(int m, int n) { return 2 * m < n ? 2 * m : 2 * (n - 1 - m) + 1; }
 
+// L2 prefetch of a strided tile (n rows of w doubles at stride st): the next
+// tile's DRAM reads overlap this tile's FFT stages, and its first stage then
+// loads from L2 (one CTA per SM leaves no other tile to hide the latency).
+// Two lines per row cover a row segment that straddles a 128-byte line.
+__device__ __forceinline__ void prefetch_rows_l2(const double* base, int n, i64 st, int w, int tid, int nt) {
+  for (int e = tid; e < 2 * n; e += nt) {
+    const double* p = base + static_cast<i64>(e >> 1) * st + ((e & 1) ? w - 1 : 0);
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
+}
+
 // Two-stage variant (four-step FFT n = N1 * N2, all points of a DFT in one
 // thread's registers): stage 1 thread (q, n2) loads its N1 points from
 // global, DFT_N1, twiddle W_n^(n2 k1), one store; stage 2 thread (q, k1)
@@ -109,6 +124,11 @@ __global__ void __launch_bounds__(two_threads<N1, N2, NSEQ>(), MB)
     const i64 hi = t / tiles_per_slab;
     const i64 lo0 = (t - hi * tiles_per_slab) * (2 * NSEQ);
     double* base = x + hi * st * N + lo0;
+    if (t + gridDim.x < ntiles) {
+      const i64 tn = t + gridDim.x, hn = tn / tiles_per_slab, ln = (tn - hn * tiles_per_slab) * (2 * NSEQ);
+      prefetch_rows_l2(x + hn * st * N + ln, N, st, static_cast<int>(st - ln < 2 * NSEQ ? st - ln : 2 * NSEQ), tid,
+                       NT);
+    }
     // 16-byte pair loads / stores need even row offsets (st even)
     const bool full = (st & 1) == 0 && lo0 + 2 * NSEQ <= st;
     const bool lo_ok = lo0 + 2 * q < st, hi_ok = lo0 + 2 * q + 1 < st;
@@ -448,6 +468,140 @@ bool launch_reg2c_t(const DctPlan& pl, double* x, i64 nfib, const double* sign, 
   return true;
 }
 
+// Mode 1 with the three-stage FFT (n = R1 R2 R3, e.g. C4's n = 1000): the
+// tile of 2 NSEQ whole fibers streams into shared memory with 8-byte
+// cp.async in the [row][pair] layout of mix_reg2c_kernel, stages A, B, C
+// run as in mix_reg3_kernel on point rows of NSEQ + 1 (conflict-free
+// k-strided epilogue reads), and the epilogue stores each fiber's results
+// in coalesced runs. One CTA per SM (the staging / stage buffer of a
+// 1000-point tile is 144 KB).
+template <int R1, int R2, int R3, int NSEQ, int MB>
+__global__ void __launch_bounds__(three_threads<R1, R2, R3, NSEQ>(), MB)
+    mix_reg3c_kernel(double* __restrict__ x, i64 nfib, const double* __restrict__ sign,
+                     const double2* __restrict__ tw, const double2* __restrict__ phase, double s0, double sk) {
+  constexpr int N = R1 * R2 * R3, NT = three_threads<R1, R2, R3, NSEQ>(), W = 2 * NSEQ;
+  constexpr int LDS = W + 1;    // staging row stride (doubles)
+  constexpr int LDB = NSEQ + 1; // point-row stride of the stage buffer (double2)
+  extern __shared__ __align__(16) double2 rsm[];
+  constexpr int BUFD = N * LDS > 2 * N * LDB ? N * LDS : 2 * N * LDB;  // doubles
+  constexpr int BUFA = (BUFD + 1) / 2 * 2;
+  double* raw = reinterpret_cast<double*>(rsm);
+  double2* buf = rsm;
+  double2* stw = reinterpret_cast<double2*>(raw + BUFA);
+  double2* sph = stw + N;
+  double* ssg = reinterpret_cast<double*>(sph + N);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < N; e += NT) {
+    stw[e] = tw[e];
+    sph[e] = phase[e];
+    ssg[e] = sign[e];
+  }
+  const int q = tid % NSEQ, part = tid / NSEQ;
+  const i64 ntiles = (nfib + W - 1) / W;
+  // (measured: double-buffered 8-fiber tiles, 2.3 TB/s on n = 1000, lose to
+  // one 16-fiber tile at a time, 2.9: the FFT stages, not the loads, bound it)
+  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const i64 f0 = t * W;
+    const int nf = static_cast<int>(nfib - f0 < W ? nfib - f0 : W);
+    {  // element e = f N + i -> raw[i LDS + f]
+      const double* src = x + f0 * N;
+      for (int e = tid; e < W * N; e += NT) {
+        const int f = e / N, i = e - f * N;
+        cp_async8(raw + i * LDS + f, f < nf ? src + e : src, f < nf ? 8 : 0);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (part < R2 * R3) {  // stage A: points m0 + R2 R3 n1, DFT over n1
+      const int n3 = part % R3, n2 = part / R3, m0 = n3 + R3 * n2;
+      double2 v[R1];
+#pragma unroll
+      for (int n1 = 0; n1 < R1; ++n1) {
+        const int i = makhoul_src(m0 + R2 * R3 * n1, N);
+        const double sg = ssg[i];
+        v[n1] = make_double2(raw[i * LDS + 2 * q] * sg, raw[i * LDS + 2 * q + 1] * sg);
+      }
+      dft_reg<R1>(v, stw, N / R1);
+      __syncthreads();  // every stage-A read of the staging rows is done
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1)
+        buf[(k1 + R1 * n2 + R1 * R2 * n3) * LDB + q] = (k1 == 0 || m0 == 0) ? v[k1] : cmulw(v[k1], stw[(m0 * k1) % N]);
+    } else {
+      __syncthreads();
+    }
+    __syncthreads();
+    if (part < R1 * R3) {  // stage B (in place)
+      const int k1 = part % R1, n3 = part / R1;
+      double2 v[R2];
+#pragma unroll
+      for (int n2 = 0; n2 < R2; ++n2) v[n2] = buf[(k1 + R1 * n2 + R1 * R2 * n3) * LDB + q];
+      dft_reg<R2>(v, stw, N / R2);
+#pragma unroll
+      for (int k2 = 0; k2 < R2; ++k2)
+        buf[(k1 + R1 * k2 + R1 * R2 * n3) * LDB + q] = (k2 == 0 || n3 == 0) ? v[k2] : cmulw(v[k2], stw[(R1 * n3 * k2) % N]);
+    }
+    __syncthreads();
+    if (part < R1 * R2) {  // stage C (in place, natural order)
+      const int k1 = part % R1, k2 = part / R1;
+      double2 v[R3];
+#pragma unroll
+      for (int n3 = 0; n3 < R3; ++n3) v[n3] = buf[(k1 + R1 * k2 + R1 * R2 * n3) * LDB + q];
+      dft_reg<R3>(v, stw, N / R3);
+#pragma unroll
+      for (int k3 = 0; k3 < R3; ++k3) buf[(k1 + R1 * k2 + R1 * R2 * k3) * LDB + q] = v[k3];
+    }
+    __syncthreads();
+    // epilogue: consecutive threads take consecutive rows k of one pair
+    double* dst = x + f0 * N;
+    for (int e = tid; e < NSEQ * (N / 2 + 1); e += NT) {
+      const int qq = e / (N / 2 + 1), k = e - qq * (N / 2 + 1);
+      const double2 z = buf[k * LDB + qq];
+      const double2 zc = buf[((N - k) % N) * LDB + qq];
+      auto val = [&](int kk, double2 a, double2 b) {
+        const double2 ph = sph[kk];
+        const double sc = kk == 0 ? s0 : sk;
+        const double ex = 0.5 * (a.x + b.x), ey = 0.5 * (a.y - b.y);
+        const double ox = 0.5 * (a.y + b.y), oy = -0.5 * (a.x - b.x);
+        return make_double2(sc * (ph.x * ex - ph.y * ey), sc * (ph.x * ox - ph.y * oy));
+      };
+      const bool f_ok = 2 * qq < nf, g_ok = 2 * qq + 1 < nf;
+      const double2 o = val(k, z, zc);
+      if (f_ok) __stcs(dst + static_cast<i64>(2 * qq) * N + k, o.x);
+      if (g_ok) __stcs(dst + static_cast<i64>(2 * qq + 1) * N + k, o.y);
+      if (k != 0 && 2 * k != N) {
+        const double2 o2 = val(N - k, zc, z);
+        if (f_ok) __stcs(dst + static_cast<i64>(2 * qq) * N + N - k, o2.x);
+        if (g_ok) __stcs(dst + static_cast<i64>(2 * qq + 1) * N + N - k, o2.y);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int R1, int R2, int R3, int NSEQ, int MB>
+bool launch_reg3c_t(const DctPlan& pl, double* x, i64 nfib, const double* sign, cudaStream_t stream, bool prepare_only) {
+  constexpr int N = R1 * R2 * R3, NT = three_threads<R1, R2, R3, NSEQ>(), W = 2 * NSEQ;
+  constexpr size_t bufd = std::max<size_t>(static_cast<size_t>(N) * (W + 1), 2 * static_cast<size_t>(N) * (NSEQ + 1));
+  const size_t smem = ((bufd + 1) / 2 * 2) * sizeof(double) + 2 * N * sizeof(double2) + N * sizeof(double);
+  auto* fn = mix_reg3c_kernel<R1, R2, R3, NSEQ, MB>;
+  static bool configured = false;
+  if (!configured) {
+    CPB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    configured = true;
+  }
+  if (prepare_only) return true;
+  const i64 ntiles = (nfib + W - 1) / W;
+  int dev = 0, sms = 148, per_sm = 1;
+  CPB_CUDA(cudaGetDevice(&dev));
+  CPB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, smem));
+  const int grid = static_cast<int>(std::min<i64>(ntiles, static_cast<i64>(std::max(per_sm, 1)) * sms));
+  fn<<<grid, NT, smem, stream>>>(x, nfib, sign, pl.tw, pl.phase, pl.s0, pl.sk);
+  CPB_LAUNCH_CHECK();
+  return true;
+}
+
 template <int N1, int N2, int NSEQ, int MB>
 bool launch_reg2_t(const DctPlan& pl, double* x, i64 st, i64 nfib, const double* sign, cudaStream_t stream,
                    bool prepare_only) {
@@ -485,6 +639,7 @@ bool launch_mix_reg(const DctPlan& pl, double* x, i64 st, i64 nfib, const double
     switch (pl.n) {
       case 256: return launch_reg2c_t<16, 16, 16, 2>(pl, x, nfib, sign, stream, prepare_only);
       case 320: return launch_reg2c_t<16, 20, 16, 2>(pl, x, nfib, sign, stream, prepare_only);
+      case 1000: return launch_reg3c_t<10, 10, 10, 8, 1>(pl, x, nfib, sign, stream, prepare_only);
       default: return false;
     }
   }

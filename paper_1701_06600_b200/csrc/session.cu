@@ -1684,9 +1684,10 @@ void Session::enqueue_iteration() {
                                  sizeof(phase_t_), cudaMemcpyHostToDevice, stream_));
     }
     if (cta_t_) CPB_CUDA(cudaMemsetAsync(cta_t_, 0, sizeof(unsigned long long) * fgrid_ * 16, stream_));
-    if (peer_) {
+    if (peer_ && nranks_ > 1) {
       // every rank's kernel (one launch per rank over NVLink, or one launch
-      // of every rank's group on a shared device)
+      // of every rank's group on a shared device); one rank has nothing to
+      // exchange and runs the single-GPU kernel on the same arguments
       const auto go = [&](const std::vector<const void*>& args, cudaStream_t st) {
         FusedLaunch l{};
         l.groups = static_cast<int>(args.size());
