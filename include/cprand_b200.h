@@ -35,7 +35,8 @@
  *   2 std::invalid_argument / std::out_of_range   (CLI exit 2)
  *   3 numerical_consistency_error                 (CLI exit 3)
  *   4 CUDA / NCCL runtime failure
- *   5 valid for the reference but outside this path (e.g. R > 64, HOSVD init)
+ *   5 valid for the reference but outside this path (e.g. R > 128, R > 64 with
+ *     mixing or sharding, HOSVD init)
  *   1 anything else
  */
 #ifndef CPRAND_B200_H

@@ -13,7 +13,8 @@ using i64 = std::int64_t;
 using u64 = std::uint64_t;
 
 constexpr int kMaxOrder = 8;  // tensor order supported by the device path
-constexpr int kMaxRank = 64;  // R supported by the fused kernels (RT buckets 16/32/64)
+constexpr int kMaxRank = 128;      // R of the multi-kernel chain (RT buckets 16/32/64/128)
+constexpr int kMaxFusedRank = 64;  // R of the persistent kernels and the sharded / mixing paths
 
 // Error taxonomy of the C ABI (include/cprand_b200.h).
 struct Error : std::runtime_error {

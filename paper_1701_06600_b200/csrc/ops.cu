@@ -142,7 +142,7 @@ int op_mode_update(const double* x, const std::vector<i64>& dims, int mode, cons
                    std::uint64_t mix_seed, double* out_factor) {
   check_mode(mode, dims.size());
   if (s < r) throw InvalidArgument("sampled_update: need at least R samples");
-  if (r < 1 || r > kMaxRank) throw Unsupported("rank outside 1..64");
+  if (r < 1 || r > kMaxFusedRank) throw Unsupported("rank outside 1..64");
   const bool mix = transform == 1;
   if (transform >= 0) require_transform(transform);
   const int n = static_cast<int>(dims.size());

@@ -313,7 +313,7 @@ __device__ bool inverse_cta(const double* __restrict__ part, int nparts, int r, 
     for (int u = 0; u < TC; ++u) a[t][u] = 0.0;
   {  // G = sum of the split partials in split order, PB partials per batch
      // (about 32 loads in flight per thread; the last batch predicated)
-    constexpr int PB = (32 / (TR * TC)) > 4 ? (32 / (TR * TC)) : 4;
+    constexpr int PB = TR * TC >= 32 ? 1 : ((32 / (TR * TC)) > 4 ? (32 / (TR * TC)) : 4);
     for (int k = 0; k < nparts; k += PB) {
       double v[PB][TR][TC];
 #pragma unroll
@@ -1054,11 +1054,11 @@ __device__ unsigned long long norms_final(int r, i64 in, const ModeWork& w, int 
 // sampling.hpp:191-210); the column scale lambda_q / prod_n norm_n(q) is
 // formed once per block in shared memory (red[256..]), so a term costs N
 // multiplies instead of N divisions (a reassociation: the estimate agrees
-// with the reference's to a few ulp). red: 256 + 64 doubles.
+// with the reference's to a few ulp). red: 256 + 128 doubles.
 template <int KM, int QC, int U>
 __device__ inline double fit_block_t(const FitArgs& a, i64 vb, double* red) {
   const int r = a.r, N = a.order;
-  double* s_sc = red + 256;  // [64]
+  double* s_sc = red + 256;  // [r <= 128]
   for (int q = threadIdx.x; q < r; q += blockDim.x) {
     double den = 1.0;
     for (int n = 0; n < N; ++n)
@@ -1131,7 +1131,7 @@ __device__ inline double fit_block_t(const FitArgs& a, i64 vb, double* red) {
   return out;
 }
 
-constexpr int kFitSmemDoubles = 256 + 64;
+constexpr int kFitSmemDoubles = 256 + 128;
 
 __device__ inline double fit_block(const FitArgs& a, i64 vb, double* red) {
   return a.order <= 4 ? fit_block_t<4, 4, 2>(a, vb, red) : fit_block_t<kMaxOrder, 1, 2>(a, vb, red);

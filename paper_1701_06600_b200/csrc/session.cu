@@ -262,7 +262,12 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
     if (transform_ == 0) cmix_ = true;  // complex mixing (cfft.cu)
   }
   if (order_ > kMaxOrder) throw Unsupported("tensor order > 8");
-  if (r > kMaxRank) throw Unsupported("rank > 64 is not supported by the fused sm_100a kernels");
+  if (r > kMaxRank) throw Unsupported("rank > 128 is not supported by the sm_100a kernels");
+  // 64 < R <= 128: CPRAND / PREMIX on one GPU through the multi-kernel chain
+  // (RT = 128 buckets); the persistent kernels, the mixing-domain solve and
+  // the sharded path stop at 64
+  if (r > kMaxFusedRank && (method == 2 || o_.comm))
+    throw Unsupported("rank > 64 runs cprand / cprand_premix on one GPU only");
   if (o_.init == 1) throw Unsupported("hosvd init is outside the randomized B200 path");
   // real orthogonal kinds (DCT-II, WHT) share the real MIX / PREMIX path
   mix_ = (method == 2 && (transform_ == 1 || transform_ == 2));
@@ -525,7 +530,8 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   gfull_ = dalloc<double>(static_cast<size_t>(gram_scratch_doubles(r_)));
   // QR path of the LS step (qr.cuh) wherever every sampled fiber is on this
   // device; the sharded and FFT-kind paths keep the pivoted-Cholesky fallback
-  if (!shard_ && !cmix_) qrws_ = dalloc<double>(static_cast<size_t>(qr_ws_doubles(static_cast<int>(max_s), rt_)));
+  if (!shard_ && !cmix_ && rt_ <= kMaxFusedRank)  // (R > 64: the pivoted-Cholesky fallback)
+    qrws_ = dalloc<double>(static_cast<size_t>(qr_ws_doubles(static_cast<int>(max_s), rt_)));
   info_ = dalloc<int>(4);
   CPB_CUDA(cudaMemsetAsync(info_, 0, 4 * sizeof(int), stream_));
   tickets_ = dalloc<unsigned>(8);
@@ -594,7 +600,7 @@ void Session::setup_fused() {
     peer_ = true;
   }
   if (o_.fused == 0 || (!all_direct && !mix_) || o_.exhaustive_samples || (shard_ && !peer_) || cmix_ ||
-      (mix_ && transform_ == 2))
+      (mix_ && transform_ == 2) || rt_ > kMaxFusedRank)
     return;
   i64 max_dim = 1;
   for (i64 d : dims_) max_dim = std::max(max_dim, d);

@@ -41,7 +41,7 @@ template <int RT>
 __global__ void __launch_bounds__(kThreads) gram_kernel(const double* __restrict__ z, int s_total, int klen,
                                                         double* __restrict__ part, const int* stop) {
   if (stop && *stop) return;
-  __shared__ double sh[GS * RT];
+  extern __shared__ __align__(16) double sh[];  // GS x RT
   const int s0 = blockIdx.x * klen;
   ph::gram_chunk<RT>(z, s0, min(s_total, s0 + klen), part + static_cast<i64>(blockIdx.x) * RT * RT, sh);
 }
@@ -94,6 +94,15 @@ __global__ void __launch_bounds__(kThreads) rhs_gemm_kernel(const double* __rest
 }
 
 constexpr int kApplyThreads = 1024;
+template <int RT>
+constexpr int apply_gi_doubles() {
+  return RT * (RT + 1) > ph::qr_rows_smem_doubles<RT, kApplyThreads>() ? RT * (RT + 1)
+                                                                     : ph::qr_rows_smem_doubles<RT, kApplyThreads>();
+}
+template <int RT>
+constexpr size_t apply_smem() {
+  return static_cast<size_t>(apply_gi_doubles<RT>() + (kApplyThreads / RT) * (RT + 1)) * sizeof(double);
+}
 
 template <int RT>
 __global__ void __launch_bounds__(kApplyThreads) mode_apply_kernel(i64 in, int r, ModeWork w,
@@ -102,10 +111,9 @@ __global__ void __launch_bounds__(kApplyThreads) mode_apply_kernel(i64 in, int r
                                                                    unsigned long long* rng_state) {
   if (w.stop && *w.stop) return;
   constexpr int BI = kApplyThreads / RT;
-  constexpr int GI = RT * (RT + 1) > ph::qr_rows_smem_doubles<RT, kApplyThreads>()
-                         ? RT * (RT + 1) : ph::qr_rows_smem_doubles<RT, kApplyThreads>();
-  __shared__ double gi[GI];  // the inverse, or the QR rows' staging
-  __shared__ double rh[BI * (RT + 1)];
+  extern __shared__ __align__(16) double asm_[];
+  double* gi = asm_;                       // the inverse, or the QR rows' staging (apply_gi_doubles)
+  double* rh = asm_ + apply_gi_doubles<RT>();  // BI x (RT + 1)
   __shared__ bool s_last;
   // QR mode (the MIX path brings its QR rows in rhs_full, times ginv = I)
   const bool qr = w.qrws && !rhs_full && __ldcg(w.info + 2) != 0;
@@ -182,7 +190,8 @@ int rank_bucket(int r) {
   if (r <= 16) return 16;
   if (r <= 32) return 32;
   if (r <= 64) return 64;
-  throw Unsupported("rank > 64 is not supported by the fused sm_100a kernels");
+  if (r <= 128) return 128;
+  throw Unsupported("rank > 128 is not supported by the sm_100a kernels");
 }
 
 void mode_splits(i64 in, int s, int rt, int* ks, int* ks_len, int sms) {
@@ -220,7 +229,8 @@ void launch_z(const ModeView& v, double* z, const int* stop, cudaStream_t st) {
   switch (rank_bucket(v.r)) {
     case 16: z_t<16>(v, z, stop, st); break;
     case 32: z_t<32>(v, z, stop, st); break;
-    default: z_t<64>(v, z, stop, st); break;
+    case 64: z_t<64>(v, z, stop, st); break;
+    default: z_t<128>(v, z, stop, st); break;
   }
 }
 
@@ -228,7 +238,13 @@ template <int RT>
 static void gram_t(const double* z, int s, double* part, const int* stop, cudaStream_t st) {
   int parts, klen;
   gram_splits(s, &parts, &klen);
-  gram_kernel<RT><<<parts, kThreads, 0, st>>>(z, s, klen, part, stop);
+  const size_t sm = static_cast<size_t>(GS) * RT * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    CPB_CUDA(cudaFuncSetAttribute(gram_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    configured = true;
+  }
+  gram_kernel<RT><<<parts, kThreads, sm, st>>>(z, s, klen, part, stop);
   CPB_LAUNCH_CHECK();
 }
 
@@ -236,7 +252,8 @@ void launch_gram(const double* z, int s, int r, double* part, const int* stop, c
   switch (rank_bucket(r)) {
     case 16: gram_t<16>(z, s, part, stop, st); break;
     case 32: gram_t<32>(z, s, part, stop, st); break;
-    default: gram_t<64>(z, s, part, stop, st); break;
+    case 64: gram_t<64>(z, s, part, stop, st); break;
+    default: gram_t<128>(z, s, part, stop, st); break;
   }
 }
 
@@ -267,7 +284,10 @@ void launch_gram_inverse(const double* part_gram, int nparts, int r, double tol,
   switch (rank_bucket(r)) {
     case 16: inverse_t<16>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st, z, s, qtol, qrws); break;
     case 32: inverse_t<32>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st, z, s, qtol, qrws); break;
-    default: inverse_t<64>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st, z, s, qtol, qrws); break;
+    case 64: inverse_t<64>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st, z, s, qtol, qrws); break;
+    default:  // (R > 64: the pivoted-Cholesky fallback; the QR path's one-CTA factorization stops at 64)
+      inverse_t<128>(part_gram, nparts, r, tol, ginv, gfull, info, stop, st, z, s, qtol, nullptr);
+      break;
   }
 }
 
@@ -297,9 +317,13 @@ void launch_rhs_gemm(const double* xs, i64 ld, const i64* row_off, bool vec16, c
       vec16 ? gemm_t<32, true>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st)
             : gemm_t<32, false>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st);
       break;
-    default:
+    case 64:
       vec16 ? gemm_t<64, true>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st)
             : gemm_t<64, false>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st);
+      break;
+    default:
+      vec16 ? gemm_t<128, true>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st)
+            : gemm_t<128, false>(xs, ld, row_off, z, in, s, r, ks, ks_len, part, stop, st);
       break;
   }
 }
@@ -311,14 +335,27 @@ i64 gram_scratch_doubles(int r) {
 
 int apply_grid(i64 in, int r) { return ceil_div(in, kApplyThreads / rank_bucket(r)); }
 
+template <int RT>
+static void apply_t(int grid, i64 in, int r, const ModeWork& w, const double* rhs_override, int first_of_pass,
+                    unsigned long long* rng_state, cudaStream_t st) {
+  constexpr size_t sm = apply_smem<RT>();
+  static bool configured = false;
+  if (!configured) {
+    CPB_CUDA(cudaFuncSetAttribute(mode_apply_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    configured = true;
+  }
+  mode_apply_kernel<RT><<<grid, kApplyThreads, sm, st>>>(in, r, w, rhs_override, first_of_pass, rng_state);
+}
+
 void launch_mode_apply(i64 in, int r, const ModeWork& w, const double* rhs_override,
                        int first_of_pass, unsigned long long* rng_state, cudaStream_t st) {
   const int rt = rank_bucket(r);
   const int grid = ceil_div(in, kApplyThreads / rt);
   switch (rt) {
-    case 16: mode_apply_kernel<16><<<grid, kApplyThreads, 0, st>>>(in, r, w, rhs_override, first_of_pass, rng_state); break;
-    case 32: mode_apply_kernel<32><<<grid, kApplyThreads, 0, st>>>(in, r, w, rhs_override, first_of_pass, rng_state); break;
-    default: mode_apply_kernel<64><<<grid, kApplyThreads, 0, st>>>(in, r, w, rhs_override, first_of_pass, rng_state); break;
+    case 16: apply_t<16>(grid, in, r, w, rhs_override, first_of_pass, rng_state, st); break;
+    case 32: apply_t<32>(grid, in, r, w, rhs_override, first_of_pass, rng_state, st); break;
+    case 64: apply_t<64>(grid, in, r, w, rhs_override, first_of_pass, rng_state, st); break;
+    default: apply_t<128>(grid, in, r, w, rhs_override, first_of_pass, rng_state, st); break;
   }
   CPB_LAUNCH_CHECK();
 }

@@ -371,7 +371,9 @@ def test_zero_tensor_and_validation(pb, orc):
     with pytest.raises(pb.InvalidArgument):
         pb.gather_fibers(x, 0, np.zeros((2, 5), dtype=np.int64))
     with pytest.raises(pb.UnsupportedOnDevice):
-        pb.cprand(x, 65, 100)
+        pb.cprand(x, 129, 200)
+    with pytest.raises(pb.UnsupportedOnDevice):  # R > 64: cprand / premix on one GPU only
+        pb.cprand_mix(x, 65, 100, pb.SolveOptions(transform="dct"))
 
 
 def test_deterministic_bitwise(pb, orc):
@@ -733,3 +735,24 @@ def test_prime_length_mixing_matches_oracle(pb, orc, dims):
         assert max(abs(a[2] - b[2]) for a, b in zip(got.trace, ref.trace)) < 1e-8
         for a, b in zip(got.factors, ref.factors):
             assert rel(a, b) < 1e-6
+
+
+@pytest.mark.parametrize("dims,r,s,method", [((90, 80, 70), 80, 400, "rand"), ((40, 36, 30, 28), 128, 700, "rand"),
+                                              ((70, 66, 64), 72, 300, "premix")])
+def test_wide_rank_chain_matches_oracle(pb, orc, dims, r, s, method):
+    """64 < R <= 128 (the reference has no rank cap): the multi-kernel chain
+    with RT = 128 buckets (Z_S, Gram, 512-thread Gauss-Jordan inverse, split-K
+    RHS GEMM, apply) and the sampled fit, against the oracle's pivoted-QR loop."""
+    x, _ = orc.gen_baseline(dims, r, 0.0, 0.01, 31)
+    opts = dict(rng_seed=31, max_iters=6, stall_limit=1000)
+    if method == "premix":
+        opts["transform"] = "dct"
+    ref = orc.solve(method, x, r, s, orc.SolveOptions(**opts))
+    got = pb.solve(method, x, r, s, pb.SolveOptions(**opts))
+    assert got.iterations == ref.iterations == 6
+    fg = np.array([t[2] for t in got.trace])
+    fr = np.array([t[2] for t in ref.trace])
+    assert np.max(np.abs(fg - fr)) < 1e-8
+    for a, b in zip(got.factors, ref.factors):
+        assert rel(a, b) < 1e-6
+    assert rel(got.lam, ref.lam) < 1e-6
