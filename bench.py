@@ -538,7 +538,9 @@ def main() -> int:
         ms_modes = t.mix("dct", SEED)
         pbytes = 16.0 * float(p)
         gbs = [pbytes / (m * 1e-3) / 1e9 for m in ms_modes]
-        mix_pass = {"kernel": "mix_pass_fwd_kernel (whole-tensor sign + DCT-II per fiber, in place)",
+        mix_pass = {"kernel": ("mixing pass v4 (mixreg.cu, whole-tensor sign + DCT-II per fiber, in place): "
+                               "mix_reg3c_kernel on mode 1, mix_reg3_kernel on the strided modes" if cfg["dims"][0] == 1000
+                               else "mixing pass (whole-tensor sign + DCT-II per fiber, in place)"),
                     "bytes_model": "16 B per element per mode (read + write)",
                     "ms_per_mode": [round(m, 3) for m in ms_modes],
                     "gbs_per_mode": [round(g, 1) for g in gbs],
