@@ -19,10 +19,12 @@
 // Measured on B200 (tests/micro/mix_rate.py, 16 B / element): C5 (n = 320)
 // 3.7 TB/s on mode 1 and 4.4-4.6 TB/s on the strided modes (v2: 2.2 / 3.2);
 // n = 256: 4.2 / 5.0-5.2; C4 (n = 1000) strided 3.0 TB/s (v3: 2.2-2.3).
-// Round 2: the strided two-stage kernel prefetches its next tile into L2
-// (C5 strided modes 4.5 -> 5.1-5.2 TB/s; the three-stage kernel lost with it
-// and does not), and mode 1 of n = 1000 runs the three-stage FFT from a
-// cp.async-staged tile (mix_reg3c_kernel: C4 mode 1 2.16 -> 2.9 TB/s).
+// Round 2: every kernel but the strided three-stage one prefetches its next
+// tile into L2 while the current tile runs (one CTA per SM leaves no other
+// tile to hide the DRAM latency of the loads): C5 strided modes 4.5 -> 4.8-
+// 5.2 TB/s, C5 mode 1 3.7 -> 4.1; the strided three-stage kernel lost with it
+// (rows 8 MB apart) and does not. Mode 1 of n = 1000 runs the three-stage FFT
+// from a cp.async-staged tile (mix_reg3c_kernel: C4 mode 1 2.16 -> 3.4 TB/s).
 // Rounding differs from v2 / v3 in the FFT order only (parity tests: 1e-12).
 #include <algorithm>
 
@@ -383,6 +385,14 @@ __global__ void __launch_bounds__(two_threads<N1, N2, NSEQ>(), MB)
     } else {
       fetch(t, raw);
       cp_async_commit();
+      // the next tile (one contiguous block) streams into L2 meanwhile
+      if (t + gridDim.x < ntiles) {
+        const i64 fn = (t + gridDim.x) * W;
+        const i64 nb = (nfib - fn < W ? nfib - fn : W) * N * 8;
+        const char* src = reinterpret_cast<const char*>(x + fn * N);
+        for (i64 o = static_cast<i64>(tid) * 128; o < nb; o += static_cast<i64>(NT) * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(src + o));
+      }
       cp_async_wait<0>();
     }
     __syncthreads();
@@ -510,17 +520,39 @@ __global__ void __launch_bounds__(three_threads<R1, R2, R3, NSEQ>(), MB)
         cp_async8(raw + i * LDS + f, f < nf ? src + e : src, f < nf ? 8 : 0);
       }
       cp_async_commit();
+      if (t + gridDim.x < ntiles) {  // the next tile streams into L2 meanwhile
+        const i64 fn = (t + gridDim.x) * W;
+        const i64 nb = (nfib - fn < W ? nfib - fn : W) * N * 8;
+        const char* nsrc = reinterpret_cast<const char*>(x + fn * N);
+        for (i64 o = static_cast<i64>(tid) * 128; o < nb; o += static_cast<i64>(NT) * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(nsrc + o));
+      }
       cp_async_wait<0>();
     }
     __syncthreads();
     if (part < R2 * R3) {  // stage A: points m0 + R2 R3 n1, DFT over n1
       const int n3 = part % R3, n2 = part / R3, m0 = n3 + R3 * n2;
       double2 v[R1];
-#pragma unroll
-      for (int n1 = 0; n1 < R1; ++n1) {
+      auto ld = [&](int n1) {
         const int i = makhoul_src(m0 + R2 * R3 * n1, N);
         const double sg = ssg[i];
-        v[n1] = make_double2(raw[i * LDS + 2 * q] * sg, raw[i * LDS + 2 * q + 1] * sg);
+        return make_double2(raw[i * LDS + 2 * q] * sg, raw[i * LDS + 2 * q + 1] * sg);
+      };
+      if constexpr (R1 % 2 == 0) {
+        // points n1 < R1 / 2 sit on even staging rows, the others on odd
+        // rows; odd parts take the halves in the other order, so each load
+        // instruction of a warp (four parts) reads two even and two odd rows
+        // (two wavefronts instead of four with row stride 2 W + 1)
+        const bool odd = part & 1;
+#pragma unroll
+        for (int h = 0; h < R1 / 2; ++h) {
+          const double2 a = ld(odd ? h + R1 / 2 : h), b2 = ld(odd ? h : h + R1 / 2);
+          v[h] = odd ? b2 : a;
+          v[h + R1 / 2] = odd ? a : b2;
+        }
+      } else {
+#pragma unroll
+        for (int n1 = 0; n1 < R1; ++n1) v[n1] = ld(n1);
       }
       dft_reg<R1>(v, stw, N / R1);
       __syncthreads();  // every stage-A read of the staging rows is done
