@@ -22,6 +22,18 @@ $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lnccl -lcudart
 
+# device-check build (bounds asserts, flag-wait time-outs; tests/test_gpu_checked.py)
+CHK_DIR  := build/objc
+CHK_OBJS := $(patsubst $(SRC_DIR)/%.cu,$(CHK_DIR)/%.o,$(SRCS))
+CHK_LIB  := paper_1701_06600_b200/libcprand_b200_check.so
+checklib: $(CHK_LIB)
+$(CHK_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p $(CHK_DIR)
+	$(NVCC) $(NVFLAGS) -DCPB_DEVICE_CHECKS -c $< -o $@ 2> $@.log || (cat $@.log; exit 1)
+$(CHK_LIB): $(CHK_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(CHK_OBJS) -lnccl -lcudart
+.PHONY: checklib
+
 oracle:
 	$(MAKE) -s -C oracle
 

@@ -58,6 +58,9 @@ struct ModeView {
   const double* fac[kMaxOrder];    // per kept mode c: factor (row-major, ld R) used for Z
   const double* nrm[kMaxOrder];    // per kept mode c: column norms the factor is divided by (or null)
   const i64* base;                 // S base offsets sum_{k!=n} i_k stride_k
+  // bounds for the device-check build (CPB_DEVICE_CHECKS; 0 = unknown)
+  i64 xsize;                       // elements behind x (the tensor or a replica)
+  i64 kdim[kMaxOrder];             // per kept mode c: rows of fac[c]
 };
 
 inline int ceil_div(i64 a, i64 b) { return static_cast<int>((a + b - 1) / b); }

@@ -6,6 +6,25 @@
 
 namespace cpb {
 
+// Device-check build (make checklib: -DCPB_DEVICE_CHECKS): bounds asserts on
+// the sampled reads and a time-out on the persistent kernels' flag waits,
+// both trapping with a message (compute-sanitizer is not available on the
+// GPU pool). Compiles to nothing in the product build.
+#ifdef CPB_DEVICE_CHECKS
+#define CPB_DCHECK(cond, what)                                                                          \
+  do {                                                                                                  \
+    if (!(cond)) {                                                                                      \
+      printf("CPB_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,          \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                              \
+      __trap();                                                                                         \
+    }                                                                                                   \
+  } while (0)
+#else
+#define CPB_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

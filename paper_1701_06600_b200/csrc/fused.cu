@@ -623,10 +623,10 @@ __device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, co
             z_load<RT>(M.v, A.z, l0, cl, kpl, t);
           }
           gemm_tile<RT>(M.v.x, M.vec16 != 0, in, static_cast<i64>(mt) * BM, r, cl, kpl, t,
-                        A.part_rhs + static_cast<i64>(kb) * in * r);
+                        A.part_rhs + static_cast<i64>(kb) * in * r, M.v.xsize);
         } else {
           gemm_tile<RT>(M.v.x, M.vec16 != 0, in, static_cast<i64>(mt) * BM, r, cnt, kpad, t,
-                        A.part_rhs + static_cast<i64>(kb) * in * r);
+                        A.part_rhs + static_cast<i64>(kb) * in * r, M.v.xsize);
         }
         signal_add(M.mt_cnt + mt * kCS, 1u);
       }
@@ -696,6 +696,7 @@ __device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, co
           const int il = e / r, c = e - il * r;
           double o = 0.0;
           for (int cc = 0; cc < r; ++cc) o = fma(rh[il * LD + cc], gi[cc * LD + c], o);
+          CPB_DCHECK(r0 + il < in && c < r, "apply: factor row");
           if (PEER && np > 1 && n == A.order - 1) {  // slab rows into every rank's factor
             for (int q = 0; q < np; ++q) A.pfac[q][(A.slab_off + r0 + il) * r + c] = o;
           } else {

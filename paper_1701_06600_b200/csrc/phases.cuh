@@ -31,6 +31,7 @@ __device__ __forceinline__ double z_entry(const ModeView& v, int s, int rr) {
   double zv = 1.0;
   for (int c = 0; c < v.kept; ++c) {
     const int row = __ldg(v.rows[c] + s);
+    CPB_DCHECK(v.kdim[c] == 0 || (row >= 0 && row < v.kdim[c]), "z_entry: sampled row");
     double a = __ldcg(v.fac[c] + static_cast<i64>(row) * v.r + rr);  // written earlier in a persistent launch
     if (v.nrm[c]) a = a / __ldcg(v.nrm[c] + rr);
     zv = __dmul_rn(zv, a);

@@ -1561,9 +1561,11 @@ ModeView Session::view(int it, int n) const {
     v.fac[c] = cmix_ ? mixedc_[static_cast<size_t>(m)]
                      : (mix_ ? mixed_[static_cast<size_t>(m)] : fac_[static_cast<size_t>(m)]);
     v.nrm[c] = (mix_ || cmix_) ? nullptr : norms_ + static_cast<i64>(m) * r_;
+    v.kdim[c] = dims_[static_cast<size_t>(m)];
     ++c;
   }
   v.base = base_ptr(it, n);
+  v.xsize = tp_;
   return v;
 }
 

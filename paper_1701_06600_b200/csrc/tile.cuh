@@ -100,8 +100,13 @@ __device__ __forceinline__ void wait_geq(const unsigned* p, unsigned target, uns
     if (sleep_ns) {
       while (ld_relaxed(p) < target) __nanosleep(sleep_ns);
     } else {
+#ifdef CPB_DEVICE_CHECKS
+      const unsigned long long t0 = globaltimer();
+      while (ld_relaxed(p) < target) CPB_DCHECK(globaltimer() - t0 < 5000000000ull, "flag wait > 5 s");
+#else
       while (ld_relaxed(p) < target) {
       }
+#endif
     }
     asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
   }
@@ -153,6 +158,7 @@ __device__ void z_rows(const ModeView& v, int cnt, int kpad, const TileSmem& t) 
         const int sl = base + 8 * u;
         const bool okr = sl < cnt;
         const i64 row = okr ? static_cast<i64>(t.rows[c * kpad + sl]) : 0;
+        CPB_DCHECK(!okr || v.kdim[c] == 0 || (row >= 0 && row < v.kdim[c]), "z_rows: sampled row");
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
           const int rr = lane + 32 * j;
@@ -242,7 +248,10 @@ __device__ void z_rows_global(const ModeView& v, int z0, int z1, double* __restr
   for (int s = z0 + warp; s < z1; s += 8) {
     int row[KEPT];
 #pragma unroll
-    for (int c = 0; c < KEPT; ++c) row[c] = __ldg(v.rows[c] + s);
+    for (int c = 0; c < KEPT; ++c) {
+      row[c] = __ldg(v.rows[c] + s);
+      CPB_DCHECK(v.kdim[c] == 0 || (row[c] >= 0 && row[c] < v.kdim[c]), "z_rows_global: sampled row");
+    }
     double av[KEPT][CPL];
 #pragma unroll
     for (int c = 0; c < KEPT; ++c)
@@ -363,7 +372,12 @@ __device__ void gram_blocks_add(const TileSmem& t, int kpad, int nfr, int first,
 // resident in shared memory.
 template <int RT>
 __device__ void gemm_tile(const double* __restrict__ x, bool vec16, i64 in, i64 i0, int r, int cnt,
-                          int kpad, const TileSmem& t, double* __restrict__ out) {
+                          int kpad, const TileSmem& t, double* __restrict__ out, i64 xsize = 0) {
+#ifndef CPB_DEVICE_CHECKS
+  (void)xsize;
+#else
+  if (xsize == 0) xsize = i64{1} << 62;
+#endif
   using C = Cfg<RT>;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int wm = warp / C::WN, wn = warp % C::WN;
@@ -380,6 +394,7 @@ __device__ void gemm_tile(const double* __restrict__ x, bool vec16, i64 in, i64 
         const i64 i = i0 + ic;
         const bool ok = (s < cnt) && (i < in);
         const int bytes = !ok ? 0 : (i + 1 < in ? 16 : 8);
+        CPB_DCHECK(!ok || (t.roff[s] >= 0 && t.roff[s] + i + bytes / 8 <= xsize), "gemm_tile: fiber read");
         cp_async16(ab + sl * SA + ic, ok ? x + t.roff[s] + i : x, bytes);
       }
     } else {
@@ -390,6 +405,7 @@ __device__ void gemm_tile(const double* __restrict__ x, bool vec16, i64 in, i64 
         const int s = sb + sl;
         const i64 i = i0 + ic;
         const bool ok = (s < cnt) && (i < in);
+        CPB_DCHECK(!ok || (t.roff[s] >= 0 && t.roff[s] + i < xsize), "gemm_tile: fiber read");
         cp_async8(ab + sl * SA + ic, ok ? x + t.roff[s] + i : x, ok ? 8 : 0);
       }
     }

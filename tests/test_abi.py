@@ -82,3 +82,17 @@ def test_cpp_dropin_header_compiles():
     subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), src],
                    check=True)
     assert os.path.exists(src) and out
+
+
+def test_device_check_build_differs_only_by_checks():
+    """The device-check variant (make checklib) exports the same C ABI and
+    carries the trap messages; the product library has none of them."""
+    prod = os.path.join(ROOT, "paper_1701_06600_b200", "libcprand_b200.so")
+    chk = os.path.join(ROOT, "paper_1701_06600_b200", "libcprand_b200_check.so")
+    if not os.path.exists(chk):
+        pytest.skip("device-check library not built (make checklib)")
+    data_p, data_c = open(prod, "rb").read(), open(chk, "rb").read()
+    assert b"CPB_DCHECK failed" in data_c and b"CPB_DCHECK failed" not in data_p
+    sym = lambda p: set(re.findall(r"\bT (cprand_\w+)$", subprocess.run(  # noqa: E731
+        ["nm", "-D", "--defined-only", p], capture_output=True, text=True, check=True).stdout, flags=re.M))
+    assert sym(prod) == sym(chk) and len(sym(prod)) > 20
