@@ -404,6 +404,24 @@ def main() -> int:
                            comm=comm, shard_total=cfg["dims"][-1] if comm is not None else 0,
                            atomic_gram=args.atomic_gram)
     s = pb.Session(cfg["method"], t, cfg["r"], cfg["s"], opts)
+    peer_fallback = None
+    if ws > 1:
+        # the peer kernel's first multi-GPU launches: if any rank's run fails
+        # (a peer mapping or a peer wait that timed out raises), every rank
+        # agrees and re-runs on the multi-kernel chain with NCCL
+        failed = 0.0
+        try:
+            s.run(args.warmup)
+        except Exception as exc:  # noqa: BLE001 - reported in the JSON line
+            failed, peer_fallback = 1.0, f"peer kernel failed on rank {rank}: {exc}"
+        if allreduce_max(dist, failed) > 0:
+            try:
+                s.close()
+            except Exception:  # noqa: BLE001
+                pass
+            opts.fused = 0
+            s = pb.Session(cfg["method"], t, cfg["r"], cfg["s"], opts)
+            peer_fallback = peer_fallback or "peer kernel failed on another rank"
     clk = ClockSampler(dev).__enter__()
     s.run(args.warmup)
     time.sleep(0.3)  # sampler live before the timed region
@@ -604,6 +622,7 @@ def main() -> int:
             "comm": (("peer kernel: RHS rows / last-mode slabs stored into every rank's buffers "
                       "(CUDA IPC mappings over NVLink, sys-scope flags); NCCL for setup")
                      if used_fused else "NCCL allreduce / allgather / send-recv") if ws > 1 else None,
+            "peer_fallback": peer_fallback,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": kname,
                          "bytes_model": bytes_model, "per_mode_gbs": per_mode,
