@@ -68,16 +68,54 @@ __device__ __forceinline__ ModeWork work_of(const FusedIter& A, const FusedMode&
   return w;
 }
 
-template <int RT, bool MIX>
-__global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const FusedIter* __restrict__ args) {
+// Peer path: sys-scope polling with a time-out (a rank that never arrives
+// must not hang the GPU: after 20 s the wait gives up and flags *err, which
+// the host turns into an error).
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void peer_wait(const unsigned* p, unsigned target, int* err) {
+  if (threadIdx.x == 0) {
+    unsigned long long t0 = 0;
+    while (ld_relaxed_sys(p) < target) {
+      const unsigned long long now = globaltimer();
+      if (!t0) t0 = now;
+      if (now - t0 > 20000000000ull) {
+        atomicExch(err, 1);
+        break;
+      }
+    }
+    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void red_release_sys(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// PEER: the slab-sharded CPRAND-MIX iteration (FusedIter::np ranks, peer
+// memory as in rand_body): modes n < N-1 contract this rank's fibers (its
+// owner-ordered sample range) and every apply block exchanges its rows' RHS
+// sums with the same block of every rank (rank-order sum, so the mixed
+// factors stay replicated); the last mode applies the slab's rows, stores
+// them and the block's sums of squares into every rank's buffers, and CTA 0
+// of every rank forms the norms once all ranks' partials are in.
+
+template <int RT, bool MIX, bool PEER>
+__device__ __forceinline__ void iter_body(const FusedIter* __restrict__ args, const unsigned G, const unsigned b) {
   const FusedIter& A = *args;
   if (A.stop && *A.stop) return;  // uniform: the flag only changes in a previous launch
   extern __shared__ __align__(16) double fsm[];
   __shared__ int perm[RT];
   __shared__ bool s_last;
-  const unsigned G = gridDim.x, b = blockIdx.x;
   const int tid = threadIdx.x;
   const int r = A.r;
+  const int np = PEER ? A.np : 1;
+  const unsigned seq = A.seq;
+  if (PEER && np > 1 && seq > 1)  // every rank's last-mode rows of the previous launch (Z_S of mode 0 reads them)
+    peer_wait(A.mode[A.order - 1].adone + (b % kRep) * kCS, A.lastw * (seq - 1), A.perr);
   auto stamp = [&](int n, int k) {
     if (A.phase_t && b == 0 && tid == 0) A.phase_t[n * 16 + k] = globaltimer();
   };
@@ -151,12 +189,17 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
         if (tid == 0) atomicAdd(A.gram_done, 1u);
       }
       const int ntiles = M.mtiles * M.ks;
+      // peer path, modes n < N-1: this rank's fibers, the owner-ordered range [loff, loff + lcnt)
+      const bool loc = PEER && np > 1 && n < A.order - 1;
+      const i64* gbase = loc ? M.v.base + M.loff : M.v.base;
+      const double* gz = loc ? A.z + static_cast<i64>(M.loff) * RT : A.z;
+      const int gs = loc ? M.lcnt : M.v.s;
       for (int t = b; t < ntiles; t += G - 1) {
         if (M.vec16)
-          ph::gemm_tile<RT, true>(M.v.x, 0, M.v.base, A.z, M.v.in, M.v.s, r, M.ks_len, A.part_rhs, t % M.mtiles,
+          ph::gemm_tile<RT, true>(M.v.x, 0, gbase, gz, M.v.in, gs, r, M.ks_len, A.part_rhs, t % M.mtiles,
                                   t / M.mtiles, fsm);
         else
-          ph::gemm_tile<RT, false>(M.v.x, 0, M.v.base, A.z, M.v.in, M.v.s, r, M.ks_len, A.part_rhs, t % M.mtiles,
+          ph::gemm_tile<RT, false>(M.v.x, 0, gbase, gz, M.v.in, gs, r, M.ks_len, A.part_rhs, t % M.mtiles,
                                    t / M.mtiles, fsm, M.est);
       }
     }
@@ -195,6 +238,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
     {
       ModeWork wm = w;
       wm.a = M.mixed;  // the apply writes the mixed, unnormalized factor
+      const bool plast = PEER && np > 1 && n == A.order - 1;
+      if (plast) wm.a = M.mixed + A.slab_off * r;  // this rank's slab rows of the last mode
       wm.q = qs;
       wm.qrws = A.qrws;
       constexpr int BI = kFusedThreads / RT;
@@ -219,7 +264,85 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
           for (int blk = 0; blk < nblk; ++blk)
             q += ph::apply_block<RT, kFusedThreads>(M.v.in, r, wm, A.rhs_full, static_cast<i64>(blk) * BI, gi, rh);
           ph::ssq_store<RT, kFusedThreads>(q, r, A.ssq, rh);
-          remix(ph::norms_final<RT, kFusedThreads>(r, M.v.in, w, 1, n == 0, A.rng, rh));
+          remix(ph::norms_final<RT, kFusedThreads>(r, M.in_full, w, 1, n == 0, A.rng, rh));
+        }
+      } else if (PEER && np > 1) {
+        // peer path: every CTA takes its row blocks (possibly none)
+        ph::load_ginv<RT, kFusedThreads>(A.ginv, r, gi);
+        __syncthreads();
+        double q = 0.0;
+        for (int blk = b; blk < nblk; blk += G) {
+          const i64 i0 = static_cast<i64>(blk) * BI;
+          if (!plast) {
+            // this block's local RHS sums (split order) to block prank of
+            // every rank's receive buffer; the same block of every rank then
+            // sums the np blocks in rank order into rhs_full
+            const i64 tot = M.v.in * r;
+            for (int e = tid; e < BI * r; e += kFusedThreads) {
+              const i64 i = i0 + e / r;
+              if (i >= M.v.in) continue;
+              const i64 o = i * r + e % r;
+              double sum = 0.0;
+              for (int k = 0; k < M.ks; ++k) sum += __ldcg(A.part_rhs + static_cast<i64>(k) * tot + o);
+              for (int qq = 0; qq < np; ++qq) A.precv[qq][static_cast<i64>(A.prank) * A.rcv_ld + o] = sum;
+            }
+            __threadfence_system();
+            __syncthreads();
+            const i64 slot = (static_cast<i64>(n) * A.ptiles + blk) * kCS;
+            if (tid < np) red_release_sys(A.prcnt[tid] + slot, 1u);
+            peer_wait(A.prcnt[A.prank] + slot, static_cast<unsigned>(np) * seq, A.perr);
+            for (int e = tid; e < BI * r; e += kFusedThreads) {
+              const i64 i = i0 + e / r;
+              if (i >= M.v.in) continue;
+              const i64 o = i * r + e % r;
+              double sum = 0.0;
+              for (int qq = 0; qq < np; ++qq) sum += __ldcv(A.precv[A.prank] + static_cast<i64>(qq) * A.rcv_ld + o);
+              A.rhs_full[o] = sum;
+            }
+            __syncthreads();
+            q += ph::apply_block<RT, kFusedThreads>(M.v.in, r, wm, A.rhs_full, i0, gi, rh);
+          } else {
+            q += ph::apply_block<RT, kFusedThreads>(M.v.in, r, wm, nullptr, i0, gi, rh);
+            // the block's rows into every other rank's mixed factor
+            for (int e = tid; e < BI * r; e += kFusedThreads) {
+              const i64 i = i0 + e / r;
+              if (i >= M.v.in) continue;
+              const i64 o = (A.slab_off + i) * r + e % r;
+              const double v = __ldcg(M.mixed + o);
+              for (int qq = 0; qq < np; ++qq)
+                if (qq != A.prank) A.pfac[qq][o] = v;
+            }
+          }
+        }
+        if (plast) {
+          // sums of squares into every rank's [np][G] partials, then every
+          // rank's counter; CTA 0 of each rank forms the norms from all of them
+          double* own = A.pssq[A.prank] + (static_cast<i64>(A.prank) * G + b) * r;
+          ph::ssq_store<RT, kFusedThreads>(q, r, own, rh);
+          if (tid < r)
+            for (int qq = 0; qq < np; ++qq)
+              if (qq != A.prank) A.pssq[qq][(static_cast<i64>(A.prank) * G + b) * r + tid] = own[tid];
+          __threadfence_system();
+          __syncthreads();
+          if (tid < np * kRep) red_release_sys(A.pdone[tid / kRep] + (tid % kRep) * kCS, 1u);
+          if (b == 0) {
+            peer_wait(M.adone + (b % kRep) * kCS, A.lastw * seq, A.perr);
+            ModeWork wq = w;
+            wq.ssq = A.pssq[A.prank];
+            remix(ph::norms_final<RT, kFusedThreads>(r, M.in_full, wq, np * static_cast<int>(G), n == 0, A.rng, rh));
+          }
+        } else {
+          // replicated rows: the ticket-based norms below (every CTA took part)
+          ph::ssq_store<RT, kFusedThreads>(q, r, A.ssq + static_cast<i64>(b) * r, rh);
+          __threadfence();
+          __syncthreads();
+          if (tid == 0) s_last = (atomicAdd(&A.ticket[0], 1u) == G - 1u);
+          __syncthreads();
+          if (s_last) {
+            __threadfence();
+            remix(ph::norms_final<RT, kFusedThreads>(r, M.in_full, w, static_cast<int>(G), n == 0, A.rng, rh));
+            if (tid == 0) A.ticket[0] = 0u;
+          }
         }
       } else if (static_cast<int>(b) < min(static_cast<int>(G), nblk)) {
         // the CTAs that own row blocks: apply, column sums of squares, ticket;
@@ -239,7 +362,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
         __syncthreads();
         if (s_last) {
           __threadfence();
-          remix(ph::norms_final<RT, kFusedThreads>(r, M.v.in, w, static_cast<int>(napp), n == 0, A.rng, rh));
+          remix(ph::norms_final<RT, kFusedThreads>(r, M.in_full, w, static_cast<int>(napp), n == 0, A.rng, rh));
           if (tid == 0) A.ticket[0] = 0u;
         }
       }
@@ -291,6 +414,21 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const
       ph::fit_final(f, nvb, red);
     }
   }
+}
+
+template <int RT, bool MIX>
+__global__ void __launch_bounds__(kFusedThreads, 2) fused_iteration_kernel(const FusedIter* __restrict__ args) {
+  iter_body<RT, MIX, false>(args, gridDim.x, blockIdx.x);
+}
+template <int RT>
+__global__ void __launch_bounds__(kFusedThreads, 2) peer_mix_kernel(const FusedLaunch L) {
+  const unsigned G = gridDim.x / static_cast<unsigned>(L.groups);
+  const unsigned grp = blockIdx.x / G;
+  const FusedIter* ap = L.a[0];
+#pragma unroll
+  for (int q = 1; q < kMaxPeer; ++q)
+    if (static_cast<int>(grp) == q) ap = L.a[q];
+  iter_body<RT, true, true>(ap, G, blockIdx.x - grp * G);
 }
 
 // ---------------------------------------------------------------------------
@@ -362,33 +500,6 @@ __device__ __forceinline__ void prefetch_tables(const FusedIter& A, unsigned b) 
       line -= nl;
     }
   }
-}
-
-// Peer path: sys-scope polling with a time-out (a rank that never arrives
-// must not hang the GPU: after 20 s the wait gives up and flags *err, which
-// the host turns into an error).
-__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void peer_wait(const unsigned* p, unsigned target, int* err) {
-  if (threadIdx.x == 0) {
-    unsigned long long t0 = 0;
-    while (ld_relaxed_sys(p) < target) {
-      const unsigned long long now = globaltimer();
-      if (!t0) t0 = now;
-      if (now - t0 > 20000000000ull) {
-        atomicExch(err, 1);
-        break;
-      }
-    }
-    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
-  }
-  __syncthreads();
-}
-__device__ __forceinline__ void red_release_sys(unsigned* p, unsigned v) {
-  asm volatile("red.release.sys.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
 // GA: the Gram is summed with L2 fp64 atomics (FusedIter::gram_atomic).
@@ -780,8 +891,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) peer_rand_kernel(const Fused
 }
 
 template <int RT>
-void* mix_fn() {
-  return reinterpret_cast<void*>(&fused_iteration_kernel<RT, true>);
+void* mix_fn(bool peer = false) {
+  return peer ? reinterpret_cast<void*>(&peer_mix_kernel<RT>) : reinterpret_cast<void*>(&fused_iteration_kernel<RT, true>);
 }
 template <int RT>
 void* rand_fn(bool ga, bool peer = false) {
@@ -792,9 +903,9 @@ void* rand_fn(bool ga, bool peer = false) {
 
 void* pick(int rt, bool mix, bool ga = false, bool peer = false) {
   switch (rt) {
-    case 16: return mix ? mix_fn<16>() : rand_fn<16>(ga, peer);
-    case 32: return mix ? mix_fn<32>() : rand_fn<32>(ga, peer);
-    default: return mix ? mix_fn<64>() : rand_fn<64>(ga, peer);
+    case 16: return mix ? mix_fn<16>(peer) : rand_fn<16>(ga, peer);
+    case 32: return mix ? mix_fn<32>(peer) : rand_fn<32>(ga, peer);
+    default: return mix ? mix_fn<64>(peer) : rand_fn<64>(ga, peer);
   }
 }
 
@@ -868,12 +979,11 @@ int fused_max_grid(int rt, bool mix, size_t smem, int device) {
   if (!coop) return 0;
   void* fn = pick(rt, mix);
   CPB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  if (!mix) {
+  if (!mix)
     CPB_CUDA(cudaFuncSetAttribute(pick(rt, false, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-    CPB_CUDA(cudaFuncSetAttribute(pick(rt, false, false, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-  }
+  CPB_CUDA(cudaFuncSetAttribute(pick(rt, mix, false, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
   int per_sm = 0;
   CPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFusedThreads, smem));
   return per_sm * sms;
@@ -886,8 +996,8 @@ void launch_fused_iteration(const FusedIter* dev_args, int rt, bool mix, int gri
   CPB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFusedThreads), params, smem, st));
 }
 
-void launch_fused_peer(const FusedLaunch& l, int rt, int grid, size_t smem, cudaStream_t st) {
-  void* fn = pick(rt, false, false, true);
+void launch_fused_peer(const FusedLaunch& l, int rt, int grid, size_t smem, cudaStream_t st, bool mix) {
+  void* fn = pick(rt, mix, false, true);
   FusedLaunch lc = l;
   void* params[] = {&lc};
   CPB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFusedThreads), params, smem, st));

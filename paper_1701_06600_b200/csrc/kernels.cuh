@@ -338,6 +338,6 @@ int fused_max_grid(int rt, bool mix, size_t smem, int device);
 void launch_fused_iteration(const FusedIter* dev_args, int rt, bool mix, int grid, size_t smem,
                             cudaStream_t st, bool gram_atomic = false);
 // The peer path's CPRAND kernel (grid = groups x group size).
-void launch_fused_peer(const FusedLaunch& l, int rt, int grid, size_t smem, cudaStream_t st);
+void launch_fused_peer(const FusedLaunch& l, int rt, int grid, size_t smem, cudaStream_t st, bool mix = false);
 
 }  // namespace cpb

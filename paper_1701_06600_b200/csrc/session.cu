@@ -586,7 +586,7 @@ void Session::setup_fused() {
   // (collective decision: every rank takes the same path)
   if (shard_) {
     static const bool peer_env = !(std::getenv("CPRAND_PEER") && std::atoi(std::getenv("CPRAND_PEER")) == 0);
-    const bool can = !mix_ && all_direct && o_.fused != 0 && peer_env && nranks_ <= kMaxPeer &&
+    const bool can = (mix_ ? transform_ == 1 : all_direct) && o_.fused != 0 && peer_env && nranks_ <= kMaxPeer &&
                      comm_->peer_mode() != 0;
     double* f = dalloc<double>(1);
     const double v = can ? 1.0 : 0.0;
@@ -688,15 +688,21 @@ void Session::setup_fused() {
   i64 rcv_ld = 1, off_cnt = 0, off_ssq = 0, off_done = 0;
   int ptiles = 1;
   unsigned lastw = 0;
+  // per rank: the CTAs whose last-mode sums of squares the norms read (the
+  // CPRAND kernel's tile CTAs; every CTA of the MIX kernel)
+  const int gparts = mix_ ? fgrid_ : gw;
   if (peer_) {
     for (int n = 0; n + 1 < order_; ++n) {
       rcv_ld = std::max<i64>(rcv_ld, dims_[static_cast<size_t>(n)] * r_);
-      ptiles = std::max(ptiles, tm[static_cast<size_t>(n)] * tk[static_cast<size_t>(n)]);
+      // exchange slots per mode: the CPRAND kernel's apply shares (tiles), the
+      // MIX kernel's apply blocks of 256 / RT rows
+      ptiles = std::max(ptiles, mix_ ? ceil_div(dims_[static_cast<size_t>(n)], 256 / rt_)
+                                     : tm[static_cast<size_t>(n)] * tk[static_cast<size_t>(n)]);
     }
     auto al = [](i64 b) { return (b + 255) / 256 * 256; };
     off_cnt = al(static_cast<i64>(nranks_) * rcv_ld * 8);
     off_ssq = off_cnt + al(static_cast<i64>(order_) * ptiles * kCS * 4);
-    off_done = off_ssq + al(static_cast<i64>(nranks_) * gw * r_ * 8);
+    off_done = off_ssq + al(static_cast<i64>(nranks_) * gparts * r_ * 8);
     const i64 bytes = off_done + al(static_cast<i64>(kRep) * kCS * 4);
     parena_ = dalloc<char>(static_cast<size_t>(bytes));
     CPB_CUDA(cudaMemsetAsync(parena_, 0, static_cast<size_t>(bytes), stream_));
@@ -706,7 +712,7 @@ void Session::setup_fused() {
     CPB_CUDA(cudaStreamSynchronize(stream_));
     // every rank's Gw (equal on identical devices; summed, not assumed)
     double* f = dalloc<double>(1);
-    const double v = gw;
+    const double v = gparts;
     CPB_CUDA(cudaMemcpyAsync(f, &v, sizeof(double), cudaMemcpyHostToDevice, stream_));
     allreduce_sum(f, 1);
     double tot = 0.0;
@@ -714,10 +720,11 @@ void Session::setup_fused() {
     CPB_CUDA(cudaStreamSynchronize(stream_));
     dfree(f);
     lastw = static_cast<unsigned>(tot + 0.5);
-    if (lastw != static_cast<unsigned>(gw) * static_cast<unsigned>(nranks_))
+    if (lastw != static_cast<unsigned>(gparts) * static_cast<unsigned>(nranks_))
       throw Unsupported("peer path: ranks with different grids");
     parena_all_ = comm_->share_pointers(parena_);
-    pfac_all_ = comm_->share_pointers(fac_[static_cast<size_t>(order_ - 1)]);
+    // the last mode's factor every rank stores its slab rows into (MIX: the mixed image)
+    pfac_all_ = comm_->share_pointers(mix_ ? mixed_[static_cast<size_t>(order_ - 1)] : fac_[static_cast<size_t>(order_ - 1)]);
     if (parena_all_.empty() || pfac_all_.empty()) {  // no peer mapping on some rank: the chain
       comm_->release_pointers(parena_all_);
       comm_->release_pointers(pfac_all_);
@@ -750,7 +757,14 @@ void Session::setup_fused() {
         M.vec16 = 0;
         M.est = tstrides_[static_cast<size_t>(n)];
       }
-      M.mtiles = ceil_div(dims_[static_cast<size_t>(n)], 128);
+      M.mtiles = ceil_div(tdims_[static_cast<size_t>(n)], 128);
+      M.in_full = dims_[static_cast<size_t>(n)];
+      M.v.in = tdims_[static_cast<size_t>(n)];  // a sharded last mode: the slab's rows
+      if (peer_) {
+        const size_t pi = static_cast<size_t>(ti * order_ + n);
+        M.loff = ploff_[pi];
+        M.lcnt = plcnt_[pi];
+      }
       M.ks = ks_[static_cast<size_t>(n)];
       M.ks_len = ks_len_[static_cast<size_t>(n)];
       gram_splits(s_mode_[static_cast<size_t>(n)], &M.gparts, &M.gklen);
@@ -768,7 +782,9 @@ void Session::setup_fused() {
         // the multi-CTA apply beats the one-CTA tail also for C3's 80 x 10
         // factors: 10.7 k vs 9.8 k it/s; CPRAND_TAIL1_MAX re-enables the tail)
         static const i64 tail1_max = std::getenv("CPRAND_TAIL1_MAX") ? std::atoll(std::getenv("CPRAND_TAIL1_MAX")) : 0;
-        M.tail1 = (dims_[static_cast<size_t>(n)] * r_ <= tail1_max) ? 1 : 0;
+        M.tail1 = (!peer_ && dims_[static_cast<size_t>(n)] * r_ <= tail1_max) ? 1 : 0;
+        if (peer_ && nranks_ > 1 && n == order_ - 1)  // counted by every rank's CTAs
+          M.adone = reinterpret_cast<unsigned*>(parena_ + off_done);
         // the kernel keeps the mixed factors unnormalized: Z_S divides by the
         // norms (ones until a mode's first update)
         for (int m = 0, c2 = 0; m < order_; ++m) {
@@ -788,14 +804,7 @@ void Session::setup_fused() {
         M.mcnt = c + static_cast<size_t>(tm_max + tk_max_) * kCS;
         M.gm_cnt = c + static_cast<size_t>(tm_max + tk_max_ + 3) * kCS;
         M.dist_gram = (tm[k] * tk[k] <= gw) ? 1 : 0;
-        M.in_full = dims_[k];
-        M.v.in = tdims_[k];  // a sharded last mode: the slab's rows
-        if (peer_) {
-          const size_t pi = static_cast<size_t>(ti * order_ + n);
-          M.loff = ploff_[pi];
-          M.lcnt = plcnt_[pi];
-          M.tkllen = M.lcnt > 0 ? std::max(4, (ceil_div(M.lcnt, tk[k]) + 3) / 4 * 4) : 0;
-        }
+        if (peer_) M.tkllen = M.lcnt > 0 ? std::max(4, (ceil_div(M.lcnt, tk[k]) + 3) / 4 * 4) : 0;
         M.grdy = c + static_cast<size_t>(2 * tm_max + tk_max_ + 3) * kCS;
         M.adone = M.grdy + static_cast<size_t>(kRep) * kCS;
         M.nready = M.adone + static_cast<size_t>(kRep) * kCS;
@@ -1223,7 +1232,7 @@ void Session::build_tables() {
           }
         }
       }
-      if (shard_ && !mix_ && n < N - 1 && !o_.exhaustive_samples) {
+      if (shard_ && n < N - 1 && !o_.exhaustive_samples) {
         // peer path: the samples ordered by the rank that owns their fiber
         // (stable, the same order on every rank), so this rank's fibers are
         // one contiguous range; only the summation order of the Gram and the
@@ -1700,7 +1709,7 @@ void Session::enqueue_iteration() {
         FusedLaunch l{};
         l.groups = static_cast<int>(args.size());
         for (size_t q = 0; q < args.size(); ++q) l.a[q] = static_cast<const FusedIter*>(args[q]);
-        launch_fused_peer(l, rt_, fgrid_ * l.groups, fsmem_, st);
+        launch_fused_peer(l, rt_, fgrid_ * l.groups, fsmem_, st, mix_);
       };
       timed(0, 7, stream_, [&] { comm_->launch_group(fargs_ + ti, stream_, go); });
     } else {

@@ -54,7 +54,7 @@ print("rank-deficient run finite", flush=True)
 
 
 # the peer kernel: P rank groups of one launch exchanging through each other's buffers
-def peer(x, r, s, nranks):
+def peer(x, r, s, nranks, method="rand", **kw):
     group = pb.LoopbackGroup(nranks)
     out = [None] * nranks
     total = x.shape[-1]
@@ -65,8 +65,8 @@ def peer(x, r, s, nranks):
         t = pb.DeviceTensor(list(x.shape[:-1]) + [ln], device=0)
         if ln:
             t.upload(np.asfortranarray(x[..., off:off + ln]))
-        sess = pb.Session("rand", t, r, s, pb.SolveOptions(rng_seed=7, max_iters=6, stall_limit=1000, comm=comm,
-                                                            shard_total=total, device=0))
+        sess = pb.Session(method, t, r, s, pb.SolveOptions(rng_seed=7, max_iters=6, stall_limit=1000, comm=comm,
+                                                            shard_total=total, device=0, **kw))
         assert sess.fused
         sess.run(6)
         out[rank] = sess.result()
@@ -80,10 +80,10 @@ def peer(x, r, s, nranks):
     for th in ts:
         th.join()
     group.close()
-    ref = orc.cprand(x, r, s, orc.SolveOptions(rng_seed=7, max_iters=6, stall_limit=1000))
+    ref = orc.solve(method, x, r, s, orc.SolveOptions(rng_seed=7, max_iters=6, stall_limit=1000, **kw))
     d = trace_diff(out[0], ref)
     assert d < 1e-8, d
-    print(f"peer P={nranks} {x.shape} trace diff {d:.1e}", flush=True)
+    print(f"peer {method} P={nranks} {x.shape} trace diff {d:.1e}", flush=True)
 
 
 x, _ = orc.gen_baseline((24, 20, 23), 4, 0.5, 0.01, 11)
@@ -91,4 +91,6 @@ peer(x, 4, 60, 2)
 peer(x, 4, 60, 3)
 x, _ = orc.gen_baseline((130, 70, 90), 12, 0.5, 0.01, 21)
 peer(x, 12, 400, 3)
+x, _ = orc.gen_baseline((40, 36, 30, 33), 10, 0.5, 0.01, 13)
+peer(x, 10, 300, 2, method="mix", transform="dct")
 print("CHECKED OK", flush=True)

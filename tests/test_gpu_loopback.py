@@ -136,21 +136,38 @@ def test_loopback_peer_kernel_tiled(pb, orc, nranks, dims, r, s):
     check_against_unsharded(pb, x, "rand", r, s, res, **kw)
 
 
+@pytest.mark.parametrize("fused", [-1, 0])
 @pytest.mark.parametrize("nranks,dims,transform", [(2, (16, 8, 32), "dct"), (3, (16, 8, 32), "dct"),
                                                    (4, (16, 8, 32), "wht"), (3, (16, 8, 32), "wht"),
                                                    (4, (12, 10, 5), "dct")])
-def test_loopback_sharded_cprand_mix(pb, orc, nranks, dims, transform):
+def test_loopback_sharded_cprand_mix(pb, orc, nranks, dims, transform, fused):
     """Sharded CPRAND-MIX: the distributed mixing pass (row blocks of the
     slab exchanged so every rank transforms whole last-mode fibers, then
-    exchanged back), local-sample RHS + allreduce + unmix, the last mode's
-    RHS slabs allgathered and unmixed."""
+    exchanged back); then, for the DCT, the persistent MIX kernel's peer path
+    (fused=-1: local-sample RHS sums exchanged per apply block, the last
+    mode's mixed slab rows stored into every rank's factor), else the chain
+    (local-sample RHS + allreduce + unmix, the last mode's RHS slabs
+    allgathered and unmixed)."""
     r, s = 3, 60
     x, _ = orc.gen_baseline(dims, r, 0.5, 0.01, 12)
-    kw = dict(rng_seed=12, max_iters=8, stall_limit=1000, transform=transform)
-    res = sharded_solve(pb, x, "mix", r, s, nranks, **kw)
+    kw = dict(rng_seed=12, max_iters=8, stall_limit=1000, transform=transform, fused=fused)
+    res = sharded_solve(pb, x, "mix", r, s, nranks, expect_fused=(fused != 0 and transform == "dct"), **kw)
     check_against_unsharded(pb, x, "mix", r, s, res, **kw)
+    kw.pop("fused")
     o = orc.solve("mix", x, r, s, orc.SolveOptions(**kw))
     assert max(abs(a[2] - b[2]) for a, b in zip(res[0].trace, o.trace)) < 1e-8
+
+
+@pytest.mark.parametrize("nranks,dims,r,s", [(2, (40, 36, 30, 33), 10, 300), (3, (64, 50, 70), 20, 400),
+                                             (4, (48, 40, 36, 30), 32, 500)])
+def test_loopback_peer_mix_kernel(pb, orc, nranks, dims, r, s):
+    """The MIX kernel's peer path at sizes with many apply blocks, strided
+    modes read in place or from replicas, RT = 16 / 32 / 64 (R = 32), last
+    dims P does not divide."""
+    x, _ = orc.gen_baseline(dims, r, 0.5, 0.01, 13)
+    kw = dict(rng_seed=13, max_iters=6, stall_limit=1000, transform="dct")
+    res = sharded_solve(pb, x, "mix", r, s, nranks, expect_fused=True, **kw)
+    check_against_unsharded(pb, x, "mix", r, s, res, **kw)
 
 
 @pytest.mark.parametrize("extra", [dict(fit_threshold=0.97), dict(stall_limit=3)])
