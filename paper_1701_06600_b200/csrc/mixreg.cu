@@ -27,6 +27,8 @@
 // from a cp.async-staged tile (mix_reg3c_kernel: C4 mode 1 2.16 -> 3.4 TB/s).
 // Rounding differs from v2 / v3 in the FFT order only (parity tests: 1e-12).
 #include <algorithm>
+#include <cmath>
+#include <vector>
 
 #include "dct.cuh"
 #include "devutil.cuh"
@@ -50,6 +52,24 @@ constexpr int first_radix() {
   return N;
 }
 
+// The DFT's internal twiddles W_N^j for the register DFT lengths the kernels
+// use, in constant memory: with the indices compile-time constants they are
+// instruction operands, not shared-memory loads (the MIO queue bounds these
+// kernels). Filled once per device by init_wconst.
+__constant__ double2 c_w10[10];
+__constant__ double2 c_w16[16];
+__constant__ double2 c_w20[20];
+template <int N>
+constexpr bool has_wconst() {
+  return N == 10 || N == 16 || N == 20;
+}
+template <int N>
+__device__ __forceinline__ double2 wconst(int j) {
+  if constexpr (N == 10) return c_w10[j];
+  else if constexpr (N == 16) return c_w16[j];
+  else return c_w20[j];
+}
+
 // forward DFT of N points in registers (mixed radix, decimation in time);
 // roots: the n-th roots exp(-2 pi i t / n) (shared memory, broadcast reads),
 // N divides n, rs = n / N
@@ -71,7 +91,14 @@ __device__ __forceinline__ void dft_reg(double2 (&v)[N], const double2* roots, i
     for (int k = 0; k < M; ++k) {
       double2 t[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) t[r] = (r == 0 || k == 0) ? sub[r][k] : cmulw(sub[r][k], roots[r * k * rs]);
+      for (int r = 0; r < R; ++r) {
+        if (r == 0 || k == 0)
+          t[r] = sub[r][k];
+        else if constexpr (has_wconst<N>())
+          t[r] = cmulw(sub[r][k], wconst<N>((r * k) % N));  // = roots[r k rs]
+        else
+          t[r] = cmulw(sub[r][k], roots[r * k * rs]);
+      }
       dct::dft<R>(t, false);
 #pragma unroll
       for (int u = 0; u < R; ++u) v[k + M * u] = t[u];
@@ -659,6 +686,27 @@ bool launch_reg2_t(const DctPlan& pl, double* x, i64 st, i64 nfib, const double*
   return true;
 }
 
+// W_N^j = exp(-2 pi i j / N), rounded from long double as make_dct_plan rounds its tables
+void init_wconst() {
+  int dev = 0;
+  CPB_CUDA(cudaGetDevice(&dev));
+  static unsigned long long done = 0;  // devices initialized (host code runs these launches in order)
+  if (dev < 64 && ((done >> dev) & 1ull)) return;
+  const long double pi = 3.141592653589793238462643383279502884L;
+  auto fill = [&](const void* sym, int n) {
+    std::vector<double2> w(static_cast<size_t>(n));
+    for (int j = 0; j < n; ++j) {
+      const long double a = 2.0L * pi * static_cast<long double>(j) / static_cast<long double>(n);
+      w[static_cast<size_t>(j)] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(-sinl(a)));
+    }
+    CPB_CUDA(cudaMemcpyToSymbol(sym, w.data(), sizeof(double2) * n));
+  };
+  fill(c_w10, 10);
+  fill(c_w16, 16);
+  fill(c_w20, 20);
+  if (dev < 64) done |= 1ull << dev;
+}
+
 }  // namespace
 
 // v4 whole-tensor pass for a strided mode (st >= 32) of a supported length;
@@ -667,6 +715,7 @@ bool launch_mix_reg(const DctPlan& pl, double* x, i64 st, i64 nfib, const double
                     bool prepare_only) {
   if (pl.kind != 1) return false;
   if (std::getenv("CPRAND_MIX_V2") || std::getenv("CPRAND_MIX_TMA")) return false;
+  init_wconst();
   if (st == 1) {  // mode 1: contiguous fibers
     switch (pl.n) {
       case 256: return launch_reg2c_t<16, 16, 16, 2>(pl, x, nfib, sign, stream, prepare_only);

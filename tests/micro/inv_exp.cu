@@ -90,5 +90,6 @@ int main() {
   report(NAME);
   RUN(0, "la");
   RUN(1, "no-mma");
+  RUN(2, "w7-regs");
   return 0;
 }

@@ -106,11 +106,24 @@ __device__ bool inverse_x(const double* __restrict__ g, int r, double tol, doubl
   using I4 = std::integral_constant<int, 4>;
   publish(I0{}, I0{}, I0{}, I4{}, I0{}, 0, ct == 0, rbs, cbs, true);
   __syncthreads();
+  double Pr[16];  // VAR & 2: warp 7 keeps the current pivot inverse in registers (every lane)
   if (w == 7) {
-    bool ok;
-    const double v = inv4_cofactor(tmp, thr, ok);
-    if (l < 16) pin[l] = v;
-    if (l == 0) misc[2] = ok ? 0.0 : 1.0;
+    if constexpr (VAR & 2) {
+      double tv[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) tv[e] = tmp[e];
+      const bool ok = ph::inv4_minors(tv, Pr, thr);
+      if (l == 0) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pin[e] = Pr[e];
+        misc[2] = ok ? 0.0 : 1.0;
+      }
+    } else {
+      bool ok;
+      const double v = inv4_cofactor(tmp, thr, ok);
+      if (l < 16) pin[l] = v;
+      if (l == 0) misc[2] = ok ? 0.0 : 1.0;
+    }
   }
   __syncthreads();
   CPB_INV_STAMP(2);
@@ -132,7 +145,41 @@ __device__ bool inverse_x(const double* __restrict__ g, int r, double tol, doubl
       const double* P = pin + 16 * pb;
       const double* rb = rbs + pb * 8 * RT;
       const double* cb = cbs + pb * RT * 4;
-      if (w == 7 && k0 + 4 < r4) {
+      if constexpr ((VAR & 2) != 0) {
+        if (w == 7 && k0 + 4 < r4) {
+          // every lane: the next pivot block T = RAW(K+, K+) - RAW(K+, K) P ROWS_K(K+)
+          // and its inverse, all in registers (no shared-memory round trip)
+          double Rr[4][4], Wn[4][4], Wk[4][4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+              Rr[k][y] = rb[k * RT + k0 + 4 + y];
+              Wn[k][y] = rb[(4 + k) * RT + k0 + 4 + y];
+              Wk[k][y] = rb[(4 + k) * RT + k0 + y];
+            }
+          double Q[4][4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int y = 0; y < 4; ++y)
+              Q[q][y] = fma(Pr[q * 4], Rr[0][y], Pr[q * 4 + 1] * Rr[1][y]) + fma(Pr[q * 4 + 2], Rr[2][y], Pr[q * 4 + 3] * Rr[3][y]);
+          double Tm[16];
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y)
+              Tm[x * 4 + y] = (Wn[x][y] - fma(Wk[x][0], Q[0][y], Wk[x][1] * Q[1][y])) - fma(Wk[x][2], Q[2][y], Wk[x][3] * Q[3][y]);
+          CPB_INV_STAMP_AT(43, s, l == 0);
+          const bool ok = ph::inv4_minors(Tm, Pr, thr);
+          if (l == 0) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pin[16 * (pb ^ 1) + e] = Pr[e];
+            misc[2 + (pb ^ 1)] = ok ? 0.0 : 1.0;
+          }
+          CPB_INV_STAMP_AT(44, s, l == 0);
+        }
+      } else if (w == 7 && k0 + 4 < r4) {
         // warp 7: pivot block of step s+1 = rows/columns K_{s+1} after step s
         if (l < 16) {
           const int x = l >> 2, y = l & 3;
