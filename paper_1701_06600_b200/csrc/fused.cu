@@ -559,8 +559,12 @@ __device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, co
       wq.ssq = A.pssq[A.prank];
       nparts = np * static_cast<int>(Gw);
     }
-    const unsigned long long zm = ph::norms_final<RT, kFusedThreads>(
-        r, Q.in_full, wq, nparts, m == 0, A.rng, fsm, nullptr, m >= 1 ? A.mode[m - 1].norms : nullptr);
+    // the column scale the solution carries: the norms of the factor that
+    // entered this mode's Z_S unnormalized (mode m-1; for mode 0 under
+    // lazy_last, the last mode)
+    const double* lam_scale = m >= 1 ? A.mode[m - 1].norms : (A.lazy_last ? A.mode[A.order - 1].norms : nullptr);
+    const unsigned long long zm =
+        ph::norms_final<RT, kFusedThreads>(r, Q.in_full, wq, nparts, m == 0, A.rng, fsm, nullptr, lam_scale);
     signal_add_rep(Q.nready, 1u, kRep);
     return zm;
   };
@@ -588,7 +592,15 @@ __device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, co
       // refilled here (kruskal.hpp:57-63) may race with the tile CTAs reading
       // the previous factor's rows for this mode's Z_S: the mode then takes
       // the QR path on a Z_S rebuilt below from the refilled factor.
-      const unsigned long long zmask = n >= 1 ? form_norms(n - 1) : 0ull;
+      unsigned long long zmask = 0ull;
+      if (n >= 1) {
+        zmask = form_norms(n - 1);
+      } else if (!PEER && A.lazy_last && seq > 1 && *reinterpret_cast<volatile int*>(A.npend)) {
+        // the previous launch's last-mode norms (it ended without forming them)
+        wait_geq(A.mode[A.order - 1].adone + (b % kRep) * kCS, (seq - 1) * Gw);
+        zmask = form_norms(A.order - 1);
+        if (tid == 0) *A.npend = 0;
+      }
       if (A.phase_t && tid == 0) A.phase_t[n * 16 + 13] = globaltimer();
       // ---- Gram: the row-block reducers summed it (dist_gram), or sum the
       // split partials of every 8 x 8 block here (split order)
@@ -666,6 +678,8 @@ __device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, co
       const TileSmem t = tile_smem<RT>(fsm, M.zcap);
       if (n >= 2)  // Z_S divides by the norms of the modes before n-1
         wait_geq(A.mode[n - 2].nready + (b % kRep) * kCS, seq);
+      if (!PEER && A.lazy_last && n == 1 && seq > 1 && A.order >= 3)  // ... and the previous launch's last mode
+        wait_geq(A.mode[A.order - 1].nready + (b % kRep) * kCS, seq - 1);
       // this CTA's share of every one of its splits' Z rows, then signal
       // (no waiting here, so CTAs with several tiles cannot deadlock)
       for (int tt = rank; tt < ntiles; tt += Gw) {
@@ -838,7 +852,12 @@ __device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, co
   if (A.next) prefetch_tables(*A.next, b);
   {  // norms of the last mode (the next launch's Z_S and the fit need them)
     const FusedMode& Lm = A.mode[A.order - 1];
-    if (is_inv) {
+    if (is_inv && !PEER && A.lazy_last) {
+      // the next launch (or fused_finish) forms them; this CTA need not wait
+      if constexpr (GA)  // the last mode's buffer, for the next launch
+        for (int e = tid; e < RT * RT; e += kFusedThreads) A.gsum[((A.order - 1) & 1) * RT * RT + e] = 0.0;
+      if (tid == 0) *A.npend = 1;
+    } else if (is_inv) {
       if (PEER && np > 1)
         peer_wait(Lm.adone + (b % kRep) * kCS, A.lastw * seq, A.perr);
       else
@@ -888,6 +907,23 @@ __global__ void __launch_bounds__(kFusedThreads, 2) peer_rand_kernel(const Fused
   for (int q = 1; q < kMaxPeer; ++q)  // unrolled selects (a dynamic index would go through local memory)
     if (static_cast<int>(grp) == q) ap = L.a[q];
   rand_body<RT, false, true>(ap, G, blockIdx.x - grp * G);
+}
+
+// lazy_last: the last launch's last-mode norms, before the host reads the
+// model (one CTA; the same norms_final call as the persistent kernel's)
+template <int RT>
+__global__ void __launch_bounds__(kFusedThreads) fused_finish_kernel(const FusedIter* __restrict__ args) {
+  const FusedIter& A = *args;
+  if (!*reinterpret_cast<volatile int*>(A.npend)) return;
+  __shared__ double red[(kFusedThreads / RT) * (RT + 1)];
+  const int m = A.order - 1;
+  const FusedMode& Q = A.mode[m];
+  const int gw = A.grid - 1 - (A.idle_cta >= 0 ? 1 : 0);
+  ModeWork wq = work_of(A, Q);
+  wq.ssq = A.ssq + static_cast<i64>(m & 1) * A.grid * A.r;
+  ph::norms_final<RT, kFusedThreads>(A.r, Q.in_full, wq, gw, m == 0, A.rng, red, nullptr, A.mode[m - 1].norms);
+  tl::signal_add_rep(Q.nready, 1u, kRep);
+  if (threadIdx.x == 0) *A.npend = 0;
 }
 
 template <int RT>
@@ -994,6 +1030,15 @@ void launch_fused_iteration(const FusedIter* dev_args, int rt, bool mix, int gri
   void* fn = pick(rt, mix, gram_atomic);
   void* params[] = {const_cast<FusedIter**>(&dev_args)};
   CPB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFusedThreads), params, smem, st));
+}
+
+void launch_fused_finish(const FusedIter* dev_args, int rt, cudaStream_t st) {
+  switch (rt) {
+    case 16: fused_finish_kernel<16><<<1, kFusedThreads, 0, st>>>(dev_args); break;
+    case 32: fused_finish_kernel<32><<<1, kFusedThreads, 0, st>>>(dev_args); break;
+    default: fused_finish_kernel<64><<<1, kFusedThreads, 0, st>>>(dev_args); break;
+  }
+  CPB_LAUNCH_CHECK();
 }
 
 void launch_fused_peer(const FusedLaunch& l, int rt, int grid, size_t smem, cudaStream_t st, bool mix) {

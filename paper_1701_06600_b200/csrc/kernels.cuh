@@ -289,6 +289,13 @@ struct FusedIter {
   unsigned* lbar;        // MIX kernel: this launch's own grid-barrier arrival counter (zeroed once)
   const int* stop;
   int has_fit;
+  // CPRAND kernel, bench mode (no fit): the last mode's norms are formed at
+  // the next launch's mode 0 (or by fused_finish before the model is read):
+  // mode 0's Z_S reads the last factor unnormalized, like every mode n >= 1
+  // reads mode n-1's. npend: device flag "the last launch's norms are pending".
+  int lazy_last;
+  int* npend;
+  int grid;  // CTAs of the persistent launch (the finishing kernel's ssq layout)
   FitArgs fit;
   unsigned long long* phase_t;  // optional: CTA 0 stamps globaltimer at phase edges [order][16]
   // CPRAND kernel roles: the Gram-inverse CTA and an idle CTA sharing its SM
@@ -337,6 +344,8 @@ void fused_rand_tiles(i64 in, int s, int gw, int zcap, int* tm, int* tk, int* tk
 int fused_max_grid(int rt, bool mix, size_t smem, int device);
 void launch_fused_iteration(const FusedIter* dev_args, int rt, bool mix, int grid, size_t smem,
                             cudaStream_t st, bool gram_atomic = false);
+// lazy_last: form the last launch's pending last-mode norms (one CTA)
+void launch_fused_finish(const FusedIter* dev_args, int rt, cudaStream_t st);
 // The peer path's CPRAND kernel (grid = groups x group size).
 void launch_fused_peer(const FusedLaunch& l, int rt, int grid, size_t smem, cudaStream_t st, bool mix = false);
 

@@ -356,6 +356,7 @@ Session::~Session() {
   dfree(zloc_);
   dfree(sh_part_);
   dfree(gpart_);
+  dfree(npend_);
   if (comm_) {
     comm_->release_pointers(parena_all_);
     comm_->release_pointers(pfac_all_);
@@ -736,6 +737,15 @@ void Session::setup_fused() {
   CPB_CUDA(cudaMemsetAsync(fsync_, 0, kSyncWords * sizeof(unsigned), stream_));
   lbar_ = dalloc<unsigned>(static_cast<size_t>(table_iters_) * kCS);  // one barrier counter per launch
   CPB_CUDA(cudaMemsetAsync(lbar_, 0, static_cast<size_t>(table_iters_) * kCS * sizeof(unsigned), stream_));
+  // bench mode without exchanges: the last mode's norms move off the
+  // iteration boundary (formed at the next launch's mode 0, or before the
+  // model is read; fused_finish_kernel)
+  lazy_ = !mix_ && !has_fit_ && !(peer_ && nranks_ > 1) && order_ >= 2 &&
+          !(std::getenv("CPRAND_LAZY_LAST") && std::atoi(std::getenv("CPRAND_LAZY_LAST")) == 0);
+  if (lazy_) {
+    npend_ = dalloc<int>(1);
+    CPB_CUDA(cudaMemsetAsync(npend_, 0, sizeof(int), stream_));
+  }
   std::vector<FusedIter> host(static_cast<size_t>(table_iters_));
   fargs_ = dalloc<FusedIter>(host.size());
   for (int ti = 0; ti < table_iters_; ++ti) {
@@ -820,6 +830,8 @@ void Session::setup_fused() {
             if (m == n - 1) M.v.nrm[c2] = nullptr;
             ++c2;
           }
+        } else if (lazy_) {
+          M.v.nrm[order_ - 2] = nullptr;  // mode 0 reads the last factor unnormalized (kept column N-2)
         }
       }
     }
@@ -837,6 +849,9 @@ void Session::setup_fused() {
     A.gram_first = std::getenv("CPRAND_GRAM_FIRST") ? std::atoi(std::getenv("CPRAND_GRAM_FIRST")) : 0;
     A.gram_atomic = o_.atomic_gram ? 1 : 0;
     A.inv_cta = mix_ ? -1 : inv_cta;
+    A.lazy_last = lazy_ ? 1 : 0;
+    A.npend = npend_;
+    A.grid = fgrid_;
     A.np = 1;
     if (peer_) {
       A.np = nranks_;
@@ -2012,6 +2027,10 @@ void Session::kernel_stats(int mode, int kind, i64* launches, double* ms, double
 }
 
 void Session::download_model(HostModel& m) {
+  if (fused_ && lazy_) {  // the last launch's last-mode norms, if still pending
+    launch_fused_finish(fargs_, rt_, stream_);
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+  }
   m.lambda.resize(static_cast<size_t>(r_));
   CPB_CUDA(cudaMemcpy(m.lambda.data(), lambda_, sizeof(double) * r_, cudaMemcpyDeviceToHost));
   m.factors.clear();

@@ -211,6 +211,8 @@ class Session {
   double* gsum_ = nullptr;         // CPRAND kernel reduced Gram [RT][RT]
   // peer path (sharded CPRAND kernel exchanging through peer memory)
   bool peer_ = false;              // this session launches the peer kernel
+  bool lazy_ = false;              // CPRAND kernel, bench mode: last-mode norms formed at the next launch
+  int* npend_ = nullptr;           // device flag: the last launch's last-mode norms are pending
   char* parena_ = nullptr;         // receive buffer, counters, last-mode ssq partials
   std::vector<void*> parena_all_, pfac_all_;  // every rank's arena / last-mode factor
   int* perr_host_ = nullptr;       // pinned mapped: a peer wait timed out
