@@ -372,8 +372,9 @@ __device__ __forceinline__ void iter_body(const FusedIter* __restrict__ args, co
     stamp(n, 6);
   }
   // ---- the unmixed factors A_un = D DCT-III(mixed) of every mode (the fit
-  // and the result read A_un / norms), one transform group per task
-  {
+  // and the result read A_un / norms), one transform group per task; bench
+  // mode (lazy_last) defers it to before the host reads the model
+  if (A.has_fit || !A.lazy_last) {
     int tasks = 0;
     for (int m = 0; m < A.order; ++m) {
       const int dFm = min(A.mode[m].dctF, (r + 1) & ~1);

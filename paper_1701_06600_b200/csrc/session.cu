@@ -740,7 +740,9 @@ void Session::setup_fused() {
   // bench mode without exchanges: the last mode's norms move off the
   // iteration boundary (formed at the next launch's mode 0, or before the
   // model is read; fused_finish_kernel)
-  lazy_ = !mix_ && !has_fit_ && !(peer_ && nranks_ > 1) && order_ >= 2 &&
+  // (the MIX kernel: the unmix of every factor, needed only by the fit and
+  // the result, moves to download_model)
+  lazy_ = !has_fit_ && !(peer_ && nranks_ > 1) && order_ >= 2 &&
           !(std::getenv("CPRAND_LAZY_LAST") && std::atoi(std::getenv("CPRAND_LAZY_LAST")) == 0);
   if (lazy_) {
     npend_ = dalloc<int>(1);
@@ -2027,8 +2029,15 @@ void Session::kernel_stats(int mode, int kind, i64* launches, double* ms, double
 }
 
 void Session::download_model(HostModel& m) {
-  if (fused_ && lazy_) {  // the last launch's last-mode norms, if still pending
+  if (fused_ && lazy_ && !mix_) {  // the last launch's last-mode norms, if still pending
     launch_fused_finish(fargs_, rt_, stream_);
+    CPB_CUDA(cudaStreamSynchronize(stream_));
+  }
+  if (fused_ && lazy_ && mix_) {  // A_un = D DCT-III(mixed), deferred by the bench-mode MIX kernel
+    for (int n = 0; n < order_; ++n) {
+      const size_t k = static_cast<size_t>(n);
+      launch_mode_transform(plans_[k], mixed_[k], fac_[k], r_, r_, signs_[k], 0, nullptr, stream_);
+    }
     CPB_CUDA(cudaStreamSynchronize(stream_));
   }
   m.lambda.resize(static_cast<size_t>(r_));
