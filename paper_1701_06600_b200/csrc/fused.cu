@@ -375,21 +375,16 @@ __device__ __forceinline__ void iter_body(const FusedIter* __restrict__ args, co
   // and the result read A_un / norms), one transform group per task; bench
   // mode (lazy_last) defers it to before the host reads the model
   if (A.has_fit || !A.lazy_last) {
-    int tasks = 0;
-    for (int m = 0; m < A.order; ++m) {
-      const int dFm = min(A.mode[m].dctF, (r + 1) & ~1);
-      tasks += (r + dFm - 1) / dFm;
-    }
+    // groups of kUnmixF columns (one complex sequence): many small tasks over
+    // the grid instead of one task of every column per mode (measured: C5,
+    // R = 20, one 20-column task per mode took ~34 us of the iteration)
+    constexpr int kUnmixF = 2;
+    const int gm = (r + kUnmixF - 1) / kUnmixF;
+    const int tasks = A.order * gm;
     for (int t = b; t < tasks; t += G) {
-      int m = 0, g = t;
-      for (;; ++m) {
-        const int dFm = min(A.mode[m].dctF, (r + 1) & ~1);
-        const int gm = (r + dFm - 1) / dFm;
-        if (g < gm) break;
-        g -= gm;
-      }
+      const int m = t / gm, g = t - m * gm;
       const FusedMode& Q = A.mode[m];
-      const int dFm = min(Q.dctF, (r + 1) & ~1);
+      const int dFm = kUnmixF;
       __syncthreads();
       dct::transform_group(Q.plan, Q.mixed, Q.a, r, r, static_cast<i64>(g) * dFm, dFm, Q.sign, 0, nullptr,
                            reinterpret_cast<double2*>(fsm));
