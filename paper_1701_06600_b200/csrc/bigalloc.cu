@@ -99,4 +99,41 @@ void big_release_all() {
   g_cache.clear();
 }
 
+// Small pinned, device-mapped host blocks (a session's per-iteration stop
+// marks): cudaHostAlloc costs milliseconds, so released blocks are kept for
+// the next session (a time-to-fit measurement creates a session per run).
+namespace {
+struct HostBlock {
+  size_t bytes;
+  void* p;
+};
+std::vector<HostBlock> g_host;
+constexpr int kMaxHostCached = 8;
+}  // namespace
+
+void* pinned_mapped_alloc(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto it = g_host.begin(); it != g_host.end(); ++it)
+      if (it->bytes >= bytes && it->bytes <= 2 * bytes + 4096) {
+        void* p = it->p;
+        g_host.erase(it);
+        return p;
+      }
+  }
+  void* p = nullptr;
+  CPB_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  return p;
+}
+
+void pinned_mapped_free(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_host.push_back({bytes, p});
+  if (static_cast<int>(g_host.size()) > kMaxHostCached) {
+    cudaFreeHost(g_host.front().p);
+    g_host.erase(g_host.begin());
+  }
+}
+
 }  // namespace cpb

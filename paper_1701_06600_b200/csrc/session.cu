@@ -18,6 +18,7 @@
 
 
 #include <algorithm>
+#include <future>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -402,7 +403,7 @@ Session::~Session() {
   if (xcopy_) big_free(xcopy_, static_cast<size_t>(tp_) * sizeof(double));
   dfree(rhs_gather_);
   xcopy_ = nullptr;
-  if (stop_host_) cudaFreeHost(stop_host_);
+  if (stop_host_) pinned_mapped_free(stop_host_, (static_cast<size_t>(o_.max_iters) + 2) * sizeof(int));
   for (auto& e : it_events_) cudaEventDestroy(e);
   for (auto& e : ev_pool_) cudaEventDestroy(e);
   for (auto& p : pending_) {
@@ -435,6 +436,9 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
     }
   }
   t0_ = Clock::now();
+  // the fit estimator's offsets (sampling.hpp:155-179) on a host thread
+  if (!o_.bench_mode && !o_.exhaustive_samples && !o_.exact_fit_trace)
+    fit_offsets_ = std::async(std::launch::async, [this] { return draw_fit_offsets(); });
   const bool dbg_setup = std::getenv("CPRAND_DEBUG_SETUP") != nullptr;
   auto mark = [&](const char* what) {
     if (dbg_setup) {
@@ -480,6 +484,10 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
 
   // ---- estimator on the ORIGINAL tensor for rand / mix (mixing.hpp:268-273)
   xsolve_ = x_->d;
+  // without mixing the replicas read the tensor as it is: their kernels run
+  // while the host waits for the estimator's offsets
+  const bool early_replicas = !(mix_ || premix_ || cmix_);
+  if (early_replicas) build_replicas();
   if (!o_.bench_mode && !premix_) build_fit_estimator(x_->d);
   mark("estimator");
   if (mix_ || premix_) mix_setup();
@@ -495,7 +503,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
     build_fit_estimator(xsolve_);
   }
 
-  build_replicas();
+  if (!early_replicas) build_replicas();
   mark("replicas");
 
   // ---- per-mode work buffers
@@ -566,7 +574,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   // the same on every rank of a sharded run (the fit is replicated), so all
   // ranks enqueue the same collectives
   const size_t nmarks = static_cast<size_t>(o_.max_iters) + 2;
-  CPB_CUDA(cudaHostAlloc(&stop_host_, nmarks * sizeof(int), cudaHostAllocMapped));
+  stop_host_ = static_cast<int*>(pinned_mapped_alloc(nmarks * sizeof(int)));
   std::fill(stop_host_, stop_host_ + nmarks, 0);
   CPB_CUDA(cudaHostGetDevicePointer(&stop_dev_, stop_host_, 0));
   mark("buffers");
@@ -1366,6 +1374,11 @@ void Session::stop_table_thread() {
 
 
 
+std::vector<i64> Session::draw_fit_offsets() const {
+  auto rng = seeded_engine(o_.rng_seed, kFitStream);
+  return sample_offsets_without_replacement(p_, o_.fit_sample_count, rng);
+}
+
 void Session::build_fit_estimator(const double* xsrc) {
   // sampling.hpp:155-179 (exhaustive: sampling.hpp:182-186)
   if (o_.exact_fit_trace && p_ > (i64{1} << 26))
@@ -1375,8 +1388,9 @@ void Session::build_fit_estimator(const double* xsrc) {
     offs.resize(static_cast<size_t>(p_));
     std::iota(offs.begin(), offs.end(), i64{0});
   } else {
-    auto rng = seeded_engine(o_.rng_seed, kFitStream);
-    offs = sample_offsets_without_replacement(p_, o_.fit_sample_count, rng);
+    // drawn by a host thread started at setup entry (data independent, its
+    // own RNG stream: it overlaps the sample tables, replicas and buffers)
+    offs = fit_offsets_.valid() ? fit_offsets_.get() : draw_fit_offsets();
   }
   const bool dbg = std::getenv("CPRAND_DEBUG_SETUP") != nullptr;
   const auto te = Clock::now();
@@ -1560,7 +1574,8 @@ void Session::build_replicas() {
     launch_replica(xsolve_, tdims_[static_cast<size_t>(n)], tstrides_[static_cast<size_t>(n)], tp_,
                    rep_[static_cast<size_t>(n)], stream_);
   }
-  CPB_CUDA(cudaStreamSynchronize(stream_));
+  // (no synchronize: everything that reads a replica is ordered after these
+  // kernels on stream_, and setup ends with a synchronize)
 }
 
 const i64* Session::base_ptr(int it, int n) const {

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <atomic>
+#include <future>
 #include <chrono>
 #include <functional>
 #include <memory>
@@ -58,6 +59,9 @@ struct Trace {
 // Cache of tensor-sized device blocks (bigalloc.cu).
 void* big_alloc(size_t bytes);
 void big_free(void* p, size_t bytes);
+// small pinned device-mapped host blocks, kept for reuse after release
+void* pinned_mapped_alloc(size_t bytes);
+void pinned_mapped_free(void* p, size_t bytes);
 size_t big_cached_bytes();
 void big_release_all();
 
@@ -119,6 +123,8 @@ class Session {
   void wait_tables(int it, cudaStream_t st, int& synced);
   void stop_table_thread();
   void build_fit_estimator(const double* xsrc);
+  std::vector<i64> draw_fit_offsets() const;
+  std::future<std::vector<i64>> fit_offsets_;  // drawn by a host thread from setup entry
   void mix_setup();
   void cmix_setup();                          // FFT-kind MIX: complex X_hat, mixed factors
   void enqueue_mode_cmix(int it, int n, const int* stop);
