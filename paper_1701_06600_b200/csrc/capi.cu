@@ -1,10 +1,16 @@
 // extern "C" boundary (include/cprand_b200.h). Exceptions never cross it:
 // each entry point maps the internal error taxonomy onto status codes.
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/cprand_b200.h"
@@ -187,9 +193,76 @@ int cprand_solve(int32_t method, const double* x, const int64_t* dims, int32_t o
     Tensor t(d, dev);
     const size_t bytes = static_cast<size_t>(t.p) * sizeof(double);
     const bool on_device = opts && opts->x_is_device;
-    CPB_CUDA(cudaMemcpy(t.d, x, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    // A pinned host tensor is uploaded in parts along the last mode by an
+    // uploader thread (three parts in flight on its own stream) while the
+    // session sets up: the host-side setup (sample tables, work buffers, the
+    // kernel arguments) and each part's share of the mode-major replicas
+    // overlap the copy (Tensor::chunk_ev, Session::launch_replicas).
+    // Pageable memory is copied synchronously.
+    struct Upload {
+      cudaStream_t st = nullptr;
+      Tensor* t = nullptr;
+      std::thread th;
+      std::atomic<int> err{0};
+      ~Upload() {
+        if (th.joinable()) th.join();
+        if (st) cudaStreamSynchronize(st);
+        if (t) {
+          for (cudaEvent_t e : t->chunk_ev) cudaEventDestroy(e);
+          t->chunk_ev.clear();
+          t->chunk_end.clear();
+        }
+        if (st) cudaStreamDestroy(st);
+      }
+    } up;  // (declared after t: joined and drained before the tensor is freed)
+    bool pinned = false;
+    if (!on_device && bytes >= (size_t{64} << 20) && !std::getenv("CPRAND_SYNC_UPLOAD")) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, x) == cudaSuccess) pinned = at.type == cudaMemoryTypeHost;
+      (void)cudaGetLastError();
+    }
+    if (pinned) {
+      const i64 ilast = d.back(), slice = t.p / ilast;
+      // parts of >= 256 MB, at most 32 (CPRAND_UPLOAD_PARTS: tests)
+      const char* pe = std::getenv("CPRAND_UPLOAD_PARTS");
+      const i64 want = pe ? std::atoll(pe) : std::min<i64>(32, static_cast<i64>(bytes >> 28));
+      const i64 parts = std::min<i64>(ilast, std::max<i64>(1, want));
+      CPB_CUDA(cudaStreamCreateWithFlags(&up.st, cudaStreamNonBlocking));
+      up.t = &t;
+      for (i64 c = 0; c < parts; ++c) {
+        cudaEvent_t e = nullptr;
+        CPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        t.chunk_ev.push_back(e);
+        t.chunk_end.push_back(ilast * (c + 1) / parts);
+      }
+      t.chunk_submitted.store(0);
+      up.th = std::thread([&up, &t, x, slice, dev] {
+        cudaSetDevice(dev);
+        const auto t0 = std::chrono::steady_clock::now();
+        i64 a = 0;
+        for (size_t c = 0; c < t.chunk_ev.size(); ++c) {
+          const i64 b = t.chunk_end[c];
+          cudaError_t e = cudaMemcpyAsync(t.d + a * slice, x + a * slice, static_cast<size_t>((b - a) * slice) * sizeof(double),
+                                          cudaMemcpyHostToDevice, up.st);
+          if (e == cudaSuccess) e = cudaEventRecord(t.chunk_ev[c], up.st);
+          if (e != cudaSuccess) up.err.store(static_cast<int>(e));
+          t.chunk_submitted.store(static_cast<int>(c) + 1, std::memory_order_release);
+          if (c >= 2) cudaEventSynchronize(t.chunk_ev[c - 2]);  // three parts in flight
+          a = b;
+        }
+        if (std::getenv("CPRAND_DEBUG_SETUP")) {
+          cudaEventSynchronize(t.chunk_ev.back());
+          std::fprintf(stderr, "upload: %zu parts resident %.2f ms after the first was submitted\n", t.chunk_ev.size(),
+                       1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+        }
+      });
+    } else {
+      CPB_CUDA(cudaMemcpy(t.d, x, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    }
     o.x_mutable = true;  // t is our private copy
     Session sess(method, &t, static_cast<int>(r), static_cast<int>(s), o, init_lambda, init_factors);
+    if (up.th.joinable()) up.th.join();
+    if (up.err.load()) throw CudaError(std::string("tensor upload: ") + cudaGetErrorString(static_cast<cudaError_t>(up.err.load())));
     sess.run(o.max_iters);
     fill_result(sess, out_lambda, out_factors, trace, trace_cap, res);
   });

@@ -505,6 +505,26 @@ __device__ __forceinline__ void prefetch_tables(const FusedIter& A, unsigned b) 
 // (summed in rank order, so every rank applies the same rows); the last mode
 // applies the slab's rows and stores them, with their column sums of
 // squares, into every rank's factor.
+// The CPRAND kernel's rarely taken LS paths (QR, pseudo-inverse fallback)
+// stay out of line: inlined they sat between the phases every CTA runs each
+// mode and cost the hot path instruction fetches (C4 9.06 k -> 9.25 k it/s on
+// one box; the MIX kernel measured 1-2 % slower with them out of line, so it
+// keeps them inline).
+template <int RT>
+__device__ __noinline__ void qr_factor_cold(const double* z, int s, int r, double qtol, double* ws, double* ginv,
+                                            int* info, double* sh) {
+  ph::qr_factor<RT>(z, s, r, qtol, ws, ginv, info, sh);
+}
+template <int RT>
+__device__ __noinline__ void pinv_fallback_cold(double* gfull, int r, double tol, double* ginv, int* info, int* perm_sh) {
+  ph::pinv_fallback<RT>(gfull, r, tol, ginv, info, perm_sh);
+}
+template <int RT>
+__device__ __noinline__ void qr_rows_cold(const QrSrc& q, const double* ws, int r, i64 in, i64 i0, int nrow, double* out,
+                                          int ldo, double* stage) {
+  ph::qr_rows<RT, kFusedThreads>(q, ws, r, in, i0, nrow, out, ldo, stage);
+}
+
 template <int RT, bool GA, bool PEER>
 __device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, const unsigned G, const unsigned b) {
   using namespace tl;
@@ -663,9 +683,9 @@ __device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, co
             __syncthreads();
             zq = A.qrws;
           }
-          ph::qr_factor<RT>(zq, M.v.s, r, M.qtol, A.qrws, A.ginv, A.info, fsm);
+          qr_factor_cold<RT>(zq, M.v.s, r, M.qtol, A.qrws, A.ginv, A.info, fsm);
         } else {
-          ph::pinv_fallback<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
+          pinv_fallback_cold<RT>(A.gfull, r, M.tol, A.ginv, A.info, perm);
         }
       }
       signal_add_rep(M.grdy, 1u, kRep);
@@ -811,7 +831,7 @@ __device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, co
         if (qr) {  // QR mode: the rows from the sampled fibers (qr.cuh), times ginv = I
           constexpr int BQ = kFusedThreads / RT;
           for (int ch = 0; ch < nrow; ch += BQ)
-            ph::qr_rows<RT, kFusedThreads>(qs, A.qrws, r, in, r0 + ch, min(BQ, nrow - ch), rh + ch * LD, LD, qstage);
+            qr_rows_cold<RT>(qs, A.qrws, r, in, r0 + ch, min(BQ, nrow - ch), rh + ch * LD, LD, qstage);
         }
         for (int e = tid; e < nrow * r; e += kFusedThreads) {
           const int il = e / r, c = e - il * r;

@@ -85,6 +85,10 @@ void launch_rhs_gemm(const double* xs, i64 ld, const i64* row_off, bool vec16, c
 // Mode-major replica y = X_(n) (column-major I_n x P/I_n) of a tensor whose
 // mode n has length in and stride st.
 void launch_replica(const double* x, i64 in, i64 st, i64 p, double* y, cudaStream_t stream);
+// dst (16-byte aligned device memory) <- bytes of mapped pinned host memory, by a kernel (no copy engine)
+void launch_stage_copy(void* dst, const void* src_mapped_dev, size_t bytes, cudaStream_t stream);
+// rows [i0, i1) of the mode only (a part of the last mode's replica, whose single hi-slab is the whole tensor)
+void launch_replica_rows(const double* x, i64 in, i64 st, i64 p, double* y, i64 i0, i64 i1, cudaStream_t stream);
 // rhs_override != null: use it (I_n x R row-major, already reduced) instead of
 // summing part_rhs (the MIX path unmixes the RHS first). Writes A_un, norms,
 // lambda; zero columns refilled from the device normalize RNG.

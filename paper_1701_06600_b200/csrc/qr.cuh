@@ -164,19 +164,72 @@ __device__ void qr_factor(const double* z, int s, int r, double qtol, double* ws
       if (fabs(beta) > s_maxpivot) s_maxpivot = fabs(beta);
     }
     // apply H_k to columns j > k (a warp per column) and downdate their norms
-    for (int j = k + 1 + warp; j < r; j += NW) {
-      double* cj = P.M + static_cast<i64>(j) * s;
-      double ckj = cj[k];
-      if (tau != 0.0) {
-        double t = 0.0;
-        for (int i = k + 1 + lane; i < s; i += 32) t += ck[i] * cj[i];
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        t = (t + ckj) * tau;
-        ckj -= t;
-        for (int i = k + 1 + lane; i < s; i += 32) cj[i] -= t * ck[i];
+    // (M lives in global memory, S x r doubles: a warp's columns are taken CB
+    // at a time and U rows per lane per pass, so CB * U + U loads are in
+    // flight instead of two; every lane still adds its own rows in ascending
+    // order, so the sums are the ones the one-column loop formed)
+    constexpr int CB = 4, U = 4;
+    double ckjs[((RT + NW - 1) / NW + CB - 1) / CB * CB];
+    if (tau != 0.0) {
+      for (int jb = k + 1 + warp, q0 = 0; jb < r; jb += NW * CB, q0 += CB) {
+        double* cjp[CB];
+        double t[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+          const int j = jb + NW * c;
+          cjp[c] = P.M + static_cast<i64>(j < r ? j : jb) * s;
+          t[c] = 0.0;
+        }
+        for (int i0 = k + 1 + lane; i0 < s; i0 += 32 * U) {
+          double a[U], b[CB][U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = i0 + 32 * u;
+            a[u] = i < s ? ck[i] : 0.0;
+#pragma unroll
+            for (int c = 0; c < CB; ++c) b[c][u] = i < s ? cjp[c][i] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (i0 + 32 * u < s)
+#pragma unroll
+              for (int c = 0; c < CB; ++c) t[c] += a[u] * b[c][u];
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+          for (int o = 16; o > 0; o >>= 1) t[c] += __shfl_xor_sync(0xffffffffu, t[c], o);
+          const double ckj0 = cjp[c][k];
+          t[c] = (t[c] + ckj0) * tau;
+          ckjs[q0 + c] = ckj0 - t[c];
+        }
+        for (int i0 = k + 1 + lane; i0 < s; i0 += 32 * U) {
+          double a[U], b[CB][U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = i0 + 32 * u;
+            a[u] = i < s ? ck[i] : 0.0;
+#pragma unroll
+            for (int c = 0; c < CB; ++c) b[c][u] = i < s ? cjp[c][i] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = i0 + 32 * u;
+            if (i < s)
+#pragma unroll
+              for (int c = 0; c < CB; ++c)
+                if (jb + NW * c < r) cjp[c][i] = b[c][u] - t[c] * a[u];
+          }
+        }
         __syncwarp();
-        if (lane == 0) cj[k] = ckj;
+        if (lane == 0)
+#pragma unroll
+          for (int c = 0; c < CB; ++c)
+            if (jb + NW * c < r) cjp[c][k] = ckjs[q0 + c];
       }
+    }
+    for (int j = k + 1 + warp, q = 0; j < r; j += NW, ++q) {
+      double* cj = P.M + static_cast<i64>(j) * s;
+      const double ckj = tau != 0.0 ? ckjs[q] : cj[k];
       const double u = upd[j];
       if (u != 0.0) {
         double t = fabs(ckj) / u;

@@ -392,6 +392,10 @@ Session::~Session() {
   dfree(gfull_);
   dfree(qrws_);
   dfree(info_);
+  for (void* q : trash_) cudaFree(q);
+  trash_.clear();
+  for (auto& b : stage_blocks_) pinned_mapped_free(b.first, b.second);
+  stage_blocks_.clear();
   dfree(tickets_);
   dfree(ssq_);
   dfree(rhs_full_);
@@ -423,7 +427,11 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   const int nparts = 1024;
   fit_part_ = dalloc<double>(std::max<i64>(nparts + 1, std::max<i64>(8192, (o_.fit_sample_count + 255) / 256 + 1)));
   // ---- zero tensor short-circuit (sampling.hpp:263-264, solver.hpp:204-216)
+  // the fit estimator's offsets (sampling.hpp:155-179) on a host thread
+  if (!o_.bench_mode && !o_.exhaustive_samples && !o_.exact_fit_trace)
+    fit_offsets_ = std::async(std::launch::async, [this] { return draw_fit_offsets(); });
   if (!o_.bench_mode) {
+    wait_upload();
     launch_sumsq(x_->d, tp_, fit_part_, nparts, fit_part_ + nparts, stream_);
     if (shard_) allreduce_sum(fit_part_ + nparts, 1);
     double ss = 0.0;
@@ -436,13 +444,11 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
     }
   }
   t0_ = Clock::now();
-  // the fit estimator's offsets (sampling.hpp:155-179) on a host thread
-  if (!o_.bench_mode && !o_.exhaustive_samples && !o_.exact_fit_trace)
-    fit_offsets_ = std::async(std::launch::async, [this] { return draw_fit_offsets(); });
   const bool dbg_setup = std::getenv("CPRAND_DEBUG_SETUP") != nullptr;
+  const bool dbg_nosync = dbg_setup && std::atoi(std::getenv("CPRAND_DEBUG_SETUP")) == 2;  // host times only
   auto mark = [&](const char* what) {
     if (dbg_setup) {
-      CPB_CUDA(cudaStreamSynchronize(stream_));
+      if (!dbg_nosync) CPB_CUDA(cudaStreamSynchronize(stream_));
       std::fprintf(stderr, "setup %-12s %.2f ms\n", what, 1e3 * seconds_since(t0_));
     }
   };
@@ -460,17 +466,16 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
     const i64 alloc_rows = (shard_ && n == order_ - 1) ? std::max(rows, lmax_ * nranks_) : rows;
     fac_.push_back(dalloc<double>(static_cast<size_t>(alloc_rows * r_)));
     const auto rm = to_row_major(m.factors[static_cast<size_t>(n)].data(), rows, r_);
-    CPB_CUDA(cudaMemcpyAsync(fac_.back(), rm.data(), rm.size() * sizeof(double),
-                             cudaMemcpyHostToDevice, stream_));
+    h2d(fac_.back(), rm.data(), rm.size() * sizeof(double), stream_);
   }
   lambda_ = dalloc<double>(static_cast<size_t>(r_));
-  CPB_CUDA(cudaMemcpyAsync(lambda_, m.lambda.data(), sizeof(double) * r_, cudaMemcpyHostToDevice, stream_));
+  h2d(lambda_, m.lambda.data(), sizeof(double) * r_, stream_);
   norms_ = dalloc<double>(static_cast<size_t>(order_ * r_));
   {
     // factors are kept as A_un with per-column norms; the init model is used as is
     std::vector<double> ones(static_cast<size_t>(order_ * r_), 1.0);
-    CPB_CUDA(cudaMemcpyAsync(norms_, ones.data(), ones.size() * sizeof(double), cudaMemcpyHostToDevice, stream_));
-    CPB_CUDA(cudaStreamSynchronize(stream_));
+    h2d(norms_, ones.data(), ones.size() * sizeof(double), stream_);
+    if (!staging()) CPB_CUDA(cudaStreamSynchronize(stream_));
   }
   rng_state_ = dalloc<unsigned long long>(313);
   launch_rng_seed(rng_state_, seeded_engine_seed_value(o_.rng_seed, kInitStream + 7), stream_);
@@ -488,6 +493,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   // while the host waits for the estimator's offsets
   const bool early_replicas = !(mix_ || premix_ || cmix_);
   if (early_replicas) build_replicas();
+  if (!replicas_pending_) wait_upload();
   if (!o_.bench_mode && !premix_) build_fit_estimator(x_->d);
   mark("estimator");
   if (mix_ || premix_) mix_setup();
@@ -567,7 +573,7 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   state_ = dalloc<FitState>(1);
   FitState fs{};
   fs.best_fit = -INFINITY;
-  CPB_CUDA(cudaMemcpyAsync(state_, &fs, sizeof(fs), cudaMemcpyHostToDevice, stream_));
+  h2d(state_, &fs, sizeof(fs), stream_);
   trace_dev_ = dalloc<TraceRec>(static_cast<size_t>(o_.max_iters));
   // per-iteration stop marks (zero-copy): the host decides whether to
   // enqueue iteration k from the mark of iteration k - kInFlight, which is
@@ -579,6 +585,8 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   CPB_CUDA(cudaHostGetDevicePointer(&stop_dev_, stop_host_, 0));
   mark("buffers");
   setup_fused();
+  if (replicas_pending_) launch_replicas();
+  wait_upload();  // (a path that has not read the tensor yet)
   CPB_CUDA(cudaStreamSynchronize(stream_));
   mark("fused");
   setup_seconds_ = seconds_since(t0_);
@@ -646,21 +654,31 @@ void Session::setup_fused() {
   int inv_cta = fgrid_ - 1, idle_cta = -1;
   if (!mix_ && !emulated) {
     int* cen = dalloc<int>(static_cast<size_t>(fgrid_));
-    FusedIter* dc = dalloc<FusedIter>(1);
+    // the arguments live in mapped pinned memory (read over PCIe by the
+    // kernel): a host -> device copy would queue behind the upload parts
+    FusedIter* hc = static_cast<FusedIter*>(pinned_mapped_alloc(sizeof(FusedIter)));
+    stage_blocks_.emplace_back(hc, sizeof(FusedIter));
+    FusedIter* dc = nullptr;
+    CPB_CUDA(cudaHostGetDevicePointer(&dc, hc, 0));
     FusedIter c{};
     c.census = cen;
-    CPB_CUDA(cudaMemcpyAsync(dc, &c, sizeof(c), cudaMemcpyHostToDevice, stream_));
-    launch_fused_iteration(dc, rt_, false, fgrid_, fsmem_, stream_, o_.atomic_gram);
+    *hc = c;
+    // on its own stream: stream_ may be waiting for a tensor that is still
+    // arriving (wait_upload), and the census reads none of it; cudaFree would
+    // wait for the device too, so the two buffers are freed with the session
+    cudaStream_t cs = nullptr;
+    CPB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    launch_fused_iteration(dc, rt_, false, fgrid_, fsmem_, cs, o_.atomic_gram);
     std::vector<int> sm(static_cast<size_t>(fgrid_));
-    CPB_CUDA(cudaMemcpyAsync(sm.data(), cen, sm.size() * sizeof(int), cudaMemcpyDeviceToHost, stream_));
-    CPB_CUDA(cudaStreamSynchronize(stream_));
+    CPB_CUDA(cudaMemcpyAsync(sm.data(), cen, sm.size() * sizeof(int), cudaMemcpyDeviceToHost, cs));
+    CPB_CUDA(cudaStreamSynchronize(cs));
+    CPB_CUDA(cudaStreamDestroy(cs));
     for (int b = 0; b < fgrid_ - 1; ++b)
       if (sm[static_cast<size_t>(b)] == sm[static_cast<size_t>(inv_cta)]) {
         idle_cta = b;
         break;
       }
-    dfree(cen);
-    dfree(dc);
+    trash_.push_back(cen);
   }
   const int gw = fgrid_ - 1 - (idle_cta >= 0 ? 1 : 0);
   // CPRAND kernel tiling per mode
@@ -681,7 +699,7 @@ void Session::setup_fused() {
     for (int n = 0; n < order_; ++n)
       have = std::max(have, static_cast<i64>(ks_[static_cast<size_t>(n)]) * dims_[static_cast<size_t>(n)] * r_);
     if (max_part > have) {
-      dfree(part_rhs_);
+      trash_.push_back(part_rhs_);  // (cudaFree would wait for the device: freed with the session)
       part_rhs_ = dalloc<double>(static_cast<size_t>(max_part));
     }
     gpart_ = dalloc<double>(static_cast<size_t>(nblk) * tk_max * 64);
@@ -919,8 +937,8 @@ void Session::setup_fused() {
       f.stall_limit = o_.stall_limit;
     }
   }
-  CPB_CUDA(cudaMemcpyAsync(fargs_, host.data(), host.size() * sizeof(FusedIter), cudaMemcpyHostToDevice, stream_));
-  CPB_CUDA(cudaStreamSynchronize(stream_));
+  h2d(fargs_, host.data(), host.size() * sizeof(FusedIter), stream_);
+  if (!staging()) CPB_CUDA(cudaStreamSynchronize(stream_));
   fused_ = true;
 }
 
@@ -1178,12 +1196,28 @@ void Session::build_tables() {
   if (async) {  // kept for the drawing thread; pageable and uninitialized (every
                 // entry is written before its chunk is uploaded; pinning or
                 // zero-filling 30 MB up front costs more than the first chunk)
-    rows_hv_.reset(new int[nrows]);
-    base_hv_.reset(new i64[nbase]);
-    dbase_hv_.reset(new i64[nbase]);
-    rows = rows_hv_.get();
-    base = base_hv_.get();
-    dbase = dbase_hv_.get();
+    if (staging()) {
+      // a tensor upload is in flight: the drawing thread's chunks go to the
+      // device by the staging copy kernel from mapped pinned memory (a
+      // pageable cudaMemcpyAsync would wait for the copy engine, which the
+      // upload keeps busy until it ends)
+      auto grab = [this](size_t bytes) {
+        void* q = pinned_mapped_alloc(bytes);
+        stage_blocks_.emplace_back(q, bytes);
+        stage_used_ = bytes;  // (a dedicated block: h2d opens a new one)
+        return q;
+      };
+      rows = static_cast<int*>(grab(std::max<size_t>(nrows, 1) * sizeof(int)));
+      base = static_cast<i64*>(grab(std::max<size_t>(nbase, 1) * sizeof(i64)));
+      dbase = static_cast<i64*>(grab(std::max<size_t>(nbase, 1) * sizeof(i64)));
+    } else {
+      rows_hv_.reset(new int[nrows]);
+      base_hv_.reset(new i64[nbase]);
+      dbase_hv_.reset(new i64[nbase]);
+      rows = rows_hv_.get();
+      base = base_hv_.get();
+      dbase = dbase_hv_.get();
+    }
   } else {
     rows_v.assign(nrows, 0);
     base_v.assign(nbase, 0);
@@ -1322,9 +1356,20 @@ void Session::build_tables() {
   base_ = dalloc<i64>(nbase);
   dbase_ = dalloc<i64>(nbase);
   // iterations [a, b) of the tables: contiguous ranges of the three arrays
-  auto upload = [this, N, rows, base, dbase](int a, int b, cudaStream_t st) {
+  const bool mapped_tables = async && staging();
+  auto upload = [this, N, rows, base, dbase, mapped_tables](int a, int b, cudaStream_t st) {
     const i64 r0 = row_off_[static_cast<size_t>(a * N)], r1 = row_off_[static_cast<size_t>(b * N)];
     const i64 b0 = base_off_[static_cast<size_t>(a * N)], b1 = base_off_[static_cast<size_t>(b * N)];
+    if (mapped_tables) {
+      void *dr = nullptr, *db = nullptr, *dd = nullptr;
+      CPB_CUDA(cudaHostGetDevicePointer(&dr, rows, 0));
+      CPB_CUDA(cudaHostGetDevicePointer(&db, base, 0));
+      CPB_CUDA(cudaHostGetDevicePointer(&dd, dbase, 0));
+      launch_stage_copy(rows_ + r0, static_cast<int*>(dr) + r0, sizeof(int) * (r1 - r0), st);
+      launch_stage_copy(base_ + b0, static_cast<i64*>(db) + b0, sizeof(i64) * (b1 - b0), st);
+      launch_stage_copy(dbase_ + b0, static_cast<i64*>(dd) + b0, sizeof(i64) * (b1 - b0), st);
+      return;
+    }
     if (r1 > r0)
       CPB_CUDA(cudaMemcpyAsync(rows_ + r0, rows + r0, sizeof(int) * (r1 - r0), cudaMemcpyHostToDevice, st));
     if (b1 > b0) {
@@ -1332,8 +1377,17 @@ void Session::build_tables() {
       CPB_CUDA(cudaMemcpyAsync(dbase_ + b0, dbase + b0, sizeof(i64) * (b1 - b0), cudaMemcpyHostToDevice, st));
     }
   };
-  upload(0, first, stream_);
-  CPB_CUDA(cudaStreamSynchronize(stream_));  // the synchronous part's host vectors may die here
+  if (mapped_tables) {
+    upload(0, first, stream_);  // (from mapped pinned memory that lives as long as the session)
+  } else if (staging()) {  // (returns at once; the staging copy outlives the host vectors)
+    const i64 r1 = row_off_[static_cast<size_t>(first * N)], b1 = base_off_[static_cast<size_t>(first * N)];
+    h2d(rows_, rows, sizeof(int) * r1, stream_);
+    h2d(base_, base, sizeof(i64) * b1, stream_);
+    h2d(dbase_, dbase, sizeof(i64) * b1, stream_);
+  } else {
+    upload(0, first, stream_);
+    CPB_CUDA(cudaStreamSynchronize(stream_));  // the synchronous part's host vectors may die here
+  }
   tables_ready_.store(first);
   synced_main_ = synced_g_ = first;
   if (!async) return;
@@ -1566,11 +1620,112 @@ void Session::plan_replicas() {
         throw Unsupported("slab sharding needs the mode-major replicas of every strided mode to fit in HBM");
 }
 
+void Session::h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  if (!staging()) {
+    CPB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    return;
+  }
+  const size_t need = (bytes + 255) / 256 * 256;
+  if (stage_blocks_.empty() || stage_used_ + need > stage_blocks_.back().second) {
+    const size_t cap = std::max<size_t>(need, size_t{8} << 20);
+    stage_blocks_.emplace_back(pinned_mapped_alloc(cap), cap);
+    stage_used_ = 0;
+  }
+  char* p = static_cast<char*>(stage_blocks_.back().first) + stage_used_;
+  stage_used_ += need;
+  std::memcpy(p, src, bytes);
+  void* pd = nullptr;
+  CPB_CUDA(cudaHostGetDevicePointer(&pd, p, 0));
+  launch_stage_copy(dst, pd, bytes, st);
+}
+
+void Session::wait_part(size_t c) {
+  while (x_->chunk_submitted.load(std::memory_order_acquire) <= static_cast<int>(c)) std::this_thread::yield();
+  CPB_CUDA(cudaStreamWaitEvent(stream_, x_->chunk_ev[c], 0));
+}
+
+void Session::wait_upload() {
+  if (upload_waited_) return;
+  upload_waited_ = true;
+  for (size_t c = 0; c < x_->chunk_ev.size(); ++c) wait_part(c);
+}
+
+// Allocates the mode-major replicas; their kernels run here, or (a tensor
+// still arriving, nothing else of the setup reads the replicas' contents) at
+// the end of setup, part by part behind the upload (launch_replicas).
 void Session::build_replicas() {
   if (cmix_) return;
+  for (int n = 1; n < order_; ++n)
+    if (direct_[static_cast<size_t>(n)])
+      rep_[static_cast<size_t>(n)] = static_cast<double*>(big_alloc(static_cast<size_t>(tp_) * sizeof(double)));
+  if (!upload_waited_ && !x_->chunk_ev.empty() && xsolve_ == x_->d && !shard_ && order_ >= 2 && o_.bench_mode) {
+    replicas_pending_ = true;
+    return;
+  }
+  launch_replicas();
+}
+
+void Session::launch_replicas() {
+  if (replicas_pending_) {
+    // each part's share of every replica as soon as the part is resident. A
+    // part is a range of last-mode indices, i.e. a range of hi-slabs of the
+    // modes before the last and a range of rows of the last mode's replica.
+    // They run on their own stream, ordered only behind the parts: stream_
+    // holds setup memsets that the busy copy engine serves last.
+    replicas_pending_ = false;
+    upload_waited_ = true;
+    cudaStream_t rs = nullptr;
+    CPB_CUDA(cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking));
+    const i64 ilast = tdims_.back();
+    i64 a = 0;
+    const bool dbg = std::getenv("CPRAND_DEBUG_SETUP") != nullptr;
+    std::vector<cudaEvent_t> de;
+    for (size_t c = 0; c < x_->chunk_ev.size(); ++c) {
+      const i64 b = x_->chunk_end[c];
+      while (x_->chunk_submitted.load(std::memory_order_acquire) <= static_cast<int>(c)) std::this_thread::yield();
+      CPB_CUDA(cudaStreamWaitEvent(rs, x_->chunk_ev[c], 0));
+      if (dbg) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, rs);
+        de.push_back(e);
+      }
+      for (int n = 1; n < order_; ++n) {
+        if (!direct_[static_cast<size_t>(n)]) continue;
+        const i64 in = tdims_[static_cast<size_t>(n)], st = tstrides_[static_cast<size_t>(n)];
+        double* y = rep_[static_cast<size_t>(n)];
+        if (n == order_ - 1) {
+          launch_replica_rows(xsolve_, in, st, tp_, y, a, b, rs);
+        } else {
+          const i64 off = a * (tp_ / ilast);  // whole last-mode slices are whole hi-slabs
+          launch_replica(xsolve_ + off, in, st, (b - a) * (tp_ / ilast), y + off, rs);
+        }
+      }
+      a = b;
+    }
+    cudaEvent_t done = nullptr;
+    CPB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    CPB_CUDA(cudaEventRecord(done, rs));
+    CPB_CUDA(cudaStreamWaitEvent(stream_, done, 0));
+    if (dbg) {
+      cudaEventSynchronize(done);
+      std::fprintf(stderr, "replica parts start (ms after the first):");
+      for (size_t c = 1; c < de.size(); ++c) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, de[0], de[c]);
+        std::fprintf(stderr, " %.1f", ms);
+      }
+      std::fprintf(stderr, "; all done %.2f ms after setup start\n", 1e3 * seconds_since(t0_));
+      for (auto q : de) cudaEventDestroy(q);
+    }
+    CPB_CUDA(cudaEventDestroy(done));  // (released once it has completed)
+    CPB_CUDA(cudaStreamDestroy(rs));
+    return;
+  }
+  wait_upload();
   for (int n = 1; n < order_; ++n) {
     if (!direct_[static_cast<size_t>(n)]) continue;
-    rep_[static_cast<size_t>(n)] = static_cast<double*>(big_alloc(static_cast<size_t>(tp_) * sizeof(double)));
     launch_replica(xsolve_, tdims_[static_cast<size_t>(n)], tstrides_[static_cast<size_t>(n)], tp_,
                    rep_[static_cast<size_t>(n)], stream_);
   }
@@ -1931,6 +2086,9 @@ int Session::run(int n) {
   const int todo = std::min(n, o_.max_iters - it_);
   if (todo <= 0) return 0;
   horizon_ = it_ + todo;
+  if (std::getenv("CPRAND_DEBUG_SETUP"))
+    std::fprintf(stderr, "run: %d iterations' tables ready at loop entry, %.2f ms after setup start\n",
+                 tables_ready_.load(), 1e3 * seconds_since(t0_));
   if (it_events_.empty()) {
     it_events_.resize(kInFlight);
     for (auto& e : it_events_) CPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1951,6 +2109,8 @@ int Session::run(int n) {
     CPB_CUDA(cudaEventRecord(it_events_[static_cast<size_t>(k % kInFlight)], stream_));
   }
   sync();
+  if (std::getenv("CPRAND_DEBUG_SETUP"))
+    std::fprintf(stderr, "run: loop done %.2f ms after setup start\n", 1e3 * seconds_since(t0_));
   int ran = it_ - start;
   if (has_fit_) {
     FitState fs;

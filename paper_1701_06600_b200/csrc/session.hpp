@@ -76,6 +76,17 @@ struct Tensor {
   int device = 0;
   double* d = nullptr;
   bool owned = true;
+  // a host tensor still arriving (cprand_solve uploads it in parts along the
+  // last mode while the session sets up): part c covers last-mode indices
+  // [chunk_end[c-1], chunk_end[c]); chunk_ev[c] is recorded behind its copy.
+  // Owned by whoever filled them; empty when the tensor is resident.
+  std::vector<cudaEvent_t> chunk_ev;
+  std::vector<i64> chunk_end;
+  // events [0, chunk_submitted) have been recorded (the uploader thread keeps
+  // three parts in flight, so small setup copies are not queued behind the
+  // whole tensor on the copy engine); waiting on an unrecorded event would
+  // be a no-op, so consumers wait for the count first
+  std::atomic<int> chunk_submitted{0};
   explicit Tensor(const std::vector<i64>& dims, int device);
   ~Tensor();
 };
@@ -203,6 +214,20 @@ class Session {
   std::vector<char> vec16_;         // per mode: in-place rows are 16 B aligned
   void plan_replicas();
   void build_replicas();
+  void wait_upload();  // stream_ waits for a tensor still arriving (Tensor::chunk_ev)
+  void wait_part(size_t c);
+  void launch_replicas();
+  bool upload_waited_ = false;
+  bool replicas_pending_ = false;
+  // setup-time host -> device copies. While a tensor upload is in flight the
+  // source is first copied into pinned staging memory (kept until the session
+  // ends), so the call returns at once instead of blocking behind the upload
+  // parts queued on the copy engine; otherwise a plain cudaMemcpyAsync.
+  void h2d(void* dst, const void* src, size_t bytes, cudaStream_t st);
+  bool staging() const { return !x_->chunk_ev.empty(); }
+  std::vector<std::pair<void*, size_t>> stage_blocks_;
+  size_t stage_used_ = 0;
+  std::vector<void*> trash_;  // setup-time device buffers freed with the session (cudaFree waits for the device)
   void setup_fused();
   bool fused_ = false;
   int fgrid_ = 0;

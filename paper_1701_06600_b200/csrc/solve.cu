@@ -142,10 +142,10 @@ __global__ void __launch_bounds__(kApplyThreads) mode_apply_kernel(i64 in, int r
 // Tiles of TI = 64 tensor rows (mode-n index i) x 32 fastest-index columns:
 // 8 loads of 256-byte row runs per thread in flight, 512-byte runs written.
 __global__ void __launch_bounds__(256) replica_kernel(const double* __restrict__ x, i64 in, i64 st,
-                                                      i64 nhi, double* __restrict__ y) {
+                                                      i64 nhi, double* __restrict__ y, i64 i0, i64 i1) {
   constexpr int TI = 64;
   __shared__ double tile[TI][33];
-  const i64 tiles_lo = (st + 31) / 32, tiles_i = (in + TI - 1) / TI;
+  const i64 tiles_lo = (st + 31) / 32, tiles_i = (i1 - i0 + TI - 1) / TI;
   const i64 per_hi = tiles_lo * tiles_i;
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
   for (i64 blk = blockIdx.x; blk < nhi * per_hi; blk += gridDim.x) {
@@ -156,8 +156,8 @@ __global__ void __launch_bounds__(256) replica_kernel(const double* __restrict__
     double v[TI / 8];
 #pragma unroll
     for (int q = 0; q < TI / 8; ++q) {
-      const i64 i = ti * TI + ty + 8 * q, lo = tl * 32 + tx;
-      v[q] = (i < in && lo < st) ? __ldcs(src + i * st + lo) : 0.0;
+      const i64 i = i0 + ti * TI + ty + 8 * q, lo = tl * 32 + tx;
+      v[q] = (i < i1 && lo < st) ? __ldcs(src + i * st + lo) : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < TI / 8; ++q) tile[ty + 8 * q][tx] = v[q];
@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(256) replica_kernel(const double* __restrict__
       const i64 lo = tl * 32 + ty + 8 * q;
 #pragma unroll
       for (int h = 0; h < TI / 32; ++h) {
-        const i64 i = ti * TI + 32 * h + tx;
-        if (i < in && lo < st) __stcs(dst + lo * in + i, tile[32 * h + tx][ty + 8 * q]);
+        const i64 i = i0 + ti * TI + 32 * h + tx;
+        if (i < i1 && lo < st) __stcs(dst + lo * in + i, tile[32 * h + tx][ty + 8 * q]);
       }
     }
     __syncthreads();
@@ -178,10 +178,45 @@ __global__ void __launch_bounds__(256) replica_kernel(const double* __restrict__
 
 }  // namespace
 
+// Small host -> device copy by a kernel reading mapped pinned memory over
+// PCIe (Session::h2d): while a tensor upload keeps the copy engine busy, a
+// cudaMemcpyAsync on another stream is not served until the upload stream
+// drains (measured), and everything ordered behind it would wait with it.
+template <class W>
+__global__ void __launch_bounds__(256) stage_copy_kernel(const W* __restrict__ src, W* __restrict__ dst, size_t n) {
+  for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x)
+    dst[e] = src[e];
+}
+
+void launch_stage_copy(void* dst, const void* src_mapped_dev, size_t bytes, cudaStream_t stream) {
+  if (bytes == 0) return;
+  const size_t al = reinterpret_cast<size_t>(dst) | reinterpret_cast<size_t>(src_mapped_dev) | bytes;
+  const size_t w = (al % 16 == 0) ? 16 : (al % 4 == 0) ? 4 : 1;
+  const size_t n = bytes / w;
+  const int grid = static_cast<int>(std::min<size_t>(32, std::max<size_t>(1, (n + 255) / 256)));
+  if (w == 16)
+    stage_copy_kernel<uint4><<<grid, 256, 0, stream>>>(static_cast<const uint4*>(src_mapped_dev), static_cast<uint4*>(dst), n);
+  else if (w == 4)
+    stage_copy_kernel<unsigned><<<grid, 256, 0, stream>>>(static_cast<const unsigned*>(src_mapped_dev),
+                                                          static_cast<unsigned*>(dst), n);
+  else
+    stage_copy_kernel<unsigned char><<<grid, 256, 0, stream>>>(static_cast<const unsigned char*>(src_mapped_dev),
+                                                               static_cast<unsigned char*>(dst), n);
+  CPB_LAUNCH_CHECK();
+}
+
 void launch_replica(const double* x, i64 in, i64 st, i64 p, double* y, cudaStream_t stream) {
   if (p == 0) return;  // an empty slab
   const i64 nhi = p / (st * in);
-  replica_kernel<<<148 * 8, 256, 0, stream>>>(x, in, st, nhi, y);
+  replica_kernel<<<148 * 8, 256, 0, stream>>>(x, in, st, nhi, y, 0, in);
+  CPB_LAUNCH_CHECK();
+}
+
+void launch_replica_rows(const double* x, i64 in, i64 st, i64 p, double* y, i64 i0, i64 i1, cudaStream_t stream) {
+  if (p == 0 || i0 >= i1) return;
+  const i64 nhi = p / (st * in);
+  replica_kernel<<<148 * 8, 256, 0, stream>>>(x, in, st, nhi, y, i0, i1);
   CPB_LAUNCH_CHECK();
 }
 

@@ -327,14 +327,19 @@ __device__ void gram_blocks(const TileSmem& t, int kpad, int nfr, int first, int
   for (int q = first + warp * step; q < nblk; q += 8 * step) {
     int bi, bj;
     gram_block_coords(q, nfr, &bi, &bj);
-    double acc[2] = {0.0, 0.0};
+    // four independent accumulator chains (kpad is a multiple of BK = 16): a
+    // dependent FP64 MMA issues only every ~100 cycles, and one warp owns
+    // the whole k range of its block
+    double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
     const double* za = t.zs + (lane & 3) * SB + bi * 8 + (lane >> 2);
     const double* zb = t.zs + (lane & 3) * SB + bj * 8 + (lane >> 2);
-#pragma unroll 4
-    for (int k = 0; k < kpad; k += 4) dmma(acc, za[k * SB], zb[k * SB]);
+    for (int k = 0; k < kpad; k += 16) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma(acc[u], za[(k + 4 * u) * SB], zb[(k + 4 * u) * SB]);
+    }
     double* o = gpart + (static_cast<i64>(q) * ks + kb) * 64 + (lane >> 2) * 8 + (lane & 3) * 2;
-    o[0] = acc[0];
-    o[1] = acc[1];
+    o[0] = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+    o[1] = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
   }
 }
 
