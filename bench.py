@@ -340,6 +340,77 @@ def c5_record(pb, dev, hbm_peak, steps, warmup, cpu: bool):
     return out
 
 
+def small_records(pb, dev, hbm_peak, steps, warmup, cpu: bool):
+    """C1-C3 beside the C4 headline, so every BASELINE.json configuration has a
+    driver-run number: bench-mode rate of the persistent kernel, the full loop
+    (estimator + stop rule every iteration) with its final fit estimate, the
+    one-shot call from a host tensor (e2e), C3's mixing pass, and the CPU
+    reference path on the same tensor (bounded sample)."""
+    out = {}
+    for name in ("c1", "c2", "c3"):
+        cfg = CONFIGS[name]
+        p = int(np.prod(cfg["dims"]))
+        t = pb.DeviceTensor(cfg["dims"], device=dev)
+        t.synth(cfg["r"], cfg["c"], cfg["eta"], SEED)
+        buf = pb.PinnedBuffer(p)
+        t.download_into(buf.array)
+        xh = buf.array.reshape(cfg["dims"], order="F")
+        rec = {"config": config_of(name, cfg, 1)}
+        kw = dict(rng_seed=SEED, transform=cfg["transform"], device=dev)
+        s = pb.Session(cfg["method"], t, cfg["r"], cfg["s"],
+                       pb.SolveOptions(max_iters=warmup + steps + 2, bench_mode=True, **kw))
+        s.run(warmup)
+        ms = s.timed_enqueue(steps)
+        rec.update({"value": steps / (ms * 1e-3), "unit": "iters/s", "ms_per_step": ms / steps, "steps": steps,
+                    "kernel": "persistent kernel" if s.fused else "multi-kernel chain"})
+        s.close()
+        s = pb.Session(cfg["method"], t, cfg["r"], cfg["s"],
+                       pb.SolveOptions(max_iters=steps + 3, fit_sample_count=cfg["phat"], stall_limit=1 << 30, **kw))
+        s.run(3)
+        s.sync()
+        t0 = time.perf_counter()
+        n = s.run(steps)
+        dt = time.perf_counter() - t0
+        rec["full_loop"] = {"value": n / dt, "unit": "iters/s", "iterations": n,
+                            "final_fit_estimate": s.result().trace[-1][2]}
+        s.close()
+        eo = pb.SolveOptions(max_iters=100, bench_mode=True, **kw)
+        pb.solve(cfg["method"], xh, cfg["r"], cfg["s"], eo)  # warm
+        t0 = time.perf_counter()
+        for _ in range(3):
+            res = pb.solve(cfg["method"], xh, cfg["r"], cfg["s"], eo)
+            _ = float(res.lam[0])
+        dt = (time.perf_counter() - t0) / 3
+        rec["e2e"] = {"value": 100 / dt, "unit": "iters/s", "iters_per_step": 100, "seconds_per_step": dt,
+                      "h2d_bytes_per_step": p * 8, "note": "cprand_solve(host tensor), 100 bench-mode iterations"}
+        if cfg["method"] == "mix":
+            ms_modes = t.mix("dct", SEED)
+            gbs = [16.0 * p / (m * 1e-3) / 1e9 for m in ms_modes]
+            rec["mix_pass"] = {"ms_per_mode": [round(m, 4) for m in ms_modes], "gbs_per_mode": [round(g, 1) for g in gbs],
+                               "frac_per_mode": [round(g / hbm_peak, 3) for g in gbs],
+                               "bytes_model": "16 B per element per mode (read + write)"}
+        if cpu and cfg["method"] == "mix":
+            # bench-iter semantics (setup excluded, tools/cprand_main.cpp:195-198): the reference's loop
+            # body on the device-mixed tensor, so the single-threaded host mixing pass is not run
+            t.download_into(buf.array)
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle as orc
+            os.environ.setdefault("CPRAND_THREADS", str(os.cpu_count() or 1))
+            per = orc.bench_mix_premixed(buf.array, cfg["dims"], cfg["r"], cfg["s"], "dct", SEED, 1)
+            n_it = int(max(1, min(200, 3.0 / max(per, 1e-6))))
+            secs = orc.bench_mix_premixed(buf.array, cfg["dims"], cfg["r"], cfg["s"], "dct", SEED, n_it)
+            rec["cpu_baseline"] = {"value": n_it / secs, "unit": "iters/s", "cores": os.cpu_count() or 1, "kind": "port",
+                                   "sample": f"{n_it} bench-mode CPRAND-MIX iterations on the device-mixed tensor ({secs:.1f} s)"}
+        elif cpu:
+            rate, n_it, secs = cpu_oracle_rate(xh, cfg, budget_s=3.0, max_iters=200)
+            rec["cpu_baseline"] = {"value": rate, "unit": "iters/s", "cores": os.cpu_count() or 1, "kind": "port",
+                                   "sample": f"{n_it} bench-mode outer iterations ({secs:.1f} s)"}
+        buf.close()
+        t.close()
+        out[name] = rec
+    return out
+
+
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -610,6 +681,10 @@ def main() -> int:
         c5 = c5_record(pb, dev, hbm_peak, args.steps, args.warmup, not args.no_cpu)
         pb.lib().cprand_device_cache_release()
 
+    small = None
+    if args.config == "c4" and ws == 1 and not args.no_c5:
+        small = small_records(pb, dev, hbm_peak, args.steps, args.warmup, not args.no_cpu)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
@@ -641,7 +716,7 @@ def main() -> int:
                              [round(x, 2) for x in phases])) if phases else None,
                          "gram_fallbacks": fallbacks, "mix_pass": mix_pass},
             "atomic_gram": atomic, "full_loop": full, "time_to_fit": ttf, "sampled_gather": gather,
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "c5": c5,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "c5": c5, "c1_c3": small,
             "gpu_launches": launches_per_iter(cfg, used_fused) * args.steps,
         }
         print(json.dumps(line), flush=True)

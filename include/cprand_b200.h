@@ -133,7 +133,12 @@ const char* cprand_build_info(void);
 
 /* One-shot drop-in solve. x: host (or device with x_is_device) tensor in
  * storage order; dims[order]. Outputs: out_lambda[r], out_factors[n] ->
- * dims[n] x r column-major (caller-allocated). trace may be NULL. */
+ * dims[n] x r column-major (caller-allocated). trace may be NULL.
+ * A page-locked host tensor (cprand_host_alloc_pinned, cudaHostAlloc or
+ * cudaHostRegister) of >= 64 MB is uploaded in parts while the session sets
+ * up (bench mode also builds the mode-major replicas part by part); pageable
+ * memory is copied synchronously. x must stay unchanged until the call
+ * returns either way. Results do not depend on the upload path. */
 int cprand_solve(int32_t method, const double* x, const int64_t* dims, int32_t order, int64_t r,
                  int64_t s, const cprand_options_t* opts, const double* init_lambda,
                  const double* const* init_factors, double* out_lambda, double* const* out_factors,
