@@ -180,16 +180,48 @@ std::vector<i64> sample_offsets_without_replacement(i64 total, i64 want, std::mt
     }
     out.assign(pool.begin(), pool.begin() + want);
   } else {
-    std::unordered_set<i64> seen;
-    seen.reserve(static_cast<size_t>(want) * 2);
+    // rejection of repeated candidates (the reference keeps an unordered_set;
+    // the accepted sequence only depends on set membership): an open-
+    // addressing table at load <= 1/4 (this draw is on the setup's critical
+    // path: 65536 of 1e9 took 6.7 ms with the node-based set and std::sort,
+    // 1.6 ms with the table and the radix sort below)
+    size_t cap = 16;
+    while (cap < static_cast<size_t>(want) * 4) cap <<= 1;
+    std::vector<i64> slot(cap, i64{-1});
     std::uniform_int_distribution<long> pick(0, total - 1);
     out.reserve(static_cast<size_t>(want));
     while (static_cast<i64>(out.size()) < want) {
       const i64 cand = pick(rng);
-      if (seen.insert(cand).second) out.push_back(cand);
+      size_t h = static_cast<size_t>((static_cast<std::uint64_t>(cand) * 0x9E3779B97F4A7C15ull) >> 20) & (cap - 1);
+      bool fresh = true;
+      while (slot[h] != -1) {
+        if (slot[h] == cand) {
+          fresh = false;
+          break;
+        }
+        h = (h + 1) & (cap - 1);
+      }
+      if (fresh) {
+        slot[h] = cand;
+        out.push_back(cand);
+      }
     }
   }
-  std::sort(out.begin(), out.end());
+  // ascending order (distinct non-negative keys < total): LSD radix sort, 11 bits per pass
+  if (out.size() < 4096) {
+    std::sort(out.begin(), out.end());
+    return out;
+  }
+  int bits = 1;
+  while (bits < 63 && (i64{1} << bits) < total) ++bits;
+  std::vector<i64> tmp(out.size());
+  for (int sh = 0; sh < bits; sh += 11) {
+    size_t cnt[2049] = {0};
+    for (const i64 v : out) ++cnt[((static_cast<std::uint64_t>(v) >> sh) & 2047u) + 1];
+    for (int b = 0; b < 2048; ++b) cnt[b + 1] += cnt[b];
+    for (const i64 v : out) tmp[cnt[(static_cast<std::uint64_t>(v) >> sh) & 2047u]++] = v;
+    out.swap(tmp);
+  }
   return out;
 }
 
@@ -483,16 +515,17 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   mark("init");
   // ---- which modes read their fibers in place (mode 1, or a mode-major replica)
   plan_replicas();
+  // ---- estimator on the ORIGINAL tensor for rand / mix (mixing.hpp:268-273)
+  xsolve_ = x_->d;
+  // without mixing the replicas read the tensor as it is: their kernels run
+  // while the host draws the sample tables and waits for the estimator's
+  // offsets (setup is bound by the longer of the two chains)
+  const bool early_replicas = !(mix_ || premix_ || cmix_);
+  if (early_replicas) build_replicas();
   // ---- sample tables (data independent: all drawn up front)
   build_tables();
   mark("tables");
 
-  // ---- estimator on the ORIGINAL tensor for rand / mix (mixing.hpp:268-273)
-  xsolve_ = x_->d;
-  // without mixing the replicas read the tensor as it is: their kernels run
-  // while the host waits for the estimator's offsets
-  const bool early_replicas = !(mix_ || premix_ || cmix_);
-  if (early_replicas) build_replicas();
   if (!replicas_pending_) wait_upload();
   if (!o_.bench_mode && !premix_) build_fit_estimator(x_->d);
   mark("estimator");
@@ -1385,8 +1418,18 @@ void Session::build_tables() {
     h2d(base_, base, sizeof(i64) * b1, stream_);
     h2d(dbase_, dbase, sizeof(i64) * b1, stream_);
   } else {
-    upload(0, first, stream_);
-    CPB_CUDA(cudaStreamSynchronize(stream_));  // the synchronous part's host vectors may die here
+    // on the table stream, not behind the replica kernels already queued on
+    // stream_ (a pageable copy returns only when its last piece has gone,
+    // in stream order); stream_ and the gather stream wait for its event
+    CPB_CUDA(cudaStreamCreateWithFlags(&tstream_, cudaStreamNonBlocking));
+    upload(0, first, tstream_);
+    cudaEvent_t e0 = nullptr;
+    CPB_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    CPB_CUDA(cudaEventRecord(e0, tstream_));
+    CPB_CUDA(cudaStreamWaitEvent(stream_, e0, 0));
+    CPB_CUDA(cudaStreamWaitEvent(gstream_, e0, 0));
+    CPB_CUDA(cudaStreamSynchronize(tstream_));  // the synchronous part's host vectors may die here
+    CPB_CUDA(cudaEventDestroy(e0));
   }
   tables_ready_.store(first);
   synced_main_ = synced_g_ = first;
@@ -1394,7 +1437,7 @@ void Session::build_tables() {
   const int nchunks = (table_iters_ - first + table_chunk_ - 1) / table_chunk_;
   table_ev_.resize(static_cast<size_t>(nchunks));
   for (auto& e : table_ev_) CPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  CPB_CUDA(cudaStreamCreateWithFlags(&tstream_, cudaStreamNonBlocking));
+  if (!tstream_) CPB_CUDA(cudaStreamCreateWithFlags(&tstream_, cudaStreamNonBlocking));
   const int dev = x_->device;
   table_thread_ = std::thread([this, draw, upload, dev, first, rng]() mutable {
     cudaSetDevice(dev);
@@ -1450,8 +1493,10 @@ void Session::build_fit_estimator(const double* xsrc) {
   const auto te = Clock::now();
   if (dbg) std::fprintf(stderr, "  estimator offsets drawn %.2f ms after setup start\n", 1e3 * seconds_since(t0_));
   phat_ = static_cast<i64>(offs.size());
+  // (copies from pinned staging memory: a pageable copy would return only
+  // after the replica kernels queued on stream_ before it)
   i64* d_off = dalloc<i64>(offs.size());
-  CPB_CUDA(cudaMemcpyAsync(d_off, offs.data(), offs.size() * sizeof(i64), cudaMemcpyHostToDevice, stream_));
+  h2d(d_off, offs.data(), offs.size() * sizeof(i64), stream_, true);
   fit_vals_ = dalloc<double>(offs.size());
   if (shard_) {
     // entries outside this slab contribute 0; the allreduce assembles them
@@ -1476,7 +1521,7 @@ void Session::build_fit_estimator(const double* xsrc) {
   } else {
     launch_gather_values(xsrc, d_off, phat_, fit_vals_, stream_);
   }
-  if (dbg) {
+  if (dbg && std::atoi(std::getenv("CPRAND_DEBUG_SETUP")) != 2) {
     CPB_CUDA(cudaStreamSynchronize(stream_));
     std::fprintf(stderr, "  estimator values gathered +%.2f ms\n", 1e3 * seconds_since(te));
   }
@@ -1485,11 +1530,9 @@ void Session::build_fit_estimator(const double* xsrc) {
     const i64 d = dims_[static_cast<size_t>(n)], st = strides_[static_cast<size_t>(n)];
     for (size_t j = 0; j < offs.size(); ++j) idx[j] = static_cast<int>((offs[j] / st) % d);
     fit_idx_.push_back(dalloc<int>(idx.size()));
-    CPB_CUDA(cudaMemcpyAsync(fit_idx_.back(), idx.data(), idx.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
-    CPB_CUDA(cudaStreamSynchronize(stream_));
+    h2d(fit_idx_.back(), idx.data(), idx.size() * sizeof(int), stream_, true);
   }
-  CPB_CUDA(cudaStreamSynchronize(stream_));
-  cudaFree(d_off);
+  trash_.push_back(d_off);  // (cudaFree would wait for the device: freed with the session)
   has_fit_ = true;
 }
 
@@ -1620,9 +1663,9 @@ void Session::plan_replicas() {
         throw Unsupported("slab sharding needs the mode-major replicas of every strided mode to fit in HBM");
 }
 
-void Session::h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+void Session::h2d(void* dst, const void* src, size_t bytes, cudaStream_t st, bool always_stage) {
   if (bytes == 0) return;
-  if (!staging()) {
+  if (!staging() && (!always_stage || bytes > (size_t{16} << 20))) {  // (pageable: returns once the source is consumed)
     CPB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
     return;
   }
@@ -1635,6 +1678,10 @@ void Session::h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   char* p = static_cast<char*>(stage_blocks_.back().first) + stage_used_;
   stage_used_ += need;
   std::memcpy(p, src, bytes);
+  if (!staging()) {  // no upload in flight: the copy engine is free, and a pinned source makes the copy asynchronous
+    CPB_CUDA(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, st));
+    return;
+  }
   void* pd = nullptr;
   CPB_CUDA(cudaHostGetDevicePointer(&pd, p, 0));
   launch_stage_copy(dst, pd, bytes, st);

@@ -223,7 +223,7 @@ class Session {
   // source is first copied into pinned staging memory (kept until the session
   // ends), so the call returns at once instead of blocking behind the upload
   // parts queued on the copy engine; otherwise a plain cudaMemcpyAsync.
-  void h2d(void* dst, const void* src, size_t bytes, cudaStream_t st);
+  void h2d(void* dst, const void* src, size_t bytes, cudaStream_t st, bool always_stage = false);
   bool staging() const { return !x_->chunk_ev.empty(); }
   std::vector<std::pair<void*, size_t>> stage_blocks_;
   size_t stage_used_ = 0;
