@@ -19,7 +19,7 @@ struct Block {
   void* p;
 };
 constexpr size_t kBigMin = size_t{256} << 20;  // cache blocks of >= 256 MB
-constexpr int kMaxCached = 6;
+constexpr int kMaxCached = 8;
 std::mutex g_mu;
 std::vector<Block> g_cache;  // oldest first
 
@@ -108,28 +108,40 @@ struct HostBlock {
   void* p;
 };
 std::vector<HostBlock> g_host;
-constexpr int kMaxHostCached = 8;
+constexpr int kMaxHostCached = 32;
 }  // namespace
 
+// Requests are rounded to a power of two (>= 4 KB) on both sides, so a
+// released block serves any later request of its size class: sessions of
+// different shapes in one process (the bench, a serving loop) then reuse
+// each other's blocks instead of evicting them (cudaHostAlloc / cudaFreeHost
+// of a few MB cost milliseconds and wait for the device).
+static size_t host_class(size_t bytes) {
+  size_t c = 4096;
+  while (c < bytes) c <<= 1;
+  return c;
+}
+
 void* pinned_mapped_alloc(size_t bytes) {
+  const size_t cls = host_class(bytes);
   {
     std::lock_guard<std::mutex> lk(g_mu);
     for (auto it = g_host.begin(); it != g_host.end(); ++it)
-      if (it->bytes >= bytes && it->bytes <= 2 * bytes + 4096) {
+      if (it->bytes == cls) {
         void* p = it->p;
         g_host.erase(it);
         return p;
       }
   }
   void* p = nullptr;
-  CPB_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  CPB_CUDA(cudaHostAlloc(&p, cls, cudaHostAllocMapped | cudaHostAllocPortable));
   return p;
 }
 
 void pinned_mapped_free(void* p, size_t bytes) {
   if (!p) return;
   std::lock_guard<std::mutex> lk(g_mu);
-  g_host.push_back({bytes, p});
+  g_host.push_back({host_class(bytes), p});
   if (static_cast<int>(g_host.size()) > kMaxHostCached) {
     cudaFreeHost(g_host.front().p);
     g_host.erase(g_host.begin());

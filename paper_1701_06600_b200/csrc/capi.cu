@@ -194,7 +194,7 @@ int cprand_solve(int32_t method, const double* x, const int64_t* dims, int32_t o
     const size_t bytes = static_cast<size_t>(t.p) * sizeof(double);
     const bool on_device = opts && opts->x_is_device;
     // A pinned host tensor is uploaded in parts along the last mode by an
-    // uploader thread (three parts in flight on its own stream) while the
+    // uploader thread (every part queued at once on its own stream) while the
     // session sets up: the host-side setup (sample tables, work buffers, the
     // kernel arguments) and each part's share of the mode-major replicas
     // overlap the copy (Tensor::chunk_ev, Session::launch_replicas).
@@ -247,7 +247,6 @@ int cprand_solve(int32_t method, const double* x, const int64_t* dims, int32_t o
           if (e == cudaSuccess) e = cudaEventRecord(t.chunk_ev[c], up.st);
           if (e != cudaSuccess) up.err.store(static_cast<int>(e));
           t.chunk_submitted.store(static_cast<int>(c) + 1, std::memory_order_release);
-          if (c >= 2) cudaEventSynchronize(t.chunk_ev[c - 2]);  // three parts in flight
           a = b;
         }
         if (std::getenv("CPRAND_DEBUG_SETUP")) {

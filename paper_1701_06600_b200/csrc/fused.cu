@@ -26,6 +26,7 @@ namespace cpb {
 namespace {
 
 constexpr int kFusedThreads = 256;
+static_assert(kFusedThreads == 256, "ph::inverse_la: warps 0-6 hold the matrix, warp 7 inverts the pivot blocks");
 
 // Sense-reversing grid barrier over bar[0] (arrivals) and bar[1]
 // (generation). Requires every CTA co-resident (cooperative launch).

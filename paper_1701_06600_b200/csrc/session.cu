@@ -57,17 +57,31 @@ double host_stable_norm(const double* v, i64 n) {
   return scale * std::sqrt(ssq);
 }
 
+// the arena of the session being constructed / destroyed on this thread
+thread_local DevArena* tl_arena = nullptr;
+struct ArenaScope {
+  DevArena* prev;
+  explicit ArenaScope(DevArena* a) : prev(tl_arena) { tl_arena = a; }
+  ~ArenaScope() { tl_arena = prev; }
+};
+
 template <class T>
 T* dalloc(size_t n) {
   T* p = nullptr;
   if (n == 0) n = 1;
+  if (tl_arena)
+    if (void* q = tl_arena->take(n * sizeof(T))) return static_cast<T*>(q);
   CPB_CUDA(cudaMalloc(&p, n * sizeof(T)));
   return p;
 }
 
+void dfree_raw(void* p) {
+  if (p && !(tl_arena && tl_arena->owns(p))) cudaFree(p);
+}
+
 template <class T>
 void dfree(T*& p) {
-  if (p) cudaFree(p);
+  dfree_raw(p);
   p = nullptr;
 }
 
@@ -106,6 +120,39 @@ void Options::validate() const {  // solver.hpp:54-63
   if (!(fit_tolerance > 0.0)) throw InvalidArgument("fit_tolerance must be > 0");
   if (fit_sample_count < 1) throw InvalidArgument("fit_sample_count must be >= 1");
   if (stall_limit < 1) throw InvalidArgument("stall_limit must be >= 1");
+}
+
+void* DevArena::take(size_t bytes) {
+  constexpr size_t kBlk = size_t{256} << 20, kMaxReq = size_t{64} << 20;
+  bytes = (bytes + 255) & ~size_t{255};
+  if (bytes > kMaxReq) return nullptr;
+  if (blks.empty() || blks.back().used + bytes > blks.back().cap) {
+    blks.push_back({static_cast<char*>(big_alloc(kBlk)), kBlk, 0});
+    // debug: every byte 0xFF (NaN doubles, -1 indices), so a read of memory
+    // the session has not written shows up in the results
+    static const bool poison = std::getenv("CPRAND_ARENA_POISON") != nullptr;
+    if (poison) {
+      cudaDeviceSynchronize();
+      cudaMemset(blks.back().p, 0xFF, kBlk);
+      cudaDeviceSynchronize();
+    }
+  }
+  Blk& b = blks.back();
+  void* r = b.p + b.used;
+  b.used += bytes;
+  return r;
+}
+
+bool DevArena::owns(const void* q) const {
+  const char* c = static_cast<const char*>(q);
+  for (const Blk& b : blks)
+    if (c >= b.p && c < b.p + b.cap) return true;
+  return false;
+}
+
+void DevArena::release() {
+  for (Blk& b : blks) big_free(b.p, b.cap);
+  blks.clear();
 }
 
 Tensor::Tensor(const std::vector<i64>& d, int dev) : dims(d), device(dev) {
@@ -359,14 +406,23 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
     k_work_[k].assign(static_cast<size_t>(order_), 0.0);
   }
   try {
+    // (sharded sessions export buffers through CUDA IPC, which wants whole allocations)
+    // Off unless CPRAND_ARENA=1: it takes 2.8 ms off a one-shot C4 call (166.7 -> 163.9 ms), but with it
+    // repeated runs on one tensor were not always bitwise equal from the fourth iteration on (differences
+    // of 1e-12, tests/micro/determinism_probe2.py; equal without it in every repeat; cause not found),
+    // and bitwise repeatability is a property the default path keeps.
+    static const bool use_arena = std::getenv("CPRAND_ARENA") != nullptr && std::atoi(std::getenv("CPRAND_ARENA")) != 0;
+    ArenaScope scope((o_.comm || !use_arena) ? nullptr : &arena_);
     setup(init_lambda, init_factors);
   } catch (...) {
     stop_table_thread();  // a joinable std::thread must not outlive the failed constructor
+    cudaDeviceSynchronize();  // the arena's blocks go back to the cache with the members
     throw;
   }
 }
 
 Session::~Session() {
+  ArenaScope scope(&arena_);  // dfree leaves the arena's pointers alone; the blocks are released with arena_
   stop_table_thread();
   if (tstream_) cudaStreamSynchronize(tstream_);
   if (stream_) cudaStreamSynchronize(stream_);
@@ -424,7 +480,7 @@ Session::~Session() {
   dfree(gfull_);
   dfree(qrws_);
   dfree(info_);
-  for (void* q : trash_) cudaFree(q);
+  for (void* q : trash_) dfree_raw(q);
   trash_.clear();
   for (auto& b : stage_blocks_) pinned_mapped_free(b.first, b.second);
   stage_blocks_.clear();
@@ -691,6 +747,7 @@ void Session::setup_fused() {
     // kernel): a host -> device copy would queue behind the upload parts
     FusedIter* hc = static_cast<FusedIter*>(pinned_mapped_alloc(sizeof(FusedIter)));
     stage_blocks_.emplace_back(hc, sizeof(FusedIter));
+    stage_used_ = sizeof(FusedIter);  // (a dedicated block: h2d opens a new one)
     FusedIter* dc = nullptr;
     CPB_CUDA(cudaHostGetDevicePointer(&dc, hc, 0));
     FusedIter c{};
@@ -714,6 +771,15 @@ void Session::setup_fused() {
     trash_.push_back(cen);
   }
   const int gw = fgrid_ - 1 - (idle_cta >= 0 ? 1 : 0);
+  // The tiling (split sizes, so the summation order and the last bits of a
+  // run) must not depend on what the census found: it always assumes the
+  // inverse CTA has an idle partner. A census without one (measured: it can
+  // differ between two sessions of one process when other kernels are
+  // resident during the census launch) leaves one tile CTA without a tile.
+  const int gw_tiles = std::max(1, fgrid_ - 2);
+  if (std::getenv("CPRAND_DEBUG_SETUP"))
+    std::fprintf(stderr, "fused setup: grid %d, inverse CTA %d, idle CTA %d, smem %zu, zcap %d\n", fgrid_, inv_cta,
+                 idle_cta, fsmem_, zcap);
   // CPRAND kernel tiling per mode
   std::vector<int> tm(static_cast<size_t>(order_)), tk(tm), tkl(tm);
   const int nfr = (r_ + 7) / 8, nblk = nfr * (nfr + 1) / 2;
@@ -723,7 +789,7 @@ void Session::setup_fused() {
     int& tk_max = tk_max_;
     for (int n = 0; n < order_; ++n) {
       const size_t k = static_cast<size_t>(n);
-      fused_rand_tiles(tdims_[k], s_mode_[k], gw, zcap, &tm[k], &tk[k], &tkl[k]);
+      fused_rand_tiles(tdims_[k], s_mode_[k], gw_tiles, zcap, &tm[k], &tk[k], &tkl[k]);
       tm_max = std::max(tm_max, tm[k]);
       tk_max = std::max(tk_max, tk[k]);
       max_part = std::max(max_part, static_cast<i64>(tk[k]) * dims_[k] * r_);
@@ -874,7 +940,7 @@ void Session::setup_fused() {
         M.kb_cnt = c + static_cast<size_t>(tm_max) * kCS;
         M.mcnt = c + static_cast<size_t>(tm_max + tk_max_) * kCS;
         M.gm_cnt = c + static_cast<size_t>(tm_max + tk_max_ + 3) * kCS;
-        M.dist_gram = (tm[k] * tk[k] <= gw) ? 1 : 0;
+        M.dist_gram = (tm[k] * tk[k] <= gw_tiles) ? 1 : 0;
         if (peer_) M.tkllen = M.lcnt > 0 ? std::max(4, (ceil_div(M.lcnt, tk[k]) + 3) / 4 * 4) : 0;
         M.grdy = c + static_cast<size_t>(2 * tm_max + tk_max_ + 3) * kCS;
         M.adone = M.grdy + static_cast<size_t>(kRep) * kCS;

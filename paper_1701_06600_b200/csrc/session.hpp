@@ -82,10 +82,9 @@ struct Tensor {
   // Owned by whoever filled them; empty when the tensor is resident.
   std::vector<cudaEvent_t> chunk_ev;
   std::vector<i64> chunk_end;
-  // events [0, chunk_submitted) have been recorded (the uploader thread keeps
-  // three parts in flight, so small setup copies are not queued behind the
-  // whole tensor on the copy engine); waiting on an unrecorded event would
-  // be a no-op, so consumers wait for the count first
+  // events [0, chunk_submitted) have been recorded by the uploader thread;
+  // waiting on an unrecorded event would be a no-op, so consumers wait for
+  // the count first
   std::atomic<int> chunk_submitted{0};
   explicit Tensor(const std::vector<i64>& dims, int device);
   ~Tensor();
@@ -105,6 +104,25 @@ std::vector<std::vector<double>> mixing_signs(const std::vector<i64>& dims, int 
                                               std::uint64_t seed);                // mixing.hpp:25-49
 void baseline_factors_host(const std::vector<i64>& dims, int r, double c, std::uint64_t seed,
                            std::vector<std::vector<double>>& out);
+
+// Optional (CPRAND_ARENA=1, off by default: see Session::Session): a
+// session's small device buffers (work arrays, sample tables, kernel
+// arguments: ~45 allocations) come out of 256 MB blocks that big_alloc keeps
+// across sessions, so a session costs no cudaMalloc / cudaFree of its own
+// (each cudaFree waits for the device: ~3 ms of a one-shot call's teardown).
+// Requests above 64 MB and sharded sessions (whose buffers are exported
+// through CUDA IPC) use cudaMalloc.
+struct DevArena {
+  struct Blk {
+    char* p;
+    size_t cap, used;
+  };
+  std::vector<Blk> blks;
+  void* take(size_t bytes);
+  bool owns(const void* q) const;
+  void release();
+  ~DevArena() { release(); }
+};
 
 class Session {
  public:
@@ -227,6 +245,7 @@ class Session {
   bool staging() const { return !x_->chunk_ev.empty(); }
   std::vector<std::pair<void*, size_t>> stage_blocks_;
   size_t stage_used_ = 0;
+  DevArena arena_;
   std::vector<void*> trash_;  // setup-time device buffers freed with the session (cudaFree waits for the device)
   void setup_fused();
   bool fused_ = false;

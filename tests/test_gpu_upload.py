@@ -63,3 +63,28 @@ def test_pipelined_upload_matches_synchronous_mix():
     for fa, fb in zip(a.factors, b.factors):
         assert np.array_equal(fa, fb)
     buf.close()
+
+
+def test_repeated_solves_are_bitwise_equal():
+    """The default path is bitwise repeatable: four one-shot solves of one
+    tensor in one process (sessions reuse each other's cached device and
+    pinned blocks) return identical factors."""
+    import paper_1701_06600_b200 as pb
+    dims = (160, 230, 250)
+    t = pb.DeviceTensor(dims)
+    t.synth(6, 0.5, 0.01, 3)
+    buf = pb.PinnedBuffer(int(np.prod(dims)))
+    t.download_into(buf.array)
+    t.close()
+    xh = buf.array.reshape(dims, order="F")
+    os.environ["CPRAND_SYNC_UPLOAD"] = "1"
+    try:
+        res = [pb.solve("rand", xh, 6, 150, pb.SolveOptions(rng_seed=5, device=0, max_iters=8, bench_mode=True))
+               for _ in range(4)]
+    finally:
+        os.environ.pop("CPRAND_SYNC_UPLOAD", None)
+    for r in res[1:]:
+        assert np.array_equal(r.lam, res[0].lam)
+        for fa, fb in zip(r.factors, res[0].factors):
+            assert np.array_equal(fa, fb)
+    buf.close()
