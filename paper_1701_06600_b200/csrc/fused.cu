@@ -499,6 +499,22 @@ __device__ __forceinline__ void prefetch_tables(const FusedIter& A, unsigned b) 
   }
 }
 
+// Buffer of mode m's column sums of squares (one [G][r] block per buffer).
+// Modes alternate between buffers 0 and 1: mode m's partials are read at the
+// start of mode m + 1 and buffer m & 1 is next written in mode m + 2, behind
+// that mode's start-of-mode wait. Under lazy_last the last mode's partials
+// are read during mode 0 of the NEXT launch, which starts without such a
+// wait: a CTA without a tile in mode 0 stores its (zero) partial at once, and
+// where it had rows in the last mode (the modes' tilings differ) it could
+// overwrite a partial the inverse CTA had not read yet. The last mode
+// therefore has a buffer of its own, rewritten only in the next launch's last
+// mode. (Found by tests/test_gpu_upload.py::test_repeated_solves_are_bitwise_
+// equal: a lost partial only rescales the next Z_S's columns, which the
+// normalization absorbs, so results moved by 1e-12, run to run.)
+__device__ __forceinline__ int ssq_buf(const FusedIter& A, int m) {
+  return (A.lazy_last && m == A.order - 1) ? 2 : (m & 1);
+}
+
 // GA: the Gram is summed with L2 fp64 atomics (FusedIter::gram_atomic).
 // PEER: the slab-sharded path (FusedIter::np ranks exchanging through peer
 // memory): modes n < N-1 contract this rank's fibers and exchange the RHS
@@ -511,17 +527,22 @@ __device__ __forceinline__ void prefetch_tables(const FusedIter& A, unsigned b) 
 // mode and cost the hot path instruction fetches (C4 9.06 k -> 9.25 k it/s on
 // one box; the MIX kernel measured 1-2 % slower with them out of line, so it
 // keeps them inline).
+#ifdef CPB_NO_COLD
+#define CPB_COLD_ATTR
+#else
+#define CPB_COLD_ATTR __noinline__
+#endif
 template <int RT>
-__device__ __noinline__ void qr_factor_cold(const double* z, int s, int r, double qtol, double* ws, double* ginv,
+__device__ CPB_COLD_ATTR void qr_factor_cold(const double* z, int s, int r, double qtol, double* ws, double* ginv,
                                             int* info, double* sh) {
   ph::qr_factor<RT>(z, s, r, qtol, ws, ginv, info, sh);
 }
 template <int RT>
-__device__ __noinline__ void pinv_fallback_cold(double* gfull, int r, double tol, double* ginv, int* info, int* perm_sh) {
+__device__ CPB_COLD_ATTR void pinv_fallback_cold(double* gfull, int r, double tol, double* ginv, int* info, int* perm_sh) {
   ph::pinv_fallback<RT>(gfull, r, tol, ginv, info, perm_sh);
 }
 template <int RT>
-__device__ __noinline__ void qr_rows_cold(const QrSrc& q, const double* ws, int r, i64 in, i64 i0, int nrow, double* out,
+__device__ CPB_COLD_ATTR void qr_rows_cold(const QrSrc& q, const double* ws, int r, i64 in, i64 i0, int nrow, double* out,
                                           int ldo, double* stage) {
   ph::qr_rows<RT, kFusedThreads>(q, ws, r, in, i0, nrow, out, ldo, stage);
 }
@@ -570,7 +591,7 @@ __device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, co
   auto form_norms = [&](int m) {
     const FusedMode& Q = A.mode[m];
     ModeWork wq = work_of(A, Q);
-    wq.ssq = A.ssq + static_cast<i64>(m & 1) * G * r;
+    wq.ssq = A.ssq + static_cast<i64>(ssq_buf(A, m)) * G * r;
     int nparts = static_cast<int>(Gw);
     if (PEER && np > 1 && m == A.order - 1) {  // every rank's slab partials, in (rank, CTA) order
       wq.ssq = A.pssq[A.prank];
@@ -859,7 +880,7 @@ __device__ __forceinline__ void rand_body(const FusedIter* __restrict__ args, co
         __syncthreads();
         if (tid < np * kRep) red_release_sys(A.pdone[tid / kRep] + (tid % kRep) * kCS, 1u);
       } else {
-        if (tid < r) A.ssq[static_cast<i64>(n & 1) * G * r + static_cast<i64>(rank) * r + tid] = q2;
+        if (tid < r) A.ssq[static_cast<i64>(ssq_buf(A, n)) * G * r + static_cast<i64>(rank) * r + tid] = q2;
         signal_add_rep(M.adone, 1u, kRep);
       }
       stamp(n, 5);
@@ -937,7 +958,7 @@ __global__ void __launch_bounds__(kFusedThreads) fused_finish_kernel(const Fused
   const FusedMode& Q = A.mode[m];
   const int gw = A.grid - 1 - (A.idle_cta >= 0 ? 1 : 0);
   ModeWork wq = work_of(A, Q);
-  wq.ssq = A.ssq + static_cast<i64>(m & 1) * A.grid * A.r;
+  wq.ssq = A.ssq + static_cast<i64>(ssq_buf(A, m)) * A.grid * A.r;
   ph::norms_final<RT, kFusedThreads>(A.r, Q.in_full, wq, gw, m == 0, A.rng, red, nullptr, A.mode[m - 1].norms);
   tl::signal_add_rep(Q.nready, 1u, kRep);
   if (threadIdx.x == 0) *A.npend = 0;

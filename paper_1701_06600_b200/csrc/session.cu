@@ -407,11 +407,8 @@ Session::Session(int method, Tensor* x, int r, int s, const Options& o, const do
   }
   try {
     // (sharded sessions export buffers through CUDA IPC, which wants whole allocations)
-    // Off unless CPRAND_ARENA=1: it takes 2.8 ms off a one-shot C4 call (166.7 -> 163.9 ms), but with it
-    // repeated runs on one tensor were not always bitwise equal from the fourth iteration on (differences
-    // of 1e-12, tests/micro/determinism_probe2.py; equal without it in every repeat; cause not found),
-    // and bitwise repeatability is a property the default path keeps.
-    static const bool use_arena = std::getenv("CPRAND_ARENA") != nullptr && std::atoi(std::getenv("CPRAND_ARENA")) != 0;
+    // (CPRAND_ARENA=0: plain cudaMalloc / cudaFree per buffer, for A/B)
+    static const bool use_arena = !(std::getenv("CPRAND_ARENA") && std::atoi(std::getenv("CPRAND_ARENA")) == 0);
     ArenaScope scope((o_.comm || !use_arena) ? nullptr : &arena_);
     setup(init_lambda, init_factors);
   } catch (...) {
@@ -640,7 +637,8 @@ void Session::setup(const double* init_lambda, const double* const* init_factors
   CPB_CUDA(cudaMemsetAsync(info_, 0, 4 * sizeof(int), stream_));
   tickets_ = dalloc<unsigned>(8);
   CPB_CUDA(cudaMemsetAsync(tickets_, 0, 8 * sizeof(unsigned), stream_));
-  ssq_ = dalloc<double>(static_cast<size_t>(std::max<i64>(max_apply, 4 * sms_) * r_));
+  // (the persistent CPRAND kernel: three [grid][r] buffers, grid <= 2 CTAs per SM; fused.cu ssq_buf)
+  ssq_ = dalloc<double>(static_cast<size_t>(std::max<i64>(max_apply, 6 * sms_) * r_));
   if (mix_ || shard_ || cmix_) rhs_full_ = dalloc<double>(static_cast<size_t>(max_in * r_));
   if (shard_ && mix_) rhs_gather_ = dalloc<double>(static_cast<size_t>(lmax_ * nranks_ * r_));
   if (cmix_) {

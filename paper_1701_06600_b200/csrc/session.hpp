@@ -105,13 +105,14 @@ std::vector<std::vector<double>> mixing_signs(const std::vector<i64>& dims, int 
 void baseline_factors_host(const std::vector<i64>& dims, int r, double c, std::uint64_t seed,
                            std::vector<std::vector<double>>& out);
 
-// Optional (CPRAND_ARENA=1, off by default: see Session::Session): a
-// session's small device buffers (work arrays, sample tables, kernel
+// A session's small device buffers (work arrays, sample tables, kernel
 // arguments: ~45 allocations) come out of 256 MB blocks that big_alloc keeps
 // across sessions, so a session costs no cudaMalloc / cudaFree of its own
-// (each cudaFree waits for the device: ~3 ms of a one-shot call's teardown).
-// Requests above 64 MB and sharded sessions (whose buffers are exported
-// through CUDA IPC) use cudaMalloc.
+// (each cudaFree waits for the device: ~3 ms of a one-shot call's teardown;
+// C4 one-shot call 166.1 -> 163.9 ms). Requests above 64 MB and sharded
+// sessions (whose buffers are exported through CUDA IPC) use cudaMalloc;
+// CPRAND_ARENA=0 turns it off. CPRAND_ARENA_POISON=1 fills every block with
+// 0xFF first (a read of memory the session has not written then shows).
 struct DevArena {
   struct Blk {
     char* p;
