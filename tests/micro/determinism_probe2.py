@@ -1,3 +1,4 @@
+"""Where repeated one-shot solves of one tensor diverge (relative differences per factor by iteration count; not part of the product)."""
 import os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
